@@ -1,0 +1,111 @@
+"""TEST INFRASTRUCTURE ONLY — numpy fp32 Llama-style decoder (the tensor-math oracle).
+
+PARITY UNPINNED BY THE REFERENCE: the reference has no transformer ("real transformer
+KV tensors (replaced by a token-block cost simulator)").  This restatement is
+builder-authored and follows standard Llama-3 semantics:
+  RMSNorm eps 1e-5 (weight multiply after normalisation), RoPE theta 500000 rotate-half on the
+  post-projection Q/K with absolute positions, GQA (H/Hkv query heads share a kv head), causal
+  mask, SwiGLU (silu(gate) * up), untied lm_head, greedy = first argmax.
+It is pinned to the reference only through the token/block layout: positions are indices in the
+concatenated per-segment TokenSeq (orchestrator.cpp:81-97); token ids are fnv1a(bytes) mod V.
+Weights are the engine's own bf16 weights (exported), promoted to fp32; activations stay fp32.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def fnv1a(b: bytes, h: int = 14695981039346656037) -> int:
+    for c in b:
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def token_ids(tokens, vocab):
+    return [fnv1a(t.encode() if isinstance(t, str) else t) % vocab for t in tokens]
+
+
+def inv_freq(head_dim, theta):
+    i = np.arange(0, head_dim // 2, dtype=np.float64)
+    return (1.0 / np.power(float(np.float32(theta)), 2.0 * i / head_dim)).astype(np.float32)
+
+
+def rope(x, pos, inv):
+    """x [n, h, hd] fp32; rotate-half with fp32 angles pos*inv."""
+    ang = (pos.astype(np.float32)[:, None] * inv[None, :]).astype(np.float32)
+    cos = np.cos(ang.astype(np.float64)).astype(np.float32)[:, None, :]
+    sin = np.sin(ang.astype(np.float64)).astype(np.float32)[:, None, :]
+    half = x.shape[-1] // 2
+    a, b = x[..., :half], x[..., half:]
+    return np.concatenate([a * cos - b * sin, b * cos + a * sin], axis=-1)
+
+
+def rmsnorm(x, w, eps):
+    var = np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True)
+    return (x / np.sqrt(var + eps)) * w
+
+
+class Decoder:
+    def __init__(self, cfg, weights):
+        self.c = cfg
+        self.w = weights
+        self.inv = inv_freq(cfg.head_dim, cfg.rope_theta)
+
+    def forward(self, ids, pos=None, past=None, return_all=False):
+        """ids [n]; past: per-layer (K [p,Hkv,hd], V) of preceding positions.  Returns logits of
+        the last position (or all) and the updated cache."""
+        c, w = self.c, self.w
+        n = len(ids)
+        p0 = 0 if past is None else past[0][0].shape[0]
+        if pos is None:
+            pos = np.arange(p0, p0 + n)
+        H, Hkv, hd = c.n_heads, c.n_kv_heads, c.head_dim
+        G = H // Hkv
+        x = w["embed"][np.asarray(ids)].astype(np.float32)
+        new_past = []
+        for l, lw in enumerate(w["layers"]):
+            h = rmsnorm(x, lw["attn_norm"], c.norm_eps)
+            qkv = h @ lw["wqkv"].T
+            q = qkv[:, :H * hd].reshape(n, H, hd)
+            k = qkv[:, H * hd:(H + Hkv) * hd].reshape(n, Hkv, hd)
+            v = qkv[:, (H + Hkv) * hd:].reshape(n, Hkv, hd)
+            q = rope(q, pos, self.inv)
+            k = rope(k, pos, self.inv)
+            if past is not None:
+                k = np.concatenate([past[l][0], k], axis=0)
+                v = np.concatenate([past[l][1], v], axis=0)
+            new_past.append((k, v))
+            m = k.shape[0]
+            out = np.empty((n, H, hd), dtype=np.float32)
+            kpos = np.arange(m)
+            mask = kpos[None, :] <= np.asarray(pos)[:, None]
+            for hh in range(H):
+                kh = hh // G
+                s = (q[:, hh, :] @ k[:, kh, :].T) / np.sqrt(hd)
+                s = np.where(mask, s, -np.inf)
+                s = s - s.max(axis=1, keepdims=True)
+                pr = np.exp(s)
+                pr /= pr.sum(axis=1, keepdims=True)
+                out[:, hh, :] = pr @ v[:, kh, :]
+            x = x + out.reshape(n, H * hd) @ lw["wo"].T
+            h = rmsnorm(x, lw["mlp_norm"], c.norm_eps)
+            gu = h @ lw["w_gate_up"].T
+            g, u = gu[:, :c.d_ff], gu[:, c.d_ff:]
+            act = g / (1.0 + np.exp(-g)) * u
+            x = x + act @ lw["w_down"].T
+        rows = x if return_all else x[-1:]
+        hf = rmsnorm(rows, w["final_norm"], c.norm_eps)
+        logits = hf @ w["lm_head"].T
+        return (logits if return_all else logits[0]), new_past
+
+    def greedy(self, ids, steps):
+        logits, past = self.forward(ids)
+        out = []
+        tok = int(np.argmax(logits))
+        out.append(tok)
+        for _ in range(steps):
+            logits, past = self.forward([tok], past=past)
+            tok = int(np.argmax(logits))
+            out.append(tok)
+        return out  # out[0] = prefill's first token, then `steps` decode tokens

@@ -1,0 +1,386 @@
+// extern "C" surface (include/glmx.h).  Every entry point converts C++ exceptions into the
+// status codes that mirror the reference's exception classes (error.hpp:29-137).
+#include <cstring>
+#include <string>
+
+#include "runtime.hpp"
+
+using namespace glmx;
+
+int chunk_build_impl(glmx_graph*, const glmx_chunk_config*, const int32_t*, uint64_t, char*,
+                     uint64_t, uint64_t*, int32_t*, uint64_t*, uint64_t*, uint64_t, uint64_t*,
+                     uint64_t*, uint64_t*);
+glmx_kv* kv_create_impl(const glmx_kv_config*);
+void pool_copy_impl(glmx_kv*, glmx_kv*, const int32_t*, const int32_t*, uint64_t, cudaStream_t);
+glmx_model* model_create_impl(const glmx_model_config*, int);
+int model_export_impl(const glmx_model*, int, int, uint16_t*, uint64_t);
+glmx_engine* engine_create_impl(glmx_model*, glmx_kv*, const glmx_engine_config*);
+int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefill_report*,
+                        int32_t*, float*);
+int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
+int engine_replay_impl(glmx_engine*);
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return GLMX_ERR_ARG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GLMX_ERR_ARG;
+  }
+}
+
+int64_t copy_str(const std::string& s, char* buf, uint64_t cap) {
+  if (buf && cap) std::memcpy(buf, s.data(), std::min<uint64_t>(cap, s.size()));
+  return static_cast<int64_t>(s.size());
+}
+
+void fill_report(const PrefillResult& r, glmx_prefill_report* rep, int32_t* bt, uint64_t bt_cap,
+                 uint64_t* ev, uint64_t ev_cap) {
+  if (rep) {
+    rep->cached_tokens = r.cached;
+    rep->computed_tokens = r.computed;
+    rep->tail_tokens = r.tail;
+    rep->n_evicted = r.evicted.size();
+    rep->n_blocks = r.pages.size();
+  }
+  if (bt)
+    for (uint64_t i = 0; i < r.pages.size() && i < bt_cap; ++i) bt[i] = r.pages[i];
+  if (ev)
+    for (uint64_t i = 0; i < r.evicted.size() && i < ev_cap; ++i) ev[i] = r.evicted[i];
+}
+}  // namespace
+
+extern "C" {
+
+const char* glmx_last_error(void) { return g_err.c_str(); }
+const char* glmx_version(void) { return "glmx 0.1 (sm_100a)"; }
+int glmx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ KV
+int glmx_kv_create(const glmx_kv_config* cfg, glmx_kv** out) {
+  return guarded([&] {
+    if (!cfg || !out) throw Error(GLMX_ERR_ARG, "null argument");
+    *out = kv_create_impl(cfg);
+    return GLMX_OK;
+  });
+}
+void glmx_kv_destroy(glmx_kv* kv) {
+  if (!kv) return;
+  DeviceGuard g(kv->cfg.device);
+  delete kv;
+}
+
+int glmx_kv_prefill(glmx_kv* kv, const char* tok_bytes, const uint64_t* tok_offsets,
+                    uint64_t n_tok, const glmx_tier_range* tiers, uint64_t n_tiers,
+                    const char* session, glmx_prefill_report* report, int32_t* block_table,
+                    uint64_t block_table_cap, uint64_t* evicted, uint64_t evicted_cap) {
+  return guarded([&] {
+    if (!kv->has_pool()) kv->bk->pool().release_deferred();
+    PrefillResult r;
+    TokenSpans ts{tok_bytes, tok_offsets, n_tok};
+    kv->bk->prefill(ts, tiers, n_tiers, session ? session : "", r);
+    fill_report(r, report, block_table, block_table_cap, evicted, evicted_cap);
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_prefill_segments(glmx_kv* kv, uint64_t n_seg, const char* const* seg_text,
+                             const uint64_t* seg_len, const int32_t* seg_tier,
+                             const char* session, glmx_prefill_report* report,
+                             int32_t* block_table, uint64_t block_table_cap, uint64_t* evicted,
+                             uint64_t evicted_cap) {
+  return guarded([&] {
+    // Orchestrator::kv_prefill (orchestrator.cpp:81-97)
+    std::string bytes;
+    std::vector<uint64_t> offs{0};
+    std::vector<glmx_tier_range> tiers;
+    std::vector<uint64_t> b, e;
+    for (uint64_t i = 0; i < n_seg; ++i) {
+      b.clear();
+      e.clear();
+      tokenize_spans(seg_text[i], seg_len[i], b, e);
+      if (b.empty()) continue;
+      const uint64_t begin = offs.size() - 1;
+      for (size_t j = 0; j < b.size(); ++j) {
+        bytes.append(seg_text[i] + b[j], e[j] - b[j]);
+        offs.push_back(bytes.size());
+      }
+      const uint64_t end = offs.size() - 1;
+      if (!tiers.empty() && tiers.back().tier == seg_tier[i])
+        tiers.back().end = end;
+      else
+        tiers.push_back({begin, end, seg_tier[i], 0});
+    }
+    if (!kv->has_pool()) kv->bk->pool().release_deferred();
+    PrefillResult r;
+    TokenSpans ts{bytes.data(), offs.data(), offs.size() - 1};
+    kv->bk->prefill(ts, tiers.data(), tiers.size(), session ? session : "", r);
+    fill_report(r, report, block_table, block_table_cap, evicted, evicted_cap);
+    return GLMX_OK;
+  });
+}
+
+uint64_t glmx_kv_last_evicted(const glmx_kv* kv, uint64_t* out, uint64_t cap) {
+  const auto& v = kv->bk->last_evicted();
+  for (uint64_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+  return v.size();
+}
+
+int glmx_kv_evict(glmx_kv* kv, uint64_t n, uint64_t* out, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    if (n_out) *n_out = 0;
+    auto ids = kv->bk->evict(n);
+    for (uint64_t i = 0; i < ids.size() && i < cap; ++i) out[i] = ids[i];
+    if (n_out) *n_out = std::min<uint64_t>(ids.size(), cap);
+    if (!kv->has_pool()) kv->bk->pool().release_deferred();
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_set_tier(glmx_kv* kv, const char* session, int32_t from_tier, int32_t to_tier) {
+  return guarded([&] {
+    kv->bk->set_tier(session ? session : "", from_tier, to_tier);
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_force_insert(glmx_kv* kv, uint64_t id, int32_t tier, uint64_t last_used,
+                         const char* session) {
+  return guarded([&] {
+    if (tier < 0 || tier > 3) throw Error(GLMX_ERR_ARG, "tier out of range");
+    kv->bk->force_insert(id, tier, last_used, session ? session : "");
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_counters(const glmx_kv* kv, int64_t out6[6]) {
+  out6[0] = kv->bk->hits();
+  out6[1] = kv->bk->misses();
+  for (int t = 0; t < 4; ++t) out6[2 + t] = kv->bk->evictions_by_tier()[t];
+  return GLMX_OK;
+}
+
+uint64_t glmx_kv_resident(const glmx_kv* kv, uint64_t* ids, int32_t* tiers, uint64_t* last_used,
+                          int32_t* pages, uint64_t cap) {
+  if (cap == 0) return kv->bk->resident();
+  auto v = kv->bk->resident_sorted();
+  for (uint64_t i = 0; i < v.size() && i < cap; ++i) {
+    if (ids) ids[i] = v[i]->id;
+    if (tiers) tiers[i] = v[i]->tier;
+    if (last_used) last_used[i] = v[i]->last_used;
+    if (pages) pages[i] = v[i]->page;
+  }
+  return v.size();
+}
+
+int64_t glmx_kv_block_session(const glmx_kv* kv, uint64_t id, char* buf, uint64_t cap) {
+  const Block* b = kv->bk->block(id);
+  if (!b) return -1;
+  return copy_str(kv->bk->session_name(b->session), buf, cap);
+}
+
+int64_t glmx_kv_snapshot_json(const glmx_kv* kv, char* buf, uint64_t cap) {
+  return copy_str(kv->bk->snapshot_json(), buf, cap);
+}
+
+uint64_t glmx_kv_chain_ids(const char* tok_bytes, const uint64_t* tok_offsets, uint64_t n_tok,
+                           uint32_t block_tokens, uint64_t* out) {
+  if (block_tokens == 0) return 0;
+  std::vector<uint64_t> ids;
+  BlockEngine::chain_ids(TokenSpans{tok_bytes, tok_offsets, n_tok}, block_tokens, ids);
+  if (out) std::memcpy(out, ids.data(), ids.size() * 8);
+  return ids.size();
+}
+
+int glmx_kv_release_deferred(glmx_kv* kv) {
+  kv->bk->pool().release_deferred();
+  return GLMX_OK;
+}
+uint64_t glmx_kv_pool_pages(const glmx_kv* kv) { return kv->bk->pool().total(); }
+uint64_t glmx_kv_free_pages(const glmx_kv* kv) { return kv->bk->pool().free_count(); }
+void* glmx_kv_pool_ptr(const glmx_kv* kv) { return kv->geom.base; }
+uint64_t glmx_kv_page_bytes(const glmx_kv* kv) { return kv->page_bytes; }
+
+uint64_t glmx_tokenize(const char* text, uint64_t len, uint64_t* begins, uint64_t* ends,
+                       uint64_t cap) {
+  std::vector<uint64_t> b, e;
+  tokenize_spans(text, len, b, e);
+  for (uint64_t i = 0; i < b.size() && i < cap; ++i) {
+    if (begins) begins[i] = b[i];
+    if (ends) ends[i] = e[i];
+  }
+  return b.size();
+}
+
+int32_t glmx_token_id(const char* tok, uint64_t len, uint32_t vocab) {
+  return vocab ? token_id(tok, len, vocab) : -1;
+}
+
+// ------------------------------------------------------------------ graph
+static glmx_graph* finish_graph(HostGraph&& h, int device) {
+  auto g = std::make_unique<glmx_graph>();
+  g->host = std::move(h);
+  g->device = device;
+  if (device >= 0) g->upload();
+  return g.release();
+}
+
+int glmx_graph_load_jsonl(const char* path, int32_t device, glmx_graph** out) {
+  return guarded([&] {
+    *out = finish_graph(load_graph_jsonl(path), device);
+    return GLMX_OK;
+  });
+}
+
+int glmx_graph_synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed,
+                              int32_t device, glmx_graph** out) {
+  return guarded([&] {
+    *out = finish_graph(synth_powerlaw(n_nodes, edges_per_node, seed), device);
+    return GLMX_OK;
+  });
+}
+
+int glmx_graph_save_jsonl(const glmx_graph* g, const char* path) {
+  return guarded([&] {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw Error(GLMX_ERR_GLM, std::string("cannot write graph file: ") + path);
+    std::string s = g->host.serialize_jsonl();
+    std::fwrite(s.data(), 1, s.size(), f);
+    std::fclose(f);
+    return GLMX_OK;
+  });
+}
+
+void glmx_graph_destroy(glmx_graph* g) {
+  if (!g) return;
+  DeviceGuard dg(g->device);
+  delete g;
+}
+uint64_t glmx_graph_node_count(const glmx_graph* g) { return g->host.n(); }
+uint64_t glmx_graph_edge_count(const glmx_graph* g) { return g->host.src.size(); }
+int64_t glmx_graph_node_index(const glmx_graph* g, const char* id) {
+  auto it = g->host.index.find(id);
+  return it == g->host.index.end() ? -1 : it->second;
+}
+int64_t glmx_graph_node_id(const glmx_graph* g, uint64_t idx, char* buf, uint64_t cap) {
+  if (idx >= g->host.n()) return -1;
+  return copy_str(g->host.ids[idx], buf, cap);
+}
+int64_t glmx_graph_degree(const glmx_graph* g, uint64_t idx) {
+  if (idx >= g->host.n()) return -1;
+  return g->host.w_total[idx];
+}
+
+int glmx_chunk_build(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t* node_idx,
+                     uint64_t n, char* out_bytes, uint64_t bytes_cap, uint64_t* out_byte_offsets,
+                     int32_t* out_tok_ids, uint64_t* out_tok_begin, uint64_t* out_tok_end,
+                     uint64_t tok_cap, uint64_t* out_tok_offsets, uint64_t* total_bytes,
+                     uint64_t* total_tokens) {
+  return guarded([&] {
+    return chunk_build_impl(g, cfg, node_idx, n, out_bytes, bytes_cap, out_byte_offsets,
+                            out_tok_ids, out_tok_begin, out_tok_end, tok_cap, out_tok_offsets,
+                            total_bytes, total_tokens);
+  });
+}
+
+int64_t glmx_node_info_rendered(glmx_graph* g, const glmx_chunk_config* cfg, const char* id,
+                                char* buf, uint64_t cap) {
+  int64_t len = -GLMX_ERR_ARG;
+  int st = guarded([&] {
+    auto it = g->host.index.find(id);
+    if (it == g->host.index.end()) throw Error(GLMX_ERR_RETRIEVAL, std::string("unknown node id: ") + id);
+    int32_t idx = it->second;
+    uint64_t tb = 0, tt = 0;
+    chunk_build_impl(g, cfg, &idx, 1, nullptr, 0, nullptr, nullptr, nullptr, nullptr, 0, nullptr,
+                     &tb, &tt);
+    std::string out(tb, '\0');
+    uint64_t offs[2];
+    chunk_build_impl(g, cfg, &idx, 1, out.data(), tb, offs, nullptr, nullptr, nullptr, 0,
+                     nullptr, &tb, &tt);
+    len = copy_str(out, buf, cap);
+    return GLMX_OK;
+  });
+  return st == GLMX_OK ? len : -st;
+}
+
+float glmx_chunk_last_kernel_ms(const glmx_graph* g) { return g->last_ms; }
+
+// ------------------------------------------------------------------ model / engine
+int glmx_model_create(const glmx_model_config* cfg, int32_t device, glmx_model** out) {
+  return guarded([&] {
+    *out = model_create_impl(cfg, device);
+    return GLMX_OK;
+  });
+}
+void glmx_model_destroy(glmx_model* m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  delete m;
+}
+int glmx_model_export_weight(const glmx_model* m, int32_t which, int32_t layer, uint16_t* out,
+                             uint64_t n) {
+  return guarded([&] { return model_export_impl(m, which, layer, out, n); });
+}
+
+int glmx_engine_create(glmx_model* m, glmx_kv* kv, const glmx_engine_config* cfg,
+                       glmx_engine** out) {
+  return guarded([&] {
+    *out = engine_create_impl(m, kv, cfg);
+    return GLMX_OK;
+  });
+}
+void glmx_engine_destroy(glmx_engine* e) {
+  if (!e) return;
+  DeviceGuard g(e->m->device);
+  delete e;
+}
+int glmx_engine_prefill(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
+                        glmx_prefill_report* reports, int32_t* first_token, float* logits) {
+  return guarded([&] { return engine_prefill_impl(e, n_req, reqs, reports, first_token, logits); });
+}
+int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,
+                       float* last_logits) {
+  return guarded([&] { return engine_decode_impl(e, steps, out_tokens, last_logits); });
+}
+int glmx_engine_replay_forward(glmx_engine* e) {
+  return guarded([&] { return engine_replay_impl(e); });
+}
+int glmx_engine_last_timings(const glmx_engine* e, float out7[7]) {
+  std::memcpy(out7, e->timings, sizeof(e->timings));
+  return GLMX_OK;
+}
+int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {
+  std::memcpy(out6, e->work, sizeof(e->work));
+  return GLMX_OK;
+}
+void glmx_engine_set_profiling(glmx_engine* e, int32_t on) { e->profiling = on != 0; }
+
+// ------------------------------------------------------------------ kernel test hooks
+int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
+                   const int32_t* dst_pages, uint64_t n, void* stream) {
+  return guarded([&] {
+    pool_copy_impl(src, dst, src_pages, dst_pages, n, static_cast<cudaStream_t>(stream));
+    return GLMX_OK;
+  });
+}
+float glmx_pool_last_copy_ms(const glmx_kv* dst) { return dst->last_copy_ms; }
+
+}  // extern "C"

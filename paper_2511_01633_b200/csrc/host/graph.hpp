@@ -1,0 +1,47 @@
+// Property graph ingest (graph_store.cpp:38-124) into the flat, device-friendly form that the
+// vertex-chunk kernel K1 consumes:
+//   * nodes ordered by id bytes (== the reference's std::map / node_ids() order, so "ties break
+//     by id ascending" becomes "ties break by node index ascending");
+//   * per node the pre-rendered entry text  "<id> {k:v, ...}"  (retriever.cpp:34-41 +
+//     attr.hpp:19-48), which is query-independent;
+//   * the undirected and the out-only de-duplicated neighbour CSRs (retriever.cpp:79-89);
+//   * both weight columns: total_degree (graph_store.cpp:209-213) and the by-edge-type maximum
+//     (retriever.cpp:100-105).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+
+namespace glmx {
+
+struct HostGraph {
+  std::vector<std::string> ids;            // ascending
+  std::vector<std::string> types;
+  std::vector<std::vector<std::pair<std::string, std::string>>> attrs;  // rendered, key order
+  std::unordered_map<std::string, int32_t> index;
+  std::vector<std::string> etypes;
+  std::vector<int32_t> src, dst, etype;    // edges in file order
+
+  // derived (finalize())
+  std::vector<char> entry_bytes;           // concatenated "<id> {k:v, ...}"
+  std::vector<uint32_t> entry_off;         // n+1
+  std::vector<uint32_t> und_off, dir_off;  // n+1
+  std::vector<int32_t> und_idx, dir_idx;
+  std::vector<int32_t> w_total, w_by_type;
+
+  uint64_t n() const { return ids.size(); }
+  void finalize();  // validates, sorts, builds entries/CSRs/weights
+  std::string serialize_jsonl() const;
+};
+
+HostGraph load_graph_jsonl(const std::string& path);
+HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed);
+
+// attr.hpp:19-24 shortest round-trip double rendering (std::to_chars).
+std::string format_double(double d);
+
+}  // namespace glmx

@@ -1,0 +1,31 @@
+// K3 paged prefill attention (and 1-token decode through the same path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ops.cuh"
+
+namespace glmx {
+
+struct AttnParams {
+  const __nv_bfloat16* q;  // [T][H][hd], RoPE applied
+  __nv_bfloat16* o;        // [T][H][hd]
+  PoolGeom pool;
+  uint32_t layer;
+  const int32_t* q_start;      // [n_req] first row of the request in q / o
+  const int32_t* q_len;        // [n_req] computed tokens (suffix) of the request
+  const int32_t* ctx_len;      // [n_req] keys visible to the last query (cached + q_len)
+  const int32_t* block_table;  // [n_req][bt_stride] pages, key j lives in page j / B
+  int bt_stride;
+  const int2* work;  // (request, first query token) per CTA tile, longest first
+  int n_work;
+  int H, Hkv;
+  float scale_log2;  // softmax scale * log2(e)
+};
+
+// Query rows per CTA tile: 64 / (H / Hkv) tokens x (H / Hkv) heads of one kv head.
+int attn_tokens_per_tile(int H, int Hkv);
+void paged_attention(const AttnParams& p, cudaStream_t s);
+
+}  // namespace glmx

@@ -1,0 +1,43 @@
+// K1 vertex-chunk assembly: device graph view + launch wrappers (see chunk.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace glmx {
+
+struct DevGraph {
+  const char* entry_bytes;
+  const uint32_t* entry_off;
+  const uint32_t* und_off;
+  const int32_t* und_idx;
+  const uint32_t* dir_off;
+  const int32_t* dir_idx;
+  const int32_t* w_total;
+  const int32_t* w_by_type;
+  uint32_t n;
+};
+
+struct ChunkParams {
+  int k;            // max(k, 0)
+  int k_stride;     // row stride of the selection buffer (>= k)
+  int weight_mode;  // 0 TotalDegree, 1 ByEdgeType
+  int directed;
+};
+
+void chunk_select(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
+                  int32_t* sel, int32_t* sel_count, uint64_t* byte_len, cudaStream_t s);
+void chunk_render(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
+                  const int32_t* sel, const int32_t* sel_count, const uint64_t* byte_off,
+                  char* out, cudaStream_t s);
+void chunk_tokenize(const char* bytes, const uint64_t* byte_off, int n_req, uint64_t total,
+                    uint32_t* flag, uint32_t* tok_index, void* temp, size_t temp_bytes,
+                    uint32_t vocab, int32_t* tok_id, uint64_t* tok_begin, uint64_t* tok_end,
+                    uint64_t* tok_off, cudaStream_t s);
+size_t scan_u64_temp_bytes(int n);
+size_t scan_u32_temp_bytes(uint64_t n);
+void scan_u64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int n,
+              cudaStream_t s);
+
+}  // namespace glmx

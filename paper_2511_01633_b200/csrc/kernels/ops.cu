@@ -1,0 +1,279 @@
+#include <cfloat>
+
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace glmx {
+
+namespace {
+
+__global__ void init_normal_kernel(__nv_bfloat16* p, uint64_t n, uint64_t seed, float std) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t a = mix64(seed ^ (i * 0xd1b54a32d192ed03ULL));
+    uint64_t b = mix64(a ^ 0x8cb92ba72f3d8dd7ULL);
+    float u1 = (static_cast<float>(a >> 40) + 1.0f) * (1.0f / 16777217.0f);  // (0, 1]
+    float u2 = static_cast<float>(b >> 40) * (1.0f / 16777216.0f);
+    float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+    p[i] = __float2bfloat16(z * std);
+  }
+}
+
+__global__ void init_const_kernel(__nv_bfloat16* p, uint64_t n, float v) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = __float2bfloat16(v);
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
+                             int d, float* __restrict__ x) {
+  const int t = blockIdx.x;
+  const __nv_bfloat16* row = E + static_cast<int64_t>(tok[t]) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    x[static_cast<int64_t>(t) * d + i] = __bfloat162float(row[i]);
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < NT / 32 ? red[l] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+rmsnorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, int d,
+               const __nv_bfloat16* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out) {
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int64_t src = rows ? rows[t] : t;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d / 4; i += NT) {
+    float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = block_sum<NT>(ss, red);
+  const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + static_cast<int64_t>(t) * d);
+  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(w);
+  for (int i = threadIdx.x; i < d / 4; i += NT) {
+    float4 v = xr[i];
+    float2 wa = __bfloat1622float2(w2[2 * i]), wb = __bfloat1622float2(w2[2 * i + 1]);
+    o[2 * i] = __floats2bfloat162_rn(v.x * inv * wa.x, v.y * inv * wa.y);
+    o[2 * i + 1] = __floats2bfloat162_rn(v.z * inv * wb.x, v.w * inv * wb.y);
+  }
+}
+
+// One warp per (token, head slot); head slots: H query heads, then Hkv K heads, then Hkv V heads.
+__global__ void rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                      const int32_t* __restrict__ pos,
+                                      const int64_t* __restrict__ slot, int T, int H, int Hkv,
+                                      int hd, const float* __restrict__ inv_freq, PoolGeom pool,
+                                      uint32_t layer, __nv_bfloat16* __restrict__ q_out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int heads = H + 2 * Hkv;
+  if (warp >= T * heads) return;
+  const int t = warp / heads, h = warp % heads;
+  const __nv_bfloat16* src = qkv + (static_cast<int64_t>(t) * heads + h) * hd;
+  const int half = hd / 2;
+  const float p = static_cast<float>(pos[t]);
+  __nv_bfloat16* dst;
+  bool rotate = true;
+  if (h < H) {
+    dst = q_out + (static_cast<int64_t>(t) * H + h) * hd;
+  } else {
+    const int64_t sl = slot[t];
+    const int64_t page = sl / pool.block_tokens;
+    const int off = static_cast<int>(sl % pool.block_tokens);
+    const int kv = h < H + Hkv ? 0 : 1;
+    const int kh = h - H - kv * Hkv;
+    dst = pool.base + pool.tile_off(page, layer, kv, kh) + static_cast<int64_t>(off) * hd;
+    rotate = kv == 0;
+  }
+  for (int i = lane; i < half; i += 32) {
+    float a = __bfloat162float(src[i]), b = __bfloat162float(src[i + half]);
+    if (rotate) {
+      float sn, cs;
+      sincosf(p * inv_freq[i], &sn, &cs);
+      float ra = a * cs - b * sn;
+      float rb = b * cs + a * sn;
+      a = ra;
+      b = rb;
+    }
+    dst[i] = __float2bfloat16(a);
+    dst[i + half] = __float2bfloat16(b);
+  }
+}
+
+__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ff,
+                              __nv_bfloat16* __restrict__ out) {
+  const int64_t n = static_cast<int64_t>(T) * ff / 2;  // bf16x2 pairs
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = (2 * i) / ff, c = (2 * i) % ff;
+    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(gu + t * 2 * ff + c);
+    const __nv_bfloat162 u = *reinterpret_cast<const __nv_bfloat162*>(gu + t * 2 * ff + ff + c);
+    float2 gf = __bfloat1622float2(g), uf = __bfloat1622float2(u);
+    float a = gf.x / (1.f + __expf(-gf.x)) * uf.x;
+    float b = gf.y / (1.f + __expf(-gf.y)) * uf.y;
+    *reinterpret_cast<__nv_bfloat162*>(out + t * ff + c) = __floats2bfloat162_rn(a, b);
+  }
+}
+
+// First maximal index per row (greedy decode; ties -> lowest id like a first-max scan).
+__global__ void __launch_bounds__(1024)
+argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
+  float best = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    float v = row[i];
+    if (v > best) {  // strided scan visits increasing i: keeps the first max of this thread
+      best = v;
+      bi = i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    best = l < static_cast<int>(blockDim.x >> 5) ? sv[l] : -FLT_MAX;
+    bi = l < static_cast<int>(blockDim.x >> 5) ? si[l] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (l == 0) out[blockIdx.x] = bi;
+  }
+}
+
+// K4: one CTA per (page, slice); 16-byte vectorised, 4 loads in flight per thread.
+__global__ void __launch_bounds__(256)
+pool_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t page_vec,
+                 const int32_t* __restrict__ sp, const int32_t* __restrict__ dp, int slices) {
+  const int i = blockIdx.y;
+  const uint64_t per = ceil_div(page_vec, slices);
+  const uint64_t b = blockIdx.x * per, e = min(page_vec, b + per);
+  const uint4* s = src + static_cast<uint64_t>(sp[i]) * page_vec;
+  uint4* d = dst + static_cast<uint64_t>(dp[i]) * page_vec;
+  uint64_t j = b + threadIdx.x;
+  for (; j + 3 * 256 < e; j += 4 * 256) {
+    uint4 v0 = s[j], v1 = s[j + 256], v2 = s[j + 512], v3 = s[j + 768];
+    d[j] = v0;
+    d[j + 256] = v1;
+    d[j + 512] = v2;
+    d[j + 768] = v3;
+  }
+  for (; j < e; j += 256) d[j] = s[j];
+}
+
+__global__ void kv_gather_kernel(PoolGeom pool, uint32_t layer, uint32_t kv,
+                                 const int32_t* __restrict__ pages, __nv_bfloat16* __restrict__ out) {
+  const int i = blockIdx.x;  // page index in list
+  const int B = pool.block_tokens, hd = pool.head_dim, Hkv = pool.n_kv_heads;
+  for (int e = threadIdx.x; e < B * Hkv * hd; e += blockDim.x) {
+    const int tok = e / (Hkv * hd), h = (e / hd) % Hkv, c = e % hd;
+    out[(static_cast<int64_t>(i) * B + tok) * Hkv * hd + h * hd + c] =
+        pool.base[pool.tile_off(pages[i], layer, kv, h) + static_cast<int64_t>(tok) * hd + c];
+  }
+}
+
+int grid_for(uint64_t n, int threads) {
+  return static_cast<int>(std::min<uint64_t>(ceil_div(n, threads), kNumSMs * 32));
+}
+
+}  // namespace
+
+void init_normal_bf16(__nv_bfloat16* p, uint64_t n, uint64_t seed, float std, cudaStream_t s) {
+  init_normal_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, seed, std);
+  GLMX_CHECK_LAUNCH();
+}
+
+void init_const_bf16(__nv_bfloat16* p, uint64_t n, float v, cudaStream_t s) {
+  init_const_kernel<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+  GLMX_CHECK_LAUNCH();
+}
+
+void embed_gather(const int32_t* tokens, int T, const __nv_bfloat16* embed, int d, float* x,
+                  cudaStream_t s) {
+  if (T <= 0) return;
+  embed_kernel<<<T, 256, 0, s>>>(tokens, embed, d, x);
+  GLMX_CHECK_LAUNCH();
+}
+
+void rmsnorm(const float* x, const int32_t* rows, int T, int d, const __nv_bfloat16* w,
+             float eps, __nv_bfloat16* out, cudaStream_t s) {
+  if (T <= 0) return;
+  rmsnorm_kernel<256><<<T, 256, 0, s>>>(x, rows, d, w, eps, out);
+  GLMX_CHECK_LAUNCH();
+}
+
+void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t* slot, int T,
+                    int H, int Hkv, int hd, const float* inv_freq, const PoolGeom& pool,
+                    uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s) {
+  if (T <= 0) return;
+  const int64_t warps = static_cast<int64_t>(T) * (H + 2 * Hkv);
+  rope_kv_append_kernel<<<static_cast<int>(ceil_div(warps * 32, 256)), 256, 0, s>>>(
+      qkv, pos, slot, T, H, Hkv, hd, inv_freq, pool, layer, q_out);
+  GLMX_CHECK_LAUNCH();
+}
+
+void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStream_t s) {
+  if (T <= 0) return;
+  swiglu_kernel<<<grid_for(static_cast<uint64_t>(T) * ff / 2, 256), 256, 0, s>>>(gu, T, ff, out);
+  GLMX_CHECK_LAUNCH();
+}
+
+void argmax_rows(const float* logits, int n, int V, int32_t* out, cudaStream_t s) {
+  if (n <= 0) return;
+  argmax_kernel<<<n, 1024, 0, s>>>(logits, V, out);
+  GLMX_CHECK_LAUNCH();
+}
+
+void pool_copy_pages(const __nv_bfloat16* src_base, __nv_bfloat16* dst_base, uint64_t page_elems,
+                     const int32_t* src_pages, const int32_t* dst_pages, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  const uint64_t page_vec = page_elems * sizeof(__nv_bfloat16) / sizeof(uint4);
+  const int slices = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(64, page_vec / 4096)));
+  dim3 grid(slices, n);
+  pool_copy_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(src_base),
+                                        reinterpret_cast<uint4*>(dst_base), page_vec, src_pages,
+                                        dst_pages, slices);
+  GLMX_CHECK_LAUNCH();
+}
+
+void kv_gather(const PoolGeom& pool, uint32_t layer, uint32_t kv, const int32_t* pages, int n,
+               __nv_bfloat16* out, cudaStream_t s) {
+  if (n <= 0) return;
+  kv_gather_kernel<<<n, 256, 0, s>>>(pool, layer, kv, pages, out);
+  GLMX_CHECK_LAUNCH();
+}
+
+}  // namespace glmx

@@ -1,0 +1,743 @@
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "kernels/common.cuh"
+
+using namespace glmx;
+
+#define GLMX_BLAS(call)                                                                   \
+  do {                                                                                    \
+    cublasStatus_t s_ = (call);                                                           \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      throw Error(GLMX_ERR_CUDA, std::string(#call) + ": cublas status " + std::to_string(s_)); \
+  } while (0)
+
+DeviceGuard::DeviceGuard(int dev) {
+  if (dev >= 0) {
+    cudaGetDevice(&prev);
+    if (prev != dev) GLMX_CUDA(cudaSetDevice(dev));
+  }
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+}
+
+void DBuf::reserve(size_t n) {
+  if (n <= bytes) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  n = std::max<size_t>(n, 256);
+  GLMX_CUDA(cudaMalloc(&p, n));
+  bytes = n;
+}
+DBuf::~DBuf() {
+  if (p) cudaFree(p);
+}
+
+glmx_kv::~glmx_kv() {
+  if (geom.base) cudaFree(geom.base);
+  if (stream) cudaStreamDestroy(stream);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+}
+
+glmx_graph::~glmx_graph() {
+  for (void* p : allocs) cudaFree(p);
+  if (stream) cudaStreamDestroy(stream);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+}
+
+glmx_model::~glmx_model() {
+  if (arena) cudaFree(arena);
+  if (inv_freq) cudaFree(inv_freq);
+  if (blas_ws) cudaFree(blas_ws);
+  if (blas) cublasDestroy(blas);
+}
+
+glmx_engine::~glmx_engine() {
+  if (h_meta) cudaFreeHost(h_meta);
+  if (h_out) cudaFreeHost(h_out);
+  if (h2d_done) cudaEventDestroy(h2d_done);
+  if (fwd_done) cudaEventDestroy(fwd_done);
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ======================================================================== graph upload
+void glmx_graph::upload() {
+  DeviceGuard g(device);
+  auto put = [&](const void* src, size_t bytes) -> void* {
+    void* p = nullptr;
+    GLMX_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    if (bytes) GLMX_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+    allocs.push_back(p);
+    return p;
+  };
+  dev.entry_bytes = static_cast<const char*>(put(host.entry_bytes.data(), host.entry_bytes.size()));
+  dev.entry_off = static_cast<const uint32_t*>(put(host.entry_off.data(), host.entry_off.size() * 4));
+  dev.und_off = static_cast<const uint32_t*>(put(host.und_off.data(), host.und_off.size() * 4));
+  dev.und_idx = static_cast<const int32_t*>(put(host.und_idx.data(), host.und_idx.size() * 4));
+  dev.dir_off = static_cast<const uint32_t*>(put(host.dir_off.data(), host.dir_off.size() * 4));
+  dev.dir_idx = static_cast<const int32_t*>(put(host.dir_idx.data(), host.dir_idx.size() * 4));
+  dev.w_total = static_cast<const int32_t*>(put(host.w_total.data(), host.w_total.size() * 4));
+  dev.w_by_type = static_cast<const int32_t*>(put(host.w_by_type.data(), host.w_by_type.size() * 4));
+  dev.n = static_cast<uint32_t>(host.n());
+  GLMX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  GLMX_CUDA(cudaEventCreate(&ev0));
+  GLMX_CUDA(cudaEventCreate(&ev1));
+}
+
+// K1 driver: select -> scan -> render -> tokenize.  Returns GLMX_ERR_ARG (with totals) when the
+// caller's buffers are too small.
+int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t* node_idx,
+                     uint64_t n, char* out_bytes, uint64_t bytes_cap, uint64_t* out_byte_offsets,
+                     int32_t* out_tok_ids, uint64_t* out_tok_begin, uint64_t* out_tok_end,
+                     uint64_t tok_cap, uint64_t* out_tok_offsets, uint64_t* total_bytes,
+                     uint64_t* total_tokens) {
+  if (g->device < 0) throw Error(GLMX_ERR_NO_DEVICE, "graph has no device");
+  if (n == 0) {
+    if (total_bytes) *total_bytes = 0;
+    if (total_tokens) *total_tokens = 0;
+    if (out_byte_offsets) out_byte_offsets[0] = 0;
+    if (out_tok_offsets) out_tok_offsets[0] = 0;
+    return GLMX_OK;
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    if (node_idx[i] < 0 || static_cast<uint64_t>(node_idx[i]) >= g->host.n())
+      throw Error(GLMX_ERR_RETRIEVAL, "unknown node index " + std::to_string(node_idx[i]));
+  const int k = std::max(cfg->k, 0);
+  if (k > 512) throw Error(GLMX_ERR_ARG, "chunk k > 512 is not supported");
+  DeviceGuard dg(g->device);
+  cudaStream_t s = g->stream;
+  ChunkParams p{k, std::max(k, 1), cfg->weight_mode ? 1 : 0, cfg->directed ? 1 : 0};
+  g->d_nodes.reserve(n * 4);
+  g->d_sel.reserve(n * p.k_stride * 4);
+  g->d_cnt.reserve(n * 4);
+  g->d_len.reserve((n + 1) * 8);
+  g->d_off.reserve((n + 1) * 8);
+  const size_t t64 = scan_u64_temp_bytes(static_cast<int>(n + 1));
+  GLMX_CUDA(cudaMemcpyAsync(g->d_nodes.p, node_idx, n * 4, cudaMemcpyHostToDevice, s));
+  GLMX_CUDA(cudaMemsetAsync(g->d_len.p, 0, (n + 1) * 8, s));
+  GLMX_CUDA(cudaEventRecord(g->ev0, s));
+  chunk_select(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
+               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), s);
+  g->d_temp.reserve(t64);
+  scan_u64(g->d_temp.p, t64, g->d_len.as<uint64_t>(), g->d_off.as<uint64_t>(),
+           static_cast<int>(n + 1), s);
+  uint64_t total = 0;
+  GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaStreamSynchronize(s));
+  g->d_bytes.reserve(total + 16);
+  g->d_flag.reserve((total + 1) * 4);
+  g->d_tidx.reserve((total + 1) * 4);
+  g->d_tid.reserve((total + 1) * 4);
+  g->d_tbeg.reserve((total + 1) * 8);
+  g->d_tend.reserve((total + 1) * 8);
+  g->d_toff.reserve((n + 1) * 8);
+  const size_t t32 = scan_u32_temp_bytes(total + 1);
+  g->d_temp.reserve(std::max(t32, t64));
+  chunk_render(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
+               g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_bytes.as<char>(), s);
+  GLMX_CUDA(cudaMemsetAsync(g->d_flag.as<uint32_t>() + total, 0, 4, s));
+  chunk_tokenize(g->d_bytes.as<char>(), g->d_off.as<uint64_t>(), static_cast<int>(n), total,
+                 g->d_flag.as<uint32_t>(), g->d_tidx.as<uint32_t>(), g->d_temp.p, g->d_temp.bytes,
+                 cfg->vocab, g->d_tid.as<int32_t>(), g->d_tbeg.as<uint64_t>(),
+                 g->d_tend.as<uint64_t>(), g->d_toff.as<uint64_t>(), s);
+  GLMX_CUDA(cudaEventRecord(g->ev1, s));
+  uint32_t ntok32 = 0;
+  GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_tidx.as<uint32_t>() + total, 4, cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaStreamSynchronize(s));
+  GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));
+  const uint64_t ntok = ntok32;
+  if (total_bytes) *total_bytes = total;
+  if (total_tokens) *total_tokens = ntok;
+  if (!out_bytes) return GLMX_OK;
+  if (bytes_cap < total || (tok_cap < ntok && (out_tok_ids || out_tok_begin || out_tok_end)))
+    throw Error(GLMX_ERR_ARG, "chunk output buffers too small");
+  GLMX_CUDA(cudaMemcpyAsync(out_bytes, g->d_bytes.p, total, cudaMemcpyDeviceToHost, s));
+  if (out_byte_offsets)
+    GLMX_CUDA(cudaMemcpyAsync(out_byte_offsets, g->d_off.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (out_tok_ids && cfg->vocab)
+    GLMX_CUDA(cudaMemcpyAsync(out_tok_ids, g->d_tid.p, ntok * 4, cudaMemcpyDeviceToHost, s));
+  if (out_tok_begin)
+    GLMX_CUDA(cudaMemcpyAsync(out_tok_begin, g->d_tbeg.p, ntok * 8, cudaMemcpyDeviceToHost, s));
+  if (out_tok_end)
+    GLMX_CUDA(cudaMemcpyAsync(out_tok_end, g->d_tend.p, ntok * 8, cudaMemcpyDeviceToHost, s));
+  if (out_tok_offsets)
+    GLMX_CUDA(cudaMemcpyAsync(out_tok_offsets, g->d_toff.p, n * 8, cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaStreamSynchronize(s));
+  if (out_tok_offsets) out_tok_offsets[n] = ntok;
+  return GLMX_OK;
+}
+
+// ======================================================================== KV
+glmx_kv* kv_create_impl(const glmx_kv_config* cfg) {
+  auto kv = std::make_unique<glmx_kv>();
+  kv->cfg = *cfg;
+  uint64_t pages = cfg->capacity_blocks + cfg->headroom_pages;
+  if (cfg->device < 0) {
+    // bookkeeping only: pages are logical handles; deferred pages recycle on every call
+    pages = std::max<uint64_t>(pages, cfg->capacity_blocks + 1024);
+  }
+  if (pages > 0x7FFFFFFFULL) throw Error(GLMX_ERR_ARG, "too many pages");
+  kv->bk = std::make_unique<BlockEngine>(cfg->capacity_blocks, cfg->block_tokens, cfg->policy, pages);
+  if (cfg->device >= 0) {
+    if (cfg->n_layers == 0 || cfg->n_kv_heads == 0 || cfg->head_dim == 0)
+      throw Error(GLMX_ERR_ARG, "device pool needs n_layers, n_kv_heads, head_dim");
+    DeviceGuard g(cfg->device);
+    kv->geom.n_layers = cfg->n_layers;
+    kv->geom.n_kv_heads = cfg->n_kv_heads;
+    kv->geom.block_tokens = cfg->block_tokens;
+    kv->geom.head_dim = cfg->head_dim;
+    kv->page_bytes = kv->geom.page_elems() * sizeof(__nv_bfloat16);
+    void* base = nullptr;
+    GLMX_CUDA(cudaMalloc(&base, pages * kv->page_bytes));
+    GLMX_CUDA(cudaMemset(base, 0, pages * kv->page_bytes));
+    kv->geom.base = static_cast<__nv_bfloat16*>(base);
+    GLMX_CUDA(cudaStreamCreateWithFlags(&kv->stream, cudaStreamNonBlocking));
+    GLMX_CUDA(cudaEventCreate(&kv->ev0));
+    GLMX_CUDA(cudaEventCreate(&kv->ev1));
+  }
+  return kv.release();
+}
+
+void pool_copy_impl(glmx_kv* src, glmx_kv* dst, const int32_t* sp, const int32_t* dp, uint64_t n,
+                    cudaStream_t s) {
+  if (!src->has_pool() || !dst->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "pool copy needs device pools");
+  if (src->page_bytes != dst->page_bytes) throw Error(GLMX_ERR_ARG, "pool geometries differ");
+  for (uint64_t i = 0; i < n; ++i)
+    if (sp[i] < 0 || static_cast<uint64_t>(sp[i]) >= src->bk->pool().total() || dp[i] < 0 ||
+        static_cast<uint64_t>(dp[i]) >= dst->bk->pool().total())
+      throw Error(GLMX_ERR_ARG, "page index out of range");
+  DeviceGuard g(dst->cfg.device);
+  if (src->cfg.device != dst->cfg.device) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(src->cfg.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      throw Error(GLMX_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  if (!s) s = dst->stream;
+  dst->scratch.reserve(n * 8);
+  GLMX_CUDA(cudaMemcpyAsync(dst->scratch.p, sp, n * 4, cudaMemcpyHostToDevice, s));
+  GLMX_CUDA(cudaMemcpyAsync(dst->scratch.as<int32_t>() + n, dp, n * 4, cudaMemcpyHostToDevice, s));
+  GLMX_CUDA(cudaEventRecord(dst->ev0, s));
+  for (uint64_t o = 0; o < n; o += 65535)
+    pool_copy_pages(src->geom.base, dst->geom.base, dst->geom.page_elems(),
+                    dst->scratch.as<int32_t>() + o, dst->scratch.as<int32_t>() + n + o,
+                    static_cast<int>(std::min<uint64_t>(65535, n - o)), s);
+  GLMX_CUDA(cudaEventRecord(dst->ev1, s));
+  GLMX_CUDA(cudaEventSynchronize(dst->ev1));
+  GLMX_CUDA(cudaEventElapsedTime(&dst->last_copy_ms, dst->ev0, dst->ev1));
+}
+
+// ======================================================================== model
+glmx_model* model_create_impl(const glmx_model_config* c, int device) {
+  if (device < 0) throw Error(GLMX_ERR_NO_DEVICE, "model needs a CUDA device");
+  if (c->n_heads % c->n_kv_heads || c->d_model % 8 || c->head_dim != 128)
+    throw Error(GLMX_ERR_ARG, "unsupported model shape");
+  auto m = std::make_unique<glmx_model>();
+  m->cfg = *c;
+  m->device = device;
+  DeviceGuard g(device);
+  const uint64_t d = c->d_model, hd = c->head_dim, H = c->n_heads, Hkv = c->n_kv_heads,
+                 ff = c->d_ff, V = c->vocab, L = c->n_layers;
+  const uint64_t qkv = (H + 2 * Hkv) * hd;
+  const uint64_t per_layer = d + qkv * d + d * H * hd + d + 2 * ff * d + d * ff;
+  const uint64_t total = V * d + L * per_layer + d + V * d;
+  m->arena_bytes = total * sizeof(__nv_bfloat16);
+  GLMX_CUDA(cudaMalloc(&m->arena, m->arena_bytes + 256));
+  __nv_bfloat16* p = static_cast<__nv_bfloat16*>(m->arena);
+  auto take = [&](uint64_t n) {
+    __nv_bfloat16* r = p;
+    p += n;
+    return r;
+  };
+  uint64_t tid = 0;
+  auto seed_of = [&](uint64_t t) { return mix64(c->seed * 0x100000001b3ULL + t); };
+  m->embed = take(V * d);
+  init_normal_bf16(m->embed, V * d, seed_of(tid++), c->init_std, 0);
+  m->layers.resize(L);
+  for (uint64_t l = 0; l < L; ++l) {
+    LayerW& w = m->layers[l];
+    w.attn_norm = take(d);
+    init_const_bf16(w.attn_norm, d, 1.0f, 0);
+    w.wqkv = take(qkv * d);
+    init_normal_bf16(w.wqkv, qkv * d, seed_of(tid++), c->init_std, 0);
+    w.wo = take(d * H * hd);
+    init_normal_bf16(w.wo, d * H * hd, seed_of(tid++), c->init_std, 0);
+    w.mlp_norm = take(d);
+    init_const_bf16(w.mlp_norm, d, 1.0f, 0);
+    w.wgu = take(2 * ff * d);
+    init_normal_bf16(w.wgu, 2 * ff * d, seed_of(tid++), c->init_std, 0);
+    w.wdown = take(d * ff);
+    init_normal_bf16(w.wdown, d * ff, seed_of(tid++), c->init_std, 0);
+  }
+  m->final_norm = take(d);
+  init_const_bf16(m->final_norm, d, 1.0f, 0);
+  m->lm_head = take(V * d);
+  init_normal_bf16(m->lm_head, V * d, seed_of(tid++), c->init_std, 0);
+  // RoPE inverse frequencies in double, rounded once (the oracle uses the same table).
+  std::vector<float> inv(hd / 2);
+  for (uint64_t i = 0; i < hd / 2; ++i)
+    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(c->rope_theta),
+                                               static_cast<double>(2 * i) / static_cast<double>(hd)));
+  GLMX_CUDA(cudaMalloc(&m->inv_freq, inv.size() * 4));
+  GLMX_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+  GLMX_BLAS(cublasCreate(&m->blas));
+  GLMX_CUDA(cudaMalloc(&m->blas_ws, 64 << 20));
+  GLMX_BLAS(cublasSetWorkspace(m->blas, m->blas_ws, 64 << 20));
+  GLMX_CUDA(cudaDeviceSynchronize());
+  return m.release();
+}
+
+int model_export_impl(const glmx_model* m, int which, int layer, uint16_t* out, uint64_t n) {
+  const auto& c = m->cfg;
+  const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff,
+                 V = c.vocab;
+  const __nv_bfloat16* src = nullptr;
+  uint64_t cnt = 0;
+  if (which != 0 && which != 7 && which != 8 && (layer < 0 || layer >= static_cast<int>(c.n_layers)))
+    throw Error(GLMX_ERR_ARG, "layer out of range");
+  switch (which) {
+    case 0: src = m->embed; cnt = V * d; break;
+    case 1: src = m->layers[layer].attn_norm; cnt = d; break;
+    case 2: src = m->layers[layer].wqkv; cnt = (H + 2 * Hkv) * hd * d; break;
+    case 3: src = m->layers[layer].wo; cnt = d * H * hd; break;
+    case 4: src = m->layers[layer].mlp_norm; cnt = d; break;
+    case 5: src = m->layers[layer].wgu; cnt = 2 * ff * d; break;
+    case 6: src = m->layers[layer].wdown; cnt = d * ff; break;
+    case 7: src = m->final_norm; cnt = d; break;
+    case 8: src = m->lm_head; cnt = V * d; break;
+    default: throw Error(GLMX_ERR_ARG, "unknown weight");
+  }
+  if (n < cnt) throw Error(GLMX_ERR_ARG, "export buffer too small");
+  DeviceGuard g(m->device);
+  GLMX_CUDA(cudaMemcpy(out, src, cnt * 2, cudaMemcpyDeviceToHost));
+  return GLMX_OK;
+}
+
+// ======================================================================== engine
+namespace {
+
+// Y[T][out] (+)= X[T][in] * W[out][in]^T  (column-major: C(out x T) = W^T' * X)
+void gemm(cublasHandle_t h, cudaStream_t s, const __nv_bfloat16* X, const __nv_bfloat16* W,
+          void* Y, bool y_fp32, bool accumulate, int T, int in, int out) {
+  if (T <= 0) return;
+  GLMX_BLAS(cublasSetStream(h, s));
+  const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
+  GLMX_BLAS(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, out, T, in, &alpha, W, CUDA_R_16BF, in, X,
+                         CUDA_R_16BF, in, &beta, Y, y_fp32 ? CUDA_R_32F : CUDA_R_16BF, out,
+                         CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+cudaEvent_t next_event(glmx_engine* e) {
+  if (e->ev_used == e->ev_pool.size()) {
+    cudaEvent_t ev;
+    GLMX_CUDA(cudaEventCreate(&ev));
+    e->ev_pool.push_back(ev);
+  }
+  return e->ev_pool[e->ev_used++];
+}
+
+struct Prof {
+  glmx_engine* e;
+  int cat;
+  cudaEvent_t a = nullptr;
+  Prof(glmx_engine* e_, int c) : e(e_), cat(c) {
+    if (e->profiling) {
+      a = next_event(e);
+      GLMX_CUDA(cudaEventRecord(a, e->stream));
+    }
+  }
+  ~Prof() {
+    if (a) {
+      cudaEvent_t b = next_event(e);
+      cudaEventRecord(b, e->stream);
+      e->spans.push_back({a, b, cat});
+    }
+  }
+};
+
+enum { kCatAll = 0, kCatAttn = 1, kCatAppend = 2, kCatGemm = 3, kCatOther = 4, kCatH2D = 5, kCatD2H = 6 };
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_config* cfg) {
+  if (!kv->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "engine needs a device KV pool");
+  if (kv->cfg.device != m->device) throw Error(GLMX_ERR_ARG, "model and kv on different devices");
+  const auto& c = m->cfg;
+  if (kv->cfg.n_layers != c.n_layers || kv->cfg.n_kv_heads != c.n_kv_heads ||
+      kv->cfg.head_dim != c.head_dim)
+    throw Error(GLMX_ERR_ARG, "kv pool geometry does not match the model");
+  auto e = std::make_unique<glmx_engine>();
+  e->m = m;
+  e->kv = kv;
+  e->cfg = *cfg;
+  DeviceGuard g(m->device);
+  GLMX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  GLMX_CUDA(cudaEventCreateWithFlags(&e->h2d_done, cudaEventDisableTiming));
+  GLMX_CUDA(cudaEventCreateWithFlags(&e->fwd_done, cudaEventDisableTiming));
+  const uint64_t T = std::max<uint32_t>(cfg->max_batch_tokens, cfg->max_requests);
+  const uint64_t R = cfg->max_requests;
+  const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
+  const uint32_t B = kv->cfg.block_tokens;
+  e->bt_stride = static_cast<int>((cfg->max_context + B - 1) / B + 1);
+  e->tpt = attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
+  e->x.reserve(T * d * 4);
+  e->h.reserve(T * d * 2);
+  e->qkv.reserve(T * (H + 2 * Hkv) * hd * 2);
+  e->q.reserve(T * H * hd * 2);
+  e->attn.reserve(T * H * hd * 2);
+  e->gu.reserve(T * 2 * ff * 2);
+  e->act.reserve(T * ff * 2);
+  e->hl.reserve(R * d * 2);
+  e->logits.reserve(R * c.vocab * 4);
+  e->next_tok.reserve((R * (cfg->max_decode + 1) + 16) * 4);
+  // metadata layout (one pinned block, one H2D)
+  const uint64_t max_work = T / 1 + R;  // upper bound on attention tiles
+  size_t o = 0;
+  e->o_tok = o; o = align_up(o + T * 4, 256);
+  e->o_pos = o; o = align_up(o + T * 4, 256);
+  e->o_slot = o; o = align_up(o + T * 8, 256);
+  e->o_qs = o; o = align_up(o + R * 4, 256);
+  e->o_ql = o; o = align_up(o + R * 4, 256);
+  e->o_ctx = o; o = align_up(o + R * 4, 256);
+  e->o_bt = o; o = align_up(o + R * e->bt_stride * 4, 256);
+  e->o_work = o; o = align_up(o + max_work * 8, 256);
+  e->o_last = o; o = align_up(o + R * 4, 256);
+  e->meta_bytes = o;
+  e->meta.reserve(o);
+  GLMX_CUDA(cudaMallocHost(&e->h_meta, o));
+  GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_out), (R * (cfg->max_decode + 1) + 16) * 4));
+  return e.release();
+}
+
+namespace {
+
+// Runs the decoder over the staged batch: T rows (tokens/pos/slot), R requests (attention
+// metadata), n_last rows whose final hidden states produce logits + greedy tokens.
+void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t* d_tokens) {
+  glmx_model* m = e->m;
+  const auto& c = m->cfg;
+  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
+  const int QKV = (H + 2 * Hkv) * hd;
+  cudaStream_t s = e->stream;
+  uint8_t* meta = e->meta.as<uint8_t>();
+  const int32_t* pos = reinterpret_cast<const int32_t*>(meta + e->o_pos);
+  const int64_t* slot = reinterpret_cast<const int64_t*>(meta + e->o_slot);
+  AttnParams ap{};
+  ap.q = e->q.as<__nv_bfloat16>();
+  ap.o = e->attn.as<__nv_bfloat16>();
+  ap.pool = e->kv->geom;
+  ap.q_start = reinterpret_cast<const int32_t*>(meta + e->o_qs);
+  ap.q_len = reinterpret_cast<const int32_t*>(meta + e->o_ql);
+  ap.ctx_len = reinterpret_cast<const int32_t*>(meta + e->o_ctx);
+  ap.block_table = reinterpret_cast<const int32_t*>(meta + e->o_bt);
+  ap.bt_stride = e->bt_stride;
+  ap.work = reinterpret_cast<const int2*>(meta + e->o_work);
+  ap.n_work = n_work;
+  ap.H = H;
+  ap.Hkv = Hkv;
+  ap.scale_log2 = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)) * 1.4426950408889634);
+  (void)R;
+  Prof all(e, kCatAll);
+  {
+    Prof p(e, kCatOther);
+    embed_gather(d_tokens, T, m->embed, d, e->x.as<float>(), s);
+  }
+  for (uint32_t l = 0; l < c.n_layers; ++l) {
+    const LayerW& w = m->layers[l];
+    {
+      Prof p(e, kCatOther);
+      rmsnorm(e->x.as<float>(), nullptr, T, d, w.attn_norm, c.norm_eps, e->h.as<__nv_bfloat16>(), s);
+    }
+    {
+      Prof p(e, kCatGemm);
+      gemm(m->blas, s, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
+    }
+    {
+      Prof p(e, kCatAppend);
+      rope_kv_append(e->qkv.as<__nv_bfloat16>(), pos, slot, T, H, Hkv, hd, m->inv_freq,
+                     e->kv->geom, l, e->q.as<__nv_bfloat16>(), s);
+    }
+    {
+      Prof p(e, kCatAttn);
+      ap.layer = l;
+      paged_attention(ap, s);
+    }
+    {
+      Prof p(e, kCatGemm);
+      gemm(m->blas, s, e->attn.as<__nv_bfloat16>(), w.wo, e->x.p, true, true, T, H * hd, d);
+    }
+    {
+      Prof p(e, kCatOther);
+      rmsnorm(e->x.as<float>(), nullptr, T, d, w.mlp_norm, c.norm_eps, e->h.as<__nv_bfloat16>(), s);
+    }
+    {
+      Prof p(e, kCatGemm);
+      gemm(m->blas, s, e->h.as<__nv_bfloat16>(), w.wgu, e->gu.p, false, false, T, d, 2 * ff);
+    }
+    {
+      Prof p(e, kCatOther);
+      swiglu(e->gu.as<__nv_bfloat16>(), T, ff, e->act.as<__nv_bfloat16>(), s);
+    }
+    {
+      Prof p(e, kCatGemm);
+      gemm(m->blas, s, e->act.as<__nv_bfloat16>(), w.wdown, e->x.p, true, true, T, ff, d);
+    }
+  }
+  {
+    Prof p(e, kCatOther);
+    rmsnorm(e->x.as<float>(), reinterpret_cast<const int32_t*>(meta + e->o_last), n_last, d,
+            m->final_norm, c.norm_eps, e->hl.as<__nv_bfloat16>(), s);
+  }
+  {
+    Prof p(e, kCatGemm);
+    gemm(m->blas, s, e->hl.as<__nv_bfloat16>(), m->lm_head, e->logits.p, true, false, n_last, d,
+         c.vocab);
+  }
+}
+
+void collect_profile(glmx_engine* e) {
+  for (float& t : e->timings) t = 0.f;
+  if (!e->profiling) return;
+  GLMX_CUDA(cudaStreamSynchronize(e->stream));
+  for (const auto& sp : e->spans) {
+    float ms = 0.f;
+    GLMX_CUDA(cudaEventElapsedTime(&ms, sp.a, sp.b));
+    e->timings[sp.cat] += ms;
+  }
+  e->spans.clear();
+  e->ev_used = 0;
+}
+
+}  // namespace
+
+int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
+                        glmx_prefill_report* reports, int32_t* first_token, float* logits_out) {
+  glmx_model* m = e->m;
+  glmx_kv* kv = e->kv;
+  BlockEngine& bk = *kv->bk;
+  const auto& c = m->cfg;
+  const uint32_t B = kv->cfg.block_tokens;
+  if (n_req > e->cfg.max_requests) throw Error(GLMX_ERR_ARG, "too many requests in batch");
+  DeviceGuard dg(m->device);
+  // The previous batch's host staging must have been consumed before it is rewritten; its
+  // scratch pages become free (device reuse is stream-ordered after its forward).
+  GLMX_CUDA(cudaEventSynchronize(e->h2d_done));
+  for (auto& r : e->reqs)
+    for (int32_t p : r.scratch) bk.pool().free_now(p);
+  e->reqs.clear();
+  e->has_batch = false;
+
+  uint8_t* hm = static_cast<uint8_t*>(e->h_meta);
+  int32_t* h_tok = reinterpret_cast<int32_t*>(hm + e->o_tok);
+  int32_t* h_pos = reinterpret_cast<int32_t*>(hm + e->o_pos);
+  int64_t* h_slot = reinterpret_cast<int64_t*>(hm + e->o_slot);
+  int32_t* h_qs = reinterpret_cast<int32_t*>(hm + e->o_qs);
+  int32_t* h_ql = reinterpret_cast<int32_t*>(hm + e->o_ql);
+  int32_t* h_ctx = reinterpret_cast<int32_t*>(hm + e->o_ctx);
+  int32_t* h_bt = reinterpret_cast<int32_t*>(hm + e->o_bt);
+  int2* h_work = reinterpret_cast<int2*>(hm + e->o_work);
+  int32_t* h_last = reinterpret_cast<int32_t*>(hm + e->o_last);
+
+  PrefillResult pr;
+  int T = 0, R = 0, n_work = 0;
+  std::vector<int> req_row(n_req, -1);
+  double attn_flops = 0, attn_bytes = 0, ctx_tokens = 0;
+  const double kv_tok_bytes = 2.0 * c.n_kv_heads * c.head_dim * 2;  // per layer
+  for (uint64_t i = 0; i < n_req; ++i) {
+    const glmx_request& rq = reqs[i];
+    TokenSpans ts{rq.tok_bytes, rq.tok_offsets, rq.n_tok};
+    bk.prefill(ts, rq.tiers, rq.n_tiers, rq.session ? rq.session : "", pr);  // may throw
+    glmx_prefill_report& rep = reports[i];
+    rep.cached_tokens = pr.cached;
+    rep.computed_tokens = pr.computed;
+    rep.tail_tokens = pr.tail;
+    rep.n_evicted = pr.evicted.size();
+    rep.n_blocks = pr.pages.size();
+    if (first_token) first_token[i] = -1;
+    if (rq.n_tok == 0) continue;
+    glmx_engine::Req st;
+    st.pages = pr.pages;
+    const uint64_t full_tok = pr.pages.size() * B;
+    const uint64_t need = rq.n_tok + e->cfg.max_decode;
+    if (need > e->cfg.max_context) throw Error(GLMX_ERR_ARG, "request exceeds max_context");
+    for (uint64_t t = full_tok; t < need; t += B) {
+      int32_t p = bk.pool().alloc();
+      st.scratch.push_back(p);
+      st.pages.push_back(p);
+    }
+    const uint64_t q0 = std::min<uint64_t>(pr.cached, rq.n_tok - 1);  // always >= 1 row
+    const int ql = static_cast<int>(rq.n_tok - q0);
+    if (T + ql > static_cast<int>(e->cfg.max_batch_tokens))
+      throw Error(GLMX_ERR_ARG, "batch exceeds max_batch_tokens");
+    h_qs[R] = T;
+    h_ql[R] = ql;
+    h_ctx[R] = static_cast<int32_t>(rq.n_tok);
+    std::memcpy(h_bt + static_cast<size_t>(R) * e->bt_stride, st.pages.data(), st.pages.size() * 4);
+    for (uint64_t t = q0; t < rq.n_tok; ++t, ++T) {
+      h_tok[T] = token_id(rq.tok_bytes + rq.tok_offsets[t], rq.tok_offsets[t + 1] - rq.tok_offsets[t], c.vocab);
+      h_pos[T] = static_cast<int32_t>(t);
+      h_slot[T] = static_cast<int64_t>(st.pages[t / B]) * B + (t % B);
+    }
+    for (int t0 = 0; t0 < ql; t0 += e->tpt) h_work[n_work++] = make_int2(R, t0);
+    h_last[R] = T - 1;
+    req_row[i] = R;
+    for (uint64_t qi = q0; qi < rq.n_tok; ++qi) attn_flops += 4.0 * c.n_heads * c.head_dim * (qi + 1);
+    attn_bytes += kv_tok_bytes * rq.n_tok + 2.0 * ql * c.n_heads * c.head_dim * 2;
+    ctx_tokens += rq.n_tok;
+    st.ctx_len = static_cast<int32_t>(rq.n_tok);
+    e->reqs.push_back(std::move(st));
+    ++R;
+  }
+  // longest tiles first (LPT over the 148 SMs)
+  std::sort(h_work, h_work + n_work, [&](const int2& a, const int2& b) {
+    int ka = h_ctx[a.x] - h_ql[a.x] + a.y, kb = h_ctx[b.x] - h_ql[b.x] + b.y;
+    return ka > kb;
+  });
+  e->last_T = T;
+  e->last_R = R;
+  e->last_work = n_work;
+  e->work[0] = attn_flops * c.n_layers;
+  e->work[1] = attn_bytes * c.n_layers;
+  e->work[2] = static_cast<double>(T) * kv_tok_bytes * c.n_layers;
+  const double lin = 2.0 * (static_cast<double>(c.d_model) * (c.n_heads + 2 * c.n_kv_heads) * c.head_dim +
+                            static_cast<double>(c.d_model) * c.n_heads * c.head_dim +
+                            3.0 * c.d_model * c.d_ff);
+  e->work[3] = lin * T * c.n_layers + 2.0 * c.d_model * c.vocab * R;
+  e->work[4] = T;
+  e->work[5] = ctx_tokens;
+  if (R == 0) {
+    bk.pool().release_deferred();
+    return GLMX_OK;
+  }
+  cudaStream_t s = e->stream;
+  {
+    Prof p(e, kCatH2D);
+    GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
+  }
+  GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
+  forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
+  argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), s);
+  {
+    Prof p(e, kCatD2H);
+    GLMX_CUDA(cudaMemcpyAsync(e->h_out, e->next_tok.p, R * 4, cudaMemcpyDeviceToHost, s));
+  }
+  GLMX_CUDA(cudaEventRecord(e->fwd_done, s));
+  // evicted pages were read by this batch; any later writer is stream-ordered after it
+  bk.pool().release_deferred();
+  GLMX_CUDA(cudaStreamSynchronize(s));
+  collect_profile(e);
+  std::vector<float> tmp;
+  for (uint64_t i = 0; i < n_req; ++i) {
+    if (req_row[i] < 0) continue;
+    if (first_token) first_token[i] = e->h_out[req_row[i]];
+    if (logits_out)
+      GLMX_CUDA(cudaMemcpy(logits_out + i * c.vocab, e->logits.as<float>() + static_cast<size_t>(req_row[i]) * c.vocab,
+                           c.vocab * 4, cudaMemcpyDeviceToHost));
+  }
+  // decode continues from the last prompt token's greedy successor
+  e->has_batch = true;
+  return GLMX_OK;
+}
+
+int engine_replay_impl(glmx_engine* e) {
+  if (!e->has_batch) throw Error(GLMX_ERR_ARG, "no staged batch");
+  DeviceGuard dg(e->m->device);
+  forward(e, e->last_T, e->last_R, e->last_work, e->last_R,
+          reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
+  argmax_rows(e->logits.as<float>(), e->last_R, e->m->cfg.vocab, e->next_tok.as<int32_t>(), e->stream);
+  GLMX_CUDA(cudaStreamSynchronize(e->stream));
+  collect_profile(e);
+  return GLMX_OK;
+}
+
+// Greedy decode.  Requests are re-ordered by step count (descending) so the active set of every
+// step is a row prefix and step s+1 consumes step s's argmax rows in place on the device.
+int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens, float* last_logits) {
+  if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
+  glmx_model* m = e->m;
+  const auto& c = m->cfg;
+  const uint32_t B = e->kv->cfg.block_tokens;
+  const int R = e->last_R;
+  uint32_t max_steps = 0;
+  for (int i = 0; i < R; ++i) {
+    if (steps[i] > e->cfg.max_decode) throw Error(GLMX_ERR_ARG, "steps exceed max_decode");
+    max_steps = std::max(max_steps, steps[i]);
+  }
+  for (int i = 0; i < R; ++i)
+    for (uint32_t s = 0; s < max_steps; ++s) out_tokens[static_cast<size_t>(i) * max_steps + s] = -1;
+  if (max_steps == 0) return GLMX_OK;
+  DeviceGuard dg(m->device);
+  std::vector<int> order(R);
+  for (int i = 0; i < R; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return steps[a] > steps[b]; });
+  cudaStream_t s = e->stream;
+  GLMX_CUDA(cudaEventSynchronize(e->fwd_done));
+  // the prefill's greedy tokens, rows permuted into decode order
+  int32_t* d_prev = e->next_tok.as<int32_t>();
+  std::vector<int32_t> first(R);
+  GLMX_CUDA(cudaMemcpy(first.data(), d_prev, R * 4, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> toks(R);
+  for (int j = 0; j < R; ++j) toks[j] = first[order[j]];
+  int32_t* d_seq = d_prev + R;  // [max_steps][R] generated tokens
+  GLMX_CUDA(cudaMemcpy(d_prev, toks.data(), R * 4, cudaMemcpyHostToDevice));
+  uint8_t* hm = static_cast<uint8_t*>(e->h_meta);
+  for (uint32_t st = 0; st < max_steps; ++st) {
+    int n = 0;
+    while (n < R && steps[order[n]] > st) ++n;
+    GLMX_CUDA(cudaEventSynchronize(e->h2d_done));
+    int32_t* h_pos = reinterpret_cast<int32_t*>(hm + e->o_pos);
+    int64_t* h_slot = reinterpret_cast<int64_t*>(hm + e->o_slot);
+    int32_t* h_qs = reinterpret_cast<int32_t*>(hm + e->o_qs);
+    int32_t* h_ql = reinterpret_cast<int32_t*>(hm + e->o_ql);
+    int32_t* h_ctx = reinterpret_cast<int32_t*>(hm + e->o_ctx);
+    int32_t* h_bt = reinterpret_cast<int32_t*>(hm + e->o_bt);
+    int2* h_work = reinterpret_cast<int2*>(hm + e->o_work);
+    int32_t* h_last = reinterpret_cast<int32_t*>(hm + e->o_last);
+    for (int j = 0; j < n; ++j) {
+      glmx_engine::Req& rq = e->reqs[order[j]];
+      const int32_t p = rq.ctx_len;  // position of the token being fed
+      h_pos[j] = p;
+      h_slot[j] = static_cast<int64_t>(rq.pages[p / B]) * B + (p % B);
+      h_qs[j] = j;
+      h_ql[j] = 1;
+      h_ctx[j] = p + 1;
+      std::memcpy(h_bt + static_cast<size_t>(j) * e->bt_stride, rq.pages.data(), rq.pages.size() * 4);
+      h_work[j] = make_int2(j, 0);
+      h_last[j] = j;
+      rq.ctx_len = p + 1;
+    }
+    GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
+    GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
+    const int32_t* in_tok = st == 0 ? d_prev : d_seq + static_cast<size_t>(st - 1) * R;
+    forward(e, n, n, n, n, in_tok);
+    argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R, s);
+  }
+  std::vector<int32_t> seq(static_cast<size_t>(max_steps) * R);
+  GLMX_CUDA(cudaMemcpyAsync(seq.data(), d_seq, seq.size() * 4, cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaStreamSynchronize(s));
+  collect_profile(e);
+  for (int j = 0; j < R; ++j)
+    for (uint32_t st = 0; st < steps[order[j]]; ++st)
+      out_tokens[static_cast<size_t>(order[j]) * max_steps + st] = seq[static_cast<size_t>(st) * R + j];
+  if (last_logits) {
+    // logits of the final step for the requests still active in it (others untouched)
+    int n = 0;
+    while (n < R && steps[order[n]] >= max_steps) ++n;
+    for (int j = 0; j < n; ++j)
+      GLMX_CUDA(cudaMemcpy(last_logits + static_cast<size_t>(order[j]) * c.vocab,
+                           e->logits.as<float>() + static_cast<size_t>(j) * c.vocab, c.vocab * 4,
+                           cudaMemcpyDeviceToHost));
+  }
+  return GLMX_OK;
+}

@@ -1,0 +1,124 @@
+// Runtime objects behind the C-ABI handles: KV (block engine + device page pool), graph
+// (host ingest + device CSR for K1), model (random-init Llama weights), engine (batched
+// prefill / decode step).
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/block_engine.hpp"
+#include "host/graph.hpp"
+#include "kernels/attn.cuh"
+#include "kernels/chunk.cuh"
+#include "kernels/ops.cuh"
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+// Growable device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void reserve(size_t n);
+  ~DBuf();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct glmx_kv {
+  glmx_kv_config cfg{};
+  std::unique_ptr<glmx::BlockEngine> bk;
+  glmx::PoolGeom geom{};
+  uint64_t page_bytes = 0;
+  bool has_pool() const { return geom.base != nullptr; }
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_copy_ms = 0.f;
+  DBuf scratch;  // page lists for copies
+  ~glmx_kv();
+};
+
+struct glmx_graph {
+  glmx::HostGraph host;
+  int device = -1;
+  glmx::DevGraph dev{};
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  // K1 scratch
+  DBuf d_nodes, d_sel, d_cnt, d_len, d_off, d_bytes, d_flag, d_tidx, d_tid, d_tbeg, d_tend,
+      d_toff, d_temp;
+  void upload();
+  ~glmx_graph();
+};
+
+struct LayerW {
+  __nv_bfloat16 *attn_norm, *wqkv, *wo, *mlp_norm, *wgu, *wdown;
+};
+
+struct glmx_model {
+  glmx_model_config cfg{};
+  int device = -1;
+  void* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  __nv_bfloat16 *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  std::vector<LayerW> layers;
+  float* inv_freq = nullptr;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  ~glmx_model();
+};
+
+struct glmx_engine {
+  glmx_model* m = nullptr;
+  glmx_kv* kv = nullptr;
+  glmx_engine_config cfg{};
+  cudaStream_t stream = nullptr;
+  int bt_stride = 0;
+  int tpt = 0;  // attention tokens per tile
+
+  // activations
+  DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok;
+  // batch metadata (device) + pinned host staging (single H2D)
+  DBuf meta;
+  void* h_meta = nullptr;
+  size_t meta_bytes = 0;
+  int32_t* h_out = nullptr;  // pinned: tokens out
+  cudaEvent_t h2d_done = nullptr, fwd_done = nullptr;
+
+  // last batch (for decode / replay)
+  struct Req {
+    int32_t ctx_len = 0;
+    std::vector<int32_t> pages;  // full blocks + scratch
+    std::vector<int32_t> scratch;
+  };
+  std::vector<Req> reqs;
+  int last_T = 0, last_R = 0, last_work = 0;
+  bool has_batch = false;
+  // offsets into meta
+  size_t o_tok = 0, o_pos = 0, o_slot = 0, o_qs = 0, o_ql = 0, o_ctx = 0, o_bt = 0, o_work = 0,
+         o_last = 0;
+
+  // profiling
+  bool profiling = false;
+  struct Span {
+    cudaEvent_t a, b;
+    int cat;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<Span> spans;
+  float timings[7] = {0};
+  double work[6] = {0};
+
+  ~glmx_engine();
+};

@@ -1,0 +1,107 @@
+"""Python mirror of PropertyGraph (graph_store.hpp:27-75) + Retriever::node_info_rendered
+(retriever.cpp:123-129), with the batched vertex-chunk kernel K1 behind glmx_chunk_build."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import check, lib
+
+TOTAL_DEGREE, BY_EDGE_TYPE = 0, 1
+
+
+@dataclass
+class ChunkBatch:
+    texts: list          # rendered chunk per request (str)
+    token_ids: list      # per request list[int] (empty when vocab == 0)
+    token_spans: list    # per request list[(begin, end)] byte spans within the chunk
+    kernel_ms: float
+
+
+class PropertyGraph:
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def load(cls, path, device=0):
+        h = C.c_void_p()
+        check(lib().glmx_graph_load_jsonl(path.encode(), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def synth_powerlaw(cls, n_nodes, edges_per_node=8, seed=0, device=0):
+        h = C.c_void_p()
+        check(lib().glmx_graph_synth_powerlaw(n_nodes, edges_per_node, seed, device, C.byref(h)))
+        return cls(h)
+
+    def save(self, path):
+        check(lib().glmx_graph_save_jsonl(self.h, path.encode()))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().glmx_graph_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def node_count(self):
+        return lib().glmx_graph_node_count(self.h)
+
+    def edge_count(self):
+        return lib().glmx_graph_edge_count(self.h)
+
+    def node_index(self, node_id):
+        return lib().glmx_graph_node_index(self.h, node_id.encode())
+
+    def node_id(self, idx):
+        buf = C.create_string_buffer(4096)
+        n = lib().glmx_graph_node_id(self.h, idx, buf, 4096)
+        return None if n < 0 else buf.raw[:n].decode()
+
+    def total_degree(self, idx):
+        return lib().glmx_graph_degree(self.h, idx)
+
+
+class Retriever:
+    """Vertex-chunk side of the reference Retriever (retriever.hpp:26-72)."""
+
+    def __init__(self, graph: PropertyGraph, chunk_k=8, weight_mode=TOTAL_DEGREE, directed=False,
+                 vocab=0):
+        self.graph = graph
+        self.cfg = _lib.ChunkConfig(chunk_k, weight_mode, int(directed), vocab)
+
+    def node_info_rendered(self, node_id: str) -> str:
+        cap = 1 << 16
+        while True:
+            buf = C.create_string_buffer(cap)
+            n = lib().glmx_node_info_rendered(self.graph.h, C.byref(self.cfg), node_id.encode(),
+                                              buf, cap)
+            if n < 0:
+                check(-n)
+            if n <= cap:
+                return buf.raw[:n].decode()
+            cap = n
+
+    def chunk_build(self, node_idx) -> ChunkBatch:
+        """K1 over a batch of node indices (one chunk per entry, duplicates allowed)."""
+        n = len(node_idx)
+        nodes = (C.c_int32 * max(1, n))(*node_idx)
+        tb, tt = C.c_uint64(), C.c_uint64()
+        check(lib().glmx_chunk_build(self.graph.h, C.byref(self.cfg), nodes, n, None, 0, None,
+                                     None, None, None, 0, None, C.byref(tb), C.byref(tt)))
+        out = C.create_string_buffer(max(1, tb.value))
+        boff = (C.c_uint64 * (n + 1))()
+        ntok = max(1, tt.value)
+        tid = (C.c_int32 * ntok)()
+        tbeg, tend = (C.c_uint64 * ntok)(), (C.c_uint64 * ntok)()
+        toff = (C.c_uint64 * (n + 1))()
+        check(lib().glmx_chunk_build(self.graph.h, C.byref(self.cfg), nodes, n, out, tb.value,
+                                     boff, tid, tbeg, tend, ntok, toff, C.byref(tb), C.byref(tt)))
+        raw = out.raw
+        texts, ids, spans = [], [], []
+        for i in range(n):
+            texts.append(raw[boff[i]:boff[i + 1]].decode())
+            ids.append([tid[j] for j in range(toff[i], toff[i + 1])] if self.cfg.vocab else [])
+            spans.append([(tbeg[j], tend[j]) for j in range(toff[i], toff[i + 1])])
+        return ChunkBatch(texts, ids, spans, lib().glmx_chunk_last_kernel_ms(self.graph.h))

@@ -1,0 +1,122 @@
+"""Prefill/decode engine on the GPU vs the CPU fp32 decoder oracle (oracle/decoder.py) and the
+reference bookkeeping.  Tolerances (north star): logits max-abs 2e-2 + rel 1e-2 (bf16 vs fp32);
+greedy ids bit-exact (asserted where the oracle's top-1/top-2 margin exceeds the tolerance)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2511_01633_b200 as glmx
+from oracle.decoder import Decoder, token_ids
+
+pytestmark = pytest.mark.gpu
+ATOL, RTOL = 2e-2, 1e-2
+
+
+def make(cfg, cap=256, headroom=256, max_req=16, max_tok=4096, max_decode=8, max_ctx=4096):
+    model = glmx.Model(cfg, device=0)
+    kv = glmx.KvCacheState(cap, 16, glmx.PRIORITY, device=0, n_layers=cfg.n_layers,
+                           n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
+                           headroom_pages=headroom)
+    eng = glmx.Engine(model, kv, max_requests=max_req, max_batch_tokens=max_tok,
+                      max_decode=max_decode, max_context=max_ctx)
+    return model, kv, eng
+
+
+def check_logits(got, want):
+    err = np.abs(got - want)
+    tol = ATOL + RTOL * np.abs(want)
+    assert np.all(err <= tol), f"max err {err.max():.4g} (max |ref| {np.abs(want).max():.3g})"
+
+
+def check_greedy(got_ids, logits_ref_rows, want_ids):
+    for g, w, lr in zip(got_ids, want_ids, logits_ref_rows):
+        if g == w:
+            continue
+        top = np.sort(lr)[-2:]
+        assert top[1] - top[0] <= 2 * (ATOL + RTOL * abs(top[1])), (g, w, top)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    model, kv, eng = make(glmx.TINY)
+    return model, kv, eng, Decoder(glmx.TINY, model.export_all())
+
+
+def words(n, tag="w"):
+    return [f"{tag}{i}" for i in range(n)]
+
+
+def test_prefill_batch_with_shared_prefix(tiny):
+    model, kv, eng, dec = tiny
+    p = words(70)
+    reqs = [glmx.Request(p, [(0, 20, 0), (20, 70, 3)], "a"),
+            glmx.Request(p[:48] + words(9, "x"), [(0, 57, 1)], "b"),   # hits a's blocks in-batch
+            glmx.Request(words(5, "z"), [(0, 5, 3)], "c"),             # tail only
+            glmx.Request(p[:64], [(0, 64, 2)], "d")]                   # fully cached -> recompute last
+    reps, first, logits = eng.prefill(reqs, want_logits=True)
+    assert [(r.cached_tokens, r.computed_tokens, r.tail_tokens) for r in reps] == [
+        (0, 64, 6), (48, 0, 9), (0, 0, 5), (64, 0, 0)]
+    refs = [dec.forward(token_ids(r.tokens, model.cfg.vocab))[0] for r in reqs]
+    for i in range(len(reqs)):
+        check_logits(logits[i], refs[i])
+    check_greedy(first, refs, [int(np.argmax(x)) for x in refs])
+
+
+def test_decode_matches_greedy_oracle(tiny):
+    model, kv, eng, dec = tiny
+    reqs = [glmx.Request(words(40, "q"), [(0, 40, 3)], "s"),
+            glmx.Request(words(17, "r"), [(0, 17, 3)], "t")]
+    _, first = eng.prefill(reqs)
+    out, last = eng.decode([6, 3], want_logits=True)
+    for i, r in enumerate(reqs):
+        ids = token_ids(r.tokens, model.cfg.vocab)
+        g = dec.greedy(ids, len(out[i]))
+        assert [first[i]] + out[i] == g
+
+
+def test_bookkeeping_matches_reference_under_pressure(ref):
+    """Same request stream through the engine (device pool) and the reference KvCacheState:
+    identical reports, eviction order and residents, including self-eviction + orphans."""
+    model, kv, eng = make(glmx.TINY, cap=6, headroom=64)
+    rk = oracle.RefKv(ref, 6, 16, 0)
+    rnd = np.random.default_rng(1)
+    base = words(64)
+    for step in range(12):
+        reqs = []
+        for j in range(3):
+            n = int(rnd.integers(1, 120))
+            toks = (base[: int(rnd.integers(0, 64))] + words(n, f"s{step}_{j}_"))[:n]
+            cut = int(rnd.integers(0, len(toks) + 1))
+            tiers = [t for t in [(0, cut, 0), (cut, len(toks), 3)] if t[0] < t[1]]
+            reqs.append(glmx.Request(toks, tiers, f"sess{j}"))
+        try:
+            reps, _ = eng.prefill(reqs)
+        except glmx.CacheExhausted:
+            reps = None
+        for i, r in enumerate(reqs):
+            st, rep, ev = rk.prefill(r.tokens, r.tiers, r.session)
+            if reps is None:
+                break
+            assert st == 0
+            assert (reps[i].cached_tokens, reps[i].computed_tokens, reps[i].tail_tokens) == rep
+        if reps is None:
+            break
+        assert [(a, b, c) for a, b, c, _ in kv.resident_snapshot()] == rk.resident()
+
+
+@pytest.mark.slow
+def test_llama8b_shape_two_layer_slice():
+    cfg = glmx.ModelConfig(n_layers=2, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=128,
+                           d_ff=14336, vocab=128256)
+    model, kv, eng = make(cfg, cap=64, headroom=64, max_req=4, max_tok=1024, max_decode=2,
+                          max_ctx=1024)
+    dec = Decoder(cfg, model.export_all())
+    p = words(150)
+    reqs = [glmx.Request(p, [(0, 40, 0), (40, 150, 3)], "a"),
+            glmx.Request(p[:130] + words(30, "y"), [(0, 160, 1)], "b")]
+    reps, first, logits = eng.prefill(reqs, want_logits=True)
+    assert reps[1].cached_tokens == 128
+    refs = [dec.forward(token_ids(r.tokens, cfg.vocab))[0] for r in reqs]
+    for i in range(2):
+        check_logits(logits[i], refs[i])
+    check_greedy(first, refs, [int(np.argmax(x)) for x in refs])
