@@ -46,11 +46,21 @@ def rmsnorm(x, w, eps):
     return (x / np.sqrt(var + eps)) * w
 
 
+def bf16_round(x):
+    """Round fp32 -> bf16 (round-to-nearest-even) -> fp32."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
 class Decoder:
-    def __init__(self, cfg, weights):
+    def __init__(self, cfg, weights, emulate_bf16=False):
+        """emulate_bf16: diagnostic mode that rounds activations to bf16 where the GPU engine
+        stores them (GEMM inputs/outputs, K/V, P); the parity oracle is the fp32 default."""
         self.c = cfg
         self.w = weights
         self.inv = inv_freq(cfg.head_dim, cfg.rope_theta)
+        self.r = bf16_round if emulate_bf16 else (lambda a: a)
 
     def forward(self, ids, pos=None, past=None, return_all=False):
         """ids [n]; past: per-layer (K [p,Hkv,hd], V) of preceding positions.  Returns logits of
@@ -62,16 +72,17 @@ class Decoder:
             pos = np.arange(p0, p0 + n)
         H, Hkv, hd = c.n_heads, c.n_kv_heads, c.head_dim
         G = H // Hkv
+        r = self.r
         x = w["embed"][np.asarray(ids)].astype(np.float32)
         new_past = []
         for l, lw in enumerate(w["layers"]):
-            h = rmsnorm(x, lw["attn_norm"], c.norm_eps)
-            qkv = h @ lw["wqkv"].T
+            h = r(rmsnorm(x, lw["attn_norm"], c.norm_eps))
+            qkv = r(h @ lw["wqkv"].T)
             q = qkv[:, :H * hd].reshape(n, H, hd)
             k = qkv[:, H * hd:(H + Hkv) * hd].reshape(n, Hkv, hd)
             v = qkv[:, (H + Hkv) * hd:].reshape(n, Hkv, hd)
-            q = rope(q, pos, self.inv)
-            k = rope(k, pos, self.inv)
+            q = r(rope(q, pos, self.inv))
+            k = r(rope(k, pos, self.inv))
             if past is not None:
                 k = np.concatenate([past[l][0], k], axis=0)
                 v = np.concatenate([past[l][1], v], axis=0)
@@ -86,16 +97,16 @@ class Decoder:
                 s = np.where(mask, s, -np.inf)
                 s = s - s.max(axis=1, keepdims=True)
                 pr = np.exp(s)
-                pr /= pr.sum(axis=1, keepdims=True)
-                out[:, hh, :] = pr @ v[:, kh, :]
-            x = x + out.reshape(n, H * hd) @ lw["wo"].T
-            h = rmsnorm(x, lw["mlp_norm"], c.norm_eps)
-            gu = h @ lw["w_gate_up"].T
+                den = pr.sum(axis=1, keepdims=True)
+                out[:, hh, :] = (r(pr) @ v[:, kh, :]) / den
+            x = x + r(out.reshape(n, H * hd)) @ lw["wo"].T
+            h = r(rmsnorm(x, lw["mlp_norm"], c.norm_eps))
+            gu = r(h @ lw["w_gate_up"].T)
             g, u = gu[:, :c.d_ff], gu[:, c.d_ff:]
-            act = g / (1.0 + np.exp(-g)) * u
+            act = r(g / (1.0 + np.exp(-g)) * u)
             x = x + act @ lw["w_down"].T
         rows = x if return_all else x[-1:]
-        hf = rmsnorm(rows, w["final_norm"], c.norm_eps)
+        hf = r(rmsnorm(rows, w["final_norm"], c.norm_eps))
         logits = hf @ w["lm_head"].T
         return (logits if return_all else logits[0]), new_past
 
