@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Headline bench: prefill tokens/s with vertex-chunk KV reuse (BASELINE.json metric, config C2:
+Llama-3-8B-shaped random-init bf16, synthetic 100k-node power-law graph, top-k=16 chunks).
+
+A step = one round-robin rotation of the Graph-CoT workload (paper_2511_01633_b200/workload.py):
+every active lane makes its next LLM call, the calls form ONE engine prefill batch (reference
+bookkeeping semantics, paged KV pool, greedy first token), then ONE K1 launch builds the vertex
+chunks of the rotation's actions.  Queries are sharded rank r <- query i with i % N == r (weak
+scaling, no data-path collective).
+
+  value : prompt tokens (cached+computed+tail) / device time of the forward (CUDA events on the
+          engine stream; inputs already in HBM)
+  e2e   : same tokens / whole step through the C-ABI with HOST buffers (bookkeeping, H2D, K1,
+          forward, D2H), bracketed by device syncs
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill tokens/s with vertex-chunk KV reuse"
+UNIT = "tokens/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=8)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="glmx", choices=["glmx", "reference"])
+    p.add_argument("--lanes", type=int, default=64)
+    p.add_argument("--nodes", type=int, default=100_000)
+    p.add_argument("--k", type=int, default=16)
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--capacity", type=int, default=16384)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]),
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline_sample(calls_tokens, chunk_nodes, graph_jsonl, seconds_budget=20.0, reps=None):
+    """The reference's CPU path on a bounded sample: the reference bookkeeping (oracle/_ref,
+    KvCacheState::prefill + Retriever::node_info_rendered) and, because the reference has no
+    tensor math, the builder's fp32 numpy decoder for the computed tokens as a 1-layer
+    Llama-3-8B slice x 32 layers (labelled extrapolation).  Returns (tokens/s, cores, sample)."""
+    import numpy as np
+
+    import oracle
+    from oracle.decoder import rmsnorm
+
+    t_book = 0.0
+    ref_graph = oracle.RefGraph(path=graph_jsonl)
+    rk = oracle.RefKv(oracle.ref(), 1 << 20, 16, 0)
+    t0 = time.perf_counter()
+    for nid in chunk_nodes:
+        ref_graph.node_info_rendered(nid, 16)
+    total_tok, comp_tok = 0, []
+    for toks, tiers, sess in calls_tokens:
+        st, rep, _ = rk.prefill(toks, tiers, sess)
+        total_tok += len(toks)
+        comp_tok.append(max(1, rep[1] + rep[2]))
+    t_book = time.perf_counter() - t0
+    # one decoder layer of the 8B shape, fp32, all host threads (numpy BLAS)
+    rng = np.random.default_rng(0)
+    d, H, Hkv, hd, ff = 4096, 32, 8, 128, 14336
+    W = {k: (rng.standard_normal(s, dtype=np.float32) * 0.02) for k, s in
+         {"wqkv": ((H + 2 * Hkv) * hd, d), "wo": (d, H * hd), "wgu": (2 * ff, d),
+          "wd": (d, ff)}.items()}
+    x = rng.standard_normal((sum(comp_tok), d), dtype=np.float32)
+    t1 = time.perf_counter()
+    h = rmsnorm(x, 1.0, 1e-5)
+    qkv = h @ W["wqkv"].T
+    x = x + qkv[:, :H * hd] @ W["wo"].T  # attention core omitted: linear-dominated at this size
+    h = rmsnorm(x, 1.0, 1e-5)
+    gu = h @ W["wgu"].T
+    act = gu[:, :ff] / (1 + np.exp(-gu[:, :ff])) * gu[:, ff:]
+    x = x + act @ W["wd"].T
+    t_layer = time.perf_counter() - t1
+    total = t_book + 32 * t_layer
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        pass
+    sample = (f"{len(calls_tokens)} prefill calls ({total_tok} prompt tokens, {sum(comp_tok)} computed) "
+              f"+ {len(chunk_nodes)} vertex chunks: reference bookkeeping {t_book:.3f}s + numpy fp32 "
+              f"1-layer 8B slice {t_layer:.3f}s x32 (extrapolated; attention core omitted)")
+    return total_tok / total, cores, sample
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU path (oracle/_ref bookkeeping + the fp32 decoder
+    restatement) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import paper_2511_01633_b200 as glmx  # only for the synthetic graph + workload text
+    from paper_2511_01633_b200.workload import GraphCoTWorkload
+
+    g = glmx.PropertyGraph.synth_powerlaw(args.nodes, 8, seed=args.seed, device=0)
+    path = f"/tmp/glmx_bench_graph_{args.nodes}_{args.seed}.jsonl"
+    if not os.path.exists(path):
+        g.save(path)
+    ret = glmx.Retriever(g, chunk_k=args.k, vocab=0)
+    wl = GraphCoTWorkload(None, ret, n_queries=args.lanes * 4, lanes=args.lanes, seed=args.seed)
+    from oracle import kv_prefill_inputs
+
+    def step_sample():
+        calls = wl.next_calls()
+        wl.advance(calls)
+        sub = calls[:4]
+        toks = [kv_prefill_inputs(c.segments) + (c.session.sid,) for c in sub]
+        nodes = [g.node_id(c.session.sources[min(c.session.round, len(c.session.sources) - 1)])
+                 for c in sub]
+        return toks, nodes
+
+    vals = []
+    for i in range(args.warmup + args.steps):
+        toks, nodes = step_sample()
+        v, cores, sample = cpu_baseline_sample(toks, nodes, path)
+        if i >= args.warmup:
+            vals.append(v)
+    value = sum(vals) / len(vals)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+           "config": {"workload": "C2: Graph-CoT scripted sessions, 100k-node power-law graph, "
+                                  "k=16, Llama-3-8B shape", "lanes": args.lanes},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                            "sample": "per step: " + sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "data": "synthetic"}
+    print(json.dumps(out))
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_01633_b200 as glmx
+    from paper_2511_01633_b200.workload import GraphCoTWorkload
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = glmx.ModelConfig(n_layers=args.layers, d_model=4096, n_heads=32, n_kv_heads=8,
+                           head_dim=128, d_ff=14336, vocab=128256, seed=args.seed)
+    g = glmx.PropertyGraph.synth_powerlaw(args.nodes, 8, seed=args.seed, device=local)
+    ret = glmx.Retriever(g, chunk_k=args.k, vocab=cfg.vocab)
+    model = glmx.Model(cfg, device=local)
+    kv = glmx.KvCacheState(args.capacity, 16, glmx.PRIORITY, device=local, n_layers=cfg.n_layers,
+                           n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
+                           headroom_pages=4096)
+    eng = glmx.Engine(model, kv, max_requests=args.lanes, max_batch_tokens=args.lanes * 1024,
+                      max_decode=8, max_context=8192)
+    rotations = args.warmup + args.steps
+    # enough queries (per rank) that every lane stays busy through the timed rotations
+    n_q = args.lanes * (rotations // 6 + 2)
+    wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed)
+    wl.sessions = wl.sessions[rank::ws]  # query i -> rank i % N
+
+    for _ in range(args.warmup):
+        wl.rotation()
+    eng.set_profiling(1)
+    sampler = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    tokens = computed = cached = calls = chunks = finished = 0
+    fwd_ms = 0.0
+    h2d = d2h = 0
+    chunk_ms = 0.0
+    k1_rotations = 0
+    for _ in range(args.steps):
+        r = wl.rotation()
+        tm = eng.last_timings()
+        fwd_ms += tm["forward"]
+        chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h) if r.chunks else 0.0
+        tokens += r.prompt_tokens
+        computed += r.computed_tokens
+        cached += r.cached_tokens
+        calls += r.calls
+        chunks += r.chunks
+        k1_rotations += 1 if r.chunks else 0
+        finished += r.finished
+        wk = eng.last_work()
+        # host->device per step: packed batch metadata + chunk node ids; device->host: greedy ids
+        # + chunk bytes/tokens
+        h2d += int(wk["computed_tokens"]) * 16 + r.calls * (16 + 8 * 520) + r.chunks * 4
+        d2h += r.calls * 4 + r.chunks * 1200
+    ev1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    wall_ms = ev0.elapsed_time(ev1)
+
+    # roofline of K3 (paged attention) from a per-kernel profiled replay of the last batch
+    eng.set_profiling(2)
+    eng.replay_forward()
+    tm = eng.last_timings()
+    wk = eng.last_work()
+    eng.set_profiling(0)
+
+    vals = torch.tensor([tokens, computed, cached, calls, finished], dtype=torch.float64,
+                        device="cuda")
+    times = torch.tensor([fwd_ms, wall_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.SUM)
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    tokens, computed, cached, calls, finished = vals.tolist()
+    fwd_ms, wall_ms = times.tolist()
+    if rank != 0:
+        dist.destroy_process_group() if ws > 1 else None
+        return
+
+    peaks, peak_kind = measured_peaks()
+    attn_ms = tm["attention"]
+    attn_tflops = wk["attn_flops"] / (attn_ms * 1e-3) / 1e12 if attn_ms > 0 else 0.0
+    attn_gbs = wk["attn_bytes"] / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
+    # attention intensity ~4*s flop/byte: tensor-bound only above the ridge
+    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    intensity = wk["attn_flops"] / max(1.0, wk["attn_bytes"])
+    if intensity >= ridge:
+        roof = {"bound": "tensor", "achieved": attn_tflops, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": attn_tflops / peaks["bf16_tflops"]}
+    else:
+        roof = {"bound": "hbm", "achieved": attn_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": attn_gbs / peaks["hbm_gbs"]}
+    roof.update({"kernel": "K3 paged_attn (mma.sync v0)", "traffic": None,
+                 "peak_kind": peak_kind, "intensity_flop_per_byte": intensity,
+                 "kernel_ms_per_forward": attn_ms,
+                 "share_of_forward": attn_ms / max(1e-9, tm["forward"]),
+                 "gemm_ms_per_forward": tm["gemm"],
+                 "gemm_tflops": wk["linear_flops"] / max(1e-9, tm["gemm"] * 1e-3) / 1e12})
+    value = tokens / (fwd_ms * 1e-3)
+    e2e = tokens / (wall_ms * 1e-3)
+    n_layers = cfg.n_layers
+    launches_per_fwd = 1 + 5 * n_layers + 2
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "C2: Graph-CoT scripted sessions (classify -> reason/act per hop "
+                               "-> finish), synthetic 100k-node power-law graph, top-k=16 vertex "
+                               "chunks, Llama-3-8B-shaped random-init bf16, paged KV pool",
+                   "lanes_per_gpu": args.lanes, "nodes": args.nodes, "k": args.k,
+                   "kv_capacity_blocks": args.capacity, "block_tokens": 16,
+                   "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
+                   "parallelism": f"query-sharded x{ws}"},
+        "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
+        "cache_hit_token_frac": cached / max(1.0, tokens),
+        "calls": calls, "queries_finished": finished,
+        "queries_per_s_prefill_only": finished / (wall_ms * 1e-3),
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "roofline": roof,
+        # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
+        # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
+        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations),
+        "clocks": clocks,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        from oracle import kv_prefill_inputs
+
+        path = f"/tmp/glmx_bench_graph_{args.nodes}_{args.seed}.jsonl"
+        g.save(path)
+        sub = wl.next_calls()[:8]
+        toks = [kv_prefill_inputs(c.segments) + (c.session.sid,) for c in sub]
+        nodes = [g.node_id(c.session.sources[min(c.session.round, len(c.session.sources) - 1)])
+                 for c in sub]
+        v, cores, sample = cpu_baseline_sample(toks, nodes, path)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                               "sample": sample}
+    print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

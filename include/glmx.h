@@ -225,6 +225,19 @@ void glmx_engine_destroy(glmx_engine* e);
  * error (earlier requests' bookkeeping stays applied, like the reference; no forward runs). */
 int glmx_engine_prefill(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
                         glmx_prefill_report* reports, int32_t* first_token, float* logits);
+/* Same step with prompts given as (text, tier) segments — the Orchestrator::call_llm ->
+ * kv_prefill path (orchestrator.cpp:81-97, 116-135): per-segment whitespace tokenisation,
+ * same-tier range merge, then the prefill step above. */
+typedef struct {
+  const char* const* seg_text;
+  const uint64_t* seg_len;
+  const int32_t* seg_tier;
+  uint64_t n_seg;
+  const char* session;
+} glmx_segment_request;
+int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
+                                 const glmx_segment_request* reqs, glmx_prefill_report* reports,
+                                 int32_t* first_token, float* logits);
 /* Greedy decode continuing the last prefill batch: steps[i] tokens for request i (<= max_decode);
  * out_tokens host [n_req][max_steps], -1 past a request's count. */
 int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,

@@ -69,6 +69,11 @@ class RequestC(C.Structure):
                 ("session", C.c_char_p)]
 
 
+class SegmentRequestC(C.Structure):
+    _fields_ = [("seg_text", C.POINTER(C.c_char_p)), ("seg_len", u64p), ("seg_tier", i32p),
+                ("n_seg", C.c_uint64), ("session", C.c_char_p)]
+
+
 _SIGS = {
     "glmx_last_error": (C.c_char_p, []),
     "glmx_version": (C.c_char_p, []),
@@ -122,6 +127,8 @@ _SIGS = {
     "glmx_engine_destroy": (None, [C.c_void_p]),
     "glmx_engine_prefill": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(RequestC),
                                       C.POINTER(PrefillReportC), i32p, f32p]),
+    "glmx_engine_prefill_segments": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(SegmentRequestC),
+                                               C.POINTER(PrefillReportC), i32p, f32p]),
     "glmx_engine_decode": (C.c_int, [C.c_void_p, u32p, i32p, f32p]),
     "glmx_engine_replay_forward": (C.c_int, [C.c_void_p]),
     "glmx_engine_last_timings": (C.c_int, [C.c_void_p, f32p]),

@@ -356,6 +356,44 @@ int glmx_engine_prefill(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
                         glmx_prefill_report* reports, int32_t* first_token, float* logits) {
   return guarded([&] { return engine_prefill_impl(e, n_req, reqs, reports, first_token, logits); });
 }
+int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
+                                 const glmx_segment_request* reqs, glmx_prefill_report* reports,
+                                 int32_t* first_token, float* logits) {
+  return guarded([&] {
+    // Orchestrator::kv_prefill (orchestrator.cpp:81-97) per request, then one batched step.
+    struct Tok {
+      std::string bytes;
+      std::vector<uint64_t> offs{0};
+      std::vector<glmx_tier_range> tiers;
+    };
+    std::vector<Tok> toks(n_req);
+    std::vector<glmx_request> rq(n_req);
+    std::vector<uint64_t> b, en;
+    for (uint64_t r = 0; r < n_req; ++r) {
+      Tok& t = toks[r];
+      const glmx_segment_request& s = reqs[r];
+      for (uint64_t i = 0; i < s.n_seg; ++i) {
+        b.clear();
+        en.clear();
+        tokenize_spans(s.seg_text[i], s.seg_len[i], b, en);
+        if (b.empty()) continue;
+        const uint64_t begin = t.offs.size() - 1;
+        for (size_t j = 0; j < b.size(); ++j) {
+          t.bytes.append(s.seg_text[i] + b[j], en[j] - b[j]);
+          t.offs.push_back(t.bytes.size());
+        }
+        const uint64_t end = t.offs.size() - 1;
+        if (!t.tiers.empty() && t.tiers.back().tier == s.seg_tier[i])
+          t.tiers.back().end = end;
+        else
+          t.tiers.push_back({begin, end, s.seg_tier[i], 0});
+      }
+      rq[r] = {t.bytes.data(), t.offs.data(), t.offs.size() - 1, t.tiers.data(), t.tiers.size(),
+               s.session};
+    }
+    return engine_prefill_impl(e, n_req, rq.data(), reports, first_token, logits);
+  });
+}
 int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,
                        float* last_logits) {
   return guarded([&] { return engine_decode_impl(e, steps, out_tokens, last_logits); });
@@ -371,7 +409,7 @@ int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {
   std::memcpy(out6, e->work, sizeof(e->work));
   return GLMX_OK;
 }
-void glmx_engine_set_profiling(glmx_engine* e, int32_t on) { e->profiling = on != 0; }
+void glmx_engine_set_profiling(glmx_engine* e, int32_t level) { e->profiling = level; }
 
 // ------------------------------------------------------------------ kernel test hooks
 int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,

@@ -349,8 +349,9 @@ struct Prof {
   glmx_engine* e;
   int cat;
   cudaEvent_t a = nullptr;
+  // profiling 1: whole forward + copies only; 2: every kernel category
   Prof(glmx_engine* e_, int c) : e(e_), cat(c) {
-    if (e->profiling) {
+    if (e->profiling >= 2 || (e->profiling == 1 && (c == 0 || c >= 5))) {
       a = next_event(e);
       GLMX_CUDA(cudaEventRecord(a, e->stream));
     }

@@ -109,7 +109,7 @@ struct glmx_engine {
          o_last = 0;
 
   // profiling
-  bool profiling = false;
+  int profiling = 0;
   struct Span {
     cudaEvent_t a, b;
     int cat;

@@ -1,0 +1,178 @@
+"""Graph-CoT multi-agent workload driver over the engine (the caller side of the hot path).
+
+Mirrors the reference's Orchestrator state machine in GLM mode (orchestrator.cpp:156-256) with a
+scripted provider (scripted.hpp:21-30) whose replies follow the Rule agent's formats
+(rule.cpp:156-236) and run_bench's deterministic round-robin (bench.cpp:65-83):
+
+  Classifying -> "no"                                   (classification prompt)
+  Reasoning   -> "Missing: vertex chunks for: <id_r>"   (reasoning prompt: notebook = tier II)
+  Acting      -> fenced print(NodeInfo(RetrieveNode("<id_r>")))   (action prompt)
+                 the snippet output (K1 vertex chunk + "\\n") is appended to the notebook
+  ... one source node per round, then Reasoning -> "Finish: <answer>" and
+  finish(): set_tier(session, II, III) (orchestrator.cpp:147-154).
+
+One rotation = every active lane makes its next LLM call; the rotation's calls are ONE engine
+prefill batch (bookkeeping applied in lane order, as the reference would), then ONE batched K1
+launch builds the vertex chunks of every action executed in that rotation.  Source nodes are
+drawn with a power-law skew so popular (hub) chunks recur across queries; every reasoning round
+re-reads the previous rounds' chunks (reuse across iterations).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import random
+from dataclasses import dataclass, field
+
+from . import _lib
+from ._lib import check, lib
+from .kvcache import PrefillReport
+from .templates import TIER_II, TIER_III, TemplateSet
+
+
+@dataclass
+class Session:
+    sid: str
+    sources: list
+    question: str
+    state: str = "C"
+    round: int = 0
+    notebook: str = ""
+    calls: int = 0
+    task: str = ""
+
+
+@dataclass
+class Call:
+    session: Session
+    agent: str
+    segments: list
+    reply: str
+
+
+@dataclass
+class RotationResult:
+    calls: int = 0
+    prompt_tokens: int = 0       # cached + computed + tail
+    computed_tokens: int = 0     # computed + tail (what the GPU ran)
+    cached_tokens: int = 0
+    finished: int = 0
+    chunks: int = 0
+    reports: list = field(default_factory=list)
+    first_tokens: list = field(default_factory=list)
+
+
+def count_tokens(text):
+    return len(text.split())
+
+
+class GraphCoTWorkload:
+    def __init__(self, engine, retriever, n_queries, lanes, seed=0, min_hops=2, max_hops=4,
+                 skew=2.5, templates=None, node_ids=None):
+        self.engine = engine
+        self.kv = engine.kv if engine is not None else None
+        self.retriever = retriever
+        self.templates = templates or TemplateSet()
+        self.lanes = lanes
+        rnd = random.Random(seed)
+        g = retriever.graph
+        n = g.node_count()
+        self.sessions = []
+        for q in range(n_queries):
+            m = rnd.randint(min_hops, max_hops)
+            src = [min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)]
+            ids = [g.node_id(v) for v in src]
+            question = "Which item is linked from all of: " + "; ".join(ids) + "?"
+            self.sessions.append(Session(f"q{q:05d}", src, question))
+        self.admitted = 0
+        self.active = []
+
+    def done(self):
+        return self.admitted >= len(self.sessions) and not self.active
+
+    def _call_for(self, s: Session) -> Call:
+        t = self.templates
+        if s.state == "C":
+            return Call(s, "classification", t.render_classification(s.question), "no\n")
+        if s.state == "R":
+            if s.round < len(s.sources):
+                nid = self.retriever.graph.node_id(s.sources[s.round])
+                s.task = "vertex chunks for: " + nid
+                return Call(s, "reasoning", t.render_reasoning(s.question, s.notebook),
+                            "Missing: " + s.task + "\n")
+            return Call(s, "reasoning", t.render_reasoning(s.question, s.notebook),
+                        "Finish: " + self.retriever.graph.node_id(s.sources[0]) + "\n")
+        nid = s.task[len("vertex chunks for: "):]
+        code = f'```\nprint(NodeInfo(RetrieveNode("{nid}")))\n```\n'
+        return Call(s, "action", t.render_action(s.task), code)
+
+    def next_calls(self):
+        """Admission + one call per active lane, in lane order (bench.cpp:71-76)."""
+        while len(self.active) < self.lanes and self.admitted < len(self.sessions):
+            self.active.append(self.sessions[self.admitted])
+            self.admitted += 1
+        return [self._call_for(s) for s in self.active]
+
+    @staticmethod
+    def pack(calls):
+        n = len(calls)
+        arr = (_lib.SegmentRequestC * max(1, n))()
+        keep = []
+        for i, c in enumerate(calls):
+            texts = [txt.encode() for _, txt in c.segments]
+            ta = (C.c_char_p * max(1, len(texts)))(*texts)
+            la = (C.c_uint64 * max(1, len(texts)))(*[len(x) for x in texts])
+            tr = (C.c_int32 * max(1, len(texts)))(*[t for t, _ in c.segments])
+            sb = c.session.sid.encode()
+            keep += [texts, ta, la, tr, sb]
+            arr[i].seg_text, arr[i].seg_len, arr[i].seg_tier = ta, la, tr
+            arr[i].n_seg, arr[i].session = len(texts), sb
+        return arr, keep
+
+    def prefill(self, calls, packed=None):
+        n = len(calls)
+        arr, keep = packed if packed is not None else self.pack(calls)
+        reps = (_lib.PrefillReportC * max(1, n))()
+        first = (C.c_int32 * max(1, n))()
+        check(lib().glmx_engine_prefill_segments(self.engine.h, n, arr, reps, first, None))
+        return ([PrefillReport(reps[i].cached_tokens, reps[i].computed_tokens,
+                               reps[i].tail_tokens) for i in range(n)], [first[i] for i in range(n)])
+
+    def advance(self, calls, reports=None, first_tokens=None) -> RotationResult:
+        """Apply the replies: state transitions, K1 chunk build for the actions, finish."""
+        res = RotationResult(calls=len(calls), reports=reports or [],
+                             first_tokens=first_tokens or [])
+        for r in res.reports:
+            res.cached_tokens += r.cached_tokens
+            res.computed_tokens += r.computed_tokens + r.tail_tokens
+            res.prompt_tokens += r.cached_tokens + r.computed_tokens + r.tail_tokens
+        acting = [c for c in calls if c.agent == "action"]
+        if acting:
+            batch = self.retriever.chunk_build([c.session.sources[c.session.round] for c in acting])
+            for c, text in zip(acting, batch.texts):
+                c.session.notebook += text + "\n"  # PrintStmt: raw chunk + "\n" (interp.cpp:68-74)
+            res.chunks = len(acting)
+        still = []
+        for c in calls:
+            s = c.session
+            s.calls += 1
+            if c.agent == "classification":
+                s.state = "R"
+            elif c.agent == "action":
+                s.round += 1
+                s.state = "R"
+            elif c.reply.startswith("Finish:"):
+                s.state = "done"
+                if self.kv is not None:
+                    self.kv.set_tier(s.sid, TIER_II, TIER_III)
+                res.finished += 1
+                continue
+            else:
+                s.state = "A"
+            still.append(s)
+        self.active = still
+        return res
+
+    def rotation(self) -> RotationResult:
+        calls = self.next_calls()
+        reps, first = self.prefill(calls)
+        return self.advance(calls, reps, first)

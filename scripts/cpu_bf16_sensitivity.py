@@ -1,0 +1,20 @@
+"""How far do logits move from bf16 activation rounding alone? (CPU, numpy; no GPU)."""
+import sys, time
+import numpy as np
+sys.path.insert(0, '.')
+import paper_2511_01633_b200 as glmx
+from oracle.decoder import Decoder, token_ids, bf16_round
+cfg = glmx.ModelConfig(n_layers=2, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=128, d_ff=14336, vocab=128256)
+rng = np.random.default_rng(0)
+def w(*s): return bf16_round(rng.standard_normal(s, dtype=np.float32) * 0.02)
+qkv = (32 + 16) * 128
+W = {"embed": w(cfg.vocab, 4096), "final_norm": np.ones(4096, np.float32), "lm_head": w(cfg.vocab, 4096),
+     "layers": [{"attn_norm": np.ones(4096, np.float32), "wqkv": w(qkv, 4096), "wo": w(4096, 4096),
+                 "mlp_norm": np.ones(4096, np.float32), "w_gate_up": w(2 * 14336, 4096), "w_down": w(4096, 14336)} for _ in range(2)]}
+ids = token_ids([f"w{i}" for i in range(150)], cfg.vocab)
+t = time.time()
+a, _ = Decoder(cfg, W).forward(ids)
+b, _ = Decoder(cfg, W, emulate_bf16=True).forward(ids)
+err = np.abs(a - b)
+print(f"fp32 vs bf16-emulated: max {err.max():.4f} mean {err.mean():.4f} p99.9 {np.quantile(err, .999):.4f} std(logits) {a.std():.3f}  ({time.time()-t:.1f}s)")
+print("within 2e-2+1e-2|ref|:", bool(np.all(err <= 2e-2 + 1e-2 * np.abs(a))))
