@@ -221,7 +221,10 @@ int glmo_kv_prefill(glmo_kv* kv, const char* bytes, const uint64_t* offs, size_t
     insert_blk(kv, ids[b], tier, ++kv->clock, tier == 0 ? "" : session);
   }
   free(ids);
-  if (status) rep3[0] = rep3[1] = rep3[2] = 0; /* the reference returns no report on throw */
+  if (status) { /* the reference returns no report on throw */
+    rep3[0] = rep3[1] = rep3[2] = 0;
+    *n_ev = 0;
+  }
   return status;
 }
 

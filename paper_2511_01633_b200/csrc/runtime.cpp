@@ -391,7 +391,11 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
   const uint32_t B = kv->cfg.block_tokens;
   e->bt_stride = static_cast<int>((cfg->max_context + B - 1) / B + 1);
-  e->tpt = attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
+  const char* impl = std::getenv("GLMX_ATTN");
+  e->attn_impl = (impl && std::string(impl) == "mma") ? 1 : 0;
+  e->tpt = e->attn_impl ? attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv))
+                        : attn_tc_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
+  make_pool_tensor_map(kv->geom, kv->bk->pool().total(), e->kv_map, &e->kv_rows);
   e->x.reserve(T * d * 4);
   e->h.reserve(T * d * 2);
   e->qkv.reserve(T * (H + 2 * Hkv) * hd * 2);
@@ -472,7 +476,10 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     {
       Prof p(e, kCatAttn);
       ap.layer = l;
-      paged_attention(ap, s);
+      if (e->attn_impl)
+        paged_attention(ap, s);
+      else
+        paged_attention_tc(ap, e->kv_map, e->kv_rows, s);
     }
     {
       Prof p(e, kCatGemm);

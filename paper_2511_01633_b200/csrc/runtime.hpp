@@ -85,6 +85,9 @@ struct glmx_engine {
   cudaStream_t stream = nullptr;
   int bt_stride = 0;
   int tpt = 0;  // attention tokens per tile
+  int attn_impl = 0;  // 0 = tcgen05 (attn_tc.cu), 1 = mma.sync baseline (dev A/B only)
+  alignas(64) uint8_t kv_map[128];  // CUtensorMap over the KV pool (TMA)
+  uint32_t kv_rows = 0;
 
   // activations
   DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok;
