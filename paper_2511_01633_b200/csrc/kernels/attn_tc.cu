@@ -235,6 +235,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
         }
       }
     }
+    __syncwarp();  // reconverge before the CTA barrier (bar.sync is .aligned)
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
@@ -272,6 +273,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
       }
       issue_pv(n_kt - 1);
     }
+    __syncwarp();
   } else {
     // ---------------------------------------------------------------- softmax warps
     const int r = threadIdx.x;  // query row == TMEM lane
