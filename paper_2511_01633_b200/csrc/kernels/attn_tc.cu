@@ -63,16 +63,30 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps with a location instead of hanging the GPU.
-__device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity) {
-  printf("paged_attn_tc: mbarrier wait timeout block (%d,%d) thread %d bar 0x%x parity %u\n",
-         blockIdx.x, blockIdx.y, threadIdx.x, bar, parity);
-  __trap();
+// Bounded wait: a protocol bug traps with a location instead of hanging the GPU.  Roles record
+// their progress in shared memory (g_prog) so a stuck thread reports every role's state.
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t n = 0;
-  while (!mbar_try(bar, parity))
-    if (++n == (1u << 24)) mbar_stuck(bar, parity);
+__device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity, int tag, const volatile int* prog) {
+  printf("paged_attn_tc: wait timeout block (%d,%d) thread %d bar 0x%x parity %u tag %d | prod %d mma %d sm0 %d sm127 %d sm64 %d\n",
+         blockIdx.x, blockIdx.y, threadIdx.x, bar, parity, tag, prog[0], prog[1], prog[2], prog[3], prog[4]);
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0,
+                                          const volatile int* prog = nullptr) {
+  if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = gtime();
+  bool told = false;
+  while (!mbar_try(bar, parity)) {
+    const uint64_t dt = gtime() - t0;
+    if (!told && dt > 2000000000ull) {
+      if (prog) mbar_stuck(bar, parity, tag, prog);
+      told = true;
+    }
+    if (dt > 4000000000ull) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
@@ -163,6 +177,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
   const uint32_t b_sfull = smem_addr(bars + 8), b_pfull = smem_addr(bars + 10);
   const uint32_t b_ofull = smem_addr(bars + 11);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
+  volatile int* prog = reinterpret_cast<volatile int*>(bars + 20);  // debug progress
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kvh = blockIdx.y;
@@ -186,6 +201,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
     }
     mbar_init(b_pfull, 128);
     mbar_init(b_ofull, 1);
+    for (int i = 0; i < 5; ++i) prog[i] = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -219,7 +235,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
         const uint32_t ph = (j >> 1) & 1;
         for (int kv = 0; kv < 2; ++kv) {
           const uint32_t full = (kv ? b_vfull : b_kfull) + 8 * s;
-          if (j >= 2) mbar_wait((kv ? b_vempty : b_kempty) + 8 * s, ph ^ 1);
+          if (j >= 2) mbar_wait((kv ? b_vempty : b_kempty) + 8 * s, ph ^ 1, 100 + j * 10 + kv, prog);
           mbar_expect_tx(full, kTile);
           const uint32_t dst = sbase + (kv ? kOffV : kOffK) + s * kTile;
           for (int pg = 0; pg < kN / kB; ++pg) {
@@ -232,6 +248,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
             for (int hf = 0; hf < 2; ++hf)
               tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
           }
+          prog[0] = j * 10 + kv;
         }
       }
     }
@@ -243,8 +260,8 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
       const uint32_t q_addr = sbase + kOffQ, p_addr = sbase + kOffP;
       auto issue_pv = [&](int j) {
         const int s = j & 1;
-        mbar_wait(b_pfull, j & 1);           // P_j in smem, O rescaled
-        mbar_wait(b_vfull + 8 * s, (j >> 1) & 1);
+        mbar_wait(b_pfull, j & 1, 3000 + j * 10 + threadIdx.x % 10, prog);  // P_j in smem, O rescaled
+        mbar_wait(b_vfull + 8 * s, (j >> 1) & 1, 400 + j, prog);
         tc_fence_after();
         const uint32_t v_addr = sbase + kOffV + s * kTile;
         for (int ks = 0; ks < kN / 16; ++ks) {
@@ -254,12 +271,13 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
         }
         tc_commit(b_vempty + 8 * s);
         tc_commit(b_ofull);
+        prog[1] = j * 10 + 2;
       };
       for (int j = 0; j < n_kt; ++j) {
         const int s = j & 1;
         // S buffer s is free: softmax(j-2) arrived on pfull before issue_pv(j-2) (iteration
         // j-1) could proceed.  (Re-waiting pfull here could alias a later phase.)
-        mbar_wait(b_kfull + 8 * s, (j >> 1) & 1);
+        mbar_wait(b_kfull + 8 * s, (j >> 1) & 1, 200 + j, prog);
         tc_fence_after();
         const uint32_t k_addr = sbase + kOffK + s * kTile;
         for (int ks = 0; ks < kHD / 16; ++ks) {
@@ -269,6 +287,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
         }
         tc_commit(b_kempty + 8 * s);
         tc_commit(b_sfull + 8 * s);
+        prog[1] = j * 10 + 1;
         if (j >= 1) issue_pv(j - 1);
       }
       issue_pv(n_kt - 1);
@@ -284,7 +303,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
     uint32_t v[32];
     for (int j = 0; j < n_kt; ++j) {
       const int s = j & 1;
-      mbar_wait(b_sfull + 8 * s, (j >> 1) & 1);
+      mbar_wait(b_sfull + 8 * s, (j >> 1) & 1, 500 + j * 1000 + n_kt, prog);
       tc_fence_after();
       const uint32_t ts = t_s0 + s * kN + lane_off;
       // pass 1: masked row max
@@ -300,11 +319,15 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
       }
       // PV_{j-1} must be complete before O is rescaled or P is overwritten
       if (j >= 1) {
-        mbar_wait(b_ofull, (j - 1) & 1);
+        mbar_wait(b_ofull, (j - 1) & 1, 600 + j, prog);
         tc_fence_after();
       }
-      if (mx > m_used + 8.f) {
-        const float alpha = exp2f(m_used - mx);
+      // Lazy rescale: a row only moves its reference max when it grew by > 2^8.  The decision
+      // is made warp-uniform because tcgen05.ld/st are .sync.aligned (rows that do not need it
+      // scale by 1).
+      const bool grow = mx > m_used + 8.f;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? exp2f(m_used - mx) : 1.f;
         if (j >= 1) {
           for (int c = 0; c < 4; ++c) {
             TC_LD32(t_o + lane_off + c * 32, v);
@@ -316,7 +339,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
           tc_wait_st();
         }
         l *= alpha;
-        m_used = mx;
+        if (grow) m_used = mx;
       }
       // pass 2: p = exp2(s - m_used) -> bf16 P tile (row r, 128 keys), row sum
       for (int c = 0; c < 4; ++c) {
@@ -342,9 +365,12 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(b_pfull);
+      if (r == 0) prog[2] = j;
+      if (r == 127) prog[3] = j;
+      if (r == 64) prog[4] = j;
     }
     // epilogue
-    mbar_wait(b_ofull, (n_kt - 1) & 1);
+    mbar_wait(b_ofull, (n_kt - 1) & 1, 700 + n_kt, prog);
     tc_fence_after();
     const int t = tok0 + r / G;
     const float inv = 1.f / l;
