@@ -241,7 +241,9 @@ def main():
 
     for _ in range(args.warmup):
         wl.rotation()
-    eng.set_profiling(1)
+    # per-kernel-category CUDA events on the engine stream during the timed steps (host cost
+    # ~1 us per event record, <1% of a step)
+    eng.set_profiling(2)
     sampler = ClockSampler(local)
     if ws > 1:
         dist.barrier()
@@ -251,6 +253,8 @@ def main():
     ev0.record()
     tokens = computed = cached = calls = chunks = finished = 0
     fwd_ms = 0.0
+    cat_ms = {"attention": 0.0, "kv_append": 0.0, "gemm": 0.0, "elementwise": 0.0}
+    work = {"attn_flops": 0.0, "attn_bytes": 0.0, "append_bytes": 0.0, "linear_flops": 0.0}
     h2d = d2h = 0
     chunk_ms = 0.0
     k1_rotations = 0
@@ -258,6 +262,8 @@ def main():
         r = wl.rotation()
         tm = eng.last_timings()
         fwd_ms += tm["forward"]
+        for k in cat_ms:
+            cat_ms[k] += tm[k]
         chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h) if r.chunks else 0.0
         tokens += r.prompt_tokens
         computed += r.computed_tokens
@@ -267,6 +273,8 @@ def main():
         k1_rotations += 1 if r.chunks else 0
         finished += r.finished
         wk = eng.last_work()
+        for k in work:
+            work[k] += wk[k]
         # host->device per step: packed batch metadata + chunk node ids; device->host: greedy ids
         # + chunk bytes/tokens
         h2d += int(wk["computed_tokens"]) * 16 + r.calls * (16 + 8 * 520) + r.chunks * 4
@@ -278,12 +286,9 @@ def main():
     clocks = sampler.stop()
     wall_ms = ev0.elapsed_time(ev1)
 
-    # roofline of K3 (paged attention) from a per-kernel profiled replay of the last batch
-    eng.set_profiling(2)
-    eng.replay_forward()
-    tm = eng.last_timings()
-    wk = eng.last_work()
     eng.set_profiling(0)
+    tm = dict(cat_ms, forward=fwd_ms)
+    wk = work
 
     vals = torch.tensor([tokens, computed, cached, calls, finished], dtype=torch.float64,
                         device="cuda")
@@ -310,11 +315,13 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": attn_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": attn_gbs / peaks["hbm_gbs"]}
-    roof.update({"kernel": "K3 paged_attn (mma.sync v0)", "traffic": None,
+    roof.update({"kernel": "K3 paged_attn_tc (tcgen05/TMEM/TMA)" if os.environ.get("GLMX_ATTN", "tc") != "mma" else "K3 paged_attn_mma (mma.sync baseline)", "traffic": None,
                  "peak_kind": peak_kind, "intensity_flop_per_byte": intensity,
-                 "kernel_ms_per_forward": attn_ms,
+                 "kernel_ms_total": attn_ms, "kernel_ms_per_step": attn_ms / args.steps,
                  "share_of_forward": attn_ms / max(1e-9, tm["forward"]),
-                 "gemm_ms_per_forward": tm["gemm"],
+                 "gemm_ms_per_step": tm["gemm"] / args.steps,
+                 "elementwise_ms_per_step": tm["elementwise"] / args.steps,
+                 "append_ms_per_step": tm["kv_append"] / args.steps,
                  "gemm_tflops": wk["linear_flops"] / max(1e-9, tm["gemm"] * 1e-3) / 1e12})
     value = tokens / (fwd_ms * 1e-3)
     e2e = tokens / (wall_ms * 1e-3)
