@@ -73,60 +73,87 @@ rmsnorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, in
   }
 }
 
-// One warp per (token, head slot); head slots: H query heads, then Hkv K heads, then Hkv V heads.
-__global__ void rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv,
-                                      const int32_t* __restrict__ pos,
-                                      const int64_t* __restrict__ slot, int T, int H, int Hkv,
-                                      int hd, const float* __restrict__ inv_freq, PoolGeom pool,
-                                      uint32_t layer, __nv_bfloat16* __restrict__ q_out) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int heads = H + 2 * Hkv;
-  if (warp >= T * heads) return;
-  const int t = warp / heads, h = warp % heads;
-  const __nv_bfloat16* src = qkv + (static_cast<int64_t>(t) * heads + h) * hd;
+// One CTA per token: the token's cos/sin table (hd/2 angles, fp32 angle pos*inv_freq then
+// accurate sincosf) is built once in shared memory, then every (head slot, 8-element chunk) is
+// a 16-byte load of each rotate-half partner and 16-byte stores.  Head slots: H query heads
+// (-> q_out), Hkv K heads (roped -> pool page), Hkv V heads (copied -> pool page).
+__global__ void __launch_bounds__(256)
+rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
+                      const int64_t* __restrict__ slot, int T, int H, int Hkv, int hd,
+                      const float* __restrict__ inv_freq, PoolGeom pool, uint32_t layer,
+                      __nv_bfloat16* __restrict__ q_out) {
+  __shared__ float cs_tab[128], sn_tab[128];
+  const int t = blockIdx.x;
   const int half = hd / 2;
   const float p = static_cast<float>(pos[t]);
-  __nv_bfloat16* dst;
-  bool rotate = true;
-  if (h < H) {
-    dst = q_out + (static_cast<int64_t>(t) * H + h) * hd;
-  } else {
-    const int64_t sl = slot[t];
-    const int64_t page = sl / pool.block_tokens;
-    const int off = static_cast<int>(sl % pool.block_tokens);
-    const int kv = h < H + Hkv ? 0 : 1;
-    const int kh = h - H - kv * Hkv;
-    dst = pool.base + pool.tile_off(page, layer, kv, kh) + static_cast<int64_t>(off) * hd;
-    rotate = kv == 0;
-  }
-  for (int i = lane; i < half; i += 32) {
-    float a = __bfloat162float(src[i]), b = __bfloat162float(src[i + half]);
-    if (rotate) {
-      float sn, cs;
-      sincosf(p * inv_freq[i], &sn, &cs);
-      float ra = a * cs - b * sn;
-      float rb = b * cs + a * sn;
-      a = ra;
-      b = rb;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) sincosf(p * inv_freq[i], &sn_tab[i], &cs_tab[i]);
+  __syncthreads();
+  const int heads = H + 2 * Hkv;
+  const int chunks = half / 8;
+  const int64_t sl = slot[t];
+  const int64_t page = sl / pool.block_tokens;
+  const int off = static_cast<int>(sl % pool.block_tokens);
+  for (int w = threadIdx.x; w < heads * chunks; w += blockDim.x) {
+    const int h = w / chunks, c = w % chunks;
+    const __nv_bfloat16* src = qkv + (static_cast<int64_t>(t) * heads + h) * hd + c * 8;
+    __nv_bfloat16* dst;
+    bool rotate = true;
+    if (h < H) {
+      dst = q_out + (static_cast<int64_t>(t) * H + h) * hd + c * 8;
+    } else {
+      const int kv = h < H + Hkv ? 0 : 1;
+      const int kh = h - H - kv * Hkv;
+      dst = pool.base + pool.tile_off(page, layer, kv, kh) + static_cast<int64_t>(off) * hd + c * 8;
+      rotate = kv == 0;
     }
-    dst[i] = __float2bfloat16(a);
-    dst[i + half] = __float2bfloat16(b);
+    const uint4 av = *reinterpret_cast<const uint4*>(src);
+    const uint4 bv = *reinterpret_cast<const uint4*>(src + half);
+    if (!rotate) {
+      *reinterpret_cast<uint4*>(dst) = av;
+      *reinterpret_cast<uint4*>(dst + half) = bv;
+      continue;
+    }
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
+    uint4 ra, rb;
+    __nv_bfloat162* ra2 = reinterpret_cast<__nv_bfloat162*>(&ra);
+    __nv_bfloat162* rb2 = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(a2[k]), b = __bfloat1622float2(b2[k]);
+      const int i = c * 8 + 2 * k;
+      const float c0 = cs_tab[i], s0 = sn_tab[i], c1 = cs_tab[i + 1], s1 = sn_tab[i + 1];
+      ra2[k] = __floats2bfloat162_rn(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
+      rb2[k] = __floats2bfloat162_rn(b.x * c0 + a.x * s0, b.y * c1 + a.y * s1);
+    }
+    *reinterpret_cast<uint4*>(dst) = ra;
+    *reinterpret_cast<uint4*>(dst + half) = rb;
   }
 }
 
-__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ff,
-                              __nv_bfloat16* __restrict__ out) {
-  const int64_t n = static_cast<int64_t>(T) * ff / 2;  // bf16x2 pairs
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = (2 * i) / ff, c = (2 * i) % ff;
-    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(gu + t * 2 * ff + c);
-    const __nv_bfloat162 u = *reinterpret_cast<const __nv_bfloat162*>(gu + t * 2 * ff + ff + c);
-    float2 gf = __bfloat1622float2(g), uf = __bfloat1622float2(u);
-    float a = gf.x / (1.f + __expf(-gf.x)) * uf.x;
-    float b = gf.y / (1.f + __expf(-gf.y)) * uf.y;
-    *reinterpret_cast<__nv_bfloat162*>(out + t * ff + c) = __floats2bfloat162_rn(a, b);
+// 8 outputs per thread: two 16-byte loads (gate, up), one 16-byte store; the 64-bit integer
+// divide is hoisted by iterating rows in the grid's y dimension.
+__global__ void __launch_bounds__(256)
+swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ff, __nv_bfloat16* __restrict__ out) {
+  const int vec_per_row = ff / 8;
+  for (int t = blockIdx.y; t < T; t += gridDim.y) {
+    const uint4* g4 = reinterpret_cast<const uint4*>(gu + static_cast<int64_t>(t) * 2 * ff);
+    const uint4* u4 = g4 + vec_per_row;
+    uint4* o4 = reinterpret_cast<uint4*>(out + static_cast<int64_t>(t) * ff);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < vec_per_row; i += gridDim.x * blockDim.x) {
+      const uint4 gv = g4[i], uv = u4[i];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+      uint4 ov;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&ov);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 gf = __bfloat1622float2(g2[k]), uf = __bfloat1622float2(u2[k]);
+        o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
+                                      gf.y / (1.f + __expf(-gf.y)) * uf.y);
+      }
+      o4[i] = ov;
+    }
   }
 }
 
@@ -239,15 +266,18 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
                     int H, int Hkv, int hd, const float* inv_freq, const PoolGeom& pool,
                     uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s) {
   if (T <= 0) return;
-  const int64_t warps = static_cast<int64_t>(T) * (H + 2 * Hkv);
-  rope_kv_append_kernel<<<static_cast<int>(ceil_div(warps * 32, 256)), 256, 0, s>>>(
-      qkv, pos, slot, T, H, Hkv, hd, inv_freq, pool, layer, q_out);
+  if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
+  rope_kv_append_kernel<<<T, 256, 0, s>>>(qkv, pos, slot, T, H, Hkv, hd, inv_freq, pool, layer,
+                                          q_out);
   GLMX_CHECK_LAUNCH();
 }
 
 void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStream_t s) {
   if (T <= 0) return;
-  swiglu_kernel<<<grid_for(static_cast<uint64_t>(T) * ff / 2, 256), 256, 0, s>>>(gu, T, ff, out);
+  if (ff % 8) throw Error(GLMX_ERR_ARG, "d_ff must be a multiple of 8");
+  const int xb = static_cast<int>(ceil_div(ff / 8, 256));
+  dim3 grid(xb, std::min(T, 65535));
+  swiglu_kernel<<<grid, 256, 0, s>>>(gu, T, ff, out);
   GLMX_CHECK_LAUNCH();
 }
 
