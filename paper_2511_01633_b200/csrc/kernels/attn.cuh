@@ -34,6 +34,8 @@ namespace glmx {
 // tcgen05 / TMEM / TMA version (attn_tc.cu): 128 query rows per CTA.
 int attn_tc_tokens_per_tile(int H, int Hkv);
 void make_pool_tensor_map(const PoolGeom& g, uint64_t pages, void* out_map, uint32_t* rows_total);
+void make_q_tensor_map(const void* q, uint64_t T, int H, int Hkv, void* out_map);
+// Persistent launch: min(n_work * Hkv, 148) CTAs walk the work list.
 void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
-                        cudaStream_t s);
+                        const void* q_map, cudaStream_t s);
 }  // namespace glmx

@@ -1,14 +1,20 @@
 // K3 — paged causal GQA prefill attention on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-// CTA = one kv head x 128 query rows (128/G tokens x the G query heads sharing that kv head, so
-// every K/V page is fetched once per GQA group).  Warp roles (192 threads):
+// Persistent kernel: one CTA per SM walks a static slice of the work items (request, 128-row
+// query tile, kv head) — items are sorted longest-first on the host.  An item's 128 query rows
+// are 128/G tokens x the G query heads that share the kv head, so every K/V page is fetched once
+// per GQA group.  The pipeline runs across item boundaries:
 //   warps 0-3  softmax / correction / epilogue: thread i owns query row i == TMEM lane i
-//   warp 4     TMA producer: K and V pages of 128-key tiles -> 2-stage smem ring (16 boxes of
-//              [16 tokens][64 dims] per operand per tile, 128B-swizzled, OOB pages zero-filled)
-//   warp 5     MMA issuer (one elected thread):  S_j = Q K_j^T  (M128 N128 K128, fp32 in TMEM,
-//              double-buffered)  and  O += P_{j-1} V_{j-1}  (P from smem, V MN-major)
-// Online softmax in base 2 with a lazily updated running max (O in TMEM is only rescaled when
-// the row max grows by more than 2^8), final 1/l normalisation in the epilogue.
+//   warp 4     TMA producer: the item's Q tile (3-D map over q [T][H][hd]) and the K and V pages
+//              of each 128-key tile (2-D map over the pool, 16 boxes of [16 tok][64 dims] per
+//              operand, 128B swizzle, pages past the context are out-of-bounds -> zero fill)
+//              into a 2-stage smem ring
+//   warp 5     MMA issuer (one thread): S_g = Q K_g^T (M128 N128 K128 fp32, TMEM double-buffered)
+//              and O += P_{g-1} V_{g-1} (P from smem, V MN-major; O double-buffered per item so an
+//              item's epilogue overlaps the next item's MMAs)
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  Online softmax in base 2, single
+// pass over TMEM, lazily updated reference max (O rescaled only when a row max grows by > 2^8,
+// decided warp-uniformly), 1/l normalisation in the epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -23,9 +29,9 @@ namespace {
 
 constexpr int kHD = 128;
 constexpr int kB = 16;
-constexpr int kM = 128;        // query rows per CTA
-constexpr int kN = 128;        // keys per tile
-constexpr int kHalf = 16384;   // bytes of one [128][64] bf16 SW128 half tile
+constexpr int kM = 128;       // query rows per item
+constexpr int kN = 128;       // keys per tile
+constexpr int kHalf = 16384;  // bytes of one [128][64] bf16 SW128 half tile
 constexpr int kTile = 2 * kHalf;
 constexpr int kThreads = 192;
 // smem map (1024-aligned): Q | K0 K1 | V0 V1 | P | barriers
@@ -63,26 +69,24 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a protocol bug traps with a location instead of hanging the GPU.  Roles record
-// their progress in shared memory (g_prog) so a stuck thread reports every role's state.
 __device__ __forceinline__ uint64_t gtime() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity, int tag, const volatile int* prog) {
-  printf("paged_attn_tc: wait timeout block (%d,%d) thread %d bar 0x%x parity %u tag %d | prod %d mma %d sm0 %d sm127 %d sm64 %d\n",
-         blockIdx.x, blockIdx.y, threadIdx.x, bar, parity, tag, prog[0], prog[1], prog[2], prog[3], prog[4]);
+// Bounded wait: a protocol bug reports its location and traps instead of hanging the GPU.
+__device__ __noinline__ void mbar_stuck(uint32_t bar, uint32_t parity, int tag) {
+  printf("paged_attn_tc: wait timeout block %d thread %d bar 0x%x parity %u tag %d\n", blockIdx.x,
+         threadIdx.x, bar, parity, tag);
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0,
-                                          const volatile int* prog = nullptr) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag) {
   if (mbar_try(bar, parity)) return;
   const uint64_t t0 = gtime();
   bool told = false;
   while (!mbar_try(bar, parity)) {
     const uint64_t dt = gtime() - t0;
     if (!told && dt > 2000000000ull) {
-      if (prog) mbar_stuck(bar, parity, tag, prog);
+      mbar_stuck(bar, parity, tag);
       told = true;
     }
     if (dt > 4000000000ull) __trap();
@@ -94,6 +98,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
       "%3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
@@ -162,34 +174,46 @@ __device__ __forceinline__ uint32_t sw128(int r, int c16) {
 struct TcParams {
   AttnParams a;
   uint32_t rows_total;  // rows of the pool tensor map (OOB row -> zero fill)
+  int n_items;          // n_work * Hkv
 };
 
+struct Item {
+  int req, tok0, kvh, qlen, ctx, qs, n_kt;
+};
+
+__device__ __forceinline__ Item item_of(const AttnParams& p, int w) {
+  Item it;
+  const int2 wk = p.work[w / p.Hkv];
+  it.req = wk.x;
+  it.tok0 = wk.y;
+  it.kvh = w % p.Hkv;
+  it.qlen = p.q_len[it.req];
+  it.ctx = p.ctx_len[it.req];
+  it.qs = p.q_start[it.req];
+  const int G = p.H / p.Hkv;
+  const int max_pos = it.ctx - it.qlen + min(it.tok0 + kM / G, it.qlen) - 1;
+  it.n_kt = max_pos / kN + 1;
+  return it;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
+paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
+                     const __grid_constant__ CUtensorMap q_map, TcParams tp) {
   const AttnParams& p = tp.a;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_addr(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  // barriers: kfull[2] vfull[2] kempty[2] vempty[2] sfull[2] pfull ofull
+  // barriers (8 B each)
   const uint32_t b_kfull = smem_addr(bars + 0), b_vfull = smem_addr(bars + 2);
   const uint32_t b_kempty = smem_addr(bars + 4), b_vempty = smem_addr(bars + 6);
   const uint32_t b_sfull = smem_addr(bars + 8), b_pfull = smem_addr(bars + 10);
-  const uint32_t b_ofull = smem_addr(bars + 11);
+  const uint32_t b_pvdone = smem_addr(bars + 11), b_qfull = smem_addr(bars + 12);
+  const uint32_t b_qempty = smem_addr(bars + 13), b_ofree = smem_addr(bars + 14);  // ofree[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
-  volatile int* prog = reinterpret_cast<volatile int*>(bars + 20);  // debug progress
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kvh = blockIdx.y;
-  const int2 wk = p.work[blockIdx.x];
-  const int req = wk.x, tok0 = wk.y;
   const int G = p.H / p.Hkv;
-  const int TPT = kM / G;
-  const int qlen = p.q_len[req], ctx = p.ctx_len[req], qs = p.q_start[req];
-  const int base_pos = ctx - qlen;
-  const int max_pos = base_pos + min(tok0 + TPT, qlen) - 1;
-  const int n_kt = max_pos / kN + 1;
-  const int32_t* bt = p.block_table + static_cast<int64_t>(req) * p.bt_stride;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -198,10 +222,12 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
       mbar_init(b_kempty + 8 * s, 1);
       mbar_init(b_vempty + 8 * s, 1);
       mbar_init(b_sfull + 8 * s, 1);
+      mbar_init(b_ofree + 8 * s, 128);
     }
     mbar_init(b_pfull, 128);
-    mbar_init(b_ofull, 1);
-    for (int i = 0; i < 5; ++i) prog[i] = -1;
+    mbar_init(b_pvdone, 1);
+    mbar_init(b_qfull, 1);
+    mbar_init(b_qempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -209,46 +235,43 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
         smem_addr(tmem_holder)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // Q tile -> smem (rows m: token m/G, head kvh*G + m%G), 128B swizzle, by the softmax warps
-  if (warp < 4) {
-    for (int i = threadIdx.x; i < kM * 16; i += 128) {
-      const int m = i >> 4, c = i & 15;
-      const int t = min(tok0 + m / G, qlen - 1);
-      const int h = kvh * G + m % G;
-      const uint4 v = *reinterpret_cast<const uint4*>(p.q + (static_cast<int64_t>(qs + t) * p.H + h) * kHD + c * 8);
-      *reinterpret_cast<uint4*>(smem + kOffQ + sw128(m, c)) = v;
-    }
-    fence_async_smem();
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const uint32_t t_s0 = tmem, t_o = tmem + 256;
+  const uint32_t t_s0 = tmem, t_o0 = tmem + 256;
 
   if (warp == 4) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       const uint32_t L = p.pool.n_layers, Hkv = p.pool.n_kv_heads;
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        for (int kv = 0; kv < 2; ++kv) {
-          const uint32_t full = (kv ? b_vfull : b_kfull) + 8 * s;
-          if (j >= 2) mbar_wait((kv ? b_vempty : b_kempty) + 8 * s, ph ^ 1, 100 + j * 10 + kv, prog);
-          mbar_expect_tx(full, kTile);
-          const uint32_t dst = sbase + (kv ? kOffV : kOffK) + s * kTile;
-          for (int pg = 0; pg < kN / kB; ++pg) {
-            const int key0 = j * kN + pg * kB;
-            uint32_t row = tp.rows_total;  // out of bounds -> zeros
-            if (key0 < ctx) {
-              const uint32_t page = static_cast<uint32_t>(bt[key0 / kB]);
-              row = (((page * L + p.layer) * 2 + kv) * Hkv + kvh) * kB;
+      int g = 0, it_local = 0;
+      for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
+        const Item it = item_of(p, w);
+        const int32_t* bt = p.block_table + static_cast<int64_t>(it.req) * p.bt_stride;
+        if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // last S of prev item done
+        mbar_expect_tx(b_qfull, kTile);
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_3d(sbase + kOffQ + hf * kHalf, &q_map, hf * 64, it.kvh * G, it.qs + it.tok0, b_qfull);
+        for (int j = 0; j < it.n_kt; ++j, ++g) {
+          const int s = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          for (int kv = 0; kv < 2; ++kv) {
+            const uint32_t full = (kv ? b_vfull : b_kfull) + 8 * s;
+            if (g >= 2) mbar_wait((kv ? b_vempty : b_kempty) + 8 * s, ph ^ 1, 2 + kv);
+            mbar_expect_tx(full, kTile);
+            const uint32_t dst = sbase + (kv ? kOffV : kOffK) + s * kTile;
+            for (int pg = 0; pg < kN / kB; ++pg) {
+              const int key0 = j * kN + pg * kB;
+              uint32_t row = tp.rows_total;  // out of bounds -> zeros
+              if (key0 < it.ctx) {
+                const uint32_t page = static_cast<uint32_t>(bt[key0 / kB]);
+                row = (((page * L + p.layer) * 2 + kv) * Hkv + it.kvh) * kB;
+              }
+              for (int hf = 0; hf < 2; ++hf)
+                tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
             }
-            for (int hf = 0; hf < 2; ++hf)
-              tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
           }
-          prog[0] = j * 10 + kv;
         }
       }
     }
@@ -258,137 +281,149 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, TcParams tp) {
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(kN, false), idO = idesc_bf16(kHD, true);
       const uint32_t q_addr = sbase + kOffQ, p_addr = sbase + kOffP;
-      auto issue_pv = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(b_pfull, j & 1, 3000 + j * 10 + threadIdx.x % 10, prog);  // P_j in smem, O rescaled
-        mbar_wait(b_vfull + 8 * s, (j >> 1) & 1, 400 + j, prog);
+      // PV of global tile gp (item-local index jp, O buffer ob)
+      auto issue_pv = [&](int gp, int jp, int ob) {
+        const int s = gp & 1;
+        mbar_wait(b_pfull, gp & 1, 10);  // P_gp in smem, O rescaled
+        mbar_wait(b_vfull + 8 * s, (gp >> 1) & 1, 11);
         tc_fence_after();
         const uint32_t v_addr = sbase + kOffV + s * kTile;
         for (int ks = 0; ks < kN / 16; ++ks) {
           const uint64_t a = smem_desc(p_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
           const uint64_t b = smem_desc(v_addr + ks * 2048, kHalf >> 4, 64);
-          tc_mma(t_o, a, b, idO, (j > 0 || ks > 0) ? 1u : 0u);
+          tc_mma(t_o0 + ob * kHD, a, b, idO, (jp > 0 || ks > 0) ? 1u : 0u);
         }
         tc_commit(b_vempty + 8 * s);
-        tc_commit(b_ofull);
-        prog[1] = j * 10 + 2;
+        tc_commit(b_pvdone);
       };
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        // S buffer s is free: softmax(j-2) arrived on pfull before issue_pv(j-2) (iteration
-        // j-1) could proceed.  (Re-waiting pfull here could alias a later phase.)
-        mbar_wait(b_kfull + 8 * s, (j >> 1) & 1, 200 + j, prog);
-        tc_fence_after();
-        const uint32_t k_addr = sbase + kOffK + s * kTile;
-        for (int ks = 0; ks < kHD / 16; ++ks) {
-          const uint64_t a = smem_desc(q_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
-          const uint64_t b = smem_desc(k_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
-          tc_mma(t_s0 + s * kN, a, b, idS, ks > 0 ? 1u : 0u);
+      int g = 0, it_local = 0;
+      int pend_g = -1, pend_j = 0, pend_ob = 0;  // PV waiting to be issued
+      for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
+        const Item it = item_of(p, w);
+        const int ob = it_local & 1;
+        mbar_wait(b_qfull, it_local & 1, 12);
+        for (int j = 0; j < it.n_kt; ++j, ++g) {
+          const int s = g & 1;
+          mbar_wait(b_kfull + 8 * s, (g >> 1) & 1, 13);
+          tc_fence_after();
+          const uint32_t k_addr = sbase + kOffK + s * kTile;
+          for (int ks = 0; ks < kHD / 16; ++ks) {
+            const uint64_t a = smem_desc(q_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
+            const uint64_t b = smem_desc(k_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
+            tc_mma(t_s0 + s * kN, a, b, idS, ks > 0 ? 1u : 0u);
+          }
+          tc_commit(b_kempty + 8 * s);
+          tc_commit(b_sfull + 8 * s);
+          if (j == it.n_kt - 1) tc_commit(b_qempty);
+          if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob);
+          // before the first PV into O[ob], the epilogue of item it_local-2 must be done
+          if (j == 0 && it_local >= 2) mbar_wait(b_ofree + 8 * ob, ((it_local >> 1) - 1) & 1, 14);
+          pend_g = g;
+          pend_j = j;
+          pend_ob = ob;
         }
-        tc_commit(b_kempty + 8 * s);
-        tc_commit(b_sfull + 8 * s);
-        prog[1] = j * 10 + 1;
-        if (j >= 1) issue_pv(j - 1);
       }
-      issue_pv(n_kt - 1);
+      if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob);
     }
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- softmax warps
     const int r = threadIdx.x;  // query row == TMEM lane
-    const int tq = min(tok0 + r / G, qlen - 1);
-    const int pos = base_pos + tq;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    float m_used = -FLT_MAX, l = 0.f;
-    uint32_t v[32];
-    for (int j = 0; j < n_kt; ++j) {
-      const int s = j & 1;
-      mbar_wait(b_sfull + 8 * s, (j >> 1) & 1, 500 + j * 1000 + n_kt, prog);
-      tc_fence_after();
-      const uint32_t ts = t_s0 + s * kN + lane_off;
-      // pass 1: masked row max
-      float mx = -FLT_MAX;
-      for (int c = 0; c < 4; ++c) {
-        TC_LD32(ts + c * 32, v);
-        tc_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = j * kN + c * 32 + i;
-          if (key <= pos) mx = fmaxf(mx, __uint_as_float(v[i]) * p.scale_log2);
-        }
-      }
-      // PV_{j-1} must be complete before O is rescaled or P is overwritten
-      if (j >= 1) {
-        mbar_wait(b_ofull, (j - 1) & 1, 600 + j, prog);
+    uint32_t v[kN];
+    int g = 0, it_local = 0;
+    for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
+      const Item it = item_of(p, w);
+      const int ob = it_local & 1;
+      const uint32_t t_o = t_o0 + ob * kHD + lane_off;
+      const int tq = min(it.tok0 + r / G, it.qlen - 1);
+      const int pos = it.ctx - it.qlen + tq;
+      float m_used = -FLT_MAX, l = 0.f;
+      for (int j = 0; j < it.n_kt; ++j, ++g) {
+        const int s = g & 1;
+        mbar_wait(b_sfull + 8 * s, (g >> 1) & 1, 20);
         tc_fence_after();
-      }
-      // Lazy rescale: a row only moves its reference max when it grew by > 2^8.  The decision
-      // is made warp-uniform because tcgen05.ld/st are .sync.aligned (rows that do not need it
-      // scale by 1).
-      const bool grow = mx > m_used + 8.f;
-      if (__any_sync(0xffffffffu, grow)) {
-        const float alpha = grow ? exp2f(m_used - mx) : 1.f;
-        if (j >= 1) {
-          for (int c = 0; c < 4; ++c) {
-            TC_LD32(t_o + lane_off + c * 32, v);
-            tc_wait_ld();
+        const uint32_t ts = t_s0 + s * kN + lane_off;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            TC_ST32(t_o + lane_off + c * 32, v);
-          }
-          tc_wait_st();
-        }
-        l *= alpha;
-        if (grow) m_used = mx;
-      }
-      // pass 2: p = exp2(s - m_used) -> bf16 P tile (row r, 128 keys), row sum
-      for (int c = 0; c < 4; ++c) {
-        TC_LD32(ts + c * 32, v);
+        for (int c = 0; c < 4; ++c) TC_LD32(ts + c * 32, (v + c * 32));
         tc_wait_ld();
-        uint32_t pk[16];
+        const int kbase = j * kN;
+        float mx = -FLT_MAX;
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const int key = j * kN + c * 32 + i;
-          const float p0 = key <= pos ? exp2f(__uint_as_float(v[i]) * p.scale_log2 - m_used) : 0.f;
-          const float p1 = key + 1 <= pos ? exp2f(__uint_as_float(v[i + 1]) * p.scale_log2 - m_used) : 0.f;
-          l += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+        for (int i = 0; i < kN; ++i) {
+          const float x = __uint_as_float(v[i]) * p.scale_log2;
+          v[i] = __float_as_uint(kbase + i <= pos ? x : -FLT_MAX);
+          mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
+        // PV of the previous tile (any item) must be complete before P is overwritten / O
+        // rescaled
+        if (g >= 1) {
+          mbar_wait(b_pvdone, (g - 1) & 1, 21);
+          tc_fence_after();
+        }
+        const bool grow = mx > m_used + 8.f;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? exp2f(m_used - mx) : 1.f;
+          if (j >= 1) {
+            uint32_t o[32];
+            for (int c = 0; c < 4; ++c) {
+              TC_LD32(t_o + c * 32, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              TC_ST32(t_o + c * 32, o);
+            }
+            tc_wait_st();
+          }
+          l *= alpha;
+          if (grow) m_used = mx;
         }
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int c16 = c * 4 + q4;
-          *reinterpret_cast<uint4*>(smem + kOffP + sw128(r, c16)) =
-              make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+        for (int c16 = 0; c16 < kN / 8; ++c16) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = c16 * 8 + 2 * q;
+            const float x0 = __uint_as_float(v[i]), x1 = __uint_as_float(v[i + 1]);
+            const float p0 = x0 == -FLT_MAX ? 0.f : exp2f(x0 - m_used);
+            const float p1 = x1 == -FLT_MAX ? 0.f : exp2f(x1 - m_used);
+            l += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            pk[q] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          *reinterpret_cast<uint4*>(smem + kOffP + sw128(r, c16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(b_pfull);
+      }
+      // epilogue of this item: wait for its last PV (global tile g-1)
+      mbar_wait(b_pvdone, (g - 1) & 1, 22);
+      tc_fence_after();
+      const int t = it.tok0 + r / G;
+      const float inv = 1.f / l;
+      __nv_bfloat16* dst = p.o + (static_cast<int64_t>(it.qs + tq) * p.H + it.kvh * G + r % G) * kHD;
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        TC_LD32(t_o + c * 32, o);
+        tc_wait_ld();
+        if (t < it.qlen) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = q4 * 8 + 2 * k;
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+              pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            d4[q4] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
         }
       }
-      fence_async_smem();
       tc_fence_before();
-      mbar_arrive(b_pfull);
-      if (r == 0) prog[2] = j;
-      if (r == 127) prog[3] = j;
-      if (r == 64) prog[4] = j;
-    }
-    // epilogue
-    mbar_wait(b_ofull, (n_kt - 1) & 1, 700 + n_kt, prog);
-    tc_fence_after();
-    const int t = tok0 + r / G;
-    const float inv = 1.f / l;
-    __nv_bfloat16* dst = p.o + (static_cast<int64_t>(qs + tq) * p.H + kvh * G + r % G) * kHD;
-    for (int c = 0; c < 4; ++c) {
-      TC_LD32(t_o + lane_off + c * 32, v);
-      tc_wait_ld();
-      if (t < qlen) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
-          pk[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) d4[q4] = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
-      }
+      mbar_arrive(b_ofree + 8 * ob);
     }
   }
   tc_fence_before();
@@ -430,7 +465,23 @@ void make_pool_tensor_map(const PoolGeom& g, uint64_t pages, void* out_map, uint
   *rows_total = static_cast<uint32_t>(rows);
 }
 
-void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total, cudaStream_t s) {
+// Tensor map over the query buffer q [T][H][hd]: box [128/G tokens][G heads][64 dims] lands as
+// the item's 128 rows (row = token * G + head-in-group), 128B swizzle; tokens >= T read zeros.
+void make_q_tensor_map(const void* q, uint64_t T, int H, int Hkv, void* out_map) {
+  const int G = H / Hkv;
+  cuuint64_t dims[3] = {kHD, static_cast<cuuint64_t>(H), T};
+  cuuint64_t strides[2] = {kHD * sizeof(__nv_bfloat16), static_cast<cuuint64_t>(H) * kHD * sizeof(__nv_bfloat16)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(kM / G)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(reinterpret_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                           const_cast<void*>(q), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(GLMX_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed: " + std::to_string(r));
+}
+
+void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
+                        const void* q_map, cudaStream_t s) {
   if (p.n_work <= 0) return;
   if (p.pool.head_dim != kHD || p.pool.block_tokens != kB)
     throw Error(GLMX_ERR_ARG, "paged attention is built for head_dim 128 and 16-token pages");
@@ -441,9 +492,10 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
     GLMX_CUDA(cudaFuncSetAttribute(paged_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  TcParams tp{p, rows_total};
-  dim3 grid(p.n_work, p.Hkv);
-  paged_attn_tc_kernel<<<grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map), tp);
+  TcParams tp{p, rows_total, p.n_work * p.Hkv};
+  const int grid = std::min(tp.n_items, kNumSMs);
+  paged_attn_tc_kernel<<<grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
+                                                     *reinterpret_cast<const CUtensorMap*>(q_map), tp);
   GLMX_CHECK_LAUNCH();
 }
 

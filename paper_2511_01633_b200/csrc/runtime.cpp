@@ -400,6 +400,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->h.reserve(T * d * 2);
   e->qkv.reserve(T * (H + 2 * Hkv) * hd * 2);
   e->q.reserve(T * H * hd * 2);
+  make_q_tensor_map(e->q.p, T, static_cast<int>(H), static_cast<int>(Hkv), e->q_map);
   e->attn.reserve(T * H * hd * 2);
   e->gu.reserve(T * 2 * ff * 2);
   e->act.reserve(T * ff * 2);
@@ -479,7 +480,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
       if (e->attn_impl)
         paged_attention(ap, s);
       else
-        paged_attention_tc(ap, e->kv_map, e->kv_rows, s);
+        paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, s);
     }
     {
       Prof p(e, kCatGemm);

@@ -87,6 +87,7 @@ struct glmx_engine {
   int tpt = 0;  // attention tokens per tile
   int attn_impl = 0;  // 0 = tcgen05 (attn_tc.cu), 1 = mma.sync baseline (dev A/B only)
   alignas(64) uint8_t kv_map[128];  // CUtensorMap over the KV pool (TMA)
+  alignas(64) uint8_t q_map[128];   // CUtensorMap over the q activation buffer
   uint32_t kv_rows = 0;
 
   // activations
