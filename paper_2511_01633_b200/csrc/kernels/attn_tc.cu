@@ -38,8 +38,7 @@ constexpr int kThreads = 192;
 constexpr int kOffQ = 0;
 constexpr int kOffK = kOffQ + kTile;
 constexpr int kOffV = kOffK + 2 * kTile;
-constexpr int kOffP = kOffV + 2 * kTile;
-constexpr int kOffBar = kOffP + kTile;
+constexpr int kOffBar = kOffV + 2 * kTile;  // P lives in TMEM (aliasing its S tile)
 constexpr int kSmem = kOffBar + 256 + 1024;  // + alignment slack
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -83,14 +82,34 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
   if (mbar_try(bar, parity)) return;
   const uint64_t t0 = gtime();
   bool told = false;
-  while (!mbar_try(bar, parity)) {
-    const uint64_t dt = gtime() - t0;
-    if (!told && dt > 2000000000ull) {
-      mbar_stuck(bar, parity, tag);
-      told = true;
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(bar, parity)) return;
+    if ((n & 255) == 0) {  // the timer is read rarely: waits stay cheap in the steady state
+      const uint64_t dt = gtime() - t0;
+      if (!told && dt > 2000000000ull) {
+        mbar_stuck(bar, parity, tag);
+        told = true;
+      }
+      if (dt > 4000000000ull) __trap();
     }
-    if (dt > 4000000000ull) __trap();
   }
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// O += P V with the A operand (P, bf16, [128 rows][K]) read from TMEM.
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint32_t bar) {
@@ -210,6 +229,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   const uint32_t b_sfull = smem_addr(bars + 8), b_pfull = smem_addr(bars + 10);
   const uint32_t b_pvdone = smem_addr(bars + 11), b_qfull = smem_addr(bars + 12);
   const uint32_t b_qempty = smem_addr(bars + 13), b_ofree = smem_addr(bars + 14);  // ofree[2]
+  const uint32_t b_ofull = smem_addr(bars + 17);                                   // ofull[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -223,6 +243,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       mbar_init(b_vempty + 8 * s, 1);
       mbar_init(b_sfull + 8 * s, 1);
       mbar_init(b_ofree + 8 * s, 128);
+      mbar_init(b_ofull + 8 * s, 1);
     }
     mbar_init(b_pfull, 128);
     mbar_init(b_pvdone, 1);
@@ -280,24 +301,28 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(kN, false), idO = idesc_bf16(kHD, true);
-      const uint32_t q_addr = sbase + kOffQ, p_addr = sbase + kOffP;
-      // PV of global tile gp (item-local index jp, O buffer ob)
-      auto issue_pv = [&](int gp, int jp, int ob) {
+      const uint32_t q_addr = sbase + kOffQ;
+      // PV of global tile gp (item-local index jp, O buffer ob).  A = P_gp, bf16 packed in the
+      // first 64 TMEM columns of its S buffer (8 columns per 16-key k-step); B = V (MN-major).
+      // tcgen05.mma executes in issue order, so S_{gp+2} (issued later into the same buffer)
+      // cannot overwrite P_gp before this PV has consumed it.
+      auto issue_pv = [&](int gp, int jp, int ob, bool last) {
         const int s = gp & 1;
-        mbar_wait(b_pfull, gp & 1, 10);  // P_gp in smem, O rescaled
+        mbar_wait(b_pfull, gp & 1, 10);  // P_gp in TMEM (and O rescaled if needed)
         mbar_wait(b_vfull + 8 * s, (gp >> 1) & 1, 11);
         tc_fence_after();
         const uint32_t v_addr = sbase + kOffV + s * kTile;
         for (int ks = 0; ks < kN / 16; ++ks) {
-          const uint64_t a = smem_desc(p_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
           const uint64_t b = smem_desc(v_addr + ks * 2048, kHalf >> 4, 64);
-          tc_mma(t_o0 + ob * kHD, a, b, idO, (jp > 0 || ks > 0) ? 1u : 0u);
+          tc_mma_ts(t_o0 + ob * kHD, t_s0 + s * kN + ks * 8, b, idO, (jp > 0 || ks > 0) ? 1u : 0u);
         }
         tc_commit(b_vempty + 8 * s);
         tc_commit(b_pvdone);
+        if (last) tc_commit(b_ofull + 8 * ob);
       };
       int g = 0, it_local = 0;
       int pend_g = -1, pend_j = 0, pend_ob = 0;  // PV waiting to be issued
+      bool pend_last = false;
       for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
         const Item it = item_of(p, w);
         const int ob = it_local & 1;
@@ -315,15 +340,16 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           tc_commit(b_kempty + 8 * s);
           tc_commit(b_sfull + 8 * s);
           if (j == it.n_kt - 1) tc_commit(b_qempty);
-          if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob);
+          if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob, pend_last);
           // before the first PV into O[ob], the epilogue of item it_local-2 must be done
           if (j == 0 && it_local >= 2) mbar_wait(b_ofree + 8 * ob, ((it_local >> 1) - 1) & 1, 14);
           pend_g = g;
           pend_j = j;
           pend_ob = ob;
+          pend_last = j == it.n_kt - 1;
         }
       }
-      if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob);
+      if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob, pend_last);
     }
     __syncwarp();
   } else {
@@ -338,7 +364,8 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       const uint32_t t_o = t_o0 + ob * kHD + lane_off;
       const int tq = min(it.tok0 + r / G, it.qlen - 1);
       const int pos = it.ctx - it.qlen + tq;
-      float m_used = -FLT_MAX, l = 0.f;
+      const int pos_lo = it.ctx - it.qlen + it.tok0;  // smallest position among the item's rows
+      float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < it.n_kt; ++j, ++g) {
         const int s = g & 1;
         mbar_wait(b_sfull + 8 * s, (g >> 1) & 1, 20);
@@ -348,23 +375,31 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         for (int c = 0; c < 4; ++c) TC_LD32(ts + c * 32, (v + c * 32));
         tc_wait_ld();
         const int kbase = j * kN;
-        float mx = -FLT_MAX;
+        float mx = -INFINITY;
+        if (kbase + kN - 1 <= pos_lo) {  // tile fully visible to every row: no mask
 #pragma unroll
-        for (int i = 0; i < kN; ++i) {
-          const float x = __uint_as_float(v[i]) * p.scale_log2;
-          v[i] = __float_as_uint(kbase + i <= pos ? x : -FLT_MAX);
-          mx = fmaxf(mx, __uint_as_float(v[i]));
-        }
-        // PV of the previous tile (any item) must be complete before P is overwritten / O
-        // rescaled
-        if (g >= 1) {
-          mbar_wait(b_pvdone, (g - 1) & 1, 21);
-          tc_fence_after();
+          for (int i = 0; i < kN; ++i) {
+            const float x = __uint_as_float(v[i]) * p.scale_log2;
+            v[i] = __float_as_uint(x);
+            mx = fmaxf(mx, x);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kN; ++i) {
+            const float x = kbase + i <= pos ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
+            v[i] = __float_as_uint(x);
+            mx = fmaxf(mx, x);
+          }
         }
         const bool grow = mx > m_used + 8.f;
         if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? exp2f(m_used - mx) : 1.f;
+          const float alpha = grow ? ex2(m_used - mx) : 1.f;
           if (j >= 1) {
+            // O may only be rescaled once PV_{g-1} (the last one issued into it) completed.
+            // Here S_g is complete, hence PV_{g-2} too, and PV_g is not issued: the pvdone
+            // barrier has completed g-1 or g phases, so the parity wait is unambiguous.
+            mbar_wait(b_pvdone, (g - 1) & 1, 21);
+            tc_fence_after();
             uint32_t o[32];
             for (int c = 0; c < 4; ++c) {
               TC_LD32(t_o + c * 32, o);
@@ -378,27 +413,26 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           l *= alpha;
           if (grow) m_used = mx;
         }
+        // P = 2^(x - m_used) as bf16 pairs into the first 64 columns of this S buffer (the S
+        // values were already copied to registers); masked keys are -inf -> 0.
+        float lsum = 0.f;
 #pragma unroll
-        for (int c16 = 0; c16 < kN / 8; ++c16) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int i = c16 * 8 + 2 * q;
-            const float x0 = __uint_as_float(v[i]), x1 = __uint_as_float(v[i + 1]);
-            const float p0 = x0 == -FLT_MAX ? 0.f : exp2f(x0 - m_used);
-            const float p1 = x1 == -FLT_MAX ? 0.f : exp2f(x1 - m_used);
-            l += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            pk[q] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          *reinterpret_cast<uint4*>(smem + kOffP + sw128(r, c16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        for (int i = 0; i < kN; i += 2) {
+          const float p0 = ex2(__uint_as_float(v[i]) - m_used);
+          const float p1 = ex2(__uint_as_float(v[i + 1]) - m_used);
+          lsum += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          v[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        fence_async_smem();
+        l += lsum;
+        TC_ST32(ts, v);
+        TC_ST32(ts + 32, (v + 32));
+        tc_wait_st();
         tc_fence_before();
         mbar_arrive(b_pfull);
       }
-      // epilogue of this item: wait for its last PV (global tile g-1)
-      mbar_wait(b_pvdone, (g - 1) & 1, 22);
+      // epilogue of this item: wait for its last PV (one ofull phase per item and O buffer)
+      mbar_wait(b_ofull + 8 * ob, (it_local >> 1) & 1, 22);
       tc_fence_after();
       const int t = it.tok0 + r / G;
       const float inv = 1.f / l;
