@@ -127,6 +127,25 @@ uint64_t glmx_kv_free_pages(const glmx_kv* kv);
 void* glmx_kv_pool_ptr(const glmx_kv* kv);
 uint64_t glmx_kv_page_bytes(const glmx_kv* kv);
 
+/* ---- cross-GPU prefix hits (one process and one pool per GPU) ----------------
+ * Each rank exports its pool once (CUDA IPC) and, at every epoch (a rotation of the workload),
+ * publishes the (block id, page) pairs of its residents; a rank's engine prefill then serves the
+ * run of missed blocks that directly extends its local hit prefix from peer pools by K4 page
+ * copies instead of recomputing them.  Bookkeeping is unchanged (those blocks are misses,
+ * inserted locally with their tier/owner, exactly as G independent KvCacheStates would count
+ * them); only the compute differs.  Epoch mode keeps evicted pages deferred until the caller's
+ * epoch-end barrier (glmx_kv_release_deferred), so a page named in a directory stays intact for
+ * the whole epoch. */
+int glmx_kv_ipc_handle(const glmx_kv* kv, uint8_t out[64]);
+int glmx_kv_attach_peer(glmx_kv* kv, int32_t peer, const uint8_t handle[64]);
+/* same-process variant: another pool (possibly on another device) as peer `peer` */
+int glmx_kv_attach_peer_local(glmx_kv* kv, int32_t peer, const glmx_kv* other);
+int glmx_kv_set_peer_directory(glmx_kv* kv, uint64_t n, const uint64_t* block_ids,
+                               const int32_t* peers, const int32_t* pages);
+int glmx_kv_set_epoch_mode(glmx_kv* kv, int32_t on);
+/* blocks served by peer copies since creation */
+int64_t glmx_kv_peer_hits(const glmx_kv* kv);
+
 /* whitespace tokenizer (tokenizer.hpp:14-25): writes begin/end byte spans, returns count */
 uint64_t glmx_tokenize(const char* text, uint64_t len, uint64_t* begins, uint64_t* ends,
                        uint64_t cap);

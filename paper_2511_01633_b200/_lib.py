@@ -100,6 +100,12 @@ _SIGS = {
     "glmx_kv_free_pages": (C.c_uint64, [C.c_void_p]),
     "glmx_kv_pool_ptr": (C.c_void_p, [C.c_void_p]),
     "glmx_kv_page_bytes": (C.c_uint64, [C.c_void_p]),
+    "glmx_kv_ipc_handle": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    "glmx_kv_attach_peer": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint8)]),
+    "glmx_kv_attach_peer_local": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "glmx_kv_set_peer_directory": (C.c_int, [C.c_void_p, C.c_uint64, u64p, i32p, i32p]),
+    "glmx_kv_set_epoch_mode": (C.c_int, [C.c_void_p, C.c_int32]),
+    "glmx_kv_peer_hits": (C.c_int64, [C.c_void_p]),
     "glmx_tokenize": (C.c_uint64, [C.c_char_p, C.c_uint64, u64p, u64p, C.c_uint64]),
     "glmx_token_id": (C.c_int32, [C.c_char_p, C.c_uint64, C.c_uint32]),
     "glmx_graph_load_jsonl": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),

@@ -7,6 +7,13 @@
 
 using namespace glmx;
 
+#define GLMX_CUDA(call)                                                                       \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::glmx::Error(GLMX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
 int chunk_build_impl(glmx_graph*, const glmx_chunk_config*, const int32_t*, uint64_t, char*,
                      uint64_t, uint64_t*, int32_t*, uint64_t*, uint64_t*, uint64_t, uint64_t*,
                      uint64_t*, uint64_t*);
@@ -218,6 +225,76 @@ uint64_t glmx_kv_pool_pages(const glmx_kv* kv) { return kv->bk->pool().total(); 
 uint64_t glmx_kv_free_pages(const glmx_kv* kv) { return kv->bk->pool().free_count(); }
 void* glmx_kv_pool_ptr(const glmx_kv* kv) { return kv->geom.base; }
 uint64_t glmx_kv_page_bytes(const glmx_kv* kv) { return kv->page_bytes; }
+
+// ------------------------------------------------------------------ cross-GPU prefix hits
+int glmx_kv_ipc_handle(const glmx_kv* kv, uint8_t out[64]) {
+  return guarded([&] {
+    if (!kv->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "no device pool");
+    DeviceGuard g(kv->cfg.device);
+    cudaIpcMemHandle_t h;
+    GLMX_CUDA(cudaIpcGetMemHandle(&h, kv->geom.base));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(out, &h, 64);
+    return GLMX_OK;
+  });
+}
+
+static void set_peer(glmx_kv* kv, int32_t peer, __nv_bfloat16* base, bool ipc) {
+  if (peer < 0 || peer > 1024) throw Error(GLMX_ERR_ARG, "peer index out of range");
+  if (kv->peers.size() <= static_cast<size_t>(peer)) kv->peers.resize(peer + 1);
+  kv->peers[peer] = {base, ipc};
+}
+
+int glmx_kv_attach_peer(glmx_kv* kv, int32_t peer, const uint8_t handle[64]) {
+  return guarded([&] {
+    if (!kv->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "no device pool");
+    DeviceGuard g(kv->cfg.device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* p = nullptr;
+    GLMX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    set_peer(kv, peer, static_cast<__nv_bfloat16*>(p), true);
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_attach_peer_local(glmx_kv* kv, int32_t peer, const glmx_kv* other) {
+  return guarded([&] {
+    if (!kv->has_pool() || !other->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "no device pool");
+    if (other->page_bytes != kv->page_bytes) throw Error(GLMX_ERR_ARG, "pool geometries differ");
+    if (other->cfg.device != kv->cfg.device) {
+      DeviceGuard g(kv->cfg.device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(other->cfg.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        throw Error(GLMX_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    set_peer(kv, peer, other->geom.base, false);
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_set_peer_directory(glmx_kv* kv, uint64_t n, const uint64_t* block_ids,
+                               const int32_t* peers, const int32_t* pages) {
+  return guarded([&] {
+    kv->peer_dir.clear();
+    kv->peer_dir.reserve(n);
+    const uint64_t total = kv->bk->pool().total();
+    for (uint64_t i = 0; i < n; ++i) {
+      if (pages[i] < 0 || static_cast<uint64_t>(pages[i]) >= total)
+        throw Error(GLMX_ERR_ARG, "directory page out of range");
+      kv->peer_dir.emplace(block_ids[i], std::make_pair(peers[i], pages[i]));  // first wins
+    }
+    return GLMX_OK;
+  });
+}
+
+int glmx_kv_set_epoch_mode(glmx_kv* kv, int32_t on) {
+  kv->epoch_mode = on != 0;
+  return GLMX_OK;
+}
+
+int64_t glmx_kv_peer_hits(const glmx_kv* kv) { return kv->peer_hits; }
 
 uint64_t glmx_tokenize(const char* text, uint64_t len, uint64_t* begins, uint64_t* ends,
                        uint64_t cap) {

@@ -119,6 +119,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
   const uint64_t full = out.ids.size();
   out.tail = toks.n - full * B_;
   out.pages.resize(full, -1);
+  out.fresh.assign(full, 0);
 
   // Maximal resident chain prefix counts as cached (cache.cpp:70-81).
   uint64_t hit = 0;
@@ -161,6 +162,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
     blk.session = tier == GLMX_TIER_I ? 0 : sess;
     blk.page = pool_.alloc();
     out.pages[b] = blk.page;
+    out.fresh[b] = 1;
     order_insert(blk);
     owned_[blk.session].insert(blk.id);
     resident_.emplace(blk.id, blk);

@@ -54,6 +54,7 @@ struct PrefillResult {        // PrefillReport (cache.hpp:33-39) + block table
   std::vector<uint64_t> evicted;
   std::vector<uint64_t> ids;     // chain ids of the full blocks
   std::vector<int32_t> pages;    // physical page per full block
+  std::vector<uint8_t> fresh;    // 1 = inserted by this call (new page, KV not yet present)
   uint64_t hit_blocks = 0;
 };
 

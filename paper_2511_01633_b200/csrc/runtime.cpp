@@ -40,6 +40,8 @@ DBuf::~DBuf() {
 }
 
 glmx_kv::~glmx_kv() {
+  for (auto& p : peers)
+    if (p.ipc && p.base) cudaIpcCloseMemHandle(p.base);
   if (geom.base) cudaFree(geom.base);
   if (stream) cudaStreamDestroy(stream);
   if (ev0) cudaEventDestroy(ev0);
@@ -419,6 +421,8 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->o_bt = o; o = align_up(o + R * e->bt_stride * 4, 256);
   e->o_work = o; o = align_up(o + max_work * 8, 256);
   e->o_last = o; o = align_up(o + R * 4, 256);
+  e->max_copies = T / B + R + 16;  // peer page copies per batch (src, dst int32 each)
+  e->o_copy = o; o = align_up(o + e->max_copies * 8, 256);
   e->meta_bytes = o;
   e->meta.reserve(o);
   GLMX_CUDA(cudaMallocHost(&e->h_meta, o));
@@ -561,6 +565,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   PrefillResult pr;
   int T = 0, R = 0, n_work = 0;
   std::vector<int> req_row(n_req, -1);
+  e->copies.clear();
   double attn_flops = 0, attn_bytes = 0, ctx_tokens = 0;
   const double kv_tok_bytes = 2.0 * c.n_kv_heads * c.head_dim * 2;  // per layer
   for (uint64_t i = 0; i < n_req; ++i) {
@@ -585,7 +590,19 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
       st.scratch.push_back(p);
       st.pages.push_back(p);
     }
-    const uint64_t q0 = std::min<uint64_t>(pr.cached, rq.n_tok - 1);  // always >= 1 row
+    // Cross-GPU prefix hit: the run of freshly inserted blocks that directly extends the local
+    // hit prefix and is resident on a peer is copied instead of computed (bookkeeping already
+    // counted them as misses, like independent per-GPU caches).
+    uint64_t reuse_blocks = pr.hit_blocks;
+    if (!kv->peer_dir.empty()) {
+      for (uint64_t b = pr.hit_blocks; b < pr.pages.size() && pr.fresh[b]; ++b) {
+        auto it = kv->peer_dir.find(pr.ids[b]);
+        if (it == kv->peer_dir.end()) break;
+        e->copies.push_back({it->second.first, it->second.second, pr.pages[b]});
+        ++reuse_blocks;
+      }
+    }
+    const uint64_t q0 = std::min<uint64_t>(reuse_blocks * B, rq.n_tok - 1);  // always >= 1 row
     const int ql = static_cast<int>(rq.n_tok - q0);
     if (T + ql > static_cast<int>(e->cfg.max_batch_tokens))
       throw Error(GLMX_ERR_ARG, "batch exceeds max_batch_tokens");
@@ -626,8 +643,21 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   e->work[4] = T;
   e->work[5] = ctx_tokens;
   if (R == 0) {
-    bk.pool().release_deferred();
+    if (!kv->epoch_mode) bk.pool().release_deferred();
     return GLMX_OK;
+  }
+  // peer copies, grouped by source pool: src pages then dst pages per group in o_copy
+  if (e->copies.size() > e->max_copies) throw Error(GLMX_ERR_ARG, "too many peer copies in batch");
+  std::stable_sort(e->copies.begin(), e->copies.end(),
+                   [](const glmx_engine::Copy& a, const glmx_engine::Copy& b) { return a.peer < b.peer; });
+  {
+    int32_t* h_cp = reinterpret_cast<int32_t*>(hm + e->o_copy);
+    const size_t nc = e->copies.size();
+    for (size_t i = 0; i < nc; ++i) {
+      h_cp[i] = e->copies[i].src_page;
+      h_cp[nc + i] = e->copies[i].dst_page;
+    }
+    kv->peer_hits += static_cast<int64_t>(nc);
   }
   cudaStream_t s = e->stream;
   {
@@ -635,6 +665,23 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
   }
   GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
+  if (!e->copies.empty()) {
+    Prof p(e, kCatOther);
+    const int32_t* d_cp = reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_copy);
+    const size_t nc = e->copies.size();
+    for (size_t a = 0; a < nc;) {
+      size_t b = a;
+      while (b < nc && e->copies[b].peer == e->copies[a].peer) ++b;
+      const int32_t peer = e->copies[a].peer;
+      if (peer < 0 || static_cast<size_t>(peer) >= kv->peers.size() || !kv->peers[peer].base)
+        throw Error(GLMX_ERR_ARG, "peer " + std::to_string(peer) + " is not attached");
+      for (size_t o = a; o < b; o += 65535)
+        pool_copy_pages(kv->peers[peer].base, kv->geom.base, kv->geom.page_elems(), d_cp + o,
+                        d_cp + nc + o, static_cast<int>(std::min<size_t>(65535, b - o)), s);
+      a = b;
+    }
+    e->work[2] += 2.0 * static_cast<double>(nc) * static_cast<double>(kv->page_bytes);
+  }
   forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
   argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), s);
   {
@@ -642,8 +689,9 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     GLMX_CUDA(cudaMemcpyAsync(e->h_out, e->next_tok.p, R * 4, cudaMemcpyDeviceToHost, s));
   }
   GLMX_CUDA(cudaEventRecord(e->fwd_done, s));
-  // evicted pages were read by this batch; any later writer is stream-ordered after it
-  bk.pool().release_deferred();
+  // evicted pages were read by this batch; any later writer is stream-ordered after it.  In
+  // epoch mode peers may still copy them: the caller releases after its epoch barrier.
+  if (!kv->epoch_mode) bk.pool().release_deferred();
   GLMX_CUDA(cudaStreamSynchronize(s));
   collect_profile(e);
   std::vector<float> tmp;

@@ -43,6 +43,15 @@ struct glmx_kv {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_copy_ms = 0.f;
   DBuf scratch;  // page lists for copies
+  // cross-GPU prefix hits
+  struct Peer {
+    __nv_bfloat16* base = nullptr;
+    bool ipc = false;  // opened with cudaIpcOpenMemHandle (closed on destroy)
+  };
+  std::vector<Peer> peers;
+  std::unordered_map<uint64_t, std::pair<int32_t, int32_t>> peer_dir;  // block -> (peer, page)
+  bool epoch_mode = false;
+  int64_t peer_hits = 0;
   ~glmx_kv();
 };
 
@@ -109,6 +118,11 @@ struct glmx_engine {
   int last_T = 0, last_R = 0, last_work = 0;
   bool has_batch = false;
   // offsets into meta
+  struct Copy {
+    int32_t peer, src_page, dst_page;
+  };
+  std::vector<Copy> copies;  // peer page copies of the current batch
+  size_t max_copies = 0, o_copy = 0;
   size_t o_tok = 0, o_pos = 0, o_slot = 0, o_qs = 0, o_ql = 0, o_ctx = 0, o_bt = 0, o_work = 0,
          o_last = 0;
 

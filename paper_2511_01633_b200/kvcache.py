@@ -171,6 +171,49 @@ class KvCacheState:
     def snapshot(self):
         return json.loads(self.snapshot_json())
 
+    # ---- cross-GPU prefix hits ----------------------------------------------
+    def resident_ids_pages(self):
+        """(block ids uint64[n], pages int32[n]) of the residents — this rank's directory entry."""
+        import numpy as np
+
+        n = self.resident_blocks()
+        ids = np.zeros(max(1, n), dtype=np.uint64)
+        pages = np.zeros(max(1, n), dtype=np.int32)
+        lib().glmx_kv_resident(self.h, ids.ctypes.data_as(_lib.u64p), None, None,
+                               pages.ctypes.data_as(_lib.i32p), n)
+        return ids[:n], pages[:n]
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        check(lib().glmx_kv_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def attach_peer(self, peer: int, handle: bytes):
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        check(lib().glmx_kv_attach_peer(self.h, peer, buf))
+
+    def attach_peer_local(self, peer: int, other: "KvCacheState"):
+        check(lib().glmx_kv_attach_peer_local(self.h, peer, other.h))
+
+    def set_peer_directory(self, ids, peers, pages):
+        import numpy as np
+
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        peers = np.ascontiguousarray(peers, dtype=np.int32)
+        pages = np.ascontiguousarray(pages, dtype=np.int32)
+        check(lib().glmx_kv_set_peer_directory(self.h, len(ids), ids.ctypes.data_as(_lib.u64p),
+                                               peers.ctypes.data_as(_lib.i32p),
+                                               pages.ctypes.data_as(_lib.i32p)))
+
+    def set_epoch_mode(self, on=True):
+        check(lib().glmx_kv_set_epoch_mode(self.h, int(on)))
+
+    def release_deferred(self):
+        check(lib().glmx_kv_release_deferred(self.h))
+
+    def peer_hits(self):
+        return lib().glmx_kv_peer_hits(self.h)
+
     def pool_pages(self):
         return lib().glmx_kv_pool_pages(self.h)
 

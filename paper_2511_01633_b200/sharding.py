@@ -1,0 +1,68 @@
+"""Multi-GPU plumbing for the query-sharded hot path.
+
+One process per GPU (torch.distributed for the control plane only).  Queries are independent:
+rank r serves queries i with i % N == r.  The one exchange step is the cross-GPU prefix hit: at
+every epoch (= one rotation of the round-robin) each rank publishes the (block id, page) pairs of
+its resident blocks; a rank's engine then serves a missed run of blocks that a peer holds by
+copying the pages over NVLink (K4) instead of recomputing them.  Pages named in an epoch's
+directory stay valid for the whole epoch because every rank runs its pool in epoch mode (evicted
+pages are released only after the epoch-end barrier).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard(items, rank: int, world: int):
+    """Deterministic query -> rank map: item i goes to rank i % world."""
+    return items[rank::world]
+
+
+def merge_directories(snapshots, rank: int):
+    """snapshots[q] = (ids uint64[n_q], pages int32[n_q]) of rank q.  Returns the directory a
+    given rank installs: every other rank's residents, lower rank first for duplicated ids."""
+    ids, peers, pages = [], [], []
+    for q, (i, p) in enumerate(snapshots):
+        if q == rank or len(i) == 0:
+            continue
+        ids.append(np.asarray(i, dtype=np.uint64))
+        pages.append(np.asarray(p, dtype=np.int32))
+        peers.append(np.full(len(i), q, dtype=np.int32))
+    if not ids:
+        return (np.zeros(0, np.uint64), np.zeros(0, np.int32), np.zeros(0, np.int32))
+    return np.concatenate(ids), np.concatenate(peers), np.concatenate(pages)
+
+
+class PeerExchange:
+    """Wires a rank's KvCacheState to its peers and runs the per-epoch directory exchange."""
+
+    def __init__(self, kv, group=None, use_ipc=True):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.kv = kv
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > 1 and use_ipc:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, kv.ipc_handle(), group=group)
+            for q, h in enumerate(handles):
+                if q != self.rank:
+                    kv.attach_peer(q, h)
+        kv.set_epoch_mode(True)
+
+    def epoch_begin(self):
+        """Barrier, then exchange resident snapshots and install the merged directory."""
+        snap = self.kv.resident_ids_pages()
+        snaps = [None] * self.world
+        self.dist.all_gather_object(snaps, snap, group=self.group)
+        ids, peers, pages = merge_directories(snaps, self.rank)
+        self.kv.set_peer_directory(ids, peers, pages)
+        return len(ids)
+
+    def epoch_end(self):
+        """After this rank's epoch work completed on the device: wait for every rank, then the
+        pages evicted during the epoch may be reused."""
+        self.dist.barrier(group=self.group)
+        self.kv.release_deferred()
