@@ -279,6 +279,20 @@ void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
 int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
                    const int32_t* dst_pages, uint64_t n, void* stream);
 float glmx_pool_last_copy_ms(const glmx_kv* dst);
+/* K3 on caller-owned DEVICE buffers — the attention core of the prefill step that replaces the
+ * c_prefill cost term (orchestrator.cpp:131-132); no reference counterpart (tensor
+ * math is builder-defined).  q/o [n_q_rows][n_heads][head_dim] bf16 (q RoPE'd), pool = pages x
+ * [n_layers][K|V][n_kv_heads][block_tokens][head_dim] bf16.  Host arrays per request: q_start,
+ * q_len (suffix rows), ctx_len (cached + suffix keys), block_table [n_req][bt_stride] pages.
+ * Causal over absolute positions (query t of request r sits at ctx_len - q_len + t).
+ * impl 0 = tcgen05/TMEM/TMA kernel, 1 = mma.sync baseline.  Launches `reps` times on `stream`;
+ * out_ms = mean device time per launch (CUDA events). */
+int glmx_attention_run(int32_t impl, const void* q, void* o, uint64_t n_q_rows, int32_t n_heads,
+                       int32_t n_kv_heads, int32_t head_dim, void* pool, uint64_t n_pages,
+                       uint32_t n_layers, uint32_t layer, uint32_t block_tokens, uint64_t n_req,
+                       const int32_t* q_start, const int32_t* q_len, const int32_t* ctx_len,
+                       const int32_t* block_table, int32_t bt_stride, int32_t reps, void* stream,
+                       float* out_ms);
 
 #ifdef __cplusplus
 }

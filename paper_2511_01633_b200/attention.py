@@ -1,0 +1,71 @@
+"""K3 paged prefill attention on caller-owned device tensors (glmx_attention_run).
+
+The engine calls the same kernel inside its forward; this face exists for kernel-level parity
+tests and attention sweeps (long-context configuration C5).  Tensors are torch CUDA tensors used
+only as device memory: q/o [rows][H][hd] bf16, pool [pages][L][2][Hkv][B][hd] bf16.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._lib import check, lib
+
+TC = 0   # tcgen05 / TMEM / TMA kernel (the product path)
+MMA = 1  # mma.sync baseline (A/B only)
+
+
+def _i32(xs):
+    arr = (C.c_int32 * max(1, len(xs)))(*[int(x) for x in xs])
+    return arr
+
+
+def paged_attention(q, o, pool, q_start, q_len, ctx_len, block_table, layer=0, impl=TC,
+                    reps=1, stream=None):
+    """Run K3 over n_req requests; returns the mean device ms per launch.
+
+    q_start/q_len/ctx_len: per-request ints; block_table: list of page lists (padded here)."""
+    import torch
+
+    assert q.dtype == torch.bfloat16 and o.dtype == torch.bfloat16 and pool.dtype == torch.bfloat16
+    assert q.is_cuda and o.is_cuda and pool.is_cuda and q.is_contiguous() and o.is_contiguous()
+    n_pages, L, two, Hkv, B, hd = pool.shape
+    assert two == 2 and q.shape[2] == hd
+    rows, H = q.shape[0], q.shape[1]
+    n = len(q_len)
+    stride = max(1, max(len(b) for b in block_table))
+    bt = []
+    for b in block_table:
+        bt.extend(list(b) + [0] * (stride - len(b)))
+    ms = C.c_float(0.0)
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(lib().glmx_attention_run(impl, q.data_ptr(), o.data_ptr(), rows, H, Hkv, hd,
+                                   pool.data_ptr(), n_pages, L, layer, B, n, _i32(q_start),
+                                   _i32(q_len), _i32(ctx_len), _i32(bt), stride, reps, s,
+                                   C.byref(ms)))
+    return ms.value
+
+
+def reference_attention(q, pool, q_start, q_len, ctx_len, block_table, layer=0):
+    """Plain PyTorch fp32 restatement (causal GQA over absolute positions) for the tests."""
+    import torch
+
+    n_pages, L, _, Hkv, B, hd = pool.shape
+    H = q.shape[1]
+    G = H // Hkv
+    out = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+    scale = hd ** -0.5
+    for r in range(len(q_len)):
+        ctx, ql, qs = int(ctx_len[r]), int(q_len[r]), int(q_start[r])
+        pages = torch.tensor(block_table[r][:(ctx + B - 1) // B], device=pool.device,
+                             dtype=torch.long)
+        k = pool[pages, layer, 0].float().permute(1, 0, 2, 3).reshape(Hkv, -1, hd)[:, :ctx]
+        v = pool[pages, layer, 1].float().permute(1, 0, 2, 3).reshape(Hkv, -1, hd)[:, :ctx]
+        qq = q[qs:qs + ql].float().permute(1, 0, 2)                     # [H][ql][hd]
+        kk = k.repeat_interleave(G, dim=0)                               # [H][ctx][hd]
+        vv = v.repeat_interleave(G, dim=0)
+        s = torch.matmul(qq, kk.transpose(1, 2)) * scale                 # [H][ql][ctx]
+        pos = torch.arange(ctx - ql, ctx, device=q.device)[:, None]
+        key = torch.arange(ctx, device=q.device)[None, :]
+        s = s.masked_fill(key > pos, float("-inf"))
+        out[qs:qs + ql] = torch.matmul(torch.softmax(s, dim=-1), vv).permute(1, 0, 2)
+    return out

@@ -26,6 +26,9 @@ int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefil
                         int32_t*, float*);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
+int attention_run_impl(int, const void*, void*, uint64_t, int, int, int, void*, uint64_t, uint32_t,
+                       uint32_t, uint32_t, uint64_t, const int32_t*, const int32_t*,
+                       const int32_t*, const int32_t*, int, int, cudaStream_t, float*);
 
 namespace {
 thread_local std::string g_err;
@@ -497,5 +500,19 @@ int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
   });
 }
 float glmx_pool_last_copy_ms(const glmx_kv* dst) { return dst->last_copy_ms; }
+
+int glmx_attention_run(int32_t impl, const void* q, void* o, uint64_t n_q_rows, int32_t n_heads,
+                       int32_t n_kv_heads, int32_t head_dim, void* pool, uint64_t n_pages,
+                       uint32_t n_layers, uint32_t layer, uint32_t block_tokens, uint64_t n_req,
+                       const int32_t* q_start, const int32_t* q_len, const int32_t* ctx_len,
+                       const int32_t* block_table, int32_t bt_stride, int32_t reps, void* stream,
+                       float* out_ms) {
+  return guarded([&] {
+    return attention_run_impl(impl, q, o, n_q_rows, n_heads, n_kv_heads, head_dim, pool, n_pages,
+                              n_layers, layer, block_tokens, n_req, q_start, q_len, ctx_len,
+                              block_table, bt_stride, reps, static_cast<cudaStream_t>(stream),
+                              out_ms);
+  });
+}
 
 }  // extern "C"

@@ -1,20 +1,25 @@
 // K3 — paged causal GQA prefill attention on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-// Persistent kernel: one CTA per SM walks a static slice of the work items (request, 128-row
-// query tile, kv head) — items are sorted longest-first on the host.  An item's 128 query rows
-// are 128/G tokens x the G query heads that share the kv head, so every K/V page is fetched once
-// per GQA group.  The pipeline runs across item boundaries:
-//   warps 0-3  softmax / correction / epilogue: thread i owns query row i == TMEM lane i
-//   warp 4     TMA producer: the item's Q tile (3-D map over q [T][H][hd]) and the K and V pages
-//              of each 128-key tile (2-D map over the pool, 16 boxes of [16 tok][64 dims] per
-//              operand, 128B swizzle, pages past the context are out-of-bounds -> zero fill)
-//              into a 2-stage smem ring
-//   warp 5     MMA issuer (one thread): S_g = Q K_g^T (M128 N128 K128 fp32, TMEM double-buffered)
-//              and O += P_{g-1} V_{g-1} (P from smem, V MN-major; O double-buffered per item so an
-//              item's epilogue overlaps the next item's MMAs)
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  Online softmax in base 2, single
-// pass over TMEM, lazily updated reference max (O rescaled only when a row max grows by > 2^8,
-// decided warp-uniformly), 1/l normalisation in the epilogue.
+// Persistent kernel: one CTA per SM walks a static slice of the work items (request, 64-token
+// query block, kv head), sorted longest-first on the host.  An item holds TWO 128-row query tiles
+// (Q0 = tokens [t0, t0+32) x the G=4 query heads of one kv head, Q1 = the next 32 tokens), so
+// every K/V page is fetched once per GQA group and used for 256 query rows: per 128-key tile the
+// CTA moves 64 KB from L2 for 8.4 MFLOP of tensor work (half the single-tile design's L2 load,
+// which at 148 SMs exceeded the chip's L2 throughput).
+//   warps 0-3  softmax WG0: thread i owns row i of Q0 == TMEM lane i (S0 / P0 / O0)
+//   warps 4-7  softmax WG1: same for Q1 (S1 / P1 / O1)
+//   warp 8     TMA producer: K_0, Q0+Q1, V_0, K_1, V_1, ... through a 4-slot ring of 32 KB
+//              [128 keys][128 dims] SW128 tiles (16 page boxes per tile; pages past the context
+//              are out of bounds -> zero fill), in exactly the order the MMA warp consumes them
+//   warp 9     MMA issuer (one thread), per key tile j:
+//                PV0(j-1) S0(j) PV1(j-1) S1(j)  ... i.e. S_i(j+1) is issued right behind PV_i(j),
+//              so while WG0 runs the softmax of tile j the tensor pipe executes PV1(j-1), S1(j),
+//              and vice versa (ping-pong of the two query tiles)
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  P_i (bf16) overwrites the
+// first 64 columns of S_i and is the TMEM A operand of PV_i.  Online softmax in base 2 with a
+// lazily updated reference max (O rescaled only when a row max grows by > 2^8, decided
+// warp-uniformly because tcgen05.ld/st are .sync.aligned); 1/l normalisation in the epilogue.
+// Every mbarrier wait is bounded (%globaltimer): a protocol error prints its location and traps.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,17 +34,21 @@ namespace {
 
 constexpr int kHD = 128;
 constexpr int kB = 16;
-constexpr int kM = 128;       // query rows per item
+constexpr int kM = 128;       // query rows per tile (TMEM lanes)
+constexpr int kQT = 2;        // query tiles per item
 constexpr int kN = 128;       // keys per tile
 constexpr int kHalf = 16384;  // bytes of one [128][64] bf16 SW128 half tile
 constexpr int kTile = 2 * kHalf;
-constexpr int kThreads = 192;
-// smem map (1024-aligned): Q | K0 K1 | V0 V1 | P | barriers
+constexpr int kSlots = 4;     // K/V ring depth (32 KB slots)
+constexpr int kSoftmaxThreads = 128 * kQT;
+constexpr int kThreads = kSoftmaxThreads + 64;  // + producer warp + MMA warp
+// registers: up to 3 warps per SM sub-partition (16K regs each) -> <= 168 per thread
+// smem map (1024-aligned): Q0 Q1 | ring slots | barriers
 constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + kTile;
-constexpr int kOffV = kOffK + 2 * kTile;
-constexpr int kOffBar = kOffV + 2 * kTile;  // P lives in TMEM (aliasing its S tile)
+constexpr int kOffRing = kOffQ + kQT * kTile;
+constexpr int kOffBar = kOffRing + kSlots * kTile;
 constexpr int kSmem = kOffBar + 256 + 1024;  // + alignment slack
+static_assert(kSmem <= 232448, "shared memory budget");
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -210,9 +219,14 @@ __device__ __forceinline__ Item item_of(const AttnParams& p, int w) {
   it.ctx = p.ctx_len[it.req];
   it.qs = p.q_start[it.req];
   const int G = p.H / p.Hkv;
-  const int max_pos = it.ctx - it.qlen + min(it.tok0 + kM / G, it.qlen) - 1;
+  const int max_pos = it.ctx - it.qlen + min(it.tok0 + kQT * kM / G, it.qlen) - 1;
   it.n_kt = max_pos / kN + 1;
   return it;
+}
+
+__device__ __forceinline__ void ring_pos(int c, int& slot, uint32_t& use) {
+  slot = c % kSlots;
+  use = static_cast<uint32_t>(c / kSlots);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -223,35 +237,32 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_addr(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  // barriers (8 B each)
-  const uint32_t b_kfull = smem_addr(bars + 0), b_vfull = smem_addr(bars + 2);
-  const uint32_t b_kempty = smem_addr(bars + 4), b_vempty = smem_addr(bars + 6);
-  const uint32_t b_sfull = smem_addr(bars + 8), b_pfull = smem_addr(bars + 10);
-  const uint32_t b_pvdone = smem_addr(bars + 11), b_qfull = smem_addr(bars + 12);
-  const uint32_t b_qempty = smem_addr(bars + 13), b_ofree = smem_addr(bars + 14);  // ofree[2]
-  const uint32_t b_ofull = smem_addr(bars + 17);                                   // ofull[2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
+  // barriers (8 B each): full[kSlots] empty[kSlots] sfull[2] pfull[2] ofull[2] qfull qempty
+  const uint32_t b_full = smem_addr(bars + 0), b_empty = smem_addr(bars + kSlots);
+  const uint32_t b_sfull = smem_addr(bars + 2 * kSlots), b_pfull = smem_addr(bars + 2 * kSlots + 2);
+  const uint32_t b_ofull = smem_addr(bars + 2 * kSlots + 4);
+  const uint32_t b_qfull = smem_addr(bars + 2 * kSlots + 6), b_qempty = smem_addr(bars + 2 * kSlots + 7);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kSlots + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.H / p.Hkv;
+  constexpr int kWarpProducer = kSoftmaxThreads / 32, kWarpMma = kWarpProducer + 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(b_kfull + 8 * s, 1);
-      mbar_init(b_vfull + 8 * s, 1);
-      mbar_init(b_kempty + 8 * s, 1);
-      mbar_init(b_vempty + 8 * s, 1);
-      mbar_init(b_sfull + 8 * s, 1);
-      mbar_init(b_ofree + 8 * s, 128);
-      mbar_init(b_ofull + 8 * s, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_empty + 8 * s, 1);
     }
-    mbar_init(b_pfull, 128);
-    mbar_init(b_pvdone, 1);
+    for (int i = 0; i < kQT; ++i) {
+      mbar_init(b_sfull + 8 * i, 1);
+      mbar_init(b_pfull + 8 * i, 128);
+      mbar_init(b_ofull + 8 * i, 1);
+    }
     mbar_init(b_qfull, 1);
     mbar_init(b_qempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == kWarpMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_addr(tmem_holder)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -260,189 +271,228 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const uint32_t t_s0 = tmem, t_o0 = tmem + 256;
+  const uint32_t t_s0 = tmem, t_o0 = tmem + kQT * kN;
 
-  if (warp == 4) {
+  if (warp >= kWarpProducer) {
+    if (warp == kWarpProducer) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
       const uint32_t L = p.pool.n_layers, Hkv = p.pool.n_kv_heads;
-      int g = 0, it_local = 0;
+      int c = 0, it_local = 0;
+      // one ring load: K (kv = 0) or V (kv = 1) of key tile j of the item
+      auto load_kv = [&](const Item& it, const int32_t* bt, int j, int kv) {
+        int slot;
+        uint32_t use;
+        ring_pos(c, slot, use);
+        if (use > 0) mbar_wait(b_empty + 8 * slot, (use - 1) & 1, 2 + kv);
+        const uint32_t full = b_full + 8 * slot;
+        mbar_expect_tx(full, kTile);
+        const uint32_t dst = sbase + kOffRing + slot * kTile;
+        for (int pg = 0; pg < kN / kB; ++pg) {
+          const int key0 = j * kN + pg * kB;
+          uint32_t row = tp.rows_total;  // out of bounds -> zeros
+          if (key0 < it.ctx) {
+            const uint32_t page = static_cast<uint32_t>(bt[key0 / kB]);
+            row = (((page * L + p.layer) * 2 + kv) * Hkv + it.kvh) * kB;
+          }
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
+        }
+        ++c;
+      };
       for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
         const Item it = item_of(p, w);
         const int32_t* bt = p.block_table + static_cast<int64_t>(it.req) * p.bt_stride;
+        load_kv(it, bt, 0, 0);
         if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // last S of prev item done
-        mbar_expect_tx(b_qfull, kTile);
-        for (int hf = 0; hf < 2; ++hf)
-          tma_load_3d(sbase + kOffQ + hf * kHalf, &q_map, hf * 64, it.kvh * G, it.qs + it.tok0, b_qfull);
-        for (int j = 0; j < it.n_kt; ++j, ++g) {
-          const int s = g & 1;
-          const uint32_t ph = (g >> 1) & 1;
-          for (int kv = 0; kv < 2; ++kv) {
-            const uint32_t full = (kv ? b_vfull : b_kfull) + 8 * s;
-            if (g >= 2) mbar_wait((kv ? b_vempty : b_kempty) + 8 * s, ph ^ 1, 2 + kv);
-            mbar_expect_tx(full, kTile);
-            const uint32_t dst = sbase + (kv ? kOffV : kOffK) + s * kTile;
-            for (int pg = 0; pg < kN / kB; ++pg) {
-              const int key0 = j * kN + pg * kB;
-              uint32_t row = tp.rows_total;  // out of bounds -> zeros
-              if (key0 < it.ctx) {
-                const uint32_t page = static_cast<uint32_t>(bt[key0 / kB]);
-                row = (((page * L + p.layer) * 2 + kv) * Hkv + it.kvh) * kB;
-              }
-              for (int hf = 0; hf < 2; ++hf)
-                tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
-            }
-          }
+        mbar_expect_tx(b_qfull, kQT * kTile);
+        for (int i = 0; i < kQT; ++i)
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(sbase + kOffQ + i * kTile + hf * kHalf, &q_map, hf * 64, it.kvh * G,
+                        it.qs + it.tok0 + i * (kM / G), b_qfull);
+        load_kv(it, bt, 0, 1);
+        for (int j = 1; j < it.n_kt; ++j) {
+          load_kv(it, bt, j, 0);
+          load_kv(it, bt, j, 1);
         }
       }
     }
     __syncwarp();  // reconverge before the CTA barrier (bar.sync is .aligned)
-  } else if (warp == 5) {
+    } else if (warp == kWarpMma) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(kN, false), idO = idesc_bf16(kHD, true);
-      const uint32_t q_addr = sbase + kOffQ;
-      // PV of global tile gp (item-local index jp, O buffer ob).  A = P_gp, bf16 packed in the
-      // first 64 TMEM columns of its S buffer (8 columns per 16-key k-step); B = V (MN-major).
-      // tcgen05.mma executes in issue order, so S_{gp+2} (issued later into the same buffer)
-      // cannot overwrite P_gp before this PV has consumed it.
-      auto issue_pv = [&](int gp, int jp, int ob, bool last) {
-        const int s = gp & 1;
-        mbar_wait(b_pfull, gp & 1, 10);  // P_gp in TMEM (and O rescaled if needed)
-        mbar_wait(b_vfull + 8 * s, (gp >> 1) & 1, 11);
-        tc_fence_after();
-        const uint32_t v_addr = sbase + kOffV + s * kTile;
+      int c = 0, g = 0, it_local = 0;
+      // S_i = Q_i K^T into S buffer i (K from ring slot of load index ck)
+      auto issue_s = [&](int i, int ck) {
+        int slot;
+        uint32_t use;
+        ring_pos(ck, slot, use);
+        const uint32_t q_addr = sbase + kOffQ + i * kTile;
+        const uint32_t k_addr = sbase + kOffRing + slot * kTile;
+#pragma unroll
+        for (int ks = 0; ks < kHD / 16; ++ks) {
+          const uint64_t a = smem_desc(q_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
+          const uint64_t b = smem_desc(k_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
+          tc_mma(t_s0 + i * kN, a, b, idS, ks > 0 ? 1u : 0u);
+        }
+        tc_commit(b_sfull + 8 * i);
+      };
+      // O_i += P_i V (P from the first 64 TMEM columns of S_i, V MN-major from ring slot cv)
+      auto issue_pv = [&](int i, int cv, bool first) {
+        int slot;
+        uint32_t use;
+        ring_pos(cv, slot, use);
+        const uint32_t v_addr = sbase + kOffRing + slot * kTile;
+#pragma unroll
         for (int ks = 0; ks < kN / 16; ++ks) {
           const uint64_t b = smem_desc(v_addr + ks * 2048, kHalf >> 4, 64);
-          tc_mma_ts(t_o0 + ob * kHD, t_s0 + s * kN + ks * 8, b, idO, (jp > 0 || ks > 0) ? 1u : 0u);
+          tc_mma_ts(t_o0 + i * kHD, t_s0 + i * kN + ks * 8, b, idO, (!first || ks > 0) ? 1u : 0u);
         }
-        tc_commit(b_vempty + 8 * s);
-        tc_commit(b_pvdone);
-        if (last) tc_commit(b_ofull + 8 * ob);
       };
-      int g = 0, it_local = 0;
-      int pend_g = -1, pend_j = 0, pend_ob = 0;  // PV waiting to be issued
-      bool pend_last = false;
+      auto wait_full = [&](int cc, int tag) {
+        int slot;
+        uint32_t use;
+        ring_pos(cc, slot, use);
+        mbar_wait(b_full + 8 * slot, use & 1, tag);
+        tc_fence_after();
+      };
+      auto release = [&](int cc) {
+        int slot;
+        uint32_t use;
+        ring_pos(cc, slot, use);
+        tc_commit(b_empty + 8 * slot);
+      };
       for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
         const Item it = item_of(p, w);
-        const int ob = it_local & 1;
+        const int n = it.n_kt;
+        // load indices of this item: K_j = c + 2j, V_j = c + 2j + 1
+        wait_full(c, 13);
         mbar_wait(b_qfull, it_local & 1, 12);
-        for (int j = 0; j < it.n_kt; ++j, ++g) {
-          const int s = g & 1;
-          mbar_wait(b_kfull + 8 * s, (g >> 1) & 1, 13);
-          tc_fence_after();
-          const uint32_t k_addr = sbase + kOffK + s * kTile;
-          for (int ks = 0; ks < kHD / 16; ++ks) {
-            const uint64_t a = smem_desc(q_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
-            const uint64_t b = smem_desc(k_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
-            tc_mma(t_s0 + s * kN, a, b, idS, ks > 0 ? 1u : 0u);
+        tc_fence_after();
+        issue_s(0, c);
+        issue_s(1, c);
+        release(c);
+        if (n == 1) tc_commit(b_qempty);
+        for (int j = 0; j < n; ++j, ++g) {
+          const int ck = c + 2 * j, cv = ck + 1;
+          // ---- query tile 0: PV0(j), then S0(j+1) behind it (P0 is consumed in order)
+          mbar_wait(b_pfull, g & 1, 10);
+          wait_full(cv, 11);
+          issue_pv(0, cv, j == 0);
+          if (j == n - 1) tc_commit(b_ofull);
+          if (j + 1 < n) {
+            wait_full(ck + 2, 13);
+            issue_s(0, ck + 2);
           }
-          tc_commit(b_kempty + 8 * s);
-          tc_commit(b_sfull + 8 * s);
-          if (j == it.n_kt - 1) tc_commit(b_qempty);
-          if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob, pend_last);
-          // before the first PV into O[ob], the epilogue of item it_local-2 must be done
-          if (j == 0 && it_local >= 2) mbar_wait(b_ofree + 8 * ob, ((it_local >> 1) - 1) & 1, 14);
-          pend_g = g;
-          pend_j = j;
-          pend_ob = ob;
-          pend_last = j == it.n_kt - 1;
+          // ---- query tile 1
+          mbar_wait(b_pfull + 8, g & 1, 15);
+          tc_fence_after();
+          issue_pv(1, cv, j == 0);
+          release(cv);
+          if (j == n - 1) tc_commit(b_ofull + 8);
+          if (j + 1 < n) {
+            issue_s(1, ck + 2);
+            release(ck + 2);
+            if (j + 2 == n) tc_commit(b_qempty);
+          }
         }
+        c += 2 * n;
       }
-      if (pend_g >= 0) issue_pv(pend_g, pend_j, pend_ob, pend_last);
     }
     __syncwarp();
+    }
   } else {
-    // ---------------------------------------------------------------- softmax warps
-    const int r = threadIdx.x;  // query row == TMEM lane
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    // ---------------------------------------------------------------- softmax warpgroups
+    const int qt = warp >> 2;                  // query tile of this warpgroup
+    const int r = threadIdx.x & 127;           // row == TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t ts = t_s0 + qt * kN + lane_off;
+    const uint32_t t_o = t_o0 + qt * kHD + lane_off;
+    const uint32_t b_s = b_sfull + 8 * qt, b_p = b_pfull + 8 * qt, b_o = b_ofull + 8 * qt;
+    const float scale = p.scale_log2;
     uint32_t v[kN];
     int g = 0, it_local = 0;
     for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
       const Item it = item_of(p, w);
-      const int ob = it_local & 1;
-      const uint32_t t_o = t_o0 + ob * kHD + lane_off;
-      const int tq = min(it.tok0 + r / G, it.qlen - 1);
+      const int t_row = it.tok0 + qt * (kM / G) + r / G;  // query token of this row
+      const int tq = min(t_row, it.qlen - 1);
       const int pos = it.ctx - it.qlen + tq;
-      const int pos_lo = it.ctx - it.qlen + it.tok0;  // smallest position among the item's rows
+      const int pos_lo = it.ctx - it.qlen + it.tok0 + qt * (kM / G);  // smallest in the tile
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < it.n_kt; ++j, ++g) {
-        const int s = g & 1;
-        mbar_wait(b_sfull + 8 * s, (g >> 1) & 1, 20);
+        mbar_wait(b_s, g & 1, 20 + qt);
         tc_fence_after();
-        const uint32_t ts = t_s0 + s * kN + lane_off;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) TC_LD32(ts + c * 32, (v + c * 32));
+        for (int cc = 0; cc < 4; ++cc) TC_LD32(ts + cc * 32, (v + cc * 32));
         tc_wait_ld();
         const int kbase = j * kN;
-        float mx = -INFINITY;
-        if (kbase + kN - 1 <= pos_lo) {  // tile fully visible to every row: no mask
+        // row max of the raw scores (scale > 0 commutes with max); 8 independent chains
+        float mx8[8];
 #pragma unroll
-          for (int i = 0; i < kN; ++i) {
-            const float x = __uint_as_float(v[i]) * p.scale_log2;
-            v[i] = __float_as_uint(x);
-            mx = fmaxf(mx, x);
-          }
+        for (int a = 0; a < 8; ++a) mx8[a] = -INFINITY;
+        if (kbase + kN - 1 <= pos_lo) {  // tile fully visible to every row of the tile
+#pragma unroll
+          for (int i = 0; i < kN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
         } else {
 #pragma unroll
           for (int i = 0; i < kN; ++i) {
-            const float x = kbase + i <= pos ? __uint_as_float(v[i]) * p.scale_log2 : -INFINITY;
-            v[i] = __float_as_uint(x);
-            mx = fmaxf(mx, x);
+            if (kbase + i > pos) v[i] = __float_as_uint(-INFINITY);
+            mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(v[i]));
           }
         }
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale;
         const bool grow = mx > m_used + 8.f;
-        if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? ex2(m_used - mx) : 1.f;
-          if (j >= 1) {
-            // O may only be rescaled once PV_{g-1} (the last one issued into it) completed.
-            // Here S_g is complete, hence PV_{g-2} too, and PV_g is not issued: the pvdone
-            // barrier has completed g-1 or g phases, so the parity wait is unambiguous.
-            mbar_wait(b_pvdone, (g - 1) & 1, 21);
-            tc_fence_after();
-            uint32_t o[32];
-            for (int c = 0; c < 4; ++c) {
-              TC_LD32(t_o + c * 32, o);
-              tc_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              TC_ST32(t_o + c * 32, o);
-            }
-            tc_wait_st();
-          }
-          l *= alpha;
-          if (grow) m_used = mx;
+        const bool any_grow = __any_sync(0xffffffffu, grow);
+        float alpha = 1.f;
+        if (grow) {
+          alpha = ex2(m_used - mx);
+          m_used = mx;
         }
-        // P = 2^(x - m_used) as bf16 pairs into the first 64 columns of this S buffer (the S
-        // values were already copied to registers); masked keys are -inf -> 0.
-        float lsum = 0.f;
+        // P = 2^(s*scale - m_used) as bf16 pairs into the first 64 columns of S_i (the S values
+        // are already in registers); masked keys are -inf -> 0.
+        const float neg_m = -m_used;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < kN; i += 2) {
-          const float p0 = ex2(__uint_as_float(v[i]) - m_used);
-          const float p1 = ex2(__uint_as_float(v[i + 1]) - m_used);
-          lsum += p0 + p1;
+          const float p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
+          const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
+          ls[(i >> 1) & 3] += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           v[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        l += lsum;
+        l = l * alpha + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
         TC_ST32(ts, v);
         TC_ST32(ts + 32, (v + 32));
+        // O_i holds PV_i(0..j-1), all complete (S_i(j), which we waited for, was committed
+        // after PV_i(j-1)); PV_i(j) is not issued before our pfull arrival.
+        if (any_grow && j >= 1) {
+#pragma unroll 1
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            TC_LD32(t_o + cc * 32, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            TC_ST32(t_o + cc * 32, o);
+          }
+        }
         tc_wait_st();
         tc_fence_before();
-        mbar_arrive(b_pfull);
+        mbar_arrive(b_p);
       }
-      // epilogue of this item: wait for its last PV (one ofull phase per item and O buffer)
-      mbar_wait(b_ofull + 8 * ob, (it_local >> 1) & 1, 22);
+      // epilogue of this item: wait for its last PV_i (one ofull phase per item)
+      mbar_wait(b_o, it_local & 1, 22 + qt);
       tc_fence_after();
-      const int t = it.tok0 + r / G;
       const float inv = 1.f / l;
       __nv_bfloat16* dst = p.o + (static_cast<int64_t>(it.qs + tq) * p.H + it.kvh * G + r % G) * kHD;
-      for (int c = 0; c < 4; ++c) {
+      for (int cc = 0; cc < 4; ++cc) {
         uint32_t o[32];
-        TC_LD32(t_o + c * 32, o);
+        TC_LD32(t_o + cc * 32, o);
         tc_wait_ld();
-        if (t < it.qlen) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+        if (t_row < it.qlen) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             uint32_t pk[4];
@@ -456,13 +506,14 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           }
         }
       }
+      // the next item's PV_i(0) (accumulate = 0) is issued only after our next pfull arrival,
+      // which program order puts after these TMEM reads
       tc_fence_before();
-      mbar_arrive(b_ofree + 8 * ob);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kWarpMma) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -533,6 +584,7 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
   GLMX_CHECK_LAUNCH();
 }
 
-int attn_tc_tokens_per_tile(int H, int Hkv) { return kM / (H / Hkv); }
+// Query tokens per work item: two 128-row tiles of 128/G tokens x G heads.
+int attn_tc_tokens_per_tile(int H, int Hkv) { return kQT * kM / (H / Hkv); }
 
 }  // namespace glmx

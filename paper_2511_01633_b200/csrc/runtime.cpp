@@ -798,3 +798,87 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
   }
   return GLMX_OK;
 }
+
+// ======================================================================== K3 kernel-level hook
+// Runs the paged attention kernel on caller-owned device buffers (tests + attention sweeps):
+// uploads the request metadata, builds the same longest-first work list as the engine, launches
+// `reps` times on `stream` and reports the mean kernel time (CUDA events on that stream).
+int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int Hkv, int hd,
+                       void* pool_base, uint64_t n_pages, uint32_t n_layers, uint32_t layer,
+                       uint32_t block_tokens, uint64_t n_req, const int32_t* q_start,
+                       const int32_t* q_len, const int32_t* ctx_len, const int32_t* block_table,
+                       int bt_stride, int reps, cudaStream_t s, float* out_ms) {
+  if (n_req == 0) return GLMX_OK;
+  if (H % Hkv != 0 || reps < 1) throw Error(GLMX_ERR_ARG, "bad attention arguments");
+  PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, static_cast<uint32_t>(Hkv),
+                block_tokens, static_cast<uint32_t>(hd)};
+  const int tpt = impl ? attn_tokens_per_tile(H, Hkv) : attn_tc_tokens_per_tile(H, Hkv);
+  std::vector<int2> work;
+  for (uint64_t r = 0; r < n_req; ++r) {
+    if (q_len[r] < 1 || ctx_len[r] < q_len[r] ||
+        static_cast<uint64_t>(q_start[r]) + q_len[r] > T ||
+        (ctx_len[r] + static_cast<int>(block_tokens) - 1) / static_cast<int>(block_tokens) > bt_stride)
+      throw Error(GLMX_ERR_ARG, "bad request geometry");
+    for (int t0 = 0; t0 < q_len[r]; t0 += tpt) work.push_back(make_int2(static_cast<int>(r), t0));
+  }
+  std::stable_sort(work.begin(), work.end(), [&](const int2& a, const int2& b) {
+    return ctx_len[a.x] - q_len[a.x] + a.y > ctx_len[b.x] - q_len[b.x] + b.y;
+  });
+  const size_t nr = n_req * 4, nbt = n_req * static_cast<size_t>(bt_stride) * 4;
+  const size_t bytes = 3 * nr + nbt + work.size() * 8;
+  std::vector<uint8_t> h(bytes);
+  std::memcpy(h.data(), q_start, nr);
+  std::memcpy(h.data() + nr, q_len, nr);
+  std::memcpy(h.data() + 2 * nr, ctx_len, nr);
+  std::memcpy(h.data() + 3 * nr, block_table, nbt);
+  std::memcpy(h.data() + 3 * nr + nbt, work.data(), work.size() * 8);
+  DBuf meta;
+  meta.reserve(bytes);
+  GLMX_CUDA(cudaMemcpyAsync(meta.p, h.data(), bytes, cudaMemcpyHostToDevice, s));
+  const uint8_t* dm = meta.as<uint8_t>();
+  AttnParams ap{};
+  ap.q = static_cast<const __nv_bfloat16*>(q);
+  ap.o = static_cast<__nv_bfloat16*>(o);
+  ap.pool = geom;
+  ap.layer = layer;
+  ap.q_start = reinterpret_cast<const int32_t*>(dm);
+  ap.q_len = reinterpret_cast<const int32_t*>(dm + nr);
+  ap.ctx_len = reinterpret_cast<const int32_t*>(dm + 2 * nr);
+  ap.block_table = reinterpret_cast<const int32_t*>(dm + 3 * nr);
+  ap.bt_stride = bt_stride;
+  ap.work = reinterpret_cast<const int2*>(dm + 3 * nr + nbt);
+  ap.n_work = static_cast<int>(work.size());
+  ap.H = H;
+  ap.Hkv = Hkv;
+  ap.scale_log2 = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)) * 1.4426950408889634);
+  alignas(64) uint8_t kv_map[128], q_map[128];
+  uint32_t rows = 0;
+  if (!impl) {
+    make_pool_tensor_map(geom, n_pages, kv_map, &rows);
+    make_q_tensor_map(q, T, H, Hkv, q_map);
+  }
+  cudaEvent_t e0, e1;
+  GLMX_CUDA(cudaEventCreate(&e0));
+  GLMX_CUDA(cudaEventCreate(&e1));
+  float ms = 0.f;
+  try {
+    GLMX_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < reps; ++i) {
+      if (impl)
+        paged_attention(ap, s);
+      else
+        paged_attention_tc(ap, kv_map, rows, q_map, s);
+    }
+    GLMX_CUDA(cudaEventRecord(e1, s));
+    GLMX_CUDA(cudaEventSynchronize(e1));
+    GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  } catch (...) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (out_ms) *out_ms = ms / static_cast<float>(reps);
+  return GLMX_OK;
+}

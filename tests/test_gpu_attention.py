@@ -1,0 +1,86 @@
+"""K3 (paged causal GQA prefill attention) against a plain PyTorch fp32 reference, through the
+C-ABI kernel hook glmx_attention_run.  Tolerance from the north star: bf16 output vs fp32 within
+max-abs 2e-2 and rel 1e-2 (|err| <= 2e-2 + 1e-2 * |ref|)."""
+import random
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-2, 1e-2
+
+
+def _case(reqs, L=2, Hkv=8, G=4, hd=128, B=16, layer=1, seed=0, extra_pages=7):
+    """reqs: list of (ctx_len, q_len).  Pages are handed out in a shuffled order so block
+    tables are non-contiguous; rows of different requests are packed back to back."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    n_pages = sum((c + B - 1) // B for c, _ in reqs) + extra_pages
+    pool = torch.randn((n_pages, L, 2, Hkv, B, hd), generator=g).to(torch.bfloat16).cuda()
+    rows = sum(q for _, q in reqs)
+    q = torch.randn((rows, Hkv * G, hd), generator=g).to(torch.bfloat16).cuda()
+    perm = list(range(n_pages))
+    random.Random(seed).shuffle(perm)
+    bt, qs, ql, ctx = [], [], [], []
+    p = r = 0
+    for c, n in reqs:
+        k = (c + B - 1) // B
+        bt.append(perm[p:p + k])
+        p += k
+        qs.append(r)
+        ql.append(n)
+        ctx.append(c)
+        r += n
+    return q, pool, qs, ql, ctx, bt, layer
+
+
+def _check(impl, reqs, **kw):
+    import paper_2511_01633_b200.attention as A
+
+    q, pool, qs, ql, ctx, bt, layer = _case(reqs, **kw)
+    o = torch.full_like(q, float("nan"))
+    A.paged_attention(q, o, pool, qs, ql, ctx, bt, layer=layer, impl=impl)
+    torch.cuda.synchronize()
+    ref = A.reference_attention(q, pool, qs, ql, ctx, bt, layer=layer)
+    err = (o.float() - ref).abs()
+    bound = ATOL + RTOL * ref.abs()
+    assert torch.isfinite(o.float()).all(), "unwritten or non-finite output rows"
+    bad = (err > bound).sum().item()
+    assert bad == 0, f"{bad} elements out of tolerance, max err {err.max().item():.4g}"
+    return err.max().item()
+
+
+MIXED = [(1, 1), (16, 16), (37, 37), (200, 5), (300, 33), (129, 64), (1000, 130), (70, 65),
+         (2050, 1), (513, 97)]
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
+def test_mixed_requests(impl):
+    _check(impl, MIXED)
+
+
+def test_long_prefix_short_suffix():
+    # C5 shape: long cached prefix, ~100-token suffix
+    _check(0, [(4096 + 100, 100), (8200, 120), (3000, 64)], seed=1)
+
+
+def test_full_causal_prefill():
+    # cold prompt: every key computed in this batch (diagonal tiles everywhere)
+    _check(0, [(1100, 1100), (64, 64), (65, 65)], seed=2)
+
+
+def test_many_items_more_than_sms():
+    # > 148 work items: the persistent CTAs walk several items each (pipeline across items)
+    reqs = [(random.Random(i).randrange(40, 900), 0) for i in range(40)]
+    reqs = [(c, max(1, min(c, random.Random(100 + i).randrange(1, 200)))) for i, (c, _) in
+            enumerate(reqs)]
+    _check(0, reqs, seed=3)
+
+
+def test_gqa_8_heads_per_kv_head():
+    _check(0, [(500, 77), (40, 40)], Hkv=4, G=8, seed=4)
+
+
+def test_layer_offset_and_single_layer_pool():
+    _check(0, [(333, 33)], L=1, layer=0, seed=5)
