@@ -279,6 +279,15 @@ void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
 int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
                    const int32_t* dst_pages, uint64_t n, void* stream);
 float glmx_pool_last_copy_ms(const glmx_kv* dst);
+/* K3's stream-K schedule (host only, no device): items w = i * n_kv_heads + h of work entries
+ * work_xy[i] = (request, first token) are flattened into 128-key tiles and cut into <= n_sm
+ * equal CTA ranges.  out_pieces [(n_work*n_kv_heads + n_sm) x 4] = (item, j0, j1, partial slot or
+ * -1), out_cta_off [n_sm + 1], out_combine [n_sm x 4] = (item, first slot, n slots, 0);
+ * out_counts = {pieces, grid, combines, partial slots, total tiles}. */
+int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
+                       const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
+                       int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
+                       int32_t* out_combine, int64_t out_counts[5]);
 /* K3 on caller-owned DEVICE buffers — the attention core of the prefill step that replaces the
  * c_prefill cost term (orchestrator.cpp:131-132); no reference counterpart (tensor
  * math is builder-defined).  q/o [n_q_rows][n_heads][head_dim] bf16 (q RoPE'd), pool = pages x

@@ -501,6 +501,27 @@ int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
 }
 float glmx_pool_last_copy_ms(const glmx_kv* dst) { return dst->last_copy_ms; }
 
+int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
+                       const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
+                       int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
+                       int32_t* out_combine, int64_t out_counts[5]) {
+  return guarded([&] {
+    if (n_work < 0 || n_kv_heads < 1 || tokens_per_item < 1 || n_sm < 1)
+      throw Error(GLMX_ERR_ARG, "bad schedule arguments");
+    AttnSchedule sc;
+    sc.pieces = reinterpret_cast<AttnPiece*>(out_pieces);
+    sc.cta_off = out_cta_off;
+    sc.combine = reinterpret_cast<AttnCombine*>(out_combine);
+    build_attn_schedule(work_xy, n_work, n_kv_heads, q_len, ctx_len, tokens_per_item, 128, n_sm, sc);
+    out_counts[0] = sc.n_pieces;
+    out_counts[1] = sc.grid;
+    out_counts[2] = sc.n_combine;
+    out_counts[3] = sc.n_partials;
+    out_counts[4] = sc.total_tiles;
+    return GLMX_OK;
+  });
+}
+
 int glmx_attention_run(int32_t impl, const void* q, void* o, uint64_t n_q_rows, int32_t n_heads,
                        int32_t n_kv_heads, int32_t head_dim, void* pool, uint64_t n_pages,
                        uint32_t n_layers, uint32_t layer, uint32_t block_tokens, uint64_t n_req,

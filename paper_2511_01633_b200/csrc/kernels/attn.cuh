@@ -35,7 +35,18 @@ namespace glmx {
 int attn_tc_tokens_per_tile(int H, int Hkv);
 void make_pool_tensor_map(const PoolGeom& g, uint64_t pages, void* out_map, uint32_t* rows_total);
 void make_q_tensor_map(const void* q, uint64_t T, int H, int Hkv, void* out_map);
-// Persistent launch: min(n_work * Hkv, 148) CTAs walk the work list.
+// Stream-K schedule on the device (host/attn_sched.hpp packed by the caller) + the partial
+// workspace: part_o [2 * 148][256][128] fp32, part_ml [2 * 148][256] float2.
+struct AttnTcSched {
+  const int4* pieces;
+  const int* cta_off;
+  const int4* combine;
+  int grid, n_combine;
+  float* part_o;
+  float2* part_ml;
+};
+int attn_tc_partial_rows();  // rows per partial slot (256)
+// Persistent launch: sc.grid CTAs walk their pieces; then the combine pass for split items.
 void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
-                        const void* q_map, cudaStream_t s);
+                        const void* q_map, const AttnTcSched& sc, cudaStream_t s);
 }  // namespace glmx

@@ -202,7 +202,10 @@ __device__ __forceinline__ uint32_t sw128(int r, int c16) {
 struct TcParams {
   AttnParams a;
   uint32_t rows_total;  // rows of the pool tensor map (OOB row -> zero fill)
-  int n_items;          // n_work * Hkv
+  const int4* pieces;   // AttnPiece {item, j0, j1, part} (host/attn_sched.hpp)
+  const int* cta_off;   // pieces of CTA c: [cta_off[c], cta_off[c+1])
+  float* part_o;        // [part][256 rows][128] unnormalised O of split items
+  float2* part_ml;      // [part][256 rows] (reference max, row sum)
 };
 
 struct Item {
@@ -300,18 +303,19 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         }
         ++c;
       };
-      for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
-        const Item it = item_of(p, w);
+      for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
+        const int4 pz = tp.pieces[pc];
+        const Item it = item_of(p, pz.x);
         const int32_t* bt = p.block_table + static_cast<int64_t>(it.req) * p.bt_stride;
-        load_kv(it, bt, 0, 0);
-        if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // last S of prev item done
+        load_kv(it, bt, pz.y, 0);
+        if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // last S of prev piece done
         mbar_expect_tx(b_qfull, kQT * kTile);
         for (int i = 0; i < kQT; ++i)
           for (int hf = 0; hf < 2; ++hf)
             tma_load_3d(sbase + kOffQ + i * kTile + hf * kHalf, &q_map, hf * 64, it.kvh * G,
                         it.qs + it.tok0 + i * (kM / G), b_qfull);
-        load_kv(it, bt, 0, 1);
-        for (int j = 1; j < it.n_kt; ++j) {
+        load_kv(it, bt, pz.y, 1);
+        for (int j = pz.y + 1; j < pz.z; ++j) {
           load_kv(it, bt, j, 0);
           load_kv(it, bt, j, 1);
         }
@@ -363,9 +367,9 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         ring_pos(cc, slot, use);
         tc_commit(b_empty + 8 * slot);
       };
-      for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
-        const Item it = item_of(p, w);
-        const int n = it.n_kt;
+      for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
+        const int4 pz = tp.pieces[pc];
+        const int n = pz.z - pz.y;
         // load indices of this item: K_j = c + 2j, V_j = c + 2j + 1
         wait_full(c, 13);
         mbar_wait(b_qfull, it_local & 1, 12);
@@ -413,14 +417,15 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
     const float scale = p.scale_log2;
     uint32_t v[kN];
     int g = 0, it_local = 0;
-    for (int w = blockIdx.x; w < tp.n_items; w += gridDim.x, ++it_local) {
-      const Item it = item_of(p, w);
+    for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
+      const int4 pz = tp.pieces[pc];
+      const Item it = item_of(p, pz.x);
       const int t_row = it.tok0 + qt * (kM / G) + r / G;  // query token of this row
       const int tq = min(t_row, it.qlen - 1);
       const int pos = it.ctx - it.qlen + tq;
       const int pos_lo = it.ctx - it.qlen + it.tok0 + qt * (kM / G);  // smallest in the tile
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < it.n_kt; ++j, ++g) {
+      for (int j = pz.y; j < pz.z; ++j, ++g) {
         mbar_wait(b_s, g & 1, 20 + qt);
         tc_fence_after();
 #pragma unroll
@@ -467,7 +472,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         TC_ST32(ts + 32, (v + 32));
         // O_i holds PV_i(0..j-1), all complete (S_i(j), which we waited for, was committed
         // after PV_i(j-1)); PV_i(j) is not issued before our pfull arrival.
-        if (any_grow && j >= 1) {
+        if (any_grow && j > pz.y) {
 #pragma unroll 1
           for (int cc = 0; cc < 4; ++cc) {
             uint32_t o[32];
@@ -485,24 +490,42 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       // epilogue of this item: wait for its last PV_i (one ofull phase per item)
       mbar_wait(b_o, it_local & 1, 22 + qt);
       tc_fence_after();
-      const float inv = 1.f / l;
-      __nv_bfloat16* dst = p.o + (static_cast<int64_t>(it.qs + tq) * p.H + it.kvh * G + r % G) * kHD;
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t o[32];
-        TC_LD32(t_o + cc * 32, o);
-        tc_wait_ld();
-        if (t_row < it.qlen) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
+      if (pz.w >= 0) {
+        // split item: unnormalised O + (reference max, row sum) for the combine pass
+        const int64_t prow = static_cast<int64_t>(pz.w) * (kQT * kM) + qt * kM + r;
+        float4* dst = reinterpret_cast<float4*>(tp.part_o + prow * kHD);
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          TC_LD32(t_o + cc * 32, o);
+          tc_wait_ld();
+          if (t_row < it.qlen) {
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t pk[4];
+            for (int q4 = 0; q4 < 8; ++q4)
+              dst[cc * 8 + q4] = make_float4(__uint_as_float(o[4 * q4]), __uint_as_float(o[4 * q4 + 1]),
+                                             __uint_as_float(o[4 * q4 + 2]), __uint_as_float(o[4 * q4 + 3]));
+          }
+        }
+        if (t_row < it.qlen) tp.part_ml[prow] = make_float2(m_used, l);
+      } else {
+        const float inv = 1.f / l;
+        __nv_bfloat16* dst = p.o + (static_cast<int64_t>(it.qs + tq) * p.H + it.kvh * G + r % G) * kHD;
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          TC_LD32(t_o + cc * 32, o);
+          tc_wait_ld();
+          if (t_row < it.qlen) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int i = q4 * 8 + 2 * k;
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-              pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i = q4 * 8 + 2 * k;
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+                pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              d4[q4] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-            d4[q4] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
       }
@@ -517,6 +540,41 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// Merge the partials of split items: one warp per query row, 4 dims per lane.
+__global__ void __launch_bounds__(256)
+attn_combine_kernel(AttnParams p, const int4* __restrict__ combine, const float* __restrict__ part_o,
+                    const float2* __restrict__ part_ml) {
+  const int4 cb = combine[blockIdx.x];
+  const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);  // row of the item, [0, 256)
+  const int lane = threadIdx.x & 31;
+  const Item it = item_of(p, cb.x);
+  const int G = p.H / p.Hkv;
+  const int qt = rr / kM, r = rr % kM;
+  const int t_row = it.tok0 + qt * (kM / G) + r / G;
+  if (t_row >= it.qlen) return;
+  float m = -INFINITY;
+  for (int k = 0; k < cb.z; ++k) m = fmaxf(m, part_ml[static_cast<int64_t>(cb.y + k) * (kQT * kM) + rr].x);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float l = 0.f;
+  for (int k = 0; k < cb.z; ++k) {
+    const int64_t prow = static_cast<int64_t>(cb.y + k) * (kQT * kM) + rr;
+    const float2 ml = part_ml[prow];
+    const float wgt = ml.x == -INFINITY ? 0.f : ex2(ml.x - m);
+    const float4 o = reinterpret_cast<const float4*>(part_o + prow * kHD)[lane];
+    acc.x += wgt * o.x;
+    acc.y += wgt * o.y;
+    acc.z += wgt * o.z;
+    acc.w += wgt * o.w;
+    l += wgt * ml.y;
+  }
+  const float inv = 1.f / l;
+  __nv_bfloat16* dst = p.o + (static_cast<int64_t>(it.qs + t_row) * p.H + it.kvh * G + r % G) * kHD + lane * 4;
+  __nv_bfloat162 a = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  __nv_bfloat162 b = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  *reinterpret_cast<uint2*>(dst) = pk;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -566,8 +624,8 @@ void make_q_tensor_map(const void* q, uint64_t T, int H, int Hkv, void* out_map)
 }
 
 void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
-                        const void* q_map, cudaStream_t s) {
-  if (p.n_work <= 0) return;
+                        const void* q_map, const AttnTcSched& sc, cudaStream_t s) {
+  if (p.n_work <= 0 || sc.grid <= 0) return;
   if (p.pool.head_dim != kHD || p.pool.block_tokens != kB)
     throw Error(GLMX_ERR_ARG, "paged attention is built for head_dim 128 and 16-token pages");
   const int G = p.H / p.Hkv;
@@ -577,12 +635,17 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
     GLMX_CUDA(cudaFuncSetAttribute(paged_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr = true;
   }
-  TcParams tp{p, rows_total, p.n_work * p.Hkv};
-  const int grid = std::min(tp.n_items, kNumSMs);
-  paged_attn_tc_kernel<<<grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
-                                                     *reinterpret_cast<const CUtensorMap*>(q_map), tp);
+  TcParams tp{p, rows_total, sc.pieces, sc.cta_off, sc.part_o, sc.part_ml};
+  paged_attn_tc_kernel<<<sc.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
+                                                        *reinterpret_cast<const CUtensorMap*>(q_map), tp);
   GLMX_CHECK_LAUNCH();
+  if (sc.n_combine > 0) {
+    attn_combine_kernel<<<dim3(sc.n_combine, kQT * kM / 8), 256, 0, s>>>(p, sc.combine, sc.part_o, sc.part_ml);
+    GLMX_CHECK_LAUNCH();
+  }
 }
+
+int attn_tc_partial_rows() { return kQT * kM; }
 
 // Query tokens per work item: two 128-row tiles of 128/G tokens x G heads.
 int attn_tc_tokens_per_tile(int H, int Hkv) { return kQT * kM / (H / Hkv); }

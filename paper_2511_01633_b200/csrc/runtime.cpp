@@ -421,6 +421,11 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->o_bt = o; o = align_up(o + R * e->bt_stride * 4, 256);
   e->o_work = o; o = align_up(o + max_work * 8, 256);
   e->o_last = o; o = align_up(o + R * 4, 256);
+  e->o_sched = o;
+  o = align_up(o + attn_sched_bytes(static_cast<int>(max_work * Hkv), kNumSMs, &e->o_sc_pieces,
+                                    &e->o_sc_cta, &e->o_sc_comb), 256);
+  e->part_o.reserve(static_cast<size_t>(2 * kNumSMs) * attn_tc_partial_rows() * hd * 4);
+  e->part_ml.reserve(static_cast<size_t>(2 * kNumSMs) * attn_tc_partial_rows() * 8);
   e->max_copies = T / B + R + 16;  // peer page copies per batch (src, dst int32 each)
   e->o_copy = o; o = align_up(o + e->max_copies * 8, 256);
   e->meta_bytes = o;
@@ -431,6 +436,20 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
 }
 
 namespace {
+
+// Packs the K3 stream-K schedule of the staged work list into the host metadata block.
+void stage_attn_schedule(glmx_engine* e, uint8_t* hm, const int2* work, int n_work,
+                         const int32_t* q_len, const int32_t* ctx_len) {
+  AttnSchedule sc;
+  sc.pieces = reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_pieces);
+  sc.cta_off = reinterpret_cast<int32_t*>(hm + e->o_sched + e->o_sc_cta);
+  sc.combine = reinterpret_cast<AttnCombine*>(hm + e->o_sched + e->o_sc_comb);
+  build_attn_schedule(reinterpret_cast<const int32_t*>(work), n_work,
+                      static_cast<int>(e->m->cfg.n_kv_heads), q_len, ctx_len, e->tpt, 128,
+                      kNumSMs, sc);
+  e->sc_grid = sc.grid;
+  e->sc_ncomb = sc.n_combine;
+}
 
 // Runs the decoder over the staged batch: T rows (tokens/pos/slot), R requests (attention
 // metadata), n_last rows whose final hidden states produce logits + greedy tokens.
@@ -458,6 +477,10 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   ap.Hkv = Hkv;
   ap.scale_log2 = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)) * 1.4426950408889634);
   (void)R;
+  AttnTcSched sc{reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_pieces),
+                 reinterpret_cast<const int*>(meta + e->o_sched + e->o_sc_cta),
+                 reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_comb),
+                 e->sc_grid, e->sc_ncomb, e->part_o.as<float>(), e->part_ml.as<float2>()};
   Prof all(e, kCatAll);
   {
     Prof p(e, kCatOther);
@@ -484,7 +507,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
       if (e->attn_impl)
         paged_attention(ap, s);
       else
-        paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, s);
+        paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, sc, s);
     }
     {
       Prof p(e, kCatGemm);
@@ -630,6 +653,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     int ka = h_ctx[a.x] - h_ql[a.x] + a.y, kb = h_ctx[b.x] - h_ql[b.x] + b.y;
     return ka > kb;
   });
+  if (!e->attn_impl) stage_attn_schedule(e, hm, h_work, n_work, h_ql, h_ctx);
   e->last_T = T;
   e->last_R = R;
   e->last_work = n_work;
@@ -774,6 +798,7 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
       h_last[j] = j;
       rq.ctx_len = p + 1;
     }
+    if (!e->attn_impl) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
     GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
     GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
     const int32_t* in_tok = st == 0 ? d_prev : d_seq + static_cast<size_t>(st - 1) * R;
@@ -825,28 +850,49 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
     return ctx_len[a.x] - q_len[a.x] + a.y > ctx_len[b.x] - q_len[b.x] + b.y;
   });
   const size_t nr = n_req * 4, nbt = n_req * static_cast<size_t>(bt_stride) * 4;
-  const size_t bytes = 3 * nr + nbt + work.size() * 8;
+  auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_ql = a16(nr), o_ctx = o_ql + a16(nr), o_bt = o_ctx + a16(nr);
+  const size_t o_wk = o_bt + a16(nbt);
+  size_t o_pc = 0, o_cta = 0, o_cb = 0;
+  const size_t sched_bytes = attn_sched_bytes(static_cast<int>(work.size()) * Hkv, kNumSMs, &o_pc, &o_cta, &o_cb);
+  const size_t o_sched = (o_wk + work.size() * 8 + 255) & ~size_t(255);
+  const size_t bytes = o_sched + sched_bytes;
   std::vector<uint8_t> h(bytes);
   std::memcpy(h.data(), q_start, nr);
-  std::memcpy(h.data() + nr, q_len, nr);
-  std::memcpy(h.data() + 2 * nr, ctx_len, nr);
-  std::memcpy(h.data() + 3 * nr, block_table, nbt);
-  std::memcpy(h.data() + 3 * nr + nbt, work.data(), work.size() * 8);
-  DBuf meta;
+  std::memcpy(h.data() + o_ql, q_len, nr);
+  std::memcpy(h.data() + o_ctx, ctx_len, nr);
+  std::memcpy(h.data() + o_bt, block_table, nbt);
+  std::memcpy(h.data() + o_wk, work.data(), work.size() * 8);
+  AttnSchedule hs;
+  hs.pieces = reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pc);
+  hs.cta_off = reinterpret_cast<int32_t*>(h.data() + o_sched + o_cta);
+  hs.combine = reinterpret_cast<AttnCombine*>(h.data() + o_sched + o_cb);
+  if (!impl)
+    build_attn_schedule(reinterpret_cast<const int32_t*>(work.data()), static_cast<int>(work.size()),
+                        Hkv, q_len, ctx_len, tpt, 128, kNumSMs, hs);
+  DBuf meta, part_o, part_ml;
   meta.reserve(bytes);
   GLMX_CUDA(cudaMemcpyAsync(meta.p, h.data(), bytes, cudaMemcpyHostToDevice, s));
+  if (!impl && hs.n_combine > 0) {
+    part_o.reserve(static_cast<size_t>(hs.n_partials) * attn_tc_partial_rows() * hd * 4);
+    part_ml.reserve(static_cast<size_t>(hs.n_partials) * attn_tc_partial_rows() * 8);
+  }
   const uint8_t* dm = meta.as<uint8_t>();
+  AttnTcSched sc{reinterpret_cast<const int4*>(dm + o_sched + o_pc),
+                 reinterpret_cast<const int*>(dm + o_sched + o_cta),
+                 reinterpret_cast<const int4*>(dm + o_sched + o_cb), hs.grid, hs.n_combine,
+                 part_o.as<float>(), part_ml.as<float2>()};
   AttnParams ap{};
   ap.q = static_cast<const __nv_bfloat16*>(q);
   ap.o = static_cast<__nv_bfloat16*>(o);
   ap.pool = geom;
   ap.layer = layer;
   ap.q_start = reinterpret_cast<const int32_t*>(dm);
-  ap.q_len = reinterpret_cast<const int32_t*>(dm + nr);
-  ap.ctx_len = reinterpret_cast<const int32_t*>(dm + 2 * nr);
-  ap.block_table = reinterpret_cast<const int32_t*>(dm + 3 * nr);
+  ap.q_len = reinterpret_cast<const int32_t*>(dm + o_ql);
+  ap.ctx_len = reinterpret_cast<const int32_t*>(dm + o_ctx);
+  ap.block_table = reinterpret_cast<const int32_t*>(dm + o_bt);
   ap.bt_stride = bt_stride;
-  ap.work = reinterpret_cast<const int2*>(dm + 3 * nr + nbt);
+  ap.work = reinterpret_cast<const int2*>(dm + o_wk);
   ap.n_work = static_cast<int>(work.size());
   ap.H = H;
   ap.Hkv = Hkv;
@@ -867,7 +913,7 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
       if (impl)
         paged_attention(ap, s);
       else
-        paged_attention_tc(ap, kv_map, rows, q_map, s);
+        paged_attention_tc(ap, kv_map, rows, q_map, sc, s);
     }
     GLMX_CUDA(cudaEventRecord(e1, s));
     GLMX_CUDA(cudaEventSynchronize(e1));

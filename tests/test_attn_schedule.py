@@ -1,0 +1,91 @@
+"""K3 persistent-CTA schedule (host C++, no GPU): every key tile of every item is covered exactly
+once; with many items whole items are dealt longest-first round-robin; with few items each item is
+split into near-equal pieces (one per CTA) with consecutive partial slots for the combine pass."""
+import random
+
+import pytest
+
+from paper_2511_01633_b200.attention import schedule
+
+
+def tiles_of(t0, ql, ctx, tpi=64):
+    return (ctx - ql + min(t0 + tpi, ql) - 1) // 128 + 1
+
+
+def check(reqs, n_kv=8, n_sm=148, tpi=64):
+    work = [(r, t0) for r, (ctx, ql) in enumerate(reqs) for t0 in range(0, ql, tpi)]
+    ql = [q for _, q in reqs]
+    ctx = [c for c, _ in reqs]
+    s = schedule(work, ql, ctx, n_kv, tpi, n_sm)
+    n_items = len(work) * n_kv
+    need = [tiles_of(work[w // n_kv][1], ql[work[w // n_kv][0]], ctx[work[w // n_kv][0]], tpi)
+            for w in range(n_items)]
+    assert s["total_tiles"] == sum(need)
+    covered = [[] for _ in range(n_items)]
+    loads = []
+    for c in range(s["grid"]):
+        load = 0
+        for item, j0, j1, part in s["pieces"][s["cta_off"][c]:s["cta_off"][c + 1]]:
+            assert 0 <= j0 < j1 <= need[item]
+            covered[item].append((j0, j1, part))
+            load += j1 - j0
+        loads.append(load)
+    for w in range(n_items):
+        segs = sorted(covered[w])
+        assert segs[0][0] == 0 and segs[-1][1] == need[w]
+        assert all(a[1] == b[0] for a, b in zip(segs, segs[1:])), "gap or overlap"
+        parts = [p for _, _, p in segs]
+        if len(segs) == 1:
+            assert parts == [-1]
+        else:
+            assert sorted(parts) == list(range(min(parts), min(parts) + len(parts)))
+    assert s["n_partials"] <= 2 * n_sm and s["grid"] <= n_sm
+    if n_items * 2 > n_sm:  # round-robin of whole items, longest first
+        assert not s["combine"]
+        firsts = [s["pieces"][s["cta_off"][c]] for c in range(s["grid"])]
+        lens = [p[2] for p in firsts]
+        assert lens == sorted(lens, reverse=True)
+        assert max(loads) - min(loads) <= max(need)
+    else:  # split: one piece per CTA, pieces of an item differ by <= 1 tile
+        assert all(s["cta_off"][c + 1] - s["cta_off"][c] == 1 for c in range(s["grid"]))
+        for w in range(n_items):
+            sz = [b - a for a, b, _ in covered[w]]
+            assert max(sz) - min(sz) <= 1
+    comb_items = {c[0] for c in s["combine"]}
+    assert comb_items == {w for w in range(n_items) if len(covered[w]) > 1}
+    return s
+
+
+def test_c5_batch_uses_whole_items():
+    s = check([(8192 + 128, 128)] * 8)  # 128 items of 65 tiles on 148 SMs
+    assert s["grid"] == 128 and not s["combine"]
+
+
+def test_single_long_query_is_split_across_sms():
+    s = check([(32768 + 100, 100)])  # 16 items -> 9 pieces each
+    assert s["grid"] == 144 and len(s["combine"]) == 16 and s["n_partials"] == 144
+
+
+def test_short_items_are_never_split():
+    s = check([(200, 40)] * 64)
+    assert not s["combine"]
+
+
+def test_ragged_random_batches():
+    rnd = random.Random(0)
+    for trial in range(30):
+        reqs = []
+        for _ in range(rnd.randrange(1, 70)):
+            ql = rnd.randrange(1, 400)
+            reqs.append((ql + rnd.choice([0, rnd.randrange(0, 5000)]), ql))
+        check(reqs, n_kv=rnd.choice([8, 4]), n_sm=rnd.choice([148, 7, 1]))
+
+
+def test_fewer_tiles_than_sms():
+    s = check([(1, 1)])
+    assert s["grid"] == 8 and len(s["pieces"]) == 8
+
+
+@pytest.mark.parametrize("n_sm", [1, 2, 148])
+def test_single_long_item(n_sm):
+    check([(32768, 1)], n_kv=1, n_sm=n_sm)

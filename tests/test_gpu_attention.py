@@ -84,3 +84,9 @@ def test_gqa_8_heads_per_kv_head():
 
 def test_layer_offset_and_single_layer_pool():
     _check(0, [(333, 33)], L=1, layer=0, seed=5)
+
+
+def test_single_long_query_split_and_combined():
+    # 16 items < 148 / 2: every item's key range is split over ~9 CTAs, partials merged
+    _check(0, [(6000 + 100, 100)], seed=6)
+    _check(0, [(3000, 1)], seed=7)  # decode-like: one row, 8 items
