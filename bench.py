@@ -104,6 +104,17 @@ class ClockSampler:
                 "samples": len(rows), "reasons": sorted(reasons)}
 
 
+def load_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read + dram__bytes_write) of each kernel class from the
+    committed ncu launch list of a C2 rotation (profiles/r1_c2_traffic.json, made by
+    scripts/launch_summary.py --traffic); {} when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_c2_traffic.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -249,6 +260,9 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
+    prof_range = os.environ.get("GLMX_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     tokens = computed = cached = calls = chunks = finished = 0
@@ -257,6 +271,7 @@ def main():
     work = {"attn_flops": 0.0, "attn_bytes": 0.0, "append_bytes": 0.0, "linear_flops": 0.0}
     h2d = d2h = 0
     chunk_ms = 0.0
+    k1_bytes = 0
     k1_rotations = 0
     for _ in range(args.steps):
         r = wl.rotation()
@@ -264,7 +279,9 @@ def main():
         fwd_ms += tm["forward"]
         for k in cat_ms:
             cat_ms[k] += tm[k]
-        chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h) if r.chunks else 0.0
+        if r.chunks:
+            chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h)
+            k1_bytes += r.chunk_bytes
         tokens += r.prompt_tokens
         computed += r.computed_tokens
         cached += r.cached_tokens
@@ -281,6 +298,8 @@ def main():
         d2h += r.calls * 4 + r.chunks * 1200
     ev1.record()
     torch.cuda.synchronize()
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -303,26 +322,55 @@ def main():
         return
 
     peaks, peak_kind = measured_peaks()
+    hbm = peaks["hbm_gbs"]
+    # the timed region is a long back-to-back step: tensor work runs at the sustained (power-cap)
+    # GEMM rate; HBM-bound kernels against the copy bandwidth
+    tc_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = load_traffic()
     attn_ms = tm["attention"]
     attn_tflops = wk["attn_flops"] / (attn_ms * 1e-3) / 1e12 if attn_ms > 0 else 0.0
     attn_gbs = wk["attn_bytes"] / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
-    # attention intensity ~4*s flop/byte: tensor-bound only above the ridge
-    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    ridge = tc_peak * 1e12 / (hbm * 1e9)
     intensity = wk["attn_flops"] / max(1.0, wk["attn_bytes"])
-    if intensity >= ridge:
-        roof = {"bound": "tensor", "achieved": attn_tflops, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": attn_tflops / peaks["bf16_tflops"]}
-    else:
-        roof = {"bound": "hbm", "achieved": attn_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": attn_gbs / peaks["hbm_gbs"]}
-    roof.update({"kernel": "K3 paged_attn_tc (tcgen05/TMEM/TMA)" if os.environ.get("GLMX_ATTN", "tc") != "mma" else "K3 paged_attn_mma (mma.sync baseline)", "traffic": None,
-                 "peak_kind": peak_kind, "intensity_flop_per_byte": intensity,
-                 "kernel_ms_total": attn_ms, "kernel_ms_per_step": attn_ms / args.steps,
-                 "share_of_forward": attn_ms / max(1e-9, tm["forward"]),
-                 "gemm_ms_per_step": tm["gemm"] / args.steps,
-                 "elementwise_ms_per_step": tm["elementwise"] / args.steps,
-                 "append_ms_per_step": tm["kv_append"] / args.steps,
-                 "gemm_tflops": wk["linear_flops"] / max(1e-9, tm["gemm"] * 1e-3) / 1e12})
+    gemm_tflops = wk["linear_flops"] / max(1e-9, tm["gemm"] * 1e-3) / 1e12
+    append_gbs = wk["append_bytes"] / max(1e-9, tm["kv_append"] * 1e-3) / 1e9
+    fwd = max(1e-9, tm["forward"])
+    n_launch_layers = args.steps * cfg.n_layers
+    kernels = [
+        {"kernel": "K3 paged_attn_tc (tcgen05/TMEM/TMA)", "share_of_forward": attn_ms / fwd,
+         "ms_per_launch": attn_ms / n_launch_layers, "intensity_flop_per_byte": intensity,
+         **({"bound": "tensor", "achieved": attn_tflops, "peak": tc_peak, "unit": "TFLOP/s",
+             "frac": attn_tflops / tc_peak} if intensity >= ridge else
+            {"bound": "hbm", "achieved": attn_gbs, "peak": hbm, "unit": "GB/s",
+             "frac": attn_gbs / hbm}),
+         "note": "C2 suffixes are short (mean q 7-120 tokens over 55-280-token contexts): "
+                 "latency-bound items; the tensor-bound regime is C5 (scripts/bench_attn.py)"},
+        {"kernel": "K2 rope_kv_append (fused RoPE + paged KV append)", "bound": "hbm",
+         "share_of_forward": tm["kv_append"] / fwd, "achieved": append_gbs, "peak": hbm,
+         "unit": "GB/s", "frac": append_gbs / hbm,
+         "ms_per_launch": tm["kv_append"] / n_launch_layers},
+    ]
+    if chunk_ms > 0:
+        k1_gbs = k1_bytes / (chunk_ms * 1e-3) / 1e9
+        kernels.append({"kernel": "K1 chunk_build (select+render+emit, 2 cub scans)",
+                        "bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
+                        "frac": k1_gbs / hbm, "ms_per_rotation": chunk_ms / max(1, k1_rotations),
+                        "overlapped_with_prefill": True,
+                        "note": "64 chunks per rotation: latency-bound, hidden behind the prefill "
+                                "on the graph stream"})
+    # dominant kernel of the step by device time: the cuBLAS GEMMs (Llama-3-8B linears)
+    roof = {"bound": "tensor", "achieved": gemm_tflops, "peak": tc_peak, "unit": "TFLOP/s",
+            "frac": gemm_tflops / tc_peak,
+            "kernel": "cuBLAS bf16 GEMM (cublasGemmEx, library; QKV/O/gate-up/down/lm_head)",
+            "traffic": traffic.get("gemm"), "traffic_unit": "bytes per launch (ncu, profiles/)",
+            "peak_kind": peak_kind + " sustained bf16",
+            "share_of_forward": tm["gemm"] / fwd,
+            "gemm_ms_per_step": tm["gemm"] / args.steps,
+            "attention_ms_per_step": attn_ms / args.steps,
+            "append_ms_per_step": tm["kv_append"] / args.steps,
+            "elementwise_ms_per_step": tm["elementwise"] / args.steps}
+    for kd in kernels:
+        kd["traffic"] = traffic.get(kd["kernel"].split()[0])
     value = tokens / (fwd_ms * 1e-3)
     e2e = tokens / (wall_ms * 1e-3)
     n_layers = cfg.n_layers
@@ -345,6 +393,7 @@ def main():
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "roofline": roof,
+        "kernels": kernels,
         # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
         # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
         "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations),

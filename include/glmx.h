@@ -269,7 +269,7 @@ int glmx_engine_replay_forward(glmx_engine* e);
  * [4] other elementwise, [5] H2D, [6] D2H */
 int glmx_engine_last_timings(const glmx_engine* e, float out7[7]);
 /* algorithmic work of the last forward: [0] attention FLOPs, [1] attention bytes (KV read +
- * Q in + O out), [2] KV-append bytes, [3] linear FLOPs, [4] computed tokens, [5] context tokens */
+ * Q in + O out), [2] K2 bytes (qkv read + q write + K/V page writes), [3] linear FLOPs, [4] computed tokens, [5] context tokens */
 int glmx_engine_last_work(const glmx_engine* e, double out6[6]);
 void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
 
@@ -279,7 +279,17 @@ void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
 int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
                    const int32_t* dst_pages, uint64_t n, void* stream);
 float glmx_pool_last_copy_ms(const glmx_kv* dst);
-/* K3's stream-K schedule (host only, no device): items w = i * n_kv_heads + h of work entries
+/* K2 on caller-owned DEVICE buffers: qkv [n_tokens][(H + 2 Hkv) * head_dim] bf16 (the QKV
+ * projection), pos/slot (device int32 / int64: absolute position, page * block_tokens + offset)
+ * -> q_out [n_tokens][H][head_dim] (RoPE'd) and K (RoPE'd), V written into the pool pages of
+ * `layer`.  The KV write replaces the reference's block insert (cache.cpp:95-105 inserts the ids;
+ * the GPU fills their pages).  Launches `reps` times; out_ms = mean device ms per launch. */
+int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* slot,
+                            uint64_t n_tokens, int32_t n_heads, int32_t n_kv_heads,
+                            int32_t head_dim, float rope_theta, void* pool, uint32_t n_layers,
+                            uint32_t layer, uint32_t block_tokens, void* q_out, int32_t reps,
+                            void* stream, float* out_ms);
+/* K3's persistent-CTA schedule (host only, no device): items w = i * n_kv_heads + h of work entries
  * work_xy[i] = (request, first token) are flattened into 128-key tiles and cut into <= n_sm
  * equal CTA ranges.  out_pieces [(n_work*n_kv_heads + n_sm) x 4] = (item, j0, j1, partial slot or
  * -1), out_cta_off [n_sm + 1], out_combine [n_sm x 4] = (item, first slot, n slots, 0);

@@ -142,6 +142,10 @@ _SIGS = {
     "glmx_engine_set_profiling": (None, [C.c_void_p, C.c_int32]),
     "glmx_pool_copy": (C.c_int, [C.c_void_p, C.c_void_p, i32p, i32p, C.c_uint64, C.c_void_p]),
     "glmx_pool_last_copy_ms": (C.c_float, [C.c_void_p]),
+    "glmx_rope_kv_append_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                          C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p,
+                                          C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                          C.c_int32, C.c_void_p, f32p]),
     "glmx_attn_schedule": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
                                      C.c_int32, i32p, i32p, i32p, i64p]),
     "glmx_attention_run": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,

@@ -26,6 +26,9 @@ int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefil
                         int32_t*, float*);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
+int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
+                         float, void*, uint32_t, uint32_t, uint32_t, void*, int, cudaStream_t,
+                         float*);
 int attention_run_impl(int, const void*, void*, uint64_t, int, int, int, void*, uint64_t, uint32_t,
                        uint32_t, uint32_t, uint64_t, const int32_t*, const int32_t*,
                        const int32_t*, const int32_t*, int, int, cudaStream_t, float*);
@@ -500,6 +503,18 @@ int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
   });
 }
 float glmx_pool_last_copy_ms(const glmx_kv* dst) { return dst->last_copy_ms; }
+
+int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* slot,
+                            uint64_t n_tokens, int32_t n_heads, int32_t n_kv_heads,
+                            int32_t head_dim, float rope_theta, void* pool, uint32_t n_layers,
+                            uint32_t layer, uint32_t block_tokens, void* q_out, int32_t reps,
+                            void* stream, float* out_ms) {
+  return guarded([&] {
+    return rope_append_run_impl(qkv, pos, slot, n_tokens, n_heads, n_kv_heads, head_dim,
+                                rope_theta, pool, n_layers, layer, block_tokens, q_out, reps,
+                                static_cast<cudaStream_t>(stream), out_ms);
+  });
+}
 
 int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,

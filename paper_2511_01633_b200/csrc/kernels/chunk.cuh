@@ -26,18 +26,23 @@ struct ChunkParams {
   int directed;
 };
 
+// select: warp path + CTA path for rows queued in big_list (n_req entries) / big_count (1 int).
 void chunk_select(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
-                  int32_t* sel, int32_t* sel_count, uint64_t* byte_len, cudaStream_t s);
+                  int32_t* sel, int32_t* sel_count, uint64_t* byte_len, int32_t* big_list,
+                  int32_t* big_count, cudaStream_t s);
+// render + per-chunk whitespace token count
 void chunk_render(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
                   const int32_t* sel, const int32_t* sel_count, const uint64_t* byte_off,
-                  char* out, cudaStream_t s);
-void chunk_tokenize(const char* bytes, const uint64_t* byte_off, int n_req, uint64_t total,
-                    uint32_t* flag, uint32_t* tok_index, void* temp, size_t temp_bytes,
-                    uint32_t vocab, int32_t* tok_id, uint64_t* tok_begin, uint64_t* tok_end,
-                    uint64_t* tok_off, cudaStream_t s);
+                  char* out, uint32_t* tok_count, cudaStream_t s);
+// token spans (relative to the chunk) + fnv1a ids at tok_off[r] (exclusive scan of the counts)
+void chunk_emit(const char* bytes, const uint64_t* byte_off, int n_req, const uint32_t* tok_off,
+                uint32_t vocab, int32_t* tok_id, uint64_t* tok_begin, uint64_t* tok_end,
+                cudaStream_t s);
 size_t scan_u64_temp_bytes(int n);
 size_t scan_u32_temp_bytes(uint64_t n);
 void scan_u64(void* temp, size_t temp_bytes, const uint64_t* in, uint64_t* out, int n,
+              cudaStream_t s);
+void scan_u32(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out, uint64_t n,
               cudaStream_t s);
 
 }  // namespace glmx

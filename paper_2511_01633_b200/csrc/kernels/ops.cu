@@ -73,61 +73,85 @@ rmsnorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, in
   }
 }
 
-// One CTA per token: the token's cos/sin table (hd/2 angles, fp32 angle pos*inv_freq then
-// accurate sincosf) is built once in shared memory, then every (head slot, 8-element chunk) is
-// a 16-byte load of each rotate-half partner and 16-byte stores.  Head slots: H query heads
-// (-> q_out), Hkv K heads (roped -> pool page), Hkv V heads (copied -> pool page).
+// K2: RoPE + KV append, kTok tokens per CTA.  The CTA first builds the cos/sin tables of its
+// tokens in shared memory (fp32 angle pos * inv_freq, accurate sincosf: positions reach 32k), then
+// every (token, head slot, 8-element chunk) work unit is two 16-byte loads (the rotate-half
+// partners c and c + hd/2) and two 16-byte stores.  Head slots: H query heads (-> q_out), Hkv K
+// heads (roped -> pool page), Hkv V heads (copied -> pool page).  A warp covers 4 heads x 8 chunks
+// of one token: every load and store instruction moves two fully used 128-byte lines.  All of a
+// thread's loads are issued before its first store (kUnroll units in flight per thread).
+template <int kTok, int kUnroll>
 __global__ void __launch_bounds__(256)
 rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
                       const int64_t* __restrict__ slot, int T, int H, int Hkv, int hd,
                       const float* __restrict__ inv_freq, PoolGeom pool, uint32_t layer,
                       __nv_bfloat16* __restrict__ q_out) {
-  __shared__ float cs_tab[128], sn_tab[128];
-  const int t = blockIdx.x;
+  __shared__ float cs_tab[kTok][128], sn_tab[kTok][128];
+  const int t_base = blockIdx.x * kTok;
   const int half = hd / 2;
-  const float p = static_cast<float>(pos[t]);
-  for (int i = threadIdx.x; i < half; i += blockDim.x) sincosf(p * inv_freq[i], &sn_tab[i], &cs_tab[i]);
+  for (int i = threadIdx.x; i < kTok * half; i += blockDim.x) {
+    const int tt = i / half, k = i % half;
+    const int t = min(t_base + tt, T - 1);
+    sincosf(static_cast<float>(pos[t]) * inv_freq[k], &sn_tab[tt][k], &cs_tab[tt][k]);
+  }
   __syncthreads();
   const int heads = H + 2 * Hkv;
   const int chunks = half / 8;
-  const int64_t sl = slot[t];
-  const int64_t page = sl / pool.block_tokens;
-  const int off = static_cast<int>(sl % pool.block_tokens);
-  for (int w = threadIdx.x; w < heads * chunks; w += blockDim.x) {
-    const int h = w / chunks, c = w % chunks;
-    const __nv_bfloat16* src = qkv + (static_cast<int64_t>(t) * heads + h) * hd + c * 8;
-    __nv_bfloat16* dst;
-    bool rotate = true;
-    if (h < H) {
-      dst = q_out + (static_cast<int64_t>(t) * H + h) * hd + c * 8;
-    } else {
-      const int kv = h < H + Hkv ? 0 : 1;
-      const int kh = h - H - kv * Hkv;
-      dst = pool.base + pool.tile_off(page, layer, kv, kh) + static_cast<int64_t>(off) * hd + c * 8;
-      rotate = kv == 0;
-    }
-    const uint4 av = *reinterpret_cast<const uint4*>(src);
-    const uint4 bv = *reinterpret_cast<const uint4*>(src + half);
-    if (!rotate) {
-      *reinterpret_cast<uint4*>(dst) = av;
-      *reinterpret_cast<uint4*>(dst + half) = bv;
-      continue;
-    }
-    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
-    uint4 ra, rb;
-    __nv_bfloat162* ra2 = reinterpret_cast<__nv_bfloat162*>(&ra);
-    __nv_bfloat162* rb2 = reinterpret_cast<__nv_bfloat162*>(&rb);
+  const int per_tok = heads * chunks;
+  const int units = kTok * per_tok;
+  for (int u0 = threadIdx.x; u0 < units; u0 += blockDim.x * kUnroll) {
+    uint4 av[kUnroll], bv[kUnroll];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 a = __bfloat1622float2(a2[k]), b = __bfloat1622float2(b2[k]);
-      const int i = c * 8 + 2 * k;
-      const float c0 = cs_tab[i], s0 = sn_tab[i], c1 = cs_tab[i + 1], s1 = sn_tab[i + 1];
-      ra2[k] = __floats2bfloat162_rn(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
-      rb2[k] = __floats2bfloat162_rn(b.x * c0 + a.x * s0, b.y * c1 + a.y * s1);
+    for (int k = 0; k < kUnroll; ++k) {
+      const int u = u0 + k * blockDim.x;
+      const int tt = u / per_tok, w = u % per_tok;
+      const int t = t_base + tt;
+      if (u < units && t < T) {
+        const __nv_bfloat16* src = qkv + (static_cast<int64_t>(t) * heads + w / chunks) * hd + (w % chunks) * 8;
+        av[k] = __ldcs(reinterpret_cast<const uint4*>(src));
+        bv[k] = __ldcs(reinterpret_cast<const uint4*>(src + half));
+      }
     }
-    *reinterpret_cast<uint4*>(dst) = ra;
-    *reinterpret_cast<uint4*>(dst + half) = rb;
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int u = u0 + k * blockDim.x;
+      const int tt = u / per_tok, w = u % per_tok;
+      const int t = t_base + tt;
+      if (u >= units || t >= T) continue;
+      const int h = w / chunks, c = w % chunks;
+      __nv_bfloat16* dst;
+      bool rotate = true;
+      if (h < H) {
+        dst = q_out + (static_cast<int64_t>(t) * H + h) * hd + c * 8;
+      } else {
+        const int kv = h < H + Hkv ? 0 : 1;
+        const int kh = h - H - kv * Hkv;
+        const int64_t sl = slot[t];
+        dst = pool.base + pool.tile_off(sl / pool.block_tokens, layer, kv, kh) +
+              static_cast<int64_t>(sl % pool.block_tokens) * hd + c * 8;
+        rotate = kv == 0;
+      }
+      if (!rotate) {
+        *reinterpret_cast<uint4*>(dst) = av[k];
+        *reinterpret_cast<uint4*>(dst + half) = bv[k];
+        continue;
+      }
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[k]);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv[k]);
+      uint4 ra, rb;
+      __nv_bfloat162* ra2 = reinterpret_cast<__nv_bfloat162*>(&ra);
+      __nv_bfloat162* rb2 = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a = __bfloat1622float2(a2[q]), b = __bfloat1622float2(b2[q]);
+        const int i = c * 8 + 2 * q;
+        const float c0 = cs_tab[tt][i], s0 = sn_tab[tt][i], c1 = cs_tab[tt][i + 1], s1 = sn_tab[tt][i + 1];
+        ra2[q] = __floats2bfloat162_rn(a.x * c0 - b.x * s0, a.y * c1 - b.y * s1);
+        rb2[q] = __floats2bfloat162_rn(b.x * c0 + a.x * s0, b.y * c1 + a.y * s1);
+      }
+      *reinterpret_cast<uint4*>(dst) = ra;
+      *reinterpret_cast<uint4*>(dst + half) = rb;
+    }
   }
 }
 
@@ -267,8 +291,9 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
                     uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s) {
   if (T <= 0) return;
   if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
-  rope_kv_append_kernel<<<T, 256, 0, s>>>(qkv, pos, slot, T, H, Hkv, hd, inv_freq, pool, layer,
-                                          q_out);
+  constexpr int kTok = 2, kUnroll = 3;
+  rope_kv_append_kernel<kTok, kUnroll><<<static_cast<int>(ceil_div(T, kTok)), 256, 0, s>>>(
+      qkv, pos, slot, T, H, Hkv, hd, inv_freq, pool, layer, q_out);
   GLMX_CHECK_LAUNCH();
 }
 

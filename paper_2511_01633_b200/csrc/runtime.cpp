@@ -123,37 +123,40 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   g->d_cnt.reserve(n * 4);
   g->d_len.reserve((n + 1) * 8);
   g->d_off.reserve((n + 1) * 8);
+  g->d_flag.reserve((n + 1) * 4);   // big-row queue of the select CTA path
+  g->d_tidx.reserve((n + 1) * 4);   // token counts per chunk (+1 zero)
+  g->d_toff.reserve((n + 2) * 4);   // token offsets (exclusive scan, [n] = total); + big count
   const size_t t64 = scan_u64_temp_bytes(static_cast<int>(n + 1));
+  const size_t t32 = scan_u32_temp_bytes(n + 1);
+  g->d_temp.reserve(std::max(t32, t64));
+  int32_t* big_count = reinterpret_cast<int32_t*>(g->d_toff.as<uint32_t>() + n + 1);
   GLMX_CUDA(cudaMemcpyAsync(g->d_nodes.p, node_idx, n * 4, cudaMemcpyHostToDevice, s));
   GLMX_CUDA(cudaMemsetAsync(g->d_len.p, 0, (n + 1) * 8, s));
+  GLMX_CUDA(cudaMemsetAsync(g->d_tidx.as<uint32_t>() + n, 0, 4, s));
   GLMX_CUDA(cudaEventRecord(g->ev0, s));
   chunk_select(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), s);
-  g->d_temp.reserve(t64);
+               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), g->d_flag.as<int32_t>(), big_count, s);
   scan_u64(g->d_temp.p, t64, g->d_len.as<uint64_t>(), g->d_off.as<uint64_t>(),
            static_cast<int>(n + 1), s);
   uint64_t total = 0;
   GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaStreamSynchronize(s));
+  // a token has >= 1 byte and is followed by a space or the chunk end: <= total/2 + n tokens
+  const uint64_t tok_bound = total / 2 + n + 1;
   g->d_bytes.reserve(total + 16);
-  g->d_flag.reserve((total + 1) * 4);
-  g->d_tidx.reserve((total + 1) * 4);
-  g->d_tid.reserve((total + 1) * 4);
-  g->d_tbeg.reserve((total + 1) * 8);
-  g->d_tend.reserve((total + 1) * 8);
-  g->d_toff.reserve((n + 1) * 8);
-  const size_t t32 = scan_u32_temp_bytes(total + 1);
-  g->d_temp.reserve(std::max(t32, t64));
+  g->d_tid.reserve(tok_bound * 4);
+  g->d_tbeg.reserve(tok_bound * 8);
+  g->d_tend.reserve(tok_bound * 8);
   chunk_render(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-               g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_bytes.as<char>(), s);
-  GLMX_CUDA(cudaMemsetAsync(g->d_flag.as<uint32_t>() + total, 0, 4, s));
-  chunk_tokenize(g->d_bytes.as<char>(), g->d_off.as<uint64_t>(), static_cast<int>(n), total,
-                 g->d_flag.as<uint32_t>(), g->d_tidx.as<uint32_t>(), g->d_temp.p, g->d_temp.bytes,
-                 cfg->vocab, g->d_tid.as<int32_t>(), g->d_tbeg.as<uint64_t>(),
-                 g->d_tend.as<uint64_t>(), g->d_toff.as<uint64_t>(), s);
+               g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_bytes.as<char>(),
+               g->d_tidx.as<uint32_t>(), s);
+  scan_u32(g->d_temp.p, t32, g->d_tidx.as<uint32_t>(), g->d_toff.as<uint32_t>(), n + 1, s);
+  chunk_emit(g->d_bytes.as<char>(), g->d_off.as<uint64_t>(), static_cast<int>(n),
+             g->d_toff.as<uint32_t>(), cfg->vocab, g->d_tid.as<int32_t>(), g->d_tbeg.as<uint64_t>(),
+             g->d_tend.as<uint64_t>(), s);
   GLMX_CUDA(cudaEventRecord(g->ev1, s));
   uint32_t ntok32 = 0;
-  GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_tidx.as<uint32_t>() + total, 4, cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_toff.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaStreamSynchronize(s));
   GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));
   const uint64_t ntok = ntok32;
@@ -171,10 +174,12 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
     GLMX_CUDA(cudaMemcpyAsync(out_tok_begin, g->d_tbeg.p, ntok * 8, cudaMemcpyDeviceToHost, s));
   if (out_tok_end)
     GLMX_CUDA(cudaMemcpyAsync(out_tok_end, g->d_tend.p, ntok * 8, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> toff32(out_tok_offsets ? n + 1 : 0);
   if (out_tok_offsets)
-    GLMX_CUDA(cudaMemcpyAsync(out_tok_offsets, g->d_toff.p, n * 8, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaMemcpyAsync(toff32.data(), g->d_toff.p, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaStreamSynchronize(s));
-  if (out_tok_offsets) out_tok_offsets[n] = ntok;
+  if (out_tok_offsets)
+    for (uint64_t i = 0; i <= n; ++i) out_tok_offsets[i] = toff32[i];
   return GLMX_OK;
 }
 
@@ -659,7 +664,10 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   e->last_work = n_work;
   e->work[0] = attn_flops * c.n_layers;
   e->work[1] = attn_bytes * c.n_layers;
-  e->work[2] = static_cast<double>(T) * kv_tok_bytes * c.n_layers;
+  // K2 (fused RoPE + append) algorithmic bytes: read the qkv row, write q and the K/V rows
+  e->work[2] = static_cast<double>(T) * c.n_layers *
+               (2.0 * (c.n_heads + 2 * c.n_kv_heads) * c.head_dim + 2.0 * c.n_heads * c.head_dim +
+                kv_tok_bytes);
   const double lin = 2.0 * (static_cast<double>(c.d_model) * (c.n_heads + 2 * c.n_kv_heads) * c.head_dim +
                             static_cast<double>(c.d_model) * c.n_heads * c.head_dim +
                             3.0 * c.d_model * c.d_ff);
@@ -704,7 +712,6 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
                         d_cp + nc + o, static_cast<int>(std::min<size_t>(65535, b - o)), s);
       a = b;
     }
-    e->work[2] += 2.0 * static_cast<double>(nc) * static_cast<double>(kv->page_bytes);
   }
   forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
   argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), s);
@@ -915,6 +922,44 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
       else
         paged_attention_tc(ap, kv_map, rows, q_map, sc, s);
     }
+    GLMX_CUDA(cudaEventRecord(e1, s));
+    GLMX_CUDA(cudaEventSynchronize(e1));
+    GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  } catch (...) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (out_ms) *out_ms = ms / static_cast<float>(reps);
+  return GLMX_OK;
+}
+
+// ======================================================================== K2 kernel-level hook
+int rope_append_run_impl(const void* qkv, const int32_t* pos, const int64_t* slot, uint64_t T,
+                         int H, int Hkv, int hd, float rope_theta, void* pool_base,
+                         uint32_t n_layers, uint32_t layer, uint32_t block_tokens, void* q_out,
+                         int reps, cudaStream_t s, float* out_ms) {
+  if (T == 0) return GLMX_OK;
+  if (reps < 1 || hd % 16 || hd > 256) throw Error(GLMX_ERR_ARG, "bad append arguments");
+  std::vector<float> inv(hd / 2);
+  for (int i = 0; i < hd / 2; ++i)
+    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(rope_theta), 2.0 * i / hd));
+  DBuf d_inv;
+  d_inv.reserve(inv.size() * 4);
+  GLMX_CUDA(cudaMemcpyAsync(d_inv.p, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice, s));
+  PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, static_cast<uint32_t>(Hkv),
+                block_tokens, static_cast<uint32_t>(hd)};
+  cudaEvent_t e0, e1;
+  GLMX_CUDA(cudaEventCreate(&e0));
+  GLMX_CUDA(cudaEventCreate(&e1));
+  float ms = 0.f;
+  try {
+    GLMX_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < reps; ++i)
+      rope_kv_append(static_cast<const __nv_bfloat16*>(qkv), pos, slot, static_cast<int>(T), H, Hkv,
+                     hd, d_inv.as<float>(), geom, layer, static_cast<__nv_bfloat16*>(q_out), s);
     GLMX_CUDA(cudaEventRecord(e1, s));
     GLMX_CUDA(cudaEventSynchronize(e1));
     GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));

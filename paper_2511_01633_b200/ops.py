@@ -1,0 +1,41 @@
+"""K2 (RoPE + KV append into the paged pool) on caller-owned device tensors
+(glmx_rope_kv_append_run) — kernel-level face for parity tests and bandwidth sweeps; the engine
+launches the same kernel inside its forward."""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._lib import check, lib
+
+
+def rope_kv_append(qkv, pos, slot, pool, q_out, n_heads, n_kv_heads, layer=0,
+                   rope_theta=500000.0, reps=1, stream=None):
+    """qkv [T][(H+2Hkv)*hd] bf16, pos int32 [T], slot int64 [T] (page*B + offset), pool
+    [pages][L][2][Hkv][B][hd] bf16, q_out [T][H][hd] bf16.  Returns mean device ms per launch."""
+    import torch
+
+    T = qkv.shape[0]
+    n_pages, L, _, Hkv, B, hd = pool.shape
+    assert Hkv == n_kv_heads and qkv.shape[1] == (n_heads + 2 * n_kv_heads) * hd
+    assert pos.dtype == torch.int32 and slot.dtype == torch.int64
+    ms = C.c_float(0.0)
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(lib().glmx_rope_kv_append_run(qkv.data_ptr(), pos.data_ptr(), slot.data_ptr(), T,
+                                        n_heads, n_kv_heads, hd, rope_theta, pool.data_ptr(), L,
+                                        layer, B, q_out.data_ptr(), reps, s, C.byref(ms)))
+    return ms.value
+
+
+def reference_rope(x, pos, rope_theta=500000.0):
+    """fp32 rotate-half RoPE, angles as in oracle/decoder.py:rope (fp32 pos * fp32 inv_freq, then
+    cos/sin in fp64): x [T][heads][hd]."""
+    import torch
+
+    hd = x.shape[-1]
+    inv = (1.0 / (float(torch.tensor(rope_theta, dtype=torch.float32)) **
+                  (torch.arange(0, hd // 2, dtype=torch.float64) * 2.0 / hd))).float()
+    ang = (pos.cpu().float()[:, None] * inv[None, :]).double()
+    cos = torch.cos(ang).float().to(x.device)[:, None, :]
+    sin = torch.sin(ang).float().to(x.device)[:, None, :]
+    a, b = x[..., :hd // 2].float(), x[..., hd // 2:].float()
+    return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)

@@ -12,8 +12,9 @@ scripted provider (scripted.hpp:21-30) whose replies follow the Rule agent's for
   finish(): set_tier(session, II, III) (orchestrator.cpp:147-154).
 
 One rotation = every active lane makes its next LLM call; the rotation's calls are ONE engine
-prefill batch (bookkeeping applied in lane order, as the reference would), then ONE batched K1
-launch builds the vertex chunks of every action executed in that rotation.  Source nodes are
+prefill batch (bookkeeping applied in lane order, as the reference would), and ONE batched K1
+launch builds the vertex chunks of every action executed in that rotation, overlapped with the
+prefill on the graph's stream.  Source nodes are
 drawn with a power-law skew so popular (hub) chunks recur across queries; every reasoning round
 re-reads the previous rounds' chunks (reuse across iterations).
 """
@@ -21,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import random
+import threading
 from dataclasses import dataclass, field
 
 from . import _lib
@@ -57,6 +59,7 @@ class RotationResult:
     cached_tokens: int = 0
     finished: int = 0
     chunks: int = 0
+    chunk_bytes: int = 0         # K1 algorithmic bytes (CSR rows, neighbour pairs, entries, out)
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
 
@@ -67,8 +70,9 @@ def count_tokens(text):
 
 class GraphCoTWorkload:
     def __init__(self, engine, retriever, n_queries, lanes, seed=0, min_hops=2, max_hops=4,
-                 skew=2.5, templates=None, node_ids=None):
+                 skew=2.5, templates=None, node_ids=None, overlap_retrieval=True):
         self.engine = engine
+        self.overlap_retrieval = overlap_retrieval
         self.kv = engine.kv if engine is not None else None
         self.retriever = retriever
         self.templates = templates or TemplateSet()
@@ -137,8 +141,9 @@ class GraphCoTWorkload:
         return ([PrefillReport(reps[i].cached_tokens, reps[i].computed_tokens,
                                reps[i].tail_tokens) for i in range(n)], [first[i] for i in range(n)])
 
-    def advance(self, calls, reports=None, first_tokens=None) -> RotationResult:
-        """Apply the replies: state transitions, K1 chunk build for the actions, finish."""
+    def advance(self, calls, reports=None, first_tokens=None, chunks=None) -> RotationResult:
+        """Apply the replies: state transitions, K1 chunk build for the actions (or the batch
+        `chunks` already built for them), finish."""
         res = RotationResult(calls=len(calls), reports=reports or [],
                              first_tokens=first_tokens or [])
         for r in res.reports:
@@ -147,10 +152,16 @@ class GraphCoTWorkload:
             res.prompt_tokens += r.cached_tokens + r.computed_tokens + r.tail_tokens
         acting = [c for c in calls if c.agent == "action"]
         if acting:
-            batch = self.retriever.chunk_build([c.session.sources[c.session.round] for c in acting])
+            batch = chunks if chunks is not None else self.retriever.chunk_build(
+                [c.session.sources[c.session.round] for c in acting])
             for c, text in zip(acting, batch.texts):
                 c.session.notebook += text + "\n"  # PrintStmt: raw chunk + "\n" (interp.cpp:68-74)
             res.chunks = len(acting)
+            g = self.retriever.graph
+            res.chunk_bytes = sum(8 + 8 * g.total_degree(c.session.sources[c.session.round])
+                                  for c in acting)
+            res.chunk_bytes += sum(2 * len(t) + 20 * len(sp) for t, sp in
+                                   zip(batch.texts, batch.token_spans))
         still = []
         for c in calls:
             s = c.session
@@ -173,6 +184,23 @@ class GraphCoTWorkload:
         return res
 
     def rotation(self) -> RotationResult:
+        """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on
+        the (scripted) action code, not on this prefill, so K1 runs on the graph's own CUDA stream
+        in a second host thread while the prefill batch runs on the engine stream (the GIL is
+        released inside both C-ABI calls); the chunk texts join the notebooks afterwards, exactly
+        where the sequential order puts them."""
         calls = self.next_calls()
-        reps, first = self.prefill(calls)
-        return self.advance(calls, reps, first)
+        acting = [c for c in calls if c.agent == "action"]
+        built = {}
+        th = None
+        if acting and self.overlap_retrieval:
+            nodes = [c.session.sources[c.session.round] for c in acting]
+            th = threading.Thread(target=lambda: built.__setitem__(
+                "b", self.retriever.chunk_build(nodes)))
+            th.start()
+        try:
+            reps, first = self.prefill(calls)
+        finally:
+            if th is not None:
+                th.join()
+        return self.advance(calls, reps, first, chunks=built.get("b"))

@@ -27,10 +27,53 @@ ap.add_argument("--batch", type=int, nargs="+", default=[8])
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--check", action="store_true", help="compare against the fp32 reference")
+ap.add_argument("--shapes", default=None,
+                help="JSON list of batches [[ctx, q_len], ...] (scripts/c2_attn_shapes.py)")
 args = ap.parse_args()
 
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
 H, Hkv, hd, B = 32, 8, 128, 16
+
+
+def run_batch(reqs, tag):
+    """One ragged batch: reqs = [(ctx, q_len)]; returns the JSON row."""
+    pages_of = [(c + B - 1) // B for c, _ in reqs]
+    n_pages = sum(pages_of)
+    pool = torch.empty((n_pages, args.layers, 2, Hkv, B, hd), dtype=torch.bfloat16,
+                       device="cuda").normal_()
+    rows = sum(q for _, q in reqs)
+    q = torch.empty((rows, H, hd), dtype=torch.bfloat16, device="cuda").normal_()
+    o = torch.empty_like(q)
+    perm = list(range(n_pages))
+    random.Random(rows).shuffle(perm)
+    bt, qs, ql, cl = [], [], [], []
+    p = r = 0
+    for (c, n), k in zip(reqs, pages_of):
+        bt.append(perm[p:p + k])
+        p += k
+        qs.append(r)
+        ql.append(n)
+        cl.append(c)
+        r += n
+    A.paged_attention(q, o, pool, qs, ql, cl, bt, impl=args.impl, reps=3)
+    ms = A.paged_attention(q, o, pool, qs, ql, cl, bt, impl=args.impl, reps=args.reps)
+    flops = sum(4.0 * H * hd * (c - n + t + 1) for c, n in reqs for t in range(n))
+    kv_bytes = sum(c * Hkv * hd * 2 * 2 + 2 * n * H * hd * 2 for c, n in reqs)
+    return {"impl": "tc" if args.impl == 0 else "mma", "batch": tag, "requests": len(reqs),
+            "ms": ms, "tflops": flops / ms / 1e9, "tensor_frac": flops / ms / 1e9 / peaks["bf16_tflops"],
+            "gbs": kv_bytes / ms / 1e6, "hbm_frac": kv_bytes / ms / 1e6 / peaks["hbm_gbs"],
+            "intensity": flops / kv_bytes}
+
+
+if args.shapes:
+    tot_ms = 0.0
+    for i, reqs in enumerate(json.load(open(args.shapes))):
+        row = run_batch([tuple(x) for x in reqs], i)
+        tot_ms += row["ms"]
+        print(json.dumps(row), flush=True)
+    print(json.dumps({"total_ms_per_layer": tot_ms}))
+    sys.exit(0)
+
 for P in args.prefix:
     for s in args.suffix:
         for nb in args.batch:

@@ -1,0 +1,41 @@
+"""K2 (fused RoPE + paged KV append) against a plain PyTorch fp32 reference through the C-ABI
+hook glmx_rope_kv_append_run: V pages byte-exact, RoPE'd Q/K within one bf16 rounding of the fp32
+rotation (the kernel rotates in fp32 and rounds once), untouched pages unchanged."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("T", [1, 7, 64, 1000])
+def test_append_matches_reference(T):
+    from paper_2511_01633_b200.ops import reference_rope, rope_kv_append
+
+    H, Hkv, hd, B, L, layer = 32, 8, 128, 16, 3, 2
+    g = torch.Generator().manual_seed(T)
+    n_pages = (T + B - 1) // B + 5
+    qkv = torch.randn((T, (H + 2 * Hkv) * hd), generator=g).to(torch.bfloat16).cuda()
+    pos = torch.randint(0, 32768, (T,), generator=g, dtype=torch.int32).cuda()
+    perm = torch.randperm(n_pages, generator=g)[: (T + B - 1) // B]
+    slot = torch.tensor([int(perm[t // B]) * B + t % B for t in range(T)], dtype=torch.int64).cuda()
+    pool = torch.randn((n_pages, L, 2, Hkv, B, hd), generator=g).to(torch.bfloat16).cuda()
+    before = pool.clone()
+    q_out = torch.empty((T, H, hd), dtype=torch.bfloat16, device="cuda")
+    rope_kv_append(qkv, pos, slot, pool, q_out, H, Hkv, layer=layer)
+    torch.cuda.synchronize()
+    x = qkv.view(T, H + 2 * Hkv, hd)
+    q_ref = reference_rope(x[:, :H], pos)
+    k_ref = reference_rope(x[:, H:H + Hkv], pos)
+    v_ref = x[:, H + Hkv:]
+    tol = lambda ref: 2.0 ** -8 * ref.abs() + 1e-6  # noqa: E731  one bf16 rounding
+    assert ((q_out.float() - q_ref).abs() <= tol(q_ref)).all()
+    page, off = (slot // B).long(), (slot % B).long()
+    k_got = pool[page, layer, 0, :, off]  # [T][Hkv][hd]
+    v_got = pool[page, layer, 1, :, off]
+    assert ((k_got.float() - k_ref).abs() <= tol(k_ref)).all()
+    assert torch.equal(v_got, v_ref)
+    # nothing else written: other layers, and rows not addressed by a slot
+    mask = torch.ones_like(pool, dtype=torch.bool)
+    mask[page, layer, :, :, off] = False
+    assert torch.equal(pool[mask], before[mask])
