@@ -43,6 +43,11 @@ def parse():
     p.add_argument("--capacity", type=int, default=16384)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--question-pool", type=int, default=-1,
+                   help="draw questions with replacement from this many candidates (reference "
+                        "generate_workload style); -1 = half the total query count, 0 = all unique")
+    p.add_argument("--no-peer", action="store_true",
+                   help="N>1: disable cross-GPU prefix hits (per-epoch directory + K4 peer copies)")
     return p.parse_args()
 
 
@@ -230,9 +235,16 @@ def main():
     import paper_2511_01633_b200 as glmx
     from paper_2511_01633_b200.workload import GraphCoTWorkload
 
+    n_dev = torch.cuda.device_count()
+    local = local % max(1, n_dev)  # more ranks than GPUs only in single-GPU protocol tests
     torch.cuda.set_device(local)
+    shared_gpu = ws > n_dev
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:  # NCCL refuses two ranks on one GPU: control plane over gloo
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if shared_gpu else "cuda"
 
     cfg = glmx.ModelConfig(n_layers=args.layers, d_model=4096, n_heads=32, n_kv_heads=8,
                            head_dim=128, d_ff=14336, vocab=128256, seed=args.seed)
@@ -247,14 +259,36 @@ def main():
     rotations = args.warmup + args.steps
     # enough queries (per rank) that every lane stays busy through the timed rotations
     n_q = args.lanes * (rotations // 6 + 2)
-    wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed)
+    pool_n = args.question_pool if args.question_pool >= 0 else (n_q * ws) // 2
+    wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed,
+                          question_pool=pool_n)
     wl.sessions = wl.sessions[rank::ws]  # query i -> rank i % N
+    # cross-GPU prefix hits (C4): every rotation is an epoch; the ranks exchange their resident
+    # (block id, page) directories, and a run of blocks missing locally but resident on a peer is
+    # copied over NVLink by K4 (pool exported by CUDA IPC) instead of being recomputed
+    px = None
+    if ws > 1 and not args.no_peer:
+        from paper_2511_01633_b200.sharding import PeerExchange
+        try:
+            px = PeerExchange(kv)
+        except Exception as exc:  # noqa: BLE001 — report and run sharded without peer hits
+            print(f"rank {rank}: peer exchange disabled: {exc}", file=sys.stderr)
+            px = None
+
+    def step():
+        if px is not None:
+            px.epoch_begin()
+        r = wl.rotation()
+        if px is not None:
+            px.epoch_end()
+        return r
 
     for _ in range(args.warmup):
-        wl.rotation()
+        step()
     # per-kernel-category CUDA events on the engine stream during the timed steps (host cost
     # ~1 us per event record, <1% of a step)
     eng.set_profiling(2)
+    peer0 = kv.peer_hits() if px is not None else 0
     sampler = ClockSampler(local)
     if ws > 1:
         dist.barrier()
@@ -274,7 +308,7 @@ def main():
     k1_bytes = 0
     k1_rotations = 0
     for _ in range(args.steps):
-        r = wl.rotation()
+        r = step()
         tm = eng.last_timings()
         fwd_ms += tm["forward"]
         for k in cat_ms:
@@ -309,13 +343,14 @@ def main():
     tm = dict(cat_ms, forward=fwd_ms)
     wk = work
 
-    vals = torch.tensor([tokens, computed, cached, calls, finished], dtype=torch.float64,
-                        device="cuda")
-    times = torch.tensor([fwd_ms, wall_ms], dtype=torch.float64, device="cuda")
+    peer_blocks = float(kv.peer_hits() - peer0) if px is not None else 0.0
+    vals = torch.tensor([tokens, computed, cached, calls, finished, peer_blocks],
+                        dtype=torch.float64, device=red_dev)
+    times = torch.tensor([fwd_ms, wall_ms], dtype=torch.float64, device=red_dev)
     if ws > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.SUM)
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    tokens, computed, cached, calls, finished = vals.tolist()
+    tokens, computed, cached, calls, finished, peer_blocks = vals.tolist()
     fwd_ms, wall_ms = times.tolist()
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
@@ -383,12 +418,14 @@ def main():
                                "-> finish), synthetic 100k-node power-law graph, top-k=16 vertex "
                                "chunks, Llama-3-8B-shaped random-init bf16, paged KV pool",
                    "lanes_per_gpu": args.lanes, "nodes": args.nodes, "k": args.k,
+                   "question_pool": pool_n,
                    "kv_capacity_blocks": args.capacity, "block_tokens": 16,
                    "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
                    "parallelism": f"query-sharded x{ws}"},
         "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
         "cache_hit_token_frac": cached / max(1.0, tokens),
         "calls": calls, "queries_finished": finished,
+        "peer_hit_blocks": peer_blocks if ws > 1 else None,
         "queries_per_s_prefill_only": finished / (wall_ms * 1e-3),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},

@@ -298,6 +298,10 @@ int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_head
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
                        int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
                        int32_t* out_combine, int64_t out_counts[5]);
+/* Diagnostics: in the trace build (libglmx_trace.so, `make -C paper_2511_01633_b200/csrc trace`)
+ * copies CTA 0's K3 pipeline clock64 stamps (16 events x 1024 key tiles) and clears them;
+ * returns the count, or -1 in the product build. */
+int32_t glmx_attn_trace_read(int64_t* out, int32_t n);
 /* K3 on caller-owned DEVICE buffers — the attention core of the prefill step that replaces the
  * c_prefill cost term (orchestrator.cpp:131-132); no reference counterpart (tensor
  * math is builder-defined).  q/o [n_q_rows][n_heads][head_dim] bf16 (q RoPE'd), pool = pages x

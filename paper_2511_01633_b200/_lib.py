@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libglmx.so")
+# GLMX_LIB selects a diagnostics build (libglmx_trace.so); the default is the product library
+LIB_PATH = os.environ.get("GLMX_LIB") or os.path.join(HERE, "libglmx.so")
 
 u64p = C.POINTER(C.c_uint64)
 i64p = C.POINTER(C.c_int64)
@@ -146,6 +147,7 @@ _SIGS = {
                                           C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_void_p,
                                           C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                           C.c_int32, C.c_void_p, f32p]),
+    "glmx_attn_trace_read": (C.c_int32, [i64p, C.c_int32]),
     "glmx_attn_schedule": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
                                      C.c_int32, i32p, i32p, i32p, i64p]),
     "glmx_attention_run": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,

@@ -516,6 +516,15 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
   });
 }
 
+int32_t glmx_attn_trace_read(int64_t* out, int32_t n) {
+  int32_t r = -1;
+  guarded([&] {
+    r = attn_trace_read(reinterpret_cast<long long*>(out), n);
+    return GLMX_OK;
+  });
+  return r;
+}
+
 int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
                        int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,

@@ -46,6 +46,8 @@ struct AttnTcSched {
   float2* part_ml;
 };
 int attn_tc_partial_rows();  // rows per partial slot (256)
+// trace build only (-DGLMX_ATTN_TRACE): copy + clear CTA 0's pipeline stamps; -1 otherwise
+int attn_trace_read(long long* out, int n);
 // Persistent launch: sc.grid CTAs walk their pieces; then the combine pass for split items.
 void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
                         const void* q_map, const AttnTcSched& sc, cudaStream_t s);

@@ -39,14 +39,20 @@ constexpr int kQT = 2;        // query tiles per item
 constexpr int kN = 128;       // keys per tile
 constexpr int kHalf = 16384;  // bytes of one [128][64] bf16 SW128 half tile
 constexpr int kTile = 2 * kHalf;
-constexpr int kSlots = 4;     // K/V ring depth (32 KB slots)
+constexpr int kKSlots = 3;    // K ring depth (32 KB [128 keys][128 dims] tiles)
+constexpr int kVSlots = 2;    // V ring depth
+#ifndef GLMX_POLY_FROM
+#define GLMX_POLY_FROM 8
+#endif
+constexpr int kPolyFrom = GLMX_POLY_FROM;  // of every 8 P pairs, [kPolyFrom, 8) use the polynomial
 constexpr int kSoftmaxThreads = 128 * kQT;
-constexpr int kThreads = kSoftmaxThreads + 64;  // + producer warp + MMA warp
+constexpr int kThreads = kSoftmaxThreads + 96;  // + K producer, MMA, V producer warps
 // registers: up to 3 warps per SM sub-partition (16K regs each) -> <= 168 per thread
-// smem map (1024-aligned): Q0 Q1 | ring slots | barriers
+// smem map (1024-aligned): Q0 Q1 | K ring | V ring | barriers
 constexpr int kOffQ = 0;
-constexpr int kOffRing = kOffQ + kQT * kTile;
-constexpr int kOffBar = kOffRing + kSlots * kTile;
+constexpr int kOffK = kOffQ + kQT * kTile;
+constexpr int kOffV = kOffK + kKSlots * kTile;
+constexpr int kOffBar = kOffV + kVSlots * kTile;
 constexpr int kSmem = kOffBar + 256 + 1024;  // + alignment slack
 static_assert(kSmem <= 232448, "shared memory budget");
 
@@ -107,6 +113,48 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes' worth of FMA-pipe work per
+// issue slot.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// 2^x for a pair of x <= 8 on the FMA pipe (offloads the MUFU): round-to-nearest split by the
+// 1.5 * 2^23 magic (t's low mantissa bits hold n = rint(x)), degree-3 minimax of 2^f on
+// [-0.5, 0.5] (max rel err 7.5e-5, far below the bf16 rounding of P), exponent added as integer.
+// x is clamped to -126 (masked -inf -> 2^-126, negligible next to the row's max term).
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& p0, float& p1) {
+  const float kMagic = 12582912.f;
+  x0 = fmaxf(x0, -126.f);
+  x1 = fmaxf(x1, -126.f);
+  const uint64_t x = f2pack(x0, x1);
+  const uint64_t t = fadd2(x, f2pack(kMagic, kMagic));
+  const uint64_t n = fadd2(t, f2pack(-kMagic, -kMagic));
+  const uint64_t f = ffma2(n, f2pack(-1.f, -1.f), x);
+  uint64_t q = ffma2(f, f2pack(0.05517161265015602f, 0.05517161265015602f),
+                     f2pack(0.24261116981506348f, 0.24261116981506348f));
+  q = ffma2(q, f, f2pack(0.6932610273361206f, 0.6932610273361206f));
+  q = ffma2(q, f, f2pack(0.9999280571937561f, 0.9999280571937561f));
+  float t0, t1, q0, q1;
+  f2unpack(t, t0, t1);
+  f2unpack(q, q0, q1);
+  p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+  p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
 }
 // O += P V with the A operand (P, bf16, [128 rows][K]) read from TMEM.
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
@@ -199,6 +247,25 @@ __device__ __forceinline__ uint32_t sw128(int r, int c16) {
   return static_cast<uint32_t>((c16 >> 3) * kHalf + r * 128 + (((c16 & 7) ^ (r & 7)) << 4));
 }
 
+// Debug trace (build with -DGLMX_ATTN_TRACE, `make trace` -> libglmx_trace.so): CTA 0 records
+// clock64 stamps of the pipeline events per key tile into a global buffer (kTraceEv x kTraceN).
+#ifdef GLMX_ATTN_TRACE
+__device__ long long g_attn_trace[16 * 1024];
+void* g_attn_trace_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_attn_trace);
+  return p;
+}
+#define ATTN_TRACE(ev, j)                                                       \
+  do {                                                                          \
+    if (blockIdx.x == 0 && (j) < 1024) g_attn_trace[(ev) * 1024 + (j)] = clock64(); \
+  } while (0)
+#else
+#define ATTN_TRACE(ev, j) \
+  do {                    \
+  } while (0)
+#endif
+
 struct TcParams {
   AttnParams a;
   uint32_t rows_total;  // rows of the pool tensor map (OOB row -> zero fill)
@@ -227,11 +294,6 @@ __device__ __forceinline__ Item item_of(const AttnParams& p, int w) {
   return it;
 }
 
-__device__ __forceinline__ void ring_pos(int c, int& slot, uint32_t& use) {
-  slot = c % kSlots;
-  use = static_cast<uint32_t>(c / kSlots);
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
 paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
                      const __grid_constant__ CUtensorMap q_map, TcParams tp) {
@@ -240,21 +302,29 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_addr(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  // barriers (8 B each): full[kSlots] empty[kSlots] sfull[2] pfull[2] ofull[2] qfull qempty
-  const uint32_t b_full = smem_addr(bars + 0), b_empty = smem_addr(bars + kSlots);
-  const uint32_t b_sfull = smem_addr(bars + 2 * kSlots), b_pfull = smem_addr(bars + 2 * kSlots + 2);
-  const uint32_t b_ofull = smem_addr(bars + 2 * kSlots + 4);
-  const uint32_t b_qfull = smem_addr(bars + 2 * kSlots + 6), b_qempty = smem_addr(bars + 2 * kSlots + 7);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kSlots + 8);
+  // barriers (8 B each): kfull[kKSlots] kempty[kKSlots] vfull[kVSlots] vempty[kVSlots]
+  //                      sfull[2] pfull[2] ofull[2] qfull qempty
+  constexpr int kB0 = 2 * (kKSlots + kVSlots);
+  const uint32_t b_kfull = smem_addr(bars + 0), b_kempty = smem_addr(bars + kKSlots);
+  const uint32_t b_vfull = smem_addr(bars + 2 * kKSlots), b_vempty = smem_addr(bars + 2 * kKSlots + kVSlots);
+  const uint32_t b_sfull = smem_addr(bars + kB0), b_pfull = smem_addr(bars + kB0 + 2);
+  const uint32_t b_ofull = smem_addr(bars + kB0 + 4);
+  const uint32_t b_qfull = smem_addr(bars + kB0 + 6), b_qempty = smem_addr(bars + kB0 + 7);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + kB0 + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.H / p.Hkv;
   constexpr int kWarpProducer = kSoftmaxThreads / 32, kWarpMma = kWarpProducer + 1;
+  constexpr int kWarpVProducer = kWarpMma + 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(b_full + 8 * s, 1);
-      mbar_init(b_empty + 8 * s, 1);
+    for (int s = 0; s < kKSlots; ++s) {
+      mbar_init(b_kfull + 8 * s, 1);
+      mbar_init(b_kempty + 8 * s, 1);
+    }
+    for (int s = 0; s < kVSlots; ++s) {
+      mbar_init(b_vfull + 8 * s, 1);
+      mbar_init(b_vempty + 8 * s, 1);
     }
     for (int i = 0; i < kQT; ++i) {
       mbar_init(b_sfull + 8 * i, 1);
@@ -276,64 +346,77 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   const uint32_t tmem = *tmem_holder;
   const uint32_t t_s0 = tmem, t_o0 = tmem + kQT * kN;
 
-  if (warp >= kWarpProducer) {
-    if (warp == kWarpProducer) {
-    // ---------------------------------------------------------------- TMA producer
+  if (warp == kWarpProducer || warp == kWarpVProducer) {
+    // ---------------------------------------------------------------- TMA producers
+    // warp 8 loads Q and the K tiles through the K ring, warp 10 the V tiles through the V ring:
+    // a V slot still in use never holds back the next K load (and vice versa)
     if (lane == 0) {
+      const int kv = warp == kWarpVProducer ? 1 : 0;
       const uint32_t L = p.pool.n_layers, Hkv = p.pool.n_kv_heads;
+      const int n_slots = kv ? kVSlots : kKSlots;
+      const uint32_t ring = sbase + (kv ? kOffV : kOffK);
+      const uint32_t b_full = kv ? b_vfull : b_kfull, b_empty = kv ? b_vempty : b_kempty;
       int c = 0, it_local = 0;
-      // one ring load: K (kv = 0) or V (kv = 1) of key tile j of the item
-      auto load_kv = [&](const Item& it, const int32_t* bt, int j, int kv) {
-        int slot;
-        uint32_t use;
-        ring_pos(c, slot, use);
+      // one ring load of key tile j (global tile count c), whose 8 pages are pg[0..7]
+      auto load_tile = [&](const Item& it, const int32_t* pg, int j) {
+        const int slot = c % n_slots;
+        const uint32_t use = static_cast<uint32_t>(c / n_slots);
         if (use > 0) mbar_wait(b_empty + 8 * slot, (use - 1) & 1, 2 + kv);
         const uint32_t full = b_full + 8 * slot;
+        ATTN_TRACE(14 + kv, c);
         mbar_expect_tx(full, kTile);
-        const uint32_t dst = sbase + kOffRing + slot * kTile;
-        for (int pg = 0; pg < kN / kB; ++pg) {
-          const int key0 = j * kN + pg * kB;
+        const uint32_t dst = ring + slot * kTile;
+#pragma unroll
+        for (int q = 0; q < kN / kB; ++q) {
+          const int key0 = j * kN + q * kB;
           uint32_t row = tp.rows_total;  // out of bounds -> zeros
-          if (key0 < it.ctx) {
-            const uint32_t page = static_cast<uint32_t>(bt[key0 / kB]);
-            row = (((page * L + p.layer) * 2 + kv) * Hkv + it.kvh) * kB;
-          }
+          if (key0 < it.ctx) row = (((static_cast<uint32_t>(pg[q]) * L + p.layer) * 2 + kv) * Hkv + it.kvh) * kB;
           for (int hf = 0; hf < 2; ++hf)
-            tma_load_2d(dst + hf * kHalf + pg * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
+            tma_load_2d(dst + hf * kHalf + q * kB * 128, &kv_map, hf * 64, static_cast<int>(row), full);
         }
         ++c;
+      };
+      // the 8 block-table entries of key tile j: two 16-byte loads (rows are padded to a
+      // multiple of 8 entries), issued one tile ahead so their latency hides behind the previous
+      // tile's slot wait and TMA issue
+      auto fetch = [&](const int32_t* bt, int j, int32_t* pg) {
+        const int4 x = reinterpret_cast<const int4*>(bt + j * 8)[0];
+        const int4 y = reinterpret_cast<const int4*>(bt + j * 8)[1];
+        pg[0] = x.x; pg[1] = x.y; pg[2] = x.z; pg[3] = x.w;
+        pg[4] = y.x; pg[5] = y.y; pg[6] = y.z; pg[7] = y.w;
       };
       for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
         const int4 pz = tp.pieces[pc];
         const Item it = item_of(p, pz.x);
         const int32_t* bt = p.block_table + static_cast<int64_t>(it.req) * p.bt_stride;
-        load_kv(it, bt, pz.y, 0);
-        if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // last S of prev piece done
-        mbar_expect_tx(b_qfull, kQT * kTile);
-        for (int i = 0; i < kQT; ++i)
-          for (int hf = 0; hf < 2; ++hf)
-            tma_load_3d(sbase + kOffQ + i * kTile + hf * kHalf, &q_map, hf * 64, it.kvh * G,
-                        it.qs + it.tok0 + i * (kM / G), b_qfull);
-        load_kv(it, bt, pz.y, 1);
-        for (int j = pz.y + 1; j < pz.z; ++j) {
-          load_kv(it, bt, j, 0);
-          load_kv(it, bt, j, 1);
+        int32_t cur[8], nxt[8];
+        fetch(bt, pz.y, cur);
+        for (int j = pz.y; j < pz.z; ++j) {
+          if (j + 1 < pz.z) fetch(bt, j + 1, nxt);
+          load_tile(it, cur, j);
+          if (kv == 0 && j == pz.y) {
+            if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // prev piece's last S done
+            mbar_expect_tx(b_qfull, kQT * kTile);
+            for (int i = 0; i < kQT; ++i)
+              for (int hf = 0; hf < 2; ++hf)
+                tma_load_3d(sbase + kOffQ + i * kTile + hf * kHalf, &q_map, hf * 64, it.kvh * G,
+                            it.qs + it.tok0 + i * (kM / G), b_qfull);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
         }
       }
     }
     __syncwarp();  // reconverge before the CTA barrier (bar.sync is .aligned)
-    } else if (warp == kWarpMma) {
+  } else if (warp == kWarpMma) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(kN, false), idO = idesc_bf16(kHD, true);
-      int c = 0, g = 0, it_local = 0;
-      // S_i = Q_i K^T into S buffer i (K from ring slot of load index ck)
-      auto issue_s = [&](int i, int ck) {
-        int slot;
-        uint32_t use;
-        ring_pos(ck, slot, use);
+      int g = 0, it_local = 0;
+      // S_i = Q_i K_g^T into S buffer i
+      auto issue_s = [&](int i, int gk) {
         const uint32_t q_addr = sbase + kOffQ + i * kTile;
-        const uint32_t k_addr = sbase + kOffRing + slot * kTile;
+        const uint32_t k_addr = sbase + kOffK + (gk % kKSlots) * kTile;
 #pragma unroll
         for (int ks = 0; ks < kHD / 16; ++ks) {
           const uint64_t a = smem_desc(q_addr + (ks >> 2) * kHalf + (ks & 3) * 32, 1, 64);
@@ -342,70 +425,67 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         }
         tc_commit(b_sfull + 8 * i);
       };
-      // O_i += P_i V (P from the first 64 TMEM columns of S_i, V MN-major from ring slot cv)
-      auto issue_pv = [&](int i, int cv, bool first) {
-        int slot;
-        uint32_t use;
-        ring_pos(cv, slot, use);
-        const uint32_t v_addr = sbase + kOffRing + slot * kTile;
+      // O_i += P_i V_g (P from the first 64 TMEM columns of S_i, V MN-major)
+      auto issue_pv = [&](int i, int gv, bool first) {
+        const uint32_t v_addr = sbase + kOffV + (gv % kVSlots) * kTile;
 #pragma unroll
         for (int ks = 0; ks < kN / 16; ++ks) {
           const uint64_t b = smem_desc(v_addr + ks * 2048, kHalf >> 4, 64);
           tc_mma_ts(t_o0 + i * kHD, t_s0 + i * kN + ks * 8, b, idO, (!first || ks > 0) ? 1u : 0u);
         }
       };
-      auto wait_full = [&](int cc, int tag) {
-        int slot;
-        uint32_t use;
-        ring_pos(cc, slot, use);
-        mbar_wait(b_full + 8 * slot, use & 1, tag);
+      auto wait_k = [&](int gk, int tag) {
+        mbar_wait(b_kfull + 8 * (gk % kKSlots), (gk / kKSlots) & 1, tag);
         tc_fence_after();
       };
-      auto release = [&](int cc) {
-        int slot;
-        uint32_t use;
-        ring_pos(cc, slot, use);
-        tc_commit(b_empty + 8 * slot);
+      auto wait_v = [&](int gv, int tag) {
+        mbar_wait(b_vfull + 8 * (gv % kVSlots), (gv / kVSlots) & 1, tag);
+        tc_fence_after();
       };
       for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
         const int4 pz = tp.pieces[pc];
         const int n = pz.z - pz.y;
-        // load indices of this item: K_j = c + 2j, V_j = c + 2j + 1
-        wait_full(c, 13);
+        const int g0 = g;  // global tile count of this piece's first key tile
+        wait_k(g0, 13);
         mbar_wait(b_qfull, it_local & 1, 12);
         tc_fence_after();
-        issue_s(0, c);
-        issue_s(1, c);
-        release(c);
+        issue_s(0, g0);
+        issue_s(1, g0);
+        tc_commit(b_kempty + 8 * (g0 % kKSlots));
         if (n == 1) tc_commit(b_qempty);
         for (int j = 0; j < n; ++j, ++g) {
-          const int ck = c + 2 * j, cv = ck + 1;
           // ---- query tile 0: PV0(j), then S0(j+1) behind it (P0 is consumed in order)
+          ATTN_TRACE(0, g);
           mbar_wait(b_pfull, g & 1, 10);
-          wait_full(cv, 11);
-          issue_pv(0, cv, j == 0);
+          ATTN_TRACE(1, g);
+          wait_v(g, 11);
+          ATTN_TRACE(11, g);
+          issue_pv(0, g, j == 0);
           if (j == n - 1) tc_commit(b_ofull);
           if (j + 1 < n) {
-            wait_full(ck + 2, 13);
-            issue_s(0, ck + 2);
+            ATTN_TRACE(12, g);
+            wait_k(g + 1, 13);
+            ATTN_TRACE(13, g);
+            issue_s(0, g + 1);
           }
+          ATTN_TRACE(2, g);
           // ---- query tile 1
           mbar_wait(b_pfull + 8, g & 1, 15);
+          ATTN_TRACE(3, g);
           tc_fence_after();
-          issue_pv(1, cv, j == 0);
-          release(cv);
+          issue_pv(1, g, j == 0);
+          tc_commit(b_vempty + 8 * (g % kVSlots));
           if (j == n - 1) tc_commit(b_ofull + 8);
           if (j + 1 < n) {
-            issue_s(1, ck + 2);
-            release(ck + 2);
+            issue_s(1, g + 1);
+            tc_commit(b_kempty + 8 * ((g + 1) % kKSlots));
+            ATTN_TRACE(4, g);
             if (j + 2 == n) tc_commit(b_qempty);
           }
         }
-        c += 2 * n;
       }
     }
     __syncwarp();
-    }
   } else {
     // ---------------------------------------------------------------- softmax warpgroups
     const int qt = warp >> 2;                  // query tile of this warpgroup
@@ -426,7 +506,9 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       const int pos_lo = it.ctx - it.qlen + it.tok0 + qt * (kM / G);  // smallest in the tile
       float m_used = -INFINITY, l = 0.f;
       for (int j = pz.y; j < pz.z; ++j, ++g) {
+        if ((threadIdx.x & 127) == 0) ATTN_TRACE(5 + 3 * qt, g);
         mbar_wait(b_s, g & 1, 20 + qt);
+        if ((threadIdx.x & 127) == 0) ATTN_TRACE(6 + 3 * qt, g);
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) TC_LD32(ts + cc * 32, (v + cc * 32));
@@ -457,18 +539,28 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         }
         // P = 2^(s*scale - m_used) as bf16 pairs into the first 64 columns of S_i (the S values
         // are already in registers); masked keys are -inf -> 0.
+        // P = 2^(s*scale - m_used) as bf16 pairs into the first 64 columns of S_i (the S values
+        // are already in registers); masked keys are -inf -> 0.  The first 32 packed columns
+        // are stored while the second half is computed.  (Packed fp32x2 FFMA2/FADD2 and a
+        // polynomial exp2 for a quarter of the pairs were measured slower here: the softmax
+        // phase went from ~1650 to ~2000 cycles per tile, scripts/attn_trace.py.)
         const float neg_m = -m_used;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < kN; i += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
-          const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
+          float p0, p1;
+          if (((i >> 1) & 7) >= kPolyFrom) {
+            ex2_poly2(fmaf(__uint_as_float(v[i]), scale, neg_m), fmaf(__uint_as_float(v[i + 1]), scale, neg_m), p0, p1);
+          } else {
+            p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
+            p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
+          }
           ls[(i >> 1) & 3] += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           v[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          if (i == kN / 2 - 2) TC_ST32(ts, v);
         }
         l = l * alpha + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
-        TC_ST32(ts, v);
         TC_ST32(ts + 32, (v + 32));
         // O_i holds PV_i(0..j-1), all complete (S_i(j), which we waited for, was committed
         // after PV_i(j-1)); PV_i(j) is not issued before our pfull arrival.
@@ -485,6 +577,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         }
         tc_wait_st();
         tc_fence_before();
+        if ((threadIdx.x & 127) == 0) ATTN_TRACE(7 + 3 * qt, g);
         mbar_arrive(b_p);
       }
       // epilogue of this item: wait for its last PV_i (one ofull phase per item)
@@ -630,6 +723,8 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
     throw Error(GLMX_ERR_ARG, "paged attention is built for head_dim 128 and 16-token pages");
   const int G = p.H / p.Hkv;
   if (G * p.Hkv != p.H || kM % G != 0) throw Error(GLMX_ERR_ARG, "unsupported GQA ratio");
+  if (p.bt_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(p.block_table) & 15) != 0)
+    throw Error(GLMX_ERR_ARG, "block-table rows must be 16-byte aligned multiples of 8 entries");
   static bool attr = false;
   if (!attr) {
     GLMX_CUDA(cudaFuncSetAttribute(paged_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -646,6 +741,19 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
 }
 
 int attn_tc_partial_rows() { return kQT * kM; }
+
+int attn_trace_read(long long* out, int n) {
+#ifdef GLMX_ATTN_TRACE
+  const int m = std::min(n, 16 * 1024);
+  GLMX_CUDA(cudaMemcpyFromSymbol(out, g_attn_trace, m * sizeof(long long)));
+  GLMX_CUDA(cudaMemset(g_attn_trace_ptr(), 0, sizeof(long long) * 16 * 1024));
+  return m;
+#else
+  (void)out;
+  (void)n;
+  return -1;
+#endif
+}
 
 // Query tokens per work item: two 128-row tiles of 128/G tokens x G heads.
 int attn_tc_tokens_per_tile(int H, int Hkv) { return kQT * kM / (H / Hkv); }

@@ -397,7 +397,9 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   const uint64_t R = cfg->max_requests;
   const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
   const uint32_t B = kv->cfg.block_tokens;
-  e->bt_stride = static_cast<int>((cfg->max_context + B - 1) / B + 1);
+  // block-table rows padded to a multiple of 8 pages: K3 reads a key tile's 8 entries with two
+  // 16-byte loads
+  e->bt_stride = static_cast<int>(align_up((cfg->max_context + B - 1) / B + 1, 8));
   const char* impl = std::getenv("GLMX_ATTN");
   e->attn_impl = (impl && std::string(impl) == "mma") ? 1 : 0;
   e->tpt = e->attn_impl ? attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv))
@@ -856,6 +858,13 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   std::stable_sort(work.begin(), work.end(), [&](const int2& a, const int2& b) {
     return ctx_len[a.x] - q_len[a.x] + a.y > ctx_len[b.x] - q_len[b.x] + b.y;
   });
+  // repack the caller's block table into rows of a multiple of 8 entries (K3's 16-byte reads)
+  const int bt_pad = static_cast<int>(align_up(static_cast<size_t>(bt_stride), 8));
+  std::vector<int32_t> bt_packed(n_req * static_cast<size_t>(bt_pad), 0);
+  for (uint64_t r = 0; r < n_req; ++r)
+    std::memcpy(bt_packed.data() + r * bt_pad, block_table + r * bt_stride, bt_stride * 4);
+  block_table = bt_packed.data();
+  bt_stride = bt_pad;
   const size_t nr = n_req * 4, nbt = n_req * static_cast<size_t>(bt_stride) * 4;
   auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t o_ql = a16(nr), o_ctx = o_ql + a16(nr), o_bt = o_ctx + a16(nr);

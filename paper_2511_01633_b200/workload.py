@@ -70,7 +70,8 @@ def count_tokens(text):
 
 class GraphCoTWorkload:
     def __init__(self, engine, retriever, n_queries, lanes, seed=0, min_hops=2, max_hops=4,
-                 skew=2.5, templates=None, node_ids=None, overlap_retrieval=True):
+                 skew=2.5, templates=None, node_ids=None, overlap_retrieval=True,
+                 question_pool=0):
         self.engine = engine
         self.overlap_retrieval = overlap_retrieval
         self.kv = engine.kv if engine is not None else None
@@ -81,9 +82,19 @@ class GraphCoTWorkload:
         g = retriever.graph
         n = g.node_count()
         self.sessions = []
-        for q in range(n_queries):
+        # question_pool > 0: questions are drawn WITH replacement from that many candidate source
+        # lists, as generate_workload picks clusters (workload.cpp:216-225), so questions recur
+        # across sessions (and, sharded i mod N, across GPUs)
+        pool = []
+        for _ in range(question_pool):
             m = rnd.randint(min_hops, max_hops)
-            src = [min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)]
+            pool.append([min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)])
+        for q in range(n_queries):
+            if pool:
+                src = list(pool[rnd.randrange(len(pool))])
+            else:
+                m = rnd.randint(min_hops, max_hops)
+                src = [min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)]
             ids = [g.node_id(v) for v in src]
             question = "Which item is linked from all of: " + "; ".join(ids) + "?"
             self.sessions.append(Session(f"q{q:05d}", src, question))
