@@ -260,8 +260,9 @@ def main():
     # enough queries (per rank) that every lane stays busy through the timed rotations
     n_q = args.lanes * (rotations // 6 + 2)
     pool_n = args.question_pool if args.question_pool >= 0 else (n_q * ws) // 2
+    nidx = glmx.NodeIndex(g)  # RetrieveNode: device VectorIndex + retrieval LRU (K5)
     wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed,
-                          question_pool=pool_n)
+                          question_pool=pool_n, node_index=nidx)
     wl.sessions = wl.sessions[rank::ws]  # query i -> rank i % N
     # cross-GPU prefix hits (C4): every rotation is an epoch; the ranks exchange their resident
     # (block id, page) directories, and a run of blocks missing locally but resident on a peer is
@@ -306,6 +307,9 @@ def main():
     h2d = d2h = 0
     chunk_ms = 0.0
     k1_bytes = 0
+    k5_launches = 0
+    k5_ms = 0.0
+    probes_seen = nidx.stats()[2]
     k1_rotations = 0
     for _ in range(args.steps):
         r = step()
@@ -316,6 +320,11 @@ def main():
         if r.chunks:
             chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h)
             k1_bytes += r.chunk_bytes
+            probes = nidx.stats()[2]
+            if probes > probes_seen:  # one K5 nearest scan served this rotation's misses
+                k5_launches += 1
+                k5_ms += nidx.last_kernel_ms()
+                probes_seen = probes
         tokens += r.prompt_tokens
         computed += r.computed_tokens
         cached += r.cached_tokens
@@ -393,6 +402,15 @@ def main():
                         "overlapped_with_prefill": True,
                         "note": "64 chunks per rotation: latency-bound, hidden behind the prefill "
                                 "on the graph stream"})
+    if k5_launches:
+        k5_bytes = len(nidx) * 64 * 4  # the index is streamed once per scan
+        k5_gbs = k5_bytes * k5_launches / (k5_ms * 1e-3) / 1e9
+        kernels.append({"kernel": "K5 nearest (RetrieveNode exact scan, bit-exact 8-lane dot)",
+                        "bound": "hbm", "achieved": k5_gbs, "peak": hbm, "unit": "GB/s",
+                        "frac": k5_gbs / hbm, "ms_per_launch": k5_ms / k5_launches,
+                        "overlapped_with_prefill": True,
+                        "retrieval_stats": dict(zip(("cache_hits", "cache_misses", "index_probes"),
+                                                    nidx.stats()))})
     # dominant kernel of the step by device time: the cuBLAS GEMMs (Llama-3-8B linears)
     roof = {"bound": "tensor", "achieved": gemm_tflops, "peak": tc_peak, "unit": "TFLOP/s",
             "frac": gemm_tflops / tc_peak,
@@ -433,7 +451,7 @@ def main():
         "kernels": kernels,
         # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
         # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
-        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations),
+        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations + k5_launches),
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:

@@ -193,6 +193,23 @@ int glmx_chunk_build(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
 int64_t glmx_node_info_rendered(glmx_graph* g, const glmx_chunk_config* cfg, const char* id,
                                 char* buf, uint64_t cap);
 /* device time (ms) of the last K1 launch, measured with CUDA events on its stream */
+/* RetrieveNode (Retriever::retrieve_node_traced, retriever.cpp:49-66 over VectorIndex,
+ * index.hpp:22-41).  glmx_index_build embeds (embedder.cpp:19-36) the index text of every node —
+ * its string "title", else string "name" (index.cpp:12-25, default Config) — into a device
+ * resident [rows][dim] fp32 table and sizes the retrieval LRU (Config::retrieval_cache_capacity,
+ * 1024 by default).  glmx_retrieve_nodes resolves n texts (bytes + n+1 offsets) in order: an LRU
+ * hit returns the cached node, a miss runs the exact GPU nearest scan (K5: scores bit-identical to
+ * dot.hpp's 8-lane tree, ties to the lowest id) and caches the result.  Out: graph node indices
+ * and hit flags.  Empty index -> GLMX_ERR_RETRIEVAL (EmptyIndex). */
+int glmx_index_build(glmx_graph* g, int32_t dim, uint64_t cache_capacity);
+uint64_t glmx_index_size(const glmx_graph* g);
+int glmx_retrieve_nodes(glmx_graph* g, const char* text_bytes, const uint64_t* text_offsets,
+                        uint64_t n, int32_t* out_node_idx, uint8_t* out_cache_hit);
+/* {cache_hits, cache_misses, index_probes} since glmx_index_build (RetrievalStats) */
+void glmx_retriever_stats(const glmx_graph* g, int64_t out3[3]);
+float glmx_retrieve_last_kernel_ms(const glmx_graph* g);
+/* embed(text, dim) on the host (embedder.cpp:19-36): writes (dim + 7) / 8 * 8 floats */
+int glmx_embed_text(const char* text, uint64_t len, int32_t dim, float* out);
 float glmx_chunk_last_kernel_ms(const glmx_graph* g);
 
 /* ================================================================== model (random-init Llama) */

@@ -219,6 +219,10 @@ def ref():
                                              C.c_char_p, C.c_uint64]
         L.ref_retrieve_node.restype = C.c_int64
         L.ref_retrieve_node.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_uint64]
+        L.ref_embed.restype = C.c_int64
+        L.ref_embed.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_uint64]
+        L.ref_nearest.restype = C.c_int64
+        L.ref_nearest.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_char_p, C.c_uint64]
         L.ref_render.restype = C.c_int64
         L.ref_render.argtypes = [C.c_char_p] * 4 + [C.c_char_p, C.c_uint64]
         L.ref_trace_len.restype = C.c_uint64
@@ -260,6 +264,14 @@ def port():
         L.glmo_node_info_rendered.restype = C.c_int64
         _port = L
     return _port
+
+
+def ref_embed(text, dim=64):
+    """The reference's embed(text, dim) (embedder.cpp:19-36) as a list of floats (padded)."""
+    L = ref()
+    out = (C.c_float * 1024)()
+    n = L.ref_embed(text.encode(), dim, out, 1024)
+    return [out[i] for i in range(n)]
 
 
 def ref_chain_ids(tokens, block_tokens=16):
@@ -318,6 +330,15 @@ class RefGraph:
             n = self.L.ref_node_info_rendered(self.h, node_id.encode(), k, weight_mode,
                                               int(directed), buf, n)
         return buf.raw[:n].decode()
+
+    def nearest(self, text, k):
+        """VectorIndex::nearest(text, k) ids (index built once per call, default Config)."""
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        n = self.L.ref_nearest(self.h, text.encode(), k, buf, cap)
+        if n < 0:
+            raise LookupError(self.L.ref_last_error().decode())
+        return buf.raw[:n].decode().split("\n") if n else []
 
     def retrieve_node(self, text):
         buf = C.create_string_buffer(4096)

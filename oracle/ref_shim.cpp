@@ -29,6 +29,7 @@
 #include "glm/llm/scripted.hpp"
 #include "glm/orchestrator/orchestrator.hpp"
 #include "glm/retrieve/retriever.hpp"
+#include "glm/embed/embedder.hpp"
 #include "json.hpp"
 
 using nlohmann::json;
@@ -296,6 +297,31 @@ int64_t ref_retrieve_node(void* g, const char* text, char* buf, std::uint64_t ca
   glm::Retriever r(rg->g, index, cfg);
   try {
     return copy_out(r.retrieve_node(text), buf, cap);
+  } catch (const std::exception& e) {
+    return -status_of(e);
+  }
+}
+
+// embed(text, dim) of the reference (embedder.cpp:19-36); writes padded_size floats
+int64_t ref_embed(const char* text, int dim, float* out, std::uint64_t cap) {
+  glm::Embedding e = glm::embed(text, dim);
+  const std::uint64_t n = e.padded_size();
+  for (std::uint64_t i = 0; i < n && i < cap; ++i) out[i] = e.data()[i];
+  return static_cast<int64_t>(n);
+}
+
+// VectorIndex::nearest(text, k) ids (index.cpp:41-56), '\n'-joined; -status on error
+int64_t ref_nearest(void* g, const char* text, int k, char* buf, std::uint64_t cap) {
+  auto* rg = static_cast<RefGraph*>(g);
+  try {
+    glm::Config cfg;
+    glm::VectorIndex index = glm::VectorIndex::build(rg->g, cfg);
+    std::string out;
+    for (const auto& s : index.nearest(text, k)) {
+      if (!out.empty()) out += '\n';
+      out += s.id;
+    }
+    return copy_out(out, buf, cap);
   } catch (const std::exception& e) {
     return -status_of(e);
   }

@@ -9,4 +9,5 @@ from ._lib import (CacheExhausted, ConfigError, GlmxError, RetrievalError, lib) 
 from .kvcache import (PLAIN_LRU, PRIORITY, TIER_I, TIER_II, TIER_III, TIER_IV,  # noqa: F401
                       KvCacheState, PrefillReport, chain_ids, tokenize)
 from .model import LLAMA3_8B, TINY, Engine, Model, ModelConfig, Request  # noqa: F401
-from .retrieve import BY_EDGE_TYPE, TOTAL_DEGREE, PropertyGraph, Retriever  # noqa: F401
+from .retrieve import (BY_EDGE_TYPE, TOTAL_DEGREE, NodeIndex, PropertyGraph, Retriever,  # noqa: F401
+                       embed)

@@ -150,6 +150,13 @@ _SIGS = {
     "glmx_attn_trace_read": (C.c_int32, [i64p, C.c_int32]),
     "glmx_attn_schedule": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
                                      C.c_int32, i32p, i32p, i32p, i64p]),
+    "glmx_index_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
+    "glmx_index_size": (C.c_uint64, [C.c_void_p]),
+    "glmx_retrieve_nodes": (C.c_int, [C.c_void_p, C.c_char_p, u64p, C.c_uint64, i32p,
+                                      C.POINTER(C.c_uint8)]),
+    "glmx_retriever_stats": (None, [C.c_void_p, i64p]),
+    "glmx_retrieve_last_kernel_ms": (C.c_float, [C.c_void_p]),
+    "glmx_embed_text": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, f32p]),
     "glmx_attention_run": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                                      C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_uint64, i32p, i32p, i32p, i32p,

@@ -26,6 +26,8 @@ int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefil
                         int32_t*, float*);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
+int index_build_impl(glmx_graph*, int, uint64_t);
+int retrieve_impl(glmx_graph*, const char*, const uint64_t*, uint64_t, int32_t*, uint8_t*);
 int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
                          float, void*, uint32_t, uint32_t, uint32_t, void*, int, cudaStream_t,
                          float*);
@@ -405,6 +407,26 @@ int64_t glmx_node_info_rendered(glmx_graph* g, const glmx_chunk_config* cfg, con
 }
 
 float glmx_chunk_last_kernel_ms(const glmx_graph* g) { return g->last_ms; }
+
+int glmx_index_build(glmx_graph* g, int32_t dim, uint64_t cache_capacity) {
+  return guarded([&] { return index_build_impl(g, dim, cache_capacity); });
+}
+uint64_t glmx_index_size(const glmx_graph* g) { return g->idx_node.size(); }
+int glmx_retrieve_nodes(glmx_graph* g, const char* text_bytes, const uint64_t* text_offsets,
+                        uint64_t n, int32_t* out_node_idx, uint8_t* out_cache_hit) {
+  return guarded([&] { return retrieve_impl(g, text_bytes, text_offsets, n, out_node_idx, out_cache_hit); });
+}
+void glmx_retriever_stats(const glmx_graph* g, int64_t out3[3]) {
+  for (int i = 0; i < 3; ++i) out3[i] = g->stats[i];
+}
+float glmx_retrieve_last_kernel_ms(const glmx_graph* g) { return g->last_retrieve_ms; }
+int glmx_embed_text(const char* text, uint64_t len, int32_t dim, float* out) {
+  return guarded([&] {
+    if (dim < 1) throw Error(GLMX_ERR_ARG, "dim must be >= 1");
+    glmx::embed(text, len, dim, out);
+    return GLMX_OK;
+  });
+}
 
 // ------------------------------------------------------------------ model / engine
 int glmx_model_create(const glmx_model_config* cfg, int32_t device, glmx_model** out) {

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <fstream>
 #include <map>
+#include <set>
 #include <numeric>
 
 namespace glmx {
@@ -219,6 +220,7 @@ struct JParser {
 struct RawNode {
   std::string id, type;
   std::map<std::string, std::string> attrs;  // key -> rendered value (std::map like NodeRecord)
+  std::set<std::string> str_attrs;           // keys whose value is a JSON string scalar
 };
 struct RawEdge {
   std::string src, dst, etype;
@@ -251,6 +253,18 @@ HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges) {
     g.ids.push_back(std::move(nodes[i].id));
     g.types.push_back(std::move(nodes[i].type));
     g.attrs.emplace_back(nodes[i].attrs.begin(), nodes[i].attrs.end());
+    std::string text;
+    uint8_t has = 0;
+    for (const char* f : {"title", "name"}) {
+      auto it = nodes[i].attrs.find(f);
+      if (it != nodes[i].attrs.end() && nodes[i].str_attrs.count(f)) {
+        text = it->second;
+        has = 1;
+        break;
+      }
+    }
+    g.itext.push_back(std::move(text));
+    g.has_itext.push_back(has);
   }
   std::unordered_map<std::string, int32_t> et;
   for (const auto& e : edges) {
@@ -444,6 +458,7 @@ HostGraph load_graph_jsonl(const std::string& path) {
             n.attrs[k] = s + "]";
           } else {
             n.attrs[k] = render_scalar(v, jp);
+            if (v.kind == JVal::Str) n.str_attrs.insert(k);
           }
         }
       }
@@ -485,6 +500,7 @@ HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t see
     if (i % 10 == 9) {
       r.type = "user";
       r.attrs["name"] = std::string("user ") + idb;
+      r.str_attrs.insert("name");
     } else {
       r.type = "item";
       uint64_t x = splitmix(s);
@@ -492,6 +508,7 @@ HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t see
       r.attrs["price"] = std::to_string(1 + (x >> 16) % 999);
       r.attrs["brand"] = brand[(x >> 32) % 6];
       r.attrs["category"] = cat[(x >> 40) % 6];
+      r.str_attrs = {"title", "brand", "category"};
     }
   }
   std::vector<RawEdge> edges;

@@ -22,6 +22,10 @@ struct HostGraph {
   std::vector<std::string> ids;            // ascending
   std::vector<std::string> types;
   std::vector<std::vector<std::pair<std::string, std::string>>> attrs;  // rendered, key order
+  // VectorIndex text per node (index.cpp:12-25, default Config): the "title" attribute when it is
+  // a string, else "name" when it is a string; has_itext[v] = 0 for nodes without one
+  std::vector<std::string> itext;
+  std::vector<uint8_t> has_itext;
   std::unordered_map<std::string, int32_t> index;
   std::vector<std::string> etypes;
   std::vector<int32_t> src, dst, etype;    // edges in file order

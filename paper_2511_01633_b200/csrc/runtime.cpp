@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "kernels/common.cuh"
+#include "kernels/retrieve.cuh"
 
 using namespace glmx;
 
@@ -980,5 +981,109 @@ int rope_append_run_impl(const void* qkv, const int32_t* pos, const int64_t* slo
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (out_ms) *out_ms = ms / static_cast<float>(reps);
+  return GLMX_OK;
+}
+
+// ======================================================================== K5 RetrieveNode
+// VectorIndex::build (index.cpp:27-39) with the default Config: every node with a string "title"
+// (else "name") attribute, ascending id, embed(text, dim) computed on the host exactly as
+// embedder.cpp does, rows uploaded once.
+int index_build_impl(glmx_graph* g, int dim, uint64_t lru_capacity) {
+  if (dim < 1 || glmx::embed_padded(dim) > 128) throw Error(GLMX_ERR_ARG, "embedding dim must be in [1, 128]");
+  if (g->device < 0) throw Error(GLMX_ERR_NO_DEVICE, "graph has no device");
+  const int pad = glmx::embed_padded(dim);
+  const int dpad = pad <= 32 ? 32 : pad <= 64 ? 64 : 128;  // kernel row widths (zero-filled)
+  std::vector<float> rows;
+  g->idx_node.clear();
+  std::vector<float> e(pad);
+  for (uint64_t v = 0; v < g->host.n(); ++v) {
+    if (!g->host.has_itext[v]) continue;
+    const std::string& t = g->host.itext[v];
+    glmx::embed(t.data(), t.size(), dim, e.data());
+    rows.insert(rows.end(), e.begin(), e.end());
+    rows.insert(rows.end(), dpad - pad, 0.f);
+    g->idx_node.push_back(static_cast<int32_t>(v));
+  }
+  g->idx_dim = dim;
+  g->idx_pad = dpad;
+  DeviceGuard dg(g->device);
+  g->d_emb.reserve(std::max<size_t>(rows.size(), 1) * 4);
+  if (!rows.empty())
+    GLMX_CUDA(cudaMemcpy(g->d_emb.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+  g->lru.set_capacity(lru_capacity);
+  g->stats[0] = g->stats[1] = g->stats[2] = 0;
+  return GLMX_OK;
+}
+
+// Batched Retriever::retrieve_node_traced (retriever.cpp:49-66) in request order: LRU get ->
+// hit; else a probe, whose result is put into the LRU at that point of the sequence (value
+// resolved after the one GPU scan that serves every probe of the batch).
+int retrieve_impl(glmx_graph* g, const char* bytes, const uint64_t* offs, uint64_t n,
+                  int32_t* out_node, uint8_t* out_hit) {
+  if (g->idx_pad == 0) throw Error(GLMX_ERR_ARG, "no index: call glmx_index_build first");
+  if (g->idx_node.empty() && n) throw Error(GLMX_ERR_RETRIEVAL, "EmptyIndex: the index has no entries");
+  std::vector<int64_t> val(n);
+  std::vector<std::string> probe_text;
+  std::unordered_map<std::string, int64_t> probe_of;  // text -> probe slot of this batch
+  for (uint64_t i = 0; i < n; ++i) {
+    std::string t(bytes + offs[i], offs[i + 1] - offs[i]);
+    int64_t v;
+    if (g->lru.get(t, &v)) {
+      ++g->stats[0];
+      if (out_hit) out_hit[i] = 1;
+      val[i] = v;
+      continue;
+    }
+    ++g->stats[1];
+    ++g->stats[2];
+    if (out_hit) out_hit[i] = 0;
+    auto it = probe_of.find(t);
+    int64_t slot;
+    if (it == probe_of.end()) {
+      slot = static_cast<int64_t>(probe_text.size());
+      probe_of.emplace(t, slot);
+      probe_text.push_back(std::move(t));
+      t = probe_text.back();
+    } else {
+      slot = it->second;
+    }
+    const int64_t ph = -(slot + 1);  // placeholder until the scan resolves it
+    g->lru.put(t, ph);
+    val[i] = ph;
+  }
+  std::vector<int32_t> probe_node(probe_text.size(), -1);
+  if (!probe_text.empty()) {
+    const int pad = glmx::embed_padded(g->idx_dim), dpad = g->idx_pad;
+    const int nq = static_cast<int>(probe_text.size());
+    std::vector<float> q(static_cast<size_t>(nq) * dpad, 0.f);
+    for (int k = 0; k < nq; ++k)
+      glmx::embed(probe_text[k].data(), probe_text[k].size(), g->idx_dim, q.data() + static_cast<size_t>(k) * dpad);
+    (void)pad;
+    DeviceGuard dg(g->device);
+    cudaStream_t s = g->stream;
+    g->d_qemb.reserve(q.size() * 4);
+    g->d_best.reserve(static_cast<size_t>(nq) * 8);
+    GLMX_CUDA(cudaMemcpyAsync(g->d_qemb.p, q.data(), q.size() * 4, cudaMemcpyHostToDevice, s));
+    GLMX_CUDA(cudaMemsetAsync(g->d_best.p, 0, static_cast<size_t>(nq) * 8, s));
+    GLMX_CUDA(cudaEventRecord(g->ev0, s));
+    nearest_top1(g->d_emb.as<float>(), static_cast<int>(g->idx_node.size()), dpad, g->d_qemb.as<float>(), nq,
+                 g->d_best.as<unsigned long long>(), s);
+    GLMX_CUDA(cudaEventRecord(g->ev1, s));
+    std::vector<unsigned long long> best(nq);
+    GLMX_CUDA(cudaMemcpyAsync(best.data(), g->d_best.p, nq * 8, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaStreamSynchronize(s));
+    GLMX_CUDA(cudaEventElapsedTime(&g->last_retrieve_ms, g->ev0, g->ev1));
+    for (int k = 0; k < nq; ++k) {
+      const uint32_t row = 0xFFFFFFFFu - static_cast<uint32_t>(best[k] & 0xFFFFFFFFu);
+      if (best[k] == 0 || row >= g->idx_node.size()) throw Error(GLMX_ERR_CUDA, "nearest scan returned no row");
+      probe_node[k] = g->idx_node[row];
+      g->lru.resolve(-(k + 1), probe_node[k]);
+    }
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    int64_t v = val[i];
+    if (v < 0) v = probe_node[-v - 1];
+    if (out_node) out_node[i] = static_cast<int32_t>(v);
+  }
   return GLMX_OK;
 }

@@ -13,6 +13,7 @@
 
 #include "host/attn_sched.hpp"
 #include "host/block_engine.hpp"
+#include "host/vindex.hpp"
 #include "host/graph.hpp"
 #include "kernels/attn.cuh"
 #include "kernels/chunk.cuh"
@@ -67,6 +68,13 @@ struct glmx_graph {
   // K1 scratch
   DBuf d_nodes, d_sel, d_cnt, d_len, d_off, d_bytes, d_flag, d_tidx, d_tid, d_tbeg, d_tend,
       d_toff, d_temp;
+  // K5 RetrieveNode: device index (rows = nodes with an index text, ascending id), LRU, stats
+  int idx_dim = 0, idx_pad = 0;
+  std::vector<int32_t> idx_node;  // row -> node index
+  DBuf d_emb, d_qemb, d_best;
+  glmx::TextLru lru{1024};
+  int64_t stats[3] = {0, 0, 0};  // cache_hits, cache_misses, index_probes
+  float last_retrieve_ms = 0.f;
   void upload();
   ~glmx_graph();
 };

@@ -17,6 +17,7 @@ class ChunkBatch:
     token_ids: list      # per request list[int] (empty when vocab == 0)
     token_spans: list    # per request list[(begin, end)] byte spans within the chunk
     kernel_ms: float
+    nodes: list = None   # node index per chunk (set by the workload driver)
 
 
 class PropertyGraph:
@@ -105,3 +106,48 @@ class Retriever:
             ids.append([tid[j] for j in range(toff[i], toff[i + 1])] if self.cfg.vocab else [])
             spans.append([(tbeg[j], tend[j]) for j in range(toff[i], toff[i + 1])])
         return ChunkBatch(texts, ids, spans, lib().glmx_chunk_last_kernel_ms(self.graph.h))
+
+
+def embed(text: str, dim: int = 64):
+    """embed(text, dim) of the reference (embedder.cpp:19-36), host C++: list of padded floats."""
+    out = (C.c_float * ((dim + 7) // 8 * 8))()
+    b = text.encode()
+    check(lib().glmx_embed_text(b, len(b), dim, out))
+    return list(out)
+
+
+class NodeIndex:
+    """RetrieveNode over the device-resident VectorIndex of a graph (K5 + the retrieval LRU),
+    Retriever::retrieve_node_traced semantics (retriever.cpp:49-66)."""
+
+    def __init__(self, graph: PropertyGraph, dim: int = 64, cache_capacity: int = 1024):
+        self.graph = graph
+        check(lib().glmx_index_build(graph.h, dim, cache_capacity))
+
+    def __len__(self):
+        return lib().glmx_index_size(self.graph.h)
+
+    def retrieve_nodes(self, texts):
+        """Resolve texts in order -> (node indices, cache-hit flags)."""
+        bs = [t.encode() for t in texts]
+        offs = [0]
+        for b in bs:
+            offs.append(offs[-1] + len(b))
+        n = len(bs)
+        off_arr = (C.c_uint64 * (n + 1))(*offs)
+        out = (C.c_int32 * max(1, n))()
+        hit = (C.c_uint8 * max(1, n))()
+        check(lib().glmx_retrieve_nodes(self.graph.h, b"".join(bs), off_arr, n, out, hit))
+        return [out[i] for i in range(n)], [bool(hit[i]) for i in range(n)]
+
+    def retrieve_node(self, text):
+        return self.graph.node_id(self.retrieve_nodes([text])[0][0])
+
+    def stats(self):
+        """(cache_hits, cache_misses, index_probes)."""
+        out = (C.c_int64 * 3)()
+        lib().glmx_retriever_stats(self.graph.h, out)
+        return tuple(out)
+
+    def last_kernel_ms(self):
+        return lib().glmx_retrieve_last_kernel_ms(self.graph.h)

@@ -71,8 +71,11 @@ def count_tokens(text):
 class GraphCoTWorkload:
     def __init__(self, engine, retriever, n_queries, lanes, seed=0, min_hops=2, max_hops=4,
                  skew=2.5, templates=None, node_ids=None, overlap_retrieval=True,
-                 question_pool=0):
+                 question_pool=0, node_index=None):
         self.engine = engine
+        # node_index (NodeIndex): the action's RetrieveNode("<id>") is resolved by the K5 nearest
+        # scan + retrieval LRU (retriever.cpp:49-66) instead of taking the scripted source node
+        self.node_index = node_index
         self.overlap_retrieval = overlap_retrieval
         self.kv = engine.kv if engine is not None else None
         self.retriever = retriever
@@ -163,14 +166,12 @@ class GraphCoTWorkload:
             res.prompt_tokens += r.cached_tokens + r.computed_tokens + r.tail_tokens
         acting = [c for c in calls if c.agent == "action"]
         if acting:
-            batch = chunks if chunks is not None else self.retriever.chunk_build(
-                [c.session.sources[c.session.round] for c in acting])
+            batch = chunks if chunks is not None else self._retrieve_and_build(acting)
             for c, text in zip(acting, batch.texts):
                 c.session.notebook += text + "\n"  # PrintStmt: raw chunk + "\n" (interp.cpp:68-74)
             res.chunks = len(acting)
             g = self.retriever.graph
-            res.chunk_bytes = sum(8 + 8 * g.total_degree(c.session.sources[c.session.round])
-                                  for c in acting)
+            res.chunk_bytes = sum(8 + 8 * g.total_degree(v) for v in batch.nodes)
             res.chunk_bytes += sum(2 * len(t) + 20 * len(sp) for t, sp in
                                    zip(batch.texts, batch.token_spans))
         still = []
@@ -194,6 +195,18 @@ class GraphCoTWorkload:
         self.active = still
         return res
 
+    def _retrieve_and_build(self, acting):
+        """RetrieveNode (K5, when a node index is attached) then NodeInfo chunks (K1) for the
+        rotation's action snippets; both on the graph's stream."""
+        if self.node_index is not None:
+            texts = [c.session.task[len("vertex chunks for: "):] for c in acting]
+            nodes, _ = self.node_index.retrieve_nodes(texts)
+        else:
+            nodes = [c.session.sources[c.session.round] for c in acting]
+        batch = self.retriever.chunk_build(nodes)
+        batch.nodes = nodes
+        return batch
+
     def rotation(self) -> RotationResult:
         """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on
         the (scripted) action code, not on this prefill, so K1 runs on the graph's own CUDA stream
@@ -205,9 +218,8 @@ class GraphCoTWorkload:
         built = {}
         th = None
         if acting and self.overlap_retrieval:
-            nodes = [c.session.sources[c.session.round] for c in acting]
             th = threading.Thread(target=lambda: built.__setitem__(
-                "b", self.retriever.chunk_build(nodes)))
+                "b", self._retrieve_and_build(acting)))
             th.start()
         try:
             reps, first = self.prefill(calls)
