@@ -1,12 +1,63 @@
 #include "attn_sched.hpp"
 
 #include <algorithm>
+#include <functional>
+#include <queue>
+#include <tuple>
 #include <vector>
 
 namespace glmx {
 
 namespace {
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+void stream_k_cut(const int32_t* work_xy, int Hkv, const std::vector<int>& tiles_of, int n_sm,
+                  AttnSchedule& s, std::vector<int>& n_pieces_of) {
+  const int n_items = static_cast<int>(tiles_of.size());
+  std::vector<int> order(n_items);
+  for (int w = 0; w < n_items; ++w) order[w] = w;
+  auto key = [&](int w) {
+    return std::make_tuple(work_xy[2 * (w / Hkv)], w % Hkv, work_xy[2 * (w / Hkv) + 1]);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+  std::vector<int64_t> start(n_items + 1, 0);
+  for (int i = 0; i < n_items; ++i) start[i + 1] = start[i] + tiles_of[order[i]];
+  const int64_t W = start[n_items];
+  const int grid = static_cast<int>(std::min<int64_t>(n_sm, W));
+  const int64_t share = (W + grid - 1) / grid;
+  const int64_t snap = std::max<int64_t>(1, share / 8);
+  std::vector<int64_t> bnd(grid + 1);
+  bnd[0] = 0;
+  bnd[grid] = W;
+  int i = 0;
+  for (int c = 1; c < grid; ++c) {
+    int64_t b = W * c / grid;
+    while (i < n_items && start[i + 1] <= b) ++i;
+    if (i < n_items) {
+      if (b - start[i] <= snap) b = start[i];
+      else if (start[i + 1] - b <= snap) b = start[i + 1];
+    }
+    bnd[c] = std::max(b, bnd[c - 1]);
+  }
+  s.grid = grid;
+  i = 0;
+  for (int c = 0; c < grid; ++c) {
+    s.cta_off[c] = s.n_pieces;
+    int64_t t = bnd[c];
+    while (t < bnd[c + 1]) {
+      while (start[i + 1] <= t) ++i;
+      const int64_t e = std::min(bnd[c + 1], start[i + 1]);
+      AttnPiece& p = s.pieces[s.n_pieces++];
+      p.item = order[i];
+      p.j0 = static_cast<int32_t>(t - start[i]);
+      p.j1 = static_cast<int32_t>(e - start[i]);
+      p.part = -1;
+      ++n_pieces_of[order[i]];
+      t = e;
+    }
+  }
+  s.cta_off[grid] = s.n_pieces;
+}
 }  // namespace
 
 size_t attn_sched_bytes(int max_items, int n_sm, size_t* off_pieces, size_t* off_cta,
@@ -41,28 +92,49 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     s.total_tiles += tiles[w];
   }
   std::vector<int> n_pieces_of(n_items, 0);
+  const int64_t max_tiles = *std::max_element(tiles.begin(), tiles.end());
   if (n_items * 2 > n_sm) {
-    // Enough items to occupy the SMs: whole items, longest first, dealt round-robin to
-    // min(n_items, n_sm) persistent CTAs (no partials, no combine pass).  Splitting here does not
-    // pay: the partial O traffic (128 KB per piece) and the combine pass cost more than the
-    // idle-SM tail they remove, and the tensor-heavy kernel runs at the power cap anyway.
+    // Enough items to occupy the SMs: whole items, longest first, each to the least-loaded of
+    // min(n_items, n_sm) persistent CTAs (LPT; equal items reduce to round-robin).
     std::vector<int> order(n_items);
     for (int w = 0; w < n_items; ++w) order[w] = w;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tiles[a] > tiles[b]; });
     const int grid = std::min(n_items, n_sm);
-    s.grid = grid;
-    for (int c = 0; c < grid; ++c) {
-      s.cta_off[c] = s.n_pieces;
-      for (int i = c; i < n_items; i += grid) {
-        AttnPiece& p = s.pieces[s.n_pieces++];
-        p.item = order[i];
-        p.j0 = 0;
-        p.j1 = tiles[order[i]];
-        p.part = -1;
-        n_pieces_of[order[i]] = 1;
-      }
+    std::vector<std::vector<int>> mine(grid);
+    std::vector<int64_t> load(grid, 0);
+    using Slot = std::pair<int64_t, int>;  // (load, cta): min-heap, ties to the lower CTA
+    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+    for (int c = 0; c < grid; ++c) heap.push({0, c});
+    for (int w : order) {
+      auto [l, c] = heap.top();
+      heap.pop();
+      mine[c].push_back(w);
+      load[c] = l + tiles[w];
+      heap.push({load[c], c});
     }
-    s.cta_off[grid] = s.n_pieces;
+    const int64_t makespan = *std::max_element(load.begin(), load.end());
+    const double ideal = static_cast<double>(s.total_tiles) / n_sm;
+    if (makespan > 1.3 * ideal && max_tiles >= 16) {
+      // A long tail (e.g. 168 long items on 148 SMs: two waves): cut the flattened tile sequence
+      // into n_sm equal ranges instead (stream-K).  Items ordered by (request, kv head, first
+      // token) so the query blocks reading the same pages run on neighbouring CTAs at the same
+      // time; boundaries within share/8 tiles of an item edge snap to it.
+      stream_k_cut(work_xy, Hkv, tiles, n_sm, s, n_pieces_of);
+    } else {
+      s.grid = grid;
+      for (int c = 0; c < grid; ++c) {
+        s.cta_off[c] = s.n_pieces;
+        for (int w : mine[c]) {
+          AttnPiece& p = s.pieces[s.n_pieces++];
+          p.item = w;
+          p.j0 = 0;
+          p.j1 = tiles[w];
+          p.part = -1;
+          n_pieces_of[w] = 1;
+        }
+      }
+      s.cta_off[grid] = s.n_pieces;
+    }
   } else {
     // Few items (e.g. one long-context query): split every item's key range into up to
     // n_sm / n_items near-equal pieces, one piece per CTA; the combine pass merges them.

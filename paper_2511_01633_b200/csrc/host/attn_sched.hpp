@@ -2,9 +2,11 @@
 //
 // The kernel's unit of work is a piece: a key-tile range [j0, j1) of one item (request, 64-token
 // query block, kv head); every CTA walks its own list of pieces.  With at least n_sm / 2 items,
-// whole items are dealt longest-first round-robin (the v1 schedule).  With fewer items (a single
+// whole items go longest-first to the least-loaded CTA (LPT), unless that leaves a long tail
+// (makespan > 1.3 x total / n_sm, e.g. 168 long items on 148 SMs), in which case the flattened
+// tile sequence is cut into n_sm equal ranges (stream-K).  With fewer items (a single
 // long-context query has only 8-16), each item's key range is split into up to n_sm / n_items
-// pieces; split pieces write an unnormalised partial (O, m, l) and a combine pass merges them.
+// pieces.  Split pieces write an unnormalised partial (O, m, l) and a combine pass merges them.
 #pragma once
 
 #include <cstddef>

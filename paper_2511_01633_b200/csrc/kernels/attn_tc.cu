@@ -277,6 +277,7 @@ struct TcParams {
 
 struct Item {
   int req, tok0, kvh, qlen, ctx, qs, n_kt;
+  int nqt;  // query tiles in use: 1 when the item's block holds <= 128/G tokens
 };
 
 __device__ __forceinline__ Item item_of(const AttnParams& p, int w) {
@@ -291,6 +292,7 @@ __device__ __forceinline__ Item item_of(const AttnParams& p, int w) {
   const int G = p.H / p.Hkv;
   const int max_pos = it.ctx - it.qlen + min(it.tok0 + kQT * kM / G, it.qlen) - 1;
   it.n_kt = max_pos / kN + 1;
+  it.nqt = it.qlen - it.tok0 > kM / G ? 2 : 1;
   return it;
 }
 
@@ -396,8 +398,8 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           load_tile(it, cur, j);
           if (kv == 0 && j == pz.y) {
             if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);  // prev piece's last S done
-            mbar_expect_tx(b_qfull, kQT * kTile);
-            for (int i = 0; i < kQT; ++i)
+            mbar_expect_tx(b_qfull, it.nqt * kTile);
+            for (int i = 0; i < it.nqt; ++i)
               for (int hf = 0; hf < 2; ++hf)
                 tma_load_3d(sbase + kOffQ + i * kTile + hf * kHalf, &q_map, hf * 64, it.kvh * G,
                             it.qs + it.tok0 + i * (kM / G), b_qfull);
@@ -442,21 +444,24 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         mbar_wait(b_vfull + 8 * (gv % kVSlots), (gv / kVSlots) & 1, tag);
         tc_fence_after();
       };
+      int c0 = 0, c1 = 0;  // tiles consumed by softmax warpgroup 0 / 1 (pfull phases)
       for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
         const int4 pz = tp.pieces[pc];
         const int n = pz.z - pz.y;
+        const bool two = item_of(p, pz.x).nqt == 2;  // single-tile items leave WG1 out
         const int g0 = g;  // global tile count of this piece's first key tile
         wait_k(g0, 13);
         mbar_wait(b_qfull, it_local & 1, 12);
         tc_fence_after();
         issue_s(0, g0);
-        issue_s(1, g0);
+        if (two) issue_s(1, g0);
         tc_commit(b_kempty + 8 * (g0 % kKSlots));
         if (n == 1) tc_commit(b_qempty);
         for (int j = 0; j < n; ++j, ++g) {
           // ---- query tile 0: PV0(j), then S0(j+1) behind it (P0 is consumed in order)
           ATTN_TRACE(0, g);
-          mbar_wait(b_pfull, g & 1, 10);
+          mbar_wait(b_pfull, c0 & 1, 10);
+          ++c0;
           ATTN_TRACE(1, g);
           wait_v(g, 11);
           ATTN_TRACE(11, g);
@@ -470,14 +475,17 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           }
           ATTN_TRACE(2, g);
           // ---- query tile 1
-          mbar_wait(b_pfull + 8, g & 1, 15);
-          ATTN_TRACE(3, g);
-          tc_fence_after();
-          issue_pv(1, g, j == 0);
+          if (two) {
+            mbar_wait(b_pfull + 8, c1 & 1, 15);
+            ++c1;
+            ATTN_TRACE(3, g);
+            tc_fence_after();
+            issue_pv(1, g, j == 0);
+          }
           tc_commit(b_vempty + 8 * (g % kVSlots));
-          if (j == n - 1) tc_commit(b_ofull + 8);
+          if (two && j == n - 1) tc_commit(b_ofull + 8);
           if (j + 1 < n) {
-            issue_s(1, g + 1);
+            if (two) issue_s(1, g + 1);
             tc_commit(b_kempty + 8 * ((g + 1) % kKSlots));
             ATTN_TRACE(4, g);
             if (j + 2 == n) tc_commit(b_qempty);
@@ -497,9 +505,10 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
     const float scale = p.scale_log2;
     uint32_t v[kN];
     int g = 0, it_local = 0;
-    for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
+    for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc) {
       const int4 pz = tp.pieces[pc];
       const Item it = item_of(p, pz.x);
+      if (qt >= it.nqt) continue;  // single-tile item: this warpgroup has no rows in it
       const int t_row = it.tok0 + qt * (kM / G) + r / G;  // query token of this row
       const int tq = min(t_row, it.qlen - 1);
       const int pos = it.ctx - it.qlen + tq;
@@ -625,6 +634,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       // the next item's PV_i(0) (accumulate = 0) is issued only after our next pfull arrival,
       // which program order puts after these TMEM reads
       tc_fence_before();
+      ++it_local;  // ofull phases of this warpgroup count only its own items
     }
   }
   tc_fence_before();

@@ -35,8 +35,10 @@ t = TemplateSet()
 rows = []
 for P in args.prefix:
     B = max(1, min(args.batch, (16384 * 16) // (P + 1024)))
-    kv = glmx.KvCacheState(B * (P + 2048) // 16 + 64, 16, glmx.PRIORITY, device=0,
-                           n_layers=cfg.n_layers, n_kv_heads=8, head_dim=128, headroom_pages=2048)
+    cap = B * (P + 2048) // 16 + 64
+    # headroom: warm-up prefills of every k evict earlier notebooks; their pages are deferred-freed
+    kv = glmx.KvCacheState(cap, 16, glmx.PRIORITY, device=0,
+                           n_layers=cfg.n_layers, n_kv_heads=8, head_dim=128, headroom_pages=cap)
     eng = glmx.Engine(model, kv, max_requests=B, max_batch_tokens=max(8192, P + 2048),
                       max_decode=4, max_context=max_ctx)
     for k in args.k:
@@ -81,6 +83,9 @@ for P in args.prefix:
                "attn_tflops": tfl, "tensor_frac": tfl / peaks["bf16_tflops"],
                "attn_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
                "intensity": wk["attn_flops"] / wk["attn_bytes"], "forward_ms": fwd,
+               # effective prompt tokens/s of a 32-layer forward, extrapolated from n_layers
+               "prefill_tokens_per_s_32l": sum(r.cached_tokens + r.computed_tokens + r.tail_tokens
+                                               for r in reps) / (fwd * 1e-3 * 32 / cfg.n_layers),
                "attn_share": attn / fwd,
                "impl": os.environ.get("GLMX_ATTN", "tc")}
         rows.append(row)

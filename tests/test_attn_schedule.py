@@ -40,12 +40,16 @@ def check(reqs, n_kv=8, n_sm=148, tpi=64):
         else:
             assert sorted(parts) == list(range(min(parts), min(parts) + len(parts)))
     assert s["n_partials"] <= 2 * n_sm and s["grid"] <= n_sm
-    if n_items * 2 > n_sm:  # round-robin of whole items, longest first
-        assert not s["combine"]
+    share = -(-s["total_tiles"] // s["grid"])
+    if n_items * 2 > n_sm and not s["combine"]:  # LPT of whole items, longest first
         firsts = [s["pieces"][s["cta_off"][c]] for c in range(s["grid"])]
         lens = [p[2] for p in firsts]
         assert lens == sorted(lens, reverse=True)
         assert max(loads) - min(loads) <= max(need)
+        assert max(loads) <= 1.3 * s["total_tiles"] / n_sm or max(need) < 16
+    elif n_items * 2 > n_sm:  # stream-K cut: equal ranges, edges snapped by <= share/8
+        assert s["grid"] == min(n_sm, s["total_tiles"])
+        assert max(loads) <= share + 2 * max(1, share // 8) + 1
     else:  # split: one piece per CTA, pieces of an item differ by <= 1 tile
         assert all(s["cta_off"][c + 1] - s["cta_off"][c] == 1 for c in range(s["grid"]))
         for w in range(n_items):
@@ -59,6 +63,13 @@ def check(reqs, n_kv=8, n_sm=148, tpi=64):
 def test_c5_batch_uses_whole_items():
     s = check([(8192 + 128, 128)] * 8)  # 128 items of 65 tiles on 148 SMs
     assert s["grid"] == 128 and not s["combine"]
+
+
+def test_long_tail_falls_back_to_stream_k():
+    # 7 requests x 3 query blocks x 8 kv heads = 168 items of ~257 tiles on 148 SMs: LPT would
+    # need two waves; the stream-K cut balances the tiles
+    s = check([(32768 + 134, 134)] * 7)
+    assert s["grid"] == 148 and s["combine"] and s["n_partials"] <= 2 * 148
 
 
 def test_single_long_query_is_split_across_sms():
