@@ -205,6 +205,13 @@ int glmx_index_build(glmx_graph* g, int32_t dim, uint64_t cache_capacity);
 uint64_t glmx_index_size(const glmx_graph* g);
 int glmx_retrieve_nodes(glmx_graph* g, const char* text_bytes, const uint64_t* text_offsets,
                         uint64_t n, int32_t* out_node_idx, uint8_t* out_cache_hit);
+/* generate_workload(seed, n, nondet_ratio, graph, default Config) (workload.cpp:158-255) at
+ * scale: the per-candidate "title retrieves its own node" validation runs as one batched K5 scan;
+ * pools, mt19937_64 draws and the JSONL (Workload::serialize_jsonl) are the reference's.  Returns
+ * the JSONL length (write up to cap bytes to buf), or -status (GLMX_ERR_GLM = GraphTooSmall,
+ * GLMX_ERR_CONFIG = bad ratio).  out_scan_ms: device time of the validation scan. */
+int64_t glmx_workload_generate(glmx_graph* g, uint64_t seed, int32_t n, double nondet_ratio,
+                               char* buf, uint64_t cap, float* out_scan_ms);
 /* {cache_hits, cache_misses, index_probes} since glmx_index_build (RetrievalStats) */
 void glmx_retriever_stats(const glmx_graph* g, int64_t out3[3]);
 float glmx_retrieve_last_kernel_ms(const glmx_graph* g);

@@ -221,6 +221,9 @@ def ref():
         L.ref_retrieve_node.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_uint64]
         L.ref_embed.restype = C.c_int64
         L.ref_embed.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_uint64]
+        L.ref_generate_workload.restype = C.c_int64
+        L.ref_generate_workload.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_double, C.c_char_p,
+                                            C.c_uint64]
         L.ref_nearest.restype = C.c_int64
         L.ref_nearest.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_char_p, C.c_uint64]
         L.ref_render.restype = C.c_int64
@@ -339,6 +342,15 @@ class RefGraph:
         if n < 0:
             raise LookupError(self.L.ref_last_error().decode())
         return buf.raw[:n].decode().split("\n") if n else []
+
+    def generate_workload(self, seed, n, ratio):
+        """generate_workload(...).serialize_jsonl() of the reference (workload.cpp:158-255)."""
+        cap = 1 << 24
+        buf = C.create_string_buffer(cap)
+        m = self.L.ref_generate_workload(self.h, seed, n, ratio, buf, cap)
+        if m < 0:
+            raise LookupError(self.L.ref_last_error().decode())
+        return buf.raw[:m].decode()
 
     def retrieve_node(self, text):
         buf = C.create_string_buffer(4096)

@@ -327,6 +327,18 @@ int64_t ref_nearest(void* g, const char* text, int k, char* buf, std::uint64_t c
   }
 }
 
+// generate_workload(seed, n, ratio, graph, default Config).serialize_jsonl(); -status on error
+int64_t ref_generate_workload(void* g, std::uint64_t seed, int n, double ratio, char* buf,
+                              std::uint64_t cap) {
+  auto* rg = static_cast<RefGraph*>(g);
+  try {
+    glm::Config cfg;
+    return copy_out(glm::generate_workload(seed, n, ratio, rg->g, cfg).serialize_jsonl(), buf, cap);
+  } catch (const std::exception& e) {
+    return -status_of(e);
+  }
+}
+
 // ---------------------------------------------------------------- templates
 // Renders a builtin template into (text, tier) segments, serialised as JSON [[tier, text], ...].
 int64_t ref_render(const char* name, const char* a0, const char* a1, const char* a2, char* buf,

@@ -152,6 +152,8 @@ _SIGS = {
                                      C.c_int32, i32p, i32p, i32p, i64p]),
     "glmx_index_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
     "glmx_index_size": (C.c_uint64, [C.c_void_p]),
+    "glmx_workload_generate": (C.c_int64, [C.c_void_p, C.c_uint64, C.c_int32, C.c_double,
+                                           C.c_char_p, C.c_uint64, f32p]),
     "glmx_retrieve_nodes": (C.c_int, [C.c_void_p, C.c_char_p, u64p, C.c_uint64, i32p,
                                       C.POINTER(C.c_uint8)]),
     "glmx_retriever_stats": (None, [C.c_void_p, i64p]),

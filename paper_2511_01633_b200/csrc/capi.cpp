@@ -27,6 +27,7 @@ int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefil
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
 int index_build_impl(glmx_graph*, int, uint64_t);
+int workload_generate_impl(glmx_graph*, uint64_t, int, double, std::string*, float*);
 int retrieve_impl(glmx_graph*, const char*, const uint64_t*, uint64_t, int32_t*, uint8_t*);
 int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
                          float, void*, uint32_t, uint32_t, uint32_t, void*, int, cudaStream_t,
@@ -412,6 +413,13 @@ int glmx_index_build(glmx_graph* g, int32_t dim, uint64_t cache_capacity) {
   return guarded([&] { return index_build_impl(g, dim, cache_capacity); });
 }
 uint64_t glmx_index_size(const glmx_graph* g) { return g->idx_node.size(); }
+int64_t glmx_workload_generate(glmx_graph* g, uint64_t seed, int32_t n, double nondet_ratio,
+                               char* buf, uint64_t cap, float* out_scan_ms) {
+  std::string out;
+  const int st = guarded([&] { return workload_generate_impl(g, seed, n, nondet_ratio, &out, out_scan_ms); });
+  if (st != GLMX_OK) return -st;
+  return copy_str(out, buf, cap);
+}
 int glmx_retrieve_nodes(glmx_graph* g, const char* text_bytes, const uint64_t* text_offsets,
                         uint64_t n, int32_t* out_node_idx, uint8_t* out_cache_hit) {
   return guarded([&] { return retrieve_impl(g, text_bytes, text_offsets, n, out_node_idx, out_cache_hit); });

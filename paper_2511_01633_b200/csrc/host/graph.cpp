@@ -254,17 +254,19 @@ HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges) {
     g.types.push_back(std::move(nodes[i].type));
     g.attrs.emplace_back(nodes[i].attrs.begin(), nodes[i].attrs.end());
     std::string text;
-    uint8_t has = 0;
+    uint8_t has = 0, is_title = 0;
     for (const char* f : {"title", "name"}) {
       auto it = nodes[i].attrs.find(f);
       if (it != nodes[i].attrs.end() && nodes[i].str_attrs.count(f)) {
         text = it->second;
         has = 1;
+        is_title = f[0] == 't';
         break;
       }
     }
     g.itext.push_back(std::move(text));
     g.has_itext.push_back(has);
+    g.itext_is_title.push_back(is_title);
   }
   std::unordered_map<std::string, int32_t> et;
   for (const auto& e : edges) {

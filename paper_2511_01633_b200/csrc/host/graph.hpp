@@ -26,6 +26,7 @@ struct HostGraph {
   // a string, else "name" when it is a string; has_itext[v] = 0 for nodes without one
   std::vector<std::string> itext;
   std::vector<uint8_t> has_itext;
+  std::vector<uint8_t> itext_is_title;  // the index text is the string "title" (title_of)
   std::unordered_map<std::string, int32_t> index;
   std::vector<std::string> etypes;
   std::vector<int32_t> src, dst, etype;    // edges in file order

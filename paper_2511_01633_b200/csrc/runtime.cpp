@@ -6,6 +6,7 @@
 
 #include "kernels/common.cuh"
 #include "kernels/retrieve.cuh"
+#include "host/workload_gen.hpp"
 
 using namespace glmx;
 
@@ -1085,5 +1086,56 @@ int retrieve_impl(glmx_graph* g, const char* bytes, const uint64_t* offs, uint64
     if (v < 0) v = probe_node[-v - 1];
     if (out_node) out_node[i] = static_cast<int32_t>(v);
   }
+  return GLMX_OK;
+}
+
+// ======================================================================== scalable generate_workload
+// The validation "every title retrieves its own node" (workload.cpp:166-171), one full-scan
+// nearest per candidate in the reference (O(N^2), >10 min at 100k nodes), is one batched K5 scan
+// of all titles against the device index; the pools and draws then follow the reference exactly.
+int workload_generate_impl(glmx_graph* g, uint64_t seed, int n, double ratio, std::string* out,
+                           float* scan_ms) {
+  if (g->device < 0) throw Error(GLMX_ERR_NO_DEVICE, "graph has no device");
+  if (g->idx_pad == 0 || g->idx_dim != 64) index_build_impl(g, 64, 1024);  // Config::embed_dim
+  const uint64_t N = g->host.n();
+  std::vector<uint8_t> unique(N, 0);
+  std::vector<int32_t> qnode;
+  for (uint64_t v = 0; v < N; ++v)
+    if (g->host.has_itext[v] && g->host.itext_is_title[v]) qnode.push_back(static_cast<int32_t>(v));
+  DeviceGuard dg(g->device);
+  cudaStream_t s = g->stream;
+  const int dpad = g->idx_pad, chunk = 32768;
+  float total_ms = 0.f;
+  std::vector<float> q;
+  std::vector<unsigned long long> best;
+  for (size_t c0 = 0; c0 < qnode.size(); c0 += chunk) {
+    const int nq = static_cast<int>(std::min<size_t>(chunk, qnode.size() - c0));
+    q.assign(static_cast<size_t>(nq) * dpad, 0.f);
+    for (int k = 0; k < nq; ++k) {
+      const std::string& t = g->host.itext[qnode[c0 + k]];
+      glmx::embed(t.data(), t.size(), g->idx_dim, q.data() + static_cast<size_t>(k) * dpad);
+    }
+    g->d_qemb.reserve(q.size() * 4);
+    g->d_best.reserve(static_cast<size_t>(nq) * 8);
+    GLMX_CUDA(cudaMemcpyAsync(g->d_qemb.p, q.data(), q.size() * 4, cudaMemcpyHostToDevice, s));
+    GLMX_CUDA(cudaMemsetAsync(g->d_best.p, 0, static_cast<size_t>(nq) * 8, s));
+    GLMX_CUDA(cudaEventRecord(g->ev0, s));
+    nearest_top1(g->d_emb.as<float>(), static_cast<int>(g->idx_node.size()), dpad,
+                 g->d_qemb.as<float>(), nq, g->d_best.as<unsigned long long>(), s);
+    GLMX_CUDA(cudaEventRecord(g->ev1, s));
+    best.resize(nq);
+    GLMX_CUDA(cudaMemcpyAsync(best.data(), g->d_best.p, nq * 8, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    GLMX_CUDA(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    total_ms += ms;
+    for (int k = 0; k < nq; ++k) {
+      const uint32_t row = 0xFFFFFFFFu - static_cast<uint32_t>(best[k] & 0xFFFFFFFFu);
+      if (best[k] != 0 && row < g->idx_node.size() && g->idx_node[row] == qnode[c0 + k])
+        unique[qnode[c0 + k]] = 1;
+    }
+  }
+  if (scan_ms) *scan_ms = total_ms;
+  *out = glmx::generate_workload_jsonl(g->host, unique, seed, n, ratio);
   return GLMX_OK;
 }

@@ -151,3 +151,15 @@ class NodeIndex:
 
     def last_kernel_ms(self):
         return lib().glmx_retrieve_last_kernel_ms(self.graph.h)
+
+
+def generate_workload(graph: PropertyGraph, seed: int, n: int, nondet_ratio: float):
+    """The reference's generate_workload (workload.cpp:158-255) at scale: returns (JSONL text in
+    Workload::serialize_jsonl's format, device ms of the batched K5 validation scan)."""
+    ms = C.c_float(0.0)
+    m = lib().glmx_workload_generate(graph.h, seed, n, nondet_ratio, None, 0, C.byref(ms))
+    if m < 0:
+        check(-m)
+    buf = C.create_string_buffer(max(1, m))
+    lib().glmx_workload_generate(graph.h, seed, n, nondet_ratio, buf, m, C.byref(ms))
+    return buf.raw[:m].decode(), ms.value

@@ -31,7 +31,7 @@ def test_embedding_bit_exact(ref, dim):
 
 @pytest.mark.gpu
 def test_retrieve_matches_reference_nearest(ref, tmp_path):
-    g = glmx.PropertyGraph.synth_powerlaw(20000, 8, seed=11, device=0)
+    g = glmx.PropertyGraph.synth_powerlaw(6000, 8, seed=11, device=0)
     path = str(tmp_path / "g.jsonl")
     g.save(path)
     rg = oracle.RefGraph(path=path)
@@ -63,3 +63,40 @@ def test_retrieval_lru_counts(ref):
     assert hits + hits2 == [False, False, True, False, False, False, False, True]
     assert idx.stats() == (2, 6, 6)
     assert ids[0] == ids[2] == ids2[2] == ids2[3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nodes,n,ratio", [(500, 200, 0.5), (1200, 400, 0.25), (300, 64, 0.0)])
+def test_generate_workload_matches_reference(ref, tmp_path, nodes, n, ratio):
+    """Scalable generate_workload: identical JSONL to the reference's on its own synthetic
+    graph (synth_graph(seed 7), the C3 workload source), pools validated by one GPU scan."""
+    from paper_2511_01633_b200.retrieve import generate_workload
+
+    rg = oracle.RefGraph(synth=(7, nodes))
+    path = str(tmp_path / "synth.jsonl")
+    rg.save(path)
+    g = glmx.PropertyGraph.load(path, device=0)
+    want = rg.generate_workload(7, n, ratio)
+    got, ms = generate_workload(g, 7, n, ratio)
+    assert got == want
+    assert ms > 0
+
+
+@pytest.mark.gpu
+def test_generate_workload_errors_match(ref, tmp_path):
+    from paper_2511_01633_b200.retrieve import generate_workload
+
+    g = glmx.PropertyGraph.synth_powerlaw(800, 4, seed=2, device=0)
+    path = str(tmp_path / "p.jsonl")
+    g.save(path)
+    rg = oracle.RefGraph(path=path)
+    for ratio in (0.0, 0.5):
+        try:
+            want = rg.generate_workload(3, 100, ratio)
+        except LookupError as e:
+            with pytest.raises(glmx.GlmxError) as ei:
+                generate_workload(g, 3, 100, ratio)
+            assert str(e) in str(ei.value)
+            continue
+        got, _ = generate_workload(g, 3, 100, ratio)
+        assert got == want
