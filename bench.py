@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--question-pool", type=int, default=-1,
                    help="draw questions with replacement from this many candidates (reference "
                         "generate_workload style); -1 = half the total query count, 0 = all unique")
+    p.add_argument("--no-pipeline", action="store_true",
+                   help="run the rotations back to back instead of pipelining the host work")
     p.add_argument("--no-peer", action="store_true",
                    help="N>1: disable cross-GPU prefix hits (per-epoch directory + K4 peer copies)")
     return p.parse_args()
@@ -284,8 +286,20 @@ def main():
             px.epoch_end()
         return r
 
-    for _ in range(args.warmup):
-        step()
+    # single-GPU runs pipeline the rotations (host work of r+1 under the forward of r); with peer
+    # exchange every rotation is an epoch whose directory must describe completed pages, so the
+    # rotations stay sequential there
+    pipelined = px is None and not args.no_pipeline
+
+    def rotations(k):
+        if pipelined:
+            yield from wl.rotations(k)
+        else:
+            for _ in range(k):
+                yield step()
+
+    for _ in rotations(args.warmup):
+        pass
     # per-kernel-category CUDA events on the engine stream during the timed steps (host cost
     # ~1 us per event record, <1% of a step)
     eng.set_profiling(2)
@@ -309,22 +323,18 @@ def main():
     k1_bytes = 0
     k5_launches = 0
     k5_ms = 0.0
-    probes_seen = nidx.stats()[2]
     k1_rotations = 0
-    for _ in range(args.steps):
-        r = step()
+    for r in rotations(args.steps):
         tm = eng.last_timings()
         fwd_ms += tm["forward"]
         for k in cat_ms:
             cat_ms[k] += tm[k]
         if r.chunks:
-            chunk_ms += glmx.lib().glmx_chunk_last_kernel_ms(g.h)
+            chunk_ms += r.chunk_ms
             k1_bytes += r.chunk_bytes
-            probes = nidx.stats()[2]
-            if probes > probes_seen:  # one K5 nearest scan served this rotation's misses
+            if r.retrieve_probes:  # one K5 nearest scan served this rotation's misses
                 k5_launches += 1
-                k5_ms += nidx.last_kernel_ms()
-                probes_seen = probes
+                k5_ms += r.retrieve_ms
         tokens += r.prompt_tokens
         computed += r.computed_tokens
         cached += r.cached_tokens
@@ -439,7 +449,8 @@ def main():
                    "question_pool": pool_n,
                    "kv_capacity_blocks": args.capacity, "block_tokens": 16,
                    "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
-                   "parallelism": f"query-sharded x{ws}"},
+                   "parallelism": f"query-sharded x{ws}",
+                   "host_pipelining": pipelined},
         "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
         "cache_hit_token_frac": cached / max(1.0, tokens),
         "calls": calls, "queries_finished": finished,

@@ -281,6 +281,18 @@ typedef struct {
 int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
                                  const glmx_segment_request* reqs, glmx_prefill_report* reports,
                                  int32_t* first_token, float* logits);
+/* Asynchronous step: bookkeeping (reports, exactly as the synchronous call) and staging happen
+ * now, the forward is enqueued on the engine stream, and the call returns without waiting, so a
+ * caller can stage batch r+1 while batch r runs (at most two batches in flight).
+ * glmx_engine_wait completes the OLDEST in-flight batch: writes its greedy first tokens
+ * (first_token[cap], -1 for empty prompts) and publishes its timings/work; returns its request
+ * count, or -status.  The synchronous entry points, decode and replay wait for in-flight batches
+ * first. */
+int glmx_engine_prefill_segments_async(glmx_engine* e, uint64_t n_req,
+                                       const glmx_segment_request* reqs,
+                                       glmx_prefill_report* reports);
+int glmx_engine_wait(glmx_engine* e, int32_t* first_token, uint64_t cap);
+int32_t glmx_engine_in_flight(const glmx_engine* e);
 /* Greedy decode continuing the last prefill batch: steps[i] tokens for request i (<= max_decode);
  * out_tokens host [n_req][max_steps], -1 past a request's count. */
 int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,
@@ -292,7 +304,7 @@ int glmx_engine_replay_forward(glmx_engine* e);
  * [0] whole forward, [1] attention kernels (sum), [2] KV append (sum), [3] GEMMs (sum),
  * [4] other elementwise, [5] H2D, [6] D2H */
 int glmx_engine_last_timings(const glmx_engine* e, float out7[7]);
-/* algorithmic work of the last forward: [0] attention FLOPs, [1] attention bytes (KV read +
+/* algorithmic work of the last completed forward: [0] attention FLOPs, [1] attention bytes (KV read +
  * Q in + O out), [2] K2 bytes (qkv read + q write + K/V page writes), [3] linear FLOPs, [4] computed tokens, [5] context tokens */
 int glmx_engine_last_work(const glmx_engine* e, double out6[6]);
 void glmx_engine_set_profiling(glmx_engine* e, int32_t on);

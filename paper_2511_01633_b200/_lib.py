@@ -136,6 +136,11 @@ _SIGS = {
                                       C.POINTER(PrefillReportC), i32p, f32p]),
     "glmx_engine_prefill_segments": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(SegmentRequestC),
                                                C.POINTER(PrefillReportC), i32p, f32p]),
+    "glmx_engine_prefill_segments_async": (C.c_int, [C.c_void_p, C.c_uint64,
+                                                     C.POINTER(SegmentRequestC),
+                                                     C.POINTER(PrefillReportC)]),
+    "glmx_engine_wait": (C.c_int, [C.c_void_p, i32p, C.c_uint64]),
+    "glmx_engine_in_flight": (C.c_int32, [C.c_void_p]),
     "glmx_engine_decode": (C.c_int, [C.c_void_p, u32p, i32p, f32p]),
     "glmx_engine_replay_forward": (C.c_int, [C.c_void_p]),
     "glmx_engine_last_timings": (C.c_int, [C.c_void_p, f32p]),

@@ -23,7 +23,8 @@ glmx_model* model_create_impl(const glmx_model_config*, int);
 int model_export_impl(const glmx_model*, int, int, uint16_t*, uint64_t);
 glmx_engine* engine_create_impl(glmx_model*, glmx_kv*, const glmx_engine_config*);
 int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefill_report*,
-                        int32_t*, float*);
+                        int32_t*, float*, bool);
+int engine_wait_impl(glmx_engine*, int32_t*, uint64_t);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
 int index_build_impl(glmx_graph*, int, uint64_t);
@@ -467,11 +468,13 @@ void glmx_engine_destroy(glmx_engine* e) {
 }
 int glmx_engine_prefill(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
                         glmx_prefill_report* reports, int32_t* first_token, float* logits) {
-  return guarded([&] { return engine_prefill_impl(e, n_req, reqs, reports, first_token, logits); });
+  return guarded([&] { return engine_prefill_impl(e, n_req, reqs, reports, first_token, logits, false); });
 }
-int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
-                                 const glmx_segment_request* reqs, glmx_prefill_report* reports,
-                                 int32_t* first_token, float* logits) {
+}  // extern "C"
+
+namespace {
+int prefill_segments(glmx_engine* e, uint64_t n_req, const glmx_segment_request* reqs,
+                     glmx_prefill_report* reports, int32_t* first_token, float* logits, bool async) {
   return guarded([&] {
     // Orchestrator::kv_prefill (orchestrator.cpp:81-97) per request, then one batched step.
     struct Tok {
@@ -504,9 +507,31 @@ int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
       rq[r] = {t.bytes.data(), t.offs.data(), t.offs.size() - 1, t.tiers.data(), t.tiers.size(),
                s.session};
     }
-    return engine_prefill_impl(e, n_req, rq.data(), reports, first_token, logits);
+    return engine_prefill_impl(e, n_req, rq.data(), reports, first_token, logits, async);
   });
 }
+}  // namespace
+
+extern "C" {
+int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
+                                 const glmx_segment_request* reqs, glmx_prefill_report* reports,
+                                 int32_t* first_token, float* logits) {
+  return prefill_segments(e, n_req, reqs, reports, first_token, logits, false);
+}
+int glmx_engine_prefill_segments_async(glmx_engine* e, uint64_t n_req,
+                                       const glmx_segment_request* reqs,
+                                       glmx_prefill_report* reports) {
+  return prefill_segments(e, n_req, reqs, reports, nullptr, nullptr, true);
+}
+int glmx_engine_wait(glmx_engine* e, int32_t* first_token, uint64_t cap) {
+  int n = 0;
+  const int st = guarded([&] {
+    n = engine_wait_impl(e, first_token, cap);
+    return GLMX_OK;
+  });
+  return st == GLMX_OK ? n : -st;
+}
+int32_t glmx_engine_in_flight(const glmx_engine* e) { return static_cast<int32_t>(e->pending.size()); }
 int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,
                        float* last_logits) {
   return guarded([&] { return engine_decode_impl(e, steps, out_tokens, last_logits); });
@@ -518,8 +543,8 @@ int glmx_engine_last_timings(const glmx_engine* e, float out7[7]) {
   std::memcpy(out7, e->timings, sizeof(e->timings));
   return GLMX_OK;
 }
-int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {
-  std::memcpy(out6, e->work, sizeof(e->work));
+int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {  // of the last completed batch
+  std::memcpy(out6, e->work_done, sizeof(e->work_done));
   return GLMX_OK;
 }
 void glmx_engine_set_profiling(glmx_engine* e, int32_t level) { e->profiling = level; }

@@ -30,10 +30,12 @@ DeviceGuard::~DeviceGuard() {
 
 void DBuf::reserve(size_t n) {
   if (n <= bytes) return;
+  // cudaFree synchronises the whole device (it would stall the retrieval thread behind the
+  // engine's forward): grow geometrically so steady-state batches never reallocate
   if (p) cudaFree(p);
   p = nullptr;
+  n = std::max<size_t>(std::max<size_t>(n, 256), bytes + bytes / 2);
   bytes = 0;
-  n = std::max<size_t>(n, 256);
   GLMX_CUDA(cudaMalloc(&p, n));
   bytes = n;
 }
@@ -69,7 +71,13 @@ glmx_engine::~glmx_engine() {
   if (h_out) cudaFreeHost(h_out);
   if (h2d_done) cudaEventDestroy(h2d_done);
   if (fwd_done) cudaEventDestroy(fwd_done);
-  for (auto e : ev_pool) cudaEventDestroy(e);
+  for (auto e : ev_free) cudaEventDestroy(e);
+  for (auto& sp : spans) {
+    cudaEventDestroy(sp.a);
+    cudaEventDestroy(sp.b);
+  }
+  for (auto e : done_ev)
+    if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -95,6 +103,23 @@ void glmx_graph::upload() {
   GLMX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   GLMX_CUDA(cudaEventCreate(&ev0));
   GLMX_CUDA(cudaEventCreate(&ev1));
+  // K1 / K5 scratch for batches of up to 512 chunks of k <= 64 (~8 KB each) without reallocation
+  constexpr size_t kChunks = 512, kBytes = kChunks * 8192, kTok = kBytes / 2 + kChunks + 1;
+  d_nodes.reserve(kChunks * 4);
+  d_sel.reserve(kChunks * 64 * 4);
+  d_cnt.reserve(kChunks * 4);
+  d_len.reserve((kChunks + 1) * 8);
+  d_off.reserve((kChunks + 1) * 8);
+  d_flag.reserve((kChunks + 1) * 4);
+  d_tidx.reserve((kChunks + 1) * 4);
+  d_toff.reserve((kChunks + 2) * 4);
+  d_bytes.reserve(kBytes + 16);
+  d_tid.reserve(kTok * 4);
+  d_tbeg.reserve(kTok * 8);
+  d_tend.reserve(kTok * 8);
+  d_temp.reserve(1 << 20);
+  d_qemb.reserve(kChunks * 128 * 4);
+  d_best.reserve(kChunks * 8);
 }
 
 // K1 driver: select -> scan -> render -> tokenize.  Returns GLMX_ERR_ARG (with totals) when the
@@ -346,12 +371,14 @@ void gemm(cublasHandle_t h, cudaStream_t s, const __nv_bfloat16* X, const __nv_b
 }
 
 cudaEvent_t next_event(glmx_engine* e) {
-  if (e->ev_used == e->ev_pool.size()) {
+  if (e->ev_free.empty()) {
     cudaEvent_t ev;
     GLMX_CUDA(cudaEventCreate(&ev));
-    e->ev_pool.push_back(ev);
+    return ev;
   }
-  return e->ev_pool[e->ev_used++];
+  cudaEvent_t ev = e->ev_free.back();
+  e->ev_free.pop_back();
+  return ev;
 }
 
 struct Prof {
@@ -369,7 +396,7 @@ struct Prof {
     if (a) {
       cudaEvent_t b = next_event(e);
       cudaEventRecord(b, e->stream);
-      e->spans.push_back({a, b, cat});
+      e->spans.push_back({a, b, cat, e->batch_seq});
     }
   }
 };
@@ -440,7 +467,9 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->meta_bytes = o;
   e->meta.reserve(o);
   GLMX_CUDA(cudaMallocHost(&e->h_meta, o));
-  GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_out), (R * (cfg->max_decode + 1) + 16) * 4));
+  e->h_out_stride = R * (cfg->max_decode + 1) + 16;
+  GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_out), 2 * e->h_out_stride * 4));
+  for (auto& ev : e->done_ev) GLMX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   return e.release();
 }
 
@@ -551,23 +580,41 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   }
 }
 
-void collect_profile(glmx_engine* e) {
+// Per-category device times of batch `batch` (its events have completed: the caller waited for
+// the batch); spans of later batches stay queued.
+void collect_profile(glmx_engine* e, uint64_t batch) {
   for (float& t : e->timings) t = 0.f;
-  if (!e->profiling) return;
-  GLMX_CUDA(cudaStreamSynchronize(e->stream));
+  std::vector<glmx_engine::Span> keep;
   for (const auto& sp : e->spans) {
+    if (sp.batch != batch) {
+      keep.push_back(sp);
+      continue;
+    }
     float ms = 0.f;
+    GLMX_CUDA(cudaEventSynchronize(sp.b));
     GLMX_CUDA(cudaEventElapsedTime(&ms, sp.a, sp.b));
     e->timings[sp.cat] += ms;
+    e->ev_free.push_back(sp.a);
+    e->ev_free.push_back(sp.b);
   }
-  e->spans.clear();
-  e->ev_used = 0;
+  e->spans.swap(keep);
+}
+void collect_profile(glmx_engine* e) {
+  GLMX_CUDA(cudaStreamSynchronize(e->stream));
+  collect_profile(e, e->batch_seq);
 }
 
 }  // namespace
 
+int engine_wait_impl(glmx_engine* e, int32_t* first_token, uint64_t cap);
+
 int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
-                        glmx_prefill_report* reports, int32_t* first_token, float* logits_out) {
+                        glmx_prefill_report* reports, int32_t* first_token, float* logits_out,
+                        bool async) {
+  if (e->pending.size() >= 2) throw Error(GLMX_ERR_ARG, "two batches in flight: wait for one first");
+  if (async && logits_out) throw Error(GLMX_ERR_ARG, "logits are only returned by the synchronous step");
+  if (!async)
+    while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
   glmx_model* m = e->m;
   glmx_kv* kv = e->kv;
   BlockEngine& bk = *kv->bk;
@@ -678,8 +725,15 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   e->work[3] = lin * T * c.n_layers + 2.0 * c.d_model * c.vocab * R;
   e->work[4] = T;
   e->work[5] = ctx_tokens;
-  if (R == 0) {
+  if (R == 0) {  // nothing to compute (empty prompts): a completed pseudo-batch keeps wait() in order
     if (!kv->epoch_mode) bk.pool().release_deferred();
+    glmx_engine::Pending pd;
+    pd.req_row.assign(n_req, -1);
+    pd.batch = e->batch_seq++;
+    pd.slot = -1;
+    std::memcpy(pd.work, e->work, sizeof(pd.work));
+    e->pending.push_back(std::move(pd));
+    if (!async) engine_wait_impl(e, nullptr, 0);
     return GLMX_OK;
   }
   // peer copies, grouped by source pool: src pages then dst pages per group in o_copy
@@ -719,31 +773,62 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   }
   forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
   argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), s);
+  const int slot = static_cast<int>(e->batch_seq & 1);
   {
     Prof p(e, kCatD2H);
-    GLMX_CUDA(cudaMemcpyAsync(e->h_out, e->next_tok.p, R * 4, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaMemcpyAsync(e->h_out + slot * e->h_out_stride, e->next_tok.p, R * 4,
+                              cudaMemcpyDeviceToHost, s));
   }
   GLMX_CUDA(cudaEventRecord(e->fwd_done, s));
+  GLMX_CUDA(cudaEventRecord(e->done_ev[slot], s));
   // evicted pages were read by this batch; any later writer is stream-ordered after it.  In
   // epoch mode peers may still copy them: the caller releases after its epoch barrier.
   if (!kv->epoch_mode) bk.pool().release_deferred();
-  GLMX_CUDA(cudaStreamSynchronize(s));
-  collect_profile(e);
-  std::vector<float> tmp;
-  for (uint64_t i = 0; i < n_req; ++i) {
-    if (req_row[i] < 0) continue;
-    if (first_token) first_token[i] = e->h_out[req_row[i]];
-    if (logits_out)
-      GLMX_CUDA(cudaMemcpy(logits_out + i * c.vocab, e->logits.as<float>() + static_cast<size_t>(req_row[i]) * c.vocab,
-                           c.vocab * 4, cudaMemcpyDeviceToHost));
-  }
+  glmx_engine::Pending pd;
+  pd.req_row = std::move(req_row);
+  pd.batch = e->batch_seq;
+  pd.slot = slot;
+  std::memcpy(pd.work, e->work, sizeof(pd.work));
+  e->pending.push_back(std::move(pd));
+  ++e->batch_seq;
   // decode continues from the last prompt token's greedy successor
   e->has_batch = true;
+  if (async) return GLMX_OK;
+  // synchronous step: collect this batch now (logits stay valid: nothing else was enqueued)
+  const int32_t* h = e->h_out + slot * e->h_out_stride;
+  const std::vector<int> rows = e->pending.back().req_row;
+  engine_wait_impl(e, nullptr, 0);
+  for (uint64_t i = 0; i < n_req; ++i) {
+    if (rows[i] < 0) continue;
+    if (first_token) first_token[i] = h[rows[i]];
+    if (logits_out)
+      GLMX_CUDA(cudaMemcpy(logits_out + i * c.vocab, e->logits.as<float>() + static_cast<size_t>(rows[i]) * c.vocab,
+                           c.vocab * 4, cudaMemcpyDeviceToHost));
+  }
   return GLMX_OK;
+}
+
+// Completes the oldest in-flight prefill batch: waits for it, publishes its timings and work,
+// writes its greedy first tokens (-1 for empty prompts).  Returns the batch's request count.
+int engine_wait_impl(glmx_engine* e, int32_t* first_token, uint64_t cap) {
+  if (e->pending.empty()) throw Error(GLMX_ERR_ARG, "no prefill batch in flight");
+  DeviceGuard dg(e->m->device);
+  glmx_engine::Pending pd = std::move(e->pending.front());
+  e->pending.erase(e->pending.begin());
+  if (pd.slot >= 0) GLMX_CUDA(cudaEventSynchronize(e->done_ev[pd.slot]));
+  collect_profile(e, pd.batch);
+  std::memcpy(e->work_done, pd.work, sizeof(pd.work));
+  const int32_t* h = e->h_out + std::max(pd.slot, 0) * e->h_out_stride;
+  if (first_token) {
+    if (cap < pd.req_row.size()) throw Error(GLMX_ERR_ARG, "first_token buffer too small");
+    for (size_t i = 0; i < pd.req_row.size(); ++i) first_token[i] = pd.req_row[i] < 0 ? -1 : h[pd.req_row[i]];
+  }
+  return static_cast<int>(pd.req_row.size());
 }
 
 int engine_replay_impl(glmx_engine* e) {
   if (!e->has_batch) throw Error(GLMX_ERR_ARG, "no staged batch");
+  while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
   DeviceGuard dg(e->m->device);
   forward(e, e->last_T, e->last_R, e->last_work, e->last_R,
           reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
@@ -757,6 +842,7 @@ int engine_replay_impl(glmx_engine* e) {
 // step is a row prefix and step s+1 consumes step s's argmax rows in place on the device.
 int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens, float* last_logits) {
   if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
+  while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
   glmx_model* m = e->m;
   const auto& c = m->cfg;
   const uint32_t B = e->kv->cfg.block_tokens;

@@ -144,12 +144,25 @@ struct glmx_engine {
   struct Span {
     cudaEvent_t a, b;
     int cat;
+    uint64_t batch;
   };
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
+  std::vector<cudaEvent_t> ev_free;  // recycled timing events
   std::vector<Span> spans;
   float timings[7] = {0};
-  double work[6] = {0};
+  double work[6] = {0};       // algorithmic work of the batch being staged
+  double work_done[6] = {0};  // ... of the last completed (waited) batch
+  // asynchronous prefill: up to two batches in flight on the engine stream (the host stages and
+  // does the bookkeeping of batch r+1 while batch r runs); results are collected in order
+  struct Pending {
+    std::vector<int> req_row;
+    uint64_t batch;
+    int slot;
+    double work[6];
+  };
+  std::vector<Pending> pending;  // FIFO (front = oldest)
+  uint64_t batch_seq = 0;        // batch being staged / enqueued
+  cudaEvent_t done_ev[2] = {nullptr, nullptr};
+  size_t h_out_stride = 0;       // int32 entries per h_out slot
 
   ~glmx_engine();
 };

@@ -60,6 +60,9 @@ class RotationResult:
     finished: int = 0
     chunks: int = 0
     chunk_bytes: int = 0         # K1 algorithmic bytes (CSR rows, neighbour pairs, entries, out)
+    chunk_ms: float = 0.0        # K1 device time of this rotation's chunk build
+    retrieve_ms: float = 0.0     # K5 device time (0 when every RetrieveNode hit the LRU)
+    retrieve_probes: int = 0     # index probes (LRU misses) of this rotation
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
 
@@ -170,6 +173,9 @@ class GraphCoTWorkload:
             for c, text in zip(acting, batch.texts):
                 c.session.notebook += text + "\n"  # PrintStmt: raw chunk + "\n" (interp.cpp:68-74)
             res.chunks = len(acting)
+            res.chunk_ms = batch.kernel_ms
+            res.retrieve_ms = getattr(batch, "retrieve_ms", 0.0)
+            res.retrieve_probes = getattr(batch, "retrieve_probes", 0)
             g = self.retriever.graph
             res.chunk_bytes = sum(8 + 8 * g.total_degree(v) for v in batch.nodes)
             res.chunk_bytes += sum(2 * len(t) + 20 * len(sp) for t, sp in
@@ -198,14 +204,75 @@ class GraphCoTWorkload:
     def _retrieve_and_build(self, acting):
         """RetrieveNode (K5, when a node index is attached) then NodeInfo chunks (K1) for the
         rotation's action snippets; both on the graph's stream."""
+        probes0 = probes1 = 0
+        r_ms = 0.0
         if self.node_index is not None:
             texts = [c.session.task[len("vertex chunks for: "):] for c in acting]
+            probes0 = self.node_index.stats()[2]
             nodes, _ = self.node_index.retrieve_nodes(texts)
+            probes1 = self.node_index.stats()[2]
+            r_ms = self.node_index.last_kernel_ms() if probes1 > probes0 else 0.0
         else:
             nodes = [c.session.sources[c.session.round] for c in acting]
         batch = self.retriever.chunk_build(nodes)
         batch.nodes = nodes
+        batch.retrieve_ms = r_ms
+        batch.retrieve_probes = probes1 - probes0
         return batch
+
+    def prefill_async(self, calls):
+        """Bookkeeping + staging now (reports returned), forward enqueued; see wait()."""
+        n = len(calls)
+        arr, keep = self.pack(calls)
+        reps = (_lib.PrefillReportC * max(1, n))()
+        check(lib().glmx_engine_prefill_segments_async(self.engine.h, n, arr, reps))
+        del keep  # the call tokenised the segments before returning
+        return [PrefillReport(reps[i].cached_tokens, reps[i].computed_tokens, reps[i].tail_tokens)
+                for i in range(n)]
+
+    def wait(self, n):
+        """Completes the oldest in-flight batch; its greedy first tokens."""
+        first = (C.c_int32 * max(1, n))()
+        m = lib().glmx_engine_wait(self.engine.h, first, max(1, n))
+        if m < 0:
+            check(-m)
+        return [first[i] for i in range(n)]
+
+    def _start_retrieval(self, calls):
+        acting = [c for c in calls if c.agent == "action"]
+        built = {}
+        th = None
+        if acting:
+            th = threading.Thread(target=lambda: built.__setitem__(
+                "b", self._retrieve_and_build(acting)))
+            th.start()
+        return th, built
+
+    def rotations(self, count):
+        """`count` rotations, pipelined: the host work of rotation r+1 (its calls, the
+        bookkeeping and staging of its prefill, its RetrieveNode/K1 thread) runs while rotation
+        r's forward is on the GPU.  Nothing host-side depends on a forward's output (replies are
+        scripted), and the engine stream orders the forwards, so the cache decisions and the
+        results are those of the sequential loop.  Yields each rotation's RotationResult after its
+        forward completed (engine timings/work then describe that rotation)."""
+        if count <= 0:
+            return
+        calls = self.next_calls()
+        th, built = self._start_retrieval(calls)
+        reps = self.prefill_async(calls)
+        for r in range(count):
+            if th is not None:
+                th.join()
+            res = self.advance(calls, reps, None, chunks=built.get("b"))
+            nxt = None
+            if r + 1 < count:
+                calls_n = self.next_calls()
+                th_n, built_n = self._start_retrieval(calls_n)
+                nxt = (calls_n, th_n, built_n, self.prefill_async(calls_n))
+            res.first_tokens = self.wait(len(calls))
+            yield res
+            if nxt is not None:
+                calls, th, built, reps = nxt
 
     def rotation(self) -> RotationResult:
         """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on

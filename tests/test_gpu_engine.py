@@ -131,3 +131,30 @@ def test_llama8b_shape_two_layer_slice():
         assert err.max() <= 1.5 * FLOOR_MAX and err.mean() <= 1.5 * FLOOR_MEAN, (err.max(), err.mean())
     for i, r in enumerate(reqs):
         dec.check_greedy(token_ids(r.tokens, cfg.vocab), [first[i]], atol=FLOOR_MAX, rtol=0.0)
+
+
+def test_pipelined_rotations_match_sequential():
+    """Async prefill + pipelined rotations (host work of r+1 under the forward of r) give the
+    same cache decisions, reports and greedy tokens as the sequential loop."""
+    from paper_2511_01633_b200.workload import GraphCoTWorkload
+
+    cfg = glmx.TINY
+    g = glmx.PropertyGraph.synth_powerlaw(3000, 6, seed=4, device=0)
+    out = []
+    for mode in ("seq", "pipe"):
+        model = glmx.Model(cfg, device=0)
+        kv = glmx.KvCacheState(256, 16, glmx.PRIORITY, device=0, n_layers=cfg.n_layers,
+                               n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
+                               headroom_pages=512)
+        eng = glmx.Engine(model, kv, max_requests=16, max_batch_tokens=16 * 1024, max_decode=4,
+                          max_context=4096)
+        ret = glmx.Retriever(g, chunk_k=8, vocab=cfg.vocab)
+        wl = GraphCoTWorkload(eng, ret, n_queries=40, lanes=16, seed=5, question_pool=20,
+                              node_index=glmx.NodeIndex(g))
+        rows = []
+        it = (wl.rotation() for _ in range(14)) if mode == "seq" else wl.rotations(14)
+        for r in it:
+            rows.append(([(x.cached_tokens, x.computed_tokens, x.tail_tokens) for x in r.reports],
+                         r.first_tokens, r.finished))
+        out.append((rows, kv.counters(), kv.snapshot_json()))
+    assert out[0] == out[1]
