@@ -2,6 +2,7 @@
 // for the tcgen05 kernel.  One CTA = one kv head x 64 query rows (64/G tokens x G query heads of
 // that kv head, so each K/V page is read once for the whole GQA group); 4 warps x 16 rows.
 // K/V tiles of 64 keys = 4 pages of 16 tokens, cp.async double-buffered into XOR-swizzled smem.
+#include <atomic>
 #include <cfloat>
 
 #include "attn.cuh"
@@ -250,11 +251,13 @@ void paged_attention(const AttnParams& p, cudaStream_t s) {
   const int G = p.H / p.Hkv;
   if (G * p.Hkv != p.H || kRows % G != 0) throw Error(GLMX_ERR_ARG, "unsupported GQA ratio");
   const int smem = 5 * kTileBytes;
-  static bool attr = false;
-  if (!attr) {
-    GLMX_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+  // the attribute is per device: one flag per device ordinal (atomic, launches may race)
+  static std::atomic<bool> attr[64];
+  int dev = 0;
+  GLMX_CUDA(cudaGetDevice(&dev));
+  if (!attr[dev & 63].load(std::memory_order_acquire)) {
+    GLMX_CUDA(cudaFuncSetAttribute(paged_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr[dev & 63].store(true, std::memory_order_release);
   }
   dim3 grid(p.n_work, p.Hkv);
   paged_attn_mma_kernel<<<grid, kThreads, smem, s>>>(p);

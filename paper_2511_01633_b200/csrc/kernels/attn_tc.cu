@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cfloat>
 
 #include "attn.cuh"
@@ -735,10 +736,13 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
   if (G * p.Hkv != p.H || kM % G != 0) throw Error(GLMX_ERR_ARG, "unsupported GQA ratio");
   if (p.bt_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(p.block_table) & 15) != 0)
     throw Error(GLMX_ERR_ARG, "block-table rows must be 16-byte aligned multiples of 8 entries");
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: one flag per device ordinal (atomic, launches may race)
+  static std::atomic<bool> attr[64];
+  int dev = 0;
+  GLMX_CUDA(cudaGetDevice(&dev));
+  if (!attr[dev & 63].load(std::memory_order_acquire)) {
     GLMX_CUDA(cudaFuncSetAttribute(paged_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
+    attr[dev & 63].store(true, std::memory_order_release);
   }
   TcParams tp{p, rows_total, sc.pieces, sc.cta_off, sc.part_o, sc.part_ml};
   paged_attn_tc_kernel<<<sc.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
