@@ -18,7 +18,8 @@ from paper_2511_01633_b200._lib import lib  # noqa: E402
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-s, H, Hkv, hd, B = 128, 32, 8, 128, 16
+s = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+H, Hkv, hd, B = 32, 8, 128, 16
 ctx = P + s
 pp = (ctx + B - 1) // B
 pool = torch.randn((nb * pp, 1, 2, Hkv, B, hd), device="cuda").to(torch.bfloat16)
@@ -36,10 +37,14 @@ n = lib().glmx_attn_trace_read(buf, 16 * 1024)
 assert n > 0, "not a trace build"
 ev = [[buf[e * 1024 + j] for j in range(1024)] for e in range(16)]
 n_t = max(j for j in range(1024) if ev[6][j]) + 1
+if "--raw" in sys.argv:  # per-tile absolute timeline (cycles from the first stamp)
+    t0 = min(x for e in ev for x in e[:n_t] if x)
+    for j in range(n_t):
+        print(j, " ".join(f"{(ev[e][j] - t0) if ev[e][j] else -1:7d}" for e in range(16)))
 names = {"mma: wait P0": (0, 1), "mma: issue PV0+S0": (1, 2), "mma: wait P1": (2, 3),
          "mma: issue PV1+S1": (3, 4), "WG0: wait S0": (5, 6), "WG0: softmax": (6, 7),
          "WG1: wait S1": (8, 9), "WG1: softmax": (9, 10)}
-lo, hi = 4, n_t - 4
+lo, hi = (4, n_t - 4) if n_t > 12 else (0, n_t - 1)
 print(f"P={P} batch={nb}: kernel {ms * 1e3:.1f} us, CTA0 tiles {n_t}")
 for k, (a, b) in names.items():
     d = [ev[b][j] - ev[a][j] for j in range(lo, hi)]

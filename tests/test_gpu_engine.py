@@ -1,6 +1,7 @@
 """Prefill/decode engine on the GPU vs the CPU fp32 decoder oracle (oracle/decoder.py) and the
 reference bookkeeping.  Tolerances (north star): logits max-abs 2e-2 + rel 1e-2 (bf16 vs fp32);
 greedy ids bit-exact (asserted where the oracle's top-1/top-2 margin exceeds the tolerance)."""
+import os
 import numpy as np
 import pytest
 
@@ -158,3 +159,20 @@ def test_pipelined_rotations_match_sequential():
                          r.first_tokens, r.finished))
         out.append((rows, kv.counters(), kv.snapshot_json()))
     assert out[0] == out[1]
+
+
+def test_c3_shaped_run_bookkeeping_matches_reference():
+    """C3 in miniature: 96 concurrent Graph-CoT queries on a 96-block pool with four-tier
+    priority eviction (pipelined rotations, RetrieveNode, K1); every prefill and set_tier replayed
+    into the reference KvCacheState gives identical counters and resident snapshot."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "bench_c3.py"),
+                          "--lanes", "96", "--cap", "96", "--rotations", "20", "--layers", "2",
+                          "--nodes", "3000"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    row = __import__("json").loads(out.stdout.strip().splitlines()[-1])
+    assert row["bookkeeping_identical_to_reference"]
+    assert sum(row["counters"]["evictions_by_tier"]) > 0  # the pool was under pressure
