@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--question-pool", type=int, default=-1,
                    help="draw questions with replacement from this many candidates (reference "
                         "generate_workload style); -1 = half the total query count, 0 = all unique")
+    p.add_argument("--routing", default="mod", choices=["mod", "affinity"],
+                   help="query -> GPU: i mod N (reference sharding) or prefix affinity "
+                        "(fnv1a(question) mod N: repeated questions stay on one GPU)")
     p.add_argument("--no-pipeline", action="store_true",
                    help="run the rotations back to back instead of pipelining the host work")
     p.add_argument("--no-peer", action="store_true",
@@ -265,7 +268,11 @@ def main():
     nidx = glmx.NodeIndex(g)  # RetrieveNode: device VectorIndex + retrieval LRU (K5)
     wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed,
                           question_pool=pool_n, node_index=nidx)
-    wl.sessions = wl.sessions[rank::ws]  # query i -> rank i % N
+    if args.routing == "affinity":
+        from paper_2511_01633_b200.sharding import shard_by_affinity
+        wl.sessions = shard_by_affinity(wl.sessions, rank, ws, key=lambda s: s.question)
+    else:
+        wl.sessions = wl.sessions[rank::ws]  # query i -> rank i % N
     # cross-GPU prefix hits (C4): every rotation is an epoch; the ranks exchange their resident
     # (block id, page) directories, and a run of blocks missing locally but resident on a peer is
     # copied over NVLink by K4 (pool exported by CUDA IPC) instead of being recomputed
@@ -449,7 +456,7 @@ def main():
                    "question_pool": pool_n,
                    "kv_capacity_blocks": args.capacity, "block_tokens": 16,
                    "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
-                   "parallelism": f"query-sharded x{ws}",
+                   "parallelism": f"query-sharded x{ws}", "routing": args.routing,
                    "host_pipelining": pipelined},
         "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
         "cache_hit_token_frac": cached / max(1.0, tokens),

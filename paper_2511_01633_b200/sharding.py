@@ -18,6 +18,21 @@ def shard(items, rank: int, world: int):
     return items[rank::world]
 
 
+def affinity_rank(key: str, world: int) -> int:
+    """Prefix-affinity routing: a query goes to fnv1a(question) % world, so every
+    repetition of a question — and with it the whole chain of blocks its sessions build — lands
+    on the GPU that already caches it (local hits instead of NVLink peer copies)."""
+    h = 14695981039346656037
+    for b in key.encode():
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h % world
+
+
+def shard_by_affinity(items, rank: int, world: int, key=lambda x: x):
+    """The items whose affinity rank is `rank`, in their original order."""
+    return [x for x in items if affinity_rank(key(x), world) == rank]
+
+
 def merge_directories(snapshots, rank: int):
     """snapshots[q] = (ids uint64[n_q], pages int32[n_q]) of rank q.  Returns the directory a
     given rank installs: every other rank's residents, lower rank first for duplicated ids."""

@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 from . import _lib
 from ._lib import check, lib
 from .kvcache import PrefillReport
-from .templates import TIER_II, TIER_III, TemplateSet
+from .templates import TIER_II, TIER_III, TIER_IV, TemplateSet
 
 
 @dataclass
@@ -294,3 +294,30 @@ class GraphCoTWorkload:
             if th is not None:
                 th.join()
         return self.advance(calls, reps, first, chunks=built.get("b"))
+
+
+def adversarial_priority_ops(n_hot=8, rounds=12, n_cold=24, notebook_words=240, cold_words=300,
+                             seed=0):
+    """The priority-vs-LRU adversarial stream SPEC.md:532/778 asks for (the reference ships
+    none): n_hot reasoning sessions whose prompts re-read a long retrieved-chunk notebook
+    (tier II) every round, separated by floods of one-off agent prompts (tier IV: transient
+    task/question text, never reused).  Sized by the caller's capacity so that the hot notebooks
+    fit but hot + one flood do not: plain LRU evicts the notebooks during every flood (they are
+    the least recently used), four-tier priority evicts the tier-IV flood first and keeps them.
+
+    Returns the op list [("p", (tokens, tiers), session), ...] in the reference's prefill terms
+    (templates render_reasoning: tier I instructions, tier II notebook, tier IV question)."""
+    rnd = random.Random(seed)
+    t = TemplateSet()
+    vocab = [f"w{rnd.randrange(10**6)}" for _ in range(4096)]
+    notebooks = [" ".join(rnd.choice(vocab) for _ in range(notebook_words)) for _ in range(n_hot)]
+    questions = [f"Which item is linked from all of: h{h}a; h{h}b?" for h in range(n_hot)]
+    ops = []
+    for r in range(rounds):
+        for h in range(n_hot):
+            segs = t.render_reasoning(questions[h], notebooks[h])
+            ops.append(("p", segs, f"hot{h}"))
+        for c in range(n_cold):
+            text = " ".join(rnd.choice(vocab) for _ in range(cold_words))
+            ops.append(("p", [(TIER_IV, f"r{r}c{c} " + text)], f"cold{r}_{c}"))
+    return ops

@@ -80,3 +80,19 @@ def test_gloo_two_ranks_directory_exchange():
         # 52 tokens = 2 shared blocks + 1 per-query block + a 4-token tail: each rank computes the
         # shared blocks once (independent caches, as G reference KvCacheStates would)
         assert counters["misses"] == 2 + n_q and counters["hits"] == 2 * (n_q - 1)
+
+
+def test_affinity_routing_keeps_repeats_together():
+    from paper_2511_01633_b200.sharding import affinity_rank, shard_by_affinity
+
+    qs = [f"Which item is linked from all of: v{i % 37}; v{(i * 7) % 37}?" for i in range(400)]
+    for world in (2, 4, 8):
+        parts = [shard_by_affinity(list(range(len(qs))), r, world, key=lambda i: qs[i])
+                 for r in range(world)]
+        assert sorted(sum(parts, [])) == list(range(len(qs)))      # a partition
+        owner = {}
+        for r, p in enumerate(parts):
+            for i in p:
+                assert owner.setdefault(qs[i], r) == r              # repeats share a rank
+        assert all(affinity_rank(q, world) == owner[q] for q in qs)
+        assert min(len(p) for p in parts) > 0
