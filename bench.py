@@ -51,6 +51,9 @@ def parse():
                         "(fnv1a(question) mod N: repeated questions stay on one GPU)")
     p.add_argument("--no-pipeline", action="store_true",
                    help="run the rotations back to back instead of pipelining the host work")
+    p.add_argument("--decode-steps", type=int, default=8,
+                   help="rotations of the second phase: prefill + greedy reply decode per call "
+                        "(Graph-CoT queries/s with the full call_llm step); 0 skips it")
     p.add_argument("--no-peer", action="store_true",
                    help="N>1: disable cross-GPU prefix hits (per-epoch directory + K4 peer copies)")
     return p.parse_args()
@@ -369,6 +372,23 @@ def main():
     tm = dict(cat_ms, forward=fwd_ms)
     wk = work
 
+    # phase 2 (after the measured prefill steps): the complete call_llm step — prefill + greedy
+    # decode of each reply — for Graph-CoT queries/s; rotations sequential (decode continues the
+    # last staged batch)
+    dq_fin = dq_dec = 0
+    dq_ms = 0.0
+    if args.decode_steps > 0 and ws == 1:
+        torch.cuda.synchronize()
+        d0 = torch.cuda.Event(enable_timing=True)
+        d1 = torch.cuda.Event(enable_timing=True)
+        d0.record()
+        for _ in range(args.decode_steps):
+            rr = wl.rotation_with_decode(8)
+            dq_fin += rr.finished
+            dq_dec += rr.decoded_tokens
+        d1.record()
+        torch.cuda.synchronize()
+        dq_ms = d0.elapsed_time(d1)
     peer_blocks = float(kv.peer_hits() - peer0) if px is not None else 0.0
     vals = torch.tensor([tokens, computed, cached, calls, finished, peer_blocks],
                         dtype=torch.float64, device=red_dev)
@@ -463,6 +483,11 @@ def main():
         "calls": calls, "queries_finished": finished,
         "peer_hit_blocks": peer_blocks if ws > 1 else None,
         "queries_per_s_prefill_only": finished / (wall_ms * 1e-3),
+        "graph_cot_queries_per_s": (
+            {"value": dq_fin / (dq_ms * 1e-3), "unit": "queries/s", "rotations": args.decode_steps,
+             "queries_finished": dq_fin, "decoded_tokens": dq_dec, "ms": dq_ms,
+             "step": "prefill + greedy reply decode per call (call_llm), wall with CUDA events"}
+            if dq_ms > 0 else None),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "roofline": roof,

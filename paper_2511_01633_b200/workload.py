@@ -63,6 +63,7 @@ class RotationResult:
     chunk_ms: float = 0.0        # K1 device time of this rotation's chunk build
     retrieve_ms: float = 0.0     # K5 device time (0 when every RetrieveNode hit the LRU)
     retrieve_probes: int = 0     # index probes (LRU misses) of this rotation
+    decoded_tokens: int = 0      # reply tokens decoded after the prefill (rotation_with_decode)
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
 
@@ -273,6 +274,27 @@ class GraphCoTWorkload:
             yield res
             if nxt is not None:
                 calls, th, built, reps = nxt
+
+    def rotation_with_decode(self, max_decode) -> RotationResult:
+        """A rotation whose calls are completed like call_llm's provider step: after the prefill
+        (which yields each reply's first token) every call greedily decodes the rest of its reply,
+        tokens_out - 1 tokens (tokens_out = count_tokens(reply), finalize_completion
+        provider.cpp:12-29), capped at max_decode.  The scripted reply text still drives the
+        state machine."""
+        calls = self.next_calls()
+        steps = [max(0, min(max_decode, count_tokens(c.reply) - 1)) for c in calls]
+        acting = [c for c in calls if c.agent == "action"]
+        th, built = self._start_retrieval(calls) if self.overlap_retrieval else (None, {})
+        try:
+            reps, first = self.prefill(calls)
+        finally:
+            if th is not None:
+                th.join()
+        if any(steps):
+            self.engine.decode(steps)
+        res = self.advance(calls, reps, first, chunks=built.get("b") if acting else None)
+        res.decoded_tokens = sum(steps)
+        return res
 
     def rotation(self) -> RotationResult:
         """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on
