@@ -73,6 +73,39 @@ rmsnorm_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, in
   }
 }
 
+// d = 4096 (the Llama-3-8B width): the row stays in registers (4 float4 per thread, all issued
+// before the reduction), a single read of x; 8-byte bf16 stores.
+template <int NT, int D>
+__global__ void __launch_bounds__(NT)
+rmsnorm_reg_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                   const __nv_bfloat16* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out) {
+  constexpr int kV = D / 4 / NT;  // float4 per thread
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int64_t src = rows ? rows[t] : t;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * D);
+  float4 v[kV];
+#pragma unroll
+  for (int k = 0; k < kV; ++k) v[k] = __ldcs(xr + threadIdx.x + k * NT);
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kV; ++k) ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+  ss = block_sum<NT>(ss, red);
+  const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
+  const uint2* w4 = reinterpret_cast<const uint2*>(w);
+  uint2* o = reinterpret_cast<uint2*>(out + static_cast<int64_t>(t) * D);
+#pragma unroll
+  for (int k = 0; k < kV; ++k) {
+    const int i = threadIdx.x + k * NT;
+    const uint2 wv = w4[i];
+    const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.x));
+    const float2 wb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.y));
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[k].x * inv * wa.x, v[k].y * inv * wa.y);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[k].z * inv * wb.x, v[k].w * inv * wb.y);
+    o[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
 // K2: RoPE + KV append, kTok tokens per CTA.  The CTA first builds the cos/sin tables of its
 // tokens in shared memory (fp32 angle pos * inv_freq, accurate sincosf: positions reach 32k), then
 // every (token, head slot, 8-element chunk) work unit is two 16-byte loads (the rotate-half
@@ -89,18 +122,12 @@ rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __re
   __shared__ float cs_tab[kTok][128], sn_tab[kTok][128];
   const int t_base = blockIdx.x * kTok;
   const int half = hd / 2;
-  for (int i = threadIdx.x; i < kTok * half; i += blockDim.x) {
-    const int tt = i / half, k = i % half;
-    const int t = min(t_base + tt, T - 1);
-    sincosf(static_cast<float>(pos[t]) * inv_freq[k], &sn_tab[tt][k], &cs_tab[tt][k]);
-  }
-  __syncthreads();
   const int heads = H + 2 * Hkv;
   const int chunks = half / 8;
   const int per_tok = heads * chunks;
   const int units = kTok * per_tok;
-  for (int u0 = threadIdx.x; u0 < units; u0 += blockDim.x * kUnroll) {
-    uint4 av[kUnroll], bv[kUnroll];
+  uint4 av[kUnroll], bv[kUnroll];
+  auto load = [&](int u0) {
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int u = u0 + k * blockDim.x;
@@ -112,6 +139,8 @@ rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __re
         bv[k] = __ldcs(reinterpret_cast<const uint4*>(src + half));
       }
     }
+  };
+  auto process = [&](int u0) {
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int u = u0 + k * blockDim.x;
@@ -152,6 +181,19 @@ rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __re
       *reinterpret_cast<uint4*>(dst) = ra;
       *reinterpret_cast<uint4*>(dst + half) = rb;
     }
+  };
+  // the first loads are in flight while the cos/sin tables are built
+  load(threadIdx.x);
+  for (int i = threadIdx.x; i < kTok * half; i += blockDim.x) {
+    const int tt = i / half, k = i % half;
+    const int t = min(t_base + tt, T - 1);
+    sincosf(static_cast<float>(pos[t]) * inv_freq[k], &sn_tab[tt][k], &cs_tab[tt][k]);
+  }
+  __syncthreads();
+  process(threadIdx.x);
+  for (int u0 = threadIdx.x + blockDim.x * kUnroll; u0 < units; u0 += blockDim.x * kUnroll) {
+    load(u0);
+    process(u0);
   }
 }
 
@@ -282,7 +324,10 @@ void embed_gather(const int32_t* tokens, int T, const __nv_bfloat16* embed, int 
 void rmsnorm(const float* x, const int32_t* rows, int T, int d, const __nv_bfloat16* w,
              float eps, __nv_bfloat16* out, cudaStream_t s) {
   if (T <= 0) return;
-  rmsnorm_kernel<256><<<T, 256, 0, s>>>(x, rows, d, w, eps, out);
+  if (d == 4096)
+    rmsnorm_reg_kernel<256, 4096><<<T, 256, 0, s>>>(x, rows, w, eps, out);
+  else
+    rmsnorm_kernel<256><<<T, 256, 0, s>>>(x, rows, d, w, eps, out);
   GLMX_CHECK_LAUNCH();
 }
 
