@@ -334,6 +334,14 @@ int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_head
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
                        int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
                        int32_t* out_combine, int64_t out_counts[5]);
+/* K2 gather on caller-owned DEVICE buffers: one layer's K (kv = 0) or V (kv = 1) of the pages
+ * pages[0..n) (host array, a request's block table) into out [n * block_tokens][n_kv_heads]
+ * [head_dim] bf16 — the dense view the attention core reads through TMA; used to export a
+ * request's KV.  impl 0 = TMA-staged (bulk load + 2-D TMA store per 4 KB tile), 1 = scalar. */
+int glmx_kv_gather_run(void* pool, uint64_t n_pages, uint32_t n_layers, uint32_t n_kv_heads,
+                       uint32_t block_tokens, uint32_t head_dim, uint32_t layer, uint32_t kv,
+                       const int32_t* pages, uint64_t n, void* out, int32_t impl, int32_t reps,
+                       void* stream, float* out_ms);
 /* Diagnostics: in the trace build (libglmx_trace.so, `make -C paper_2511_01633_b200/csrc trace`)
  * copies CTA 0's K3 pipeline clock64 stamps (16 events x 1024 key tiles) and clears them;
  * returns the count, or -1 in the product build. */

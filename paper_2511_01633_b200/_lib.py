@@ -153,6 +153,9 @@ _SIGS = {
                                           C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                           C.c_int32, C.c_void_p, f32p]),
     "glmx_attn_trace_read": (C.c_int32, [i64p, C.c_int32]),
+    "glmx_kv_gather_run": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_uint32, i32p, C.c_uint64,
+                                     C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, f32p]),
     "glmx_attn_schedule": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
                                      C.c_int32, i32p, i32p, i32p, i64p]),
     "glmx_index_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),

@@ -28,6 +28,8 @@ int engine_wait_impl(glmx_engine*, int32_t*, uint64_t);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_replay_impl(glmx_engine*);
 int index_build_impl(glmx_graph*, int, uint64_t);
+int kv_gather_run_impl(void*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                       const int32_t*, uint64_t, void*, int, int, cudaStream_t, float*);
 int workload_generate_impl(glmx_graph*, uint64_t, int, double, std::string*, float*);
 int retrieve_impl(glmx_graph*, const char*, const uint64_t*, uint64_t, int32_t*, uint8_t*);
 int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
@@ -578,6 +580,16 @@ int32_t glmx_attn_trace_read(int64_t* out, int32_t n) {
     return GLMX_OK;
   });
   return r;
+}
+
+int glmx_kv_gather_run(void* pool, uint64_t n_pages, uint32_t n_layers, uint32_t n_kv_heads,
+                       uint32_t block_tokens, uint32_t head_dim, uint32_t layer, uint32_t kv,
+                       const int32_t* pages, uint64_t n, void* out, int32_t impl, int32_t reps,
+                       void* stream, float* out_ms) {
+  return guarded([&] {
+    return kv_gather_run_impl(pool, n_pages, n_layers, n_kv_heads, block_tokens, head_dim, layer, kv,
+                              pages, n, out, impl, reps, static_cast<cudaStream_t>(stream), out_ms);
+  });
 }
 
 int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,

@@ -41,7 +41,11 @@ void argmax_rows(const float* logits, int n, int V, int32_t* out, cudaStream_t s
 // K4: copy whole pages (all layers) pool_src[src[i]] -> pool_dst[dst[i]]; peer pointers allowed.
 void pool_copy_pages(const __nv_bfloat16* src_base, __nv_bfloat16* dst_base, uint64_t page_elems,
                      const int32_t* src_pages, const int32_t* dst_pages, int n, cudaStream_t s);
-// test hook: gather one layer's K or V of a page list into a dense [n*B][Hkv][hd] buffer
+// K2 gather (kernels/gather.cu): one layer's K or V of a page list into a dense
+// [n*B][Hkv][hd] buffer, TMA-staged (bulk load of each 4 KB (page, head) tile, 2-D TMA store)
+void kv_gather_tma(const PoolGeom& pool, uint32_t layer, uint32_t kv, const int32_t* pages, int n,
+                   __nv_bfloat16* out, cudaStream_t s);
+// scalar reference version (kept for A/B)
 void kv_gather(const PoolGeom& pool, uint32_t layer, uint32_t kv, const int32_t* pages, int n,
                __nv_bfloat16* out, cudaStream_t s);
 

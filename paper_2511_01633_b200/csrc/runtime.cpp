@@ -1225,3 +1225,42 @@ int workload_generate_impl(glmx_graph* g, uint64_t seed, int n, double ratio, st
   *out = glmx::generate_workload_jsonl(g->host, unique, seed, n, ratio);
   return GLMX_OK;
 }
+
+// ======================================================================== K2 gather hook
+int kv_gather_run_impl(void* pool_base, uint64_t n_pages_pool, uint32_t n_layers, uint32_t Hkv,
+                       uint32_t block_tokens, uint32_t hd, uint32_t layer, uint32_t kv,
+                       const int32_t* pages, uint64_t n, void* out, int impl, int reps,
+                       cudaStream_t s, float* out_ms) {
+  if (n == 0) return GLMX_OK;
+  if (layer >= n_layers || kv > 1 || reps < 1) throw Error(GLMX_ERR_ARG, "bad gather arguments");
+  for (uint64_t i = 0; i < n; ++i)
+    if (pages[i] < 0 || static_cast<uint64_t>(pages[i]) >= n_pages_pool) throw Error(GLMX_ERR_ARG, "page out of range");
+  PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, Hkv, block_tokens, hd};
+  DBuf d_pages;
+  d_pages.reserve(n * 4);
+  GLMX_CUDA(cudaMemcpyAsync(d_pages.p, pages, n * 4, cudaMemcpyHostToDevice, s));
+  cudaEvent_t e0, e1;
+  GLMX_CUDA(cudaEventCreate(&e0));
+  GLMX_CUDA(cudaEventCreate(&e1));
+  float ms = 0.f;
+  try {
+    GLMX_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) {
+      if (impl == 0)
+        kv_gather_tma(geom, layer, kv, d_pages.as<int32_t>(), static_cast<int>(n), static_cast<__nv_bfloat16*>(out), s);
+      else
+        kv_gather(geom, layer, kv, d_pages.as<int32_t>(), static_cast<int>(n), static_cast<__nv_bfloat16*>(out), s);
+    }
+    GLMX_CUDA(cudaEventRecord(e1, s));
+    GLMX_CUDA(cudaEventSynchronize(e1));
+    GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  } catch (...) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (out_ms) *out_ms = ms / static_cast<float>(reps);
+  return GLMX_OK;
+}

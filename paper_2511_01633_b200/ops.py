@@ -39,3 +39,17 @@ def reference_rope(x, pos, rope_theta=500000.0):
     sin = torch.sin(ang).float().to(x.device)[:, None, :]
     a, b = x[..., :hd // 2].float(), x[..., hd // 2:].float()
     return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
+
+
+def kv_gather(pool, pages, layer, kv, out, impl=0, reps=1, stream=None):
+    """K2 gather: out [len(pages)*B][Hkv][hd] <- pool[pages][layer][kv] (TMA-staged when impl=0).
+    Returns the mean device ms per launch."""
+    import torch
+
+    n_pages, L, _, Hkv, B, hd = pool.shape
+    ms = C.c_float(0.0)
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    arr = (C.c_int32 * max(1, len(pages)))(*[int(p) for p in pages])
+    check(lib().glmx_kv_gather_run(pool.data_ptr(), n_pages, L, Hkv, B, hd, layer, kv, arr,
+                                   len(pages), out.data_ptr(), impl, reps, s, C.byref(ms)))
+    return ms.value

@@ -60,6 +60,20 @@ if "K2" not in args.skip:
         del pool, qkv, q_out
         torch.cuda.empty_cache()
 
+if "K2g" not in args.skip:
+    from paper_2511_01633_b200.ops import kv_gather
+    for n, impl in ((512, 0), (4096, 0), (16384, 0), (4096, 1)):
+        pool = torch.zeros((n + 8, 4, 2, Hkv, B, hd), dtype=torch.bfloat16, device="cuda")
+        out = torch.empty((n * B, Hkv, hd), dtype=torch.bfloat16, device="cuda")
+        pages = torch.randperm(n + 8)[:n].tolist()
+        kv_gather(pool, pages, 1, 0, out, impl=impl, reps=3)
+        ms = kv_gather(pool, pages, 1, 0, out, impl=impl, reps=args.reps)
+        by = 2 * n * Hkv * B * hd * 2
+        emit({"kernel": "K2 kv_gather (" + ("TMA-staged" if impl == 0 else "scalar") + ")",
+              "pages": n, "ms": ms, "bytes": by, "gbs": by / ms / 1e6})
+        del pool, out
+        torch.cuda.empty_cache()
+
 if "K4" not in args.skip:
     for n in [64, 1024]:
         kv = glmx.KvCacheState(2 * n + 16, 16, glmx.PRIORITY, device=0, n_layers=L, n_kv_heads=Hkv,

@@ -39,3 +39,20 @@ def test_append_matches_reference(T):
     mask = torch.ones_like(pool, dtype=torch.bool)
     mask[page, layer, :, :, off] = False
     assert torch.equal(pool[mask], before[mask])
+
+
+@pytest.mark.parametrize("impl", [0, 1], ids=["tma", "scalar"])
+@pytest.mark.parametrize("n", [1, 37, 1000])
+def test_kv_gather_matches_reference(impl, n):
+    from paper_2511_01633_b200.ops import kv_gather
+
+    Hkv, hd, B, L = 8, 128, 16, 3
+    g = torch.Generator().manual_seed(n)
+    pool = torch.randn((n + 13, L, 2, Hkv, B, hd), generator=g).to(torch.bfloat16).cuda()
+    pages = torch.randperm(n + 13, generator=g)[:n].tolist()
+    for layer, kv in ((0, 0), (2, 1)):
+        out = torch.full((n * B, Hkv, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+        kv_gather(pool, pages, layer, kv, out, impl=impl)
+        torch.cuda.synchronize()
+        want = pool[torch.tensor(pages, device="cuda"), layer, kv].permute(0, 2, 1, 3).reshape(n * B, Hkv, hd)
+        assert torch.equal(out, want)
