@@ -115,47 +115,17 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes' worth of FMA-pipe work per
-// issue slot.
-__device__ __forceinline__ uint64_t f2pack(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-// 2^x for a pair of x <= 8 on the FMA pipe (offloads the MUFU): round-to-nearest split by the
-// 1.5 * 2^23 magic (t's low mantissa bits hold n = rint(x)), degree-3 minimax of 2^f on
-// [-0.5, 0.5] (max rel err 7.5e-5, far below the bf16 rounding of P), exponent added as integer.
-// x is clamped to -126 (masked -inf -> 2^-126, negligible next to the row's max term).
-__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& p0, float& p1) {
-  const float kMagic = 12582912.f;
-  x0 = fmaxf(x0, -126.f);
-  x1 = fmaxf(x1, -126.f);
-  const uint64_t x = f2pack(x0, x1);
-  const uint64_t t = fadd2(x, f2pack(kMagic, kMagic));
-  const uint64_t n = fadd2(t, f2pack(-kMagic, -kMagic));
-  const uint64_t f = ffma2(n, f2pack(-1.f, -1.f), x);
-  uint64_t q = ffma2(f, f2pack(0.05517161265015602f, 0.05517161265015602f),
-                     f2pack(0.24261116981506348f, 0.24261116981506348f));
-  q = ffma2(q, f, f2pack(0.6932610273361206f, 0.6932610273361206f));
-  q = ffma2(q, f, f2pack(0.9999280571937561f, 0.9999280571937561f));
-  float t0, t1, q0, q1;
-  f2unpack(t, t0, t1);
-  f2unpack(q, q0, q1);
-  p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
-  p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+// 2^x (x <= 8) on the FMA pipe: round-to-nearest split by the 1.5 * 2^23 magic (t's low mantissa
+// bits hold n = rint(x)), degree-3 minimax of 2^f on [-0.5, 0.5] (max rel err 7.5e-5), exponent
+// added as an integer; x clamped to -126.  Only used when GLMX_POLY_FROM < 8 (measured slower).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float q = fmaf(f, 0.05517161265015602f, 0.24261116981506348f);
+  q = fmaf(q, f, 0.6932610273361206f);
+  q = fmaf(q, f, 0.9999280571937561f);
+  return __uint_as_float(__float_as_uint(q) + (__float_as_uint(t) << 23));
 }
 // O += P V with the A operand (P, bf16, [128 rows][K]) read from TMEM.
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
@@ -560,7 +530,8 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         for (int i = 0; i < kN; i += 2) {
           float p0, p1;
           if (((i >> 1) & 7) >= kPolyFrom) {
-            ex2_poly2(fmaf(__uint_as_float(v[i]), scale, neg_m), fmaf(__uint_as_float(v[i + 1]), scale, neg_m), p0, p1);
+            p0 = ex2_poly(fmaf(__uint_as_float(v[i]), scale, neg_m));
+            p1 = ex2_poly(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
           } else {
             p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
             p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
