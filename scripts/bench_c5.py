@@ -80,7 +80,9 @@ for P in args.prefix:
         cached = sum(r.cached_tokens for r in reps) / B
         row = {"prefix": P, "k": k, "batch": B, "suffix_tokens": s, "cached_tokens": cached,
                "attn_ms_per_forward": attn, "attn_ms_per_layer": attn / cfg.n_layers,
-               "attn_tflops": tfl, "tensor_frac": tfl / peaks["bf16_tflops"],
+               "attn_tflops": tfl,
+               # timed inside the forward (GEMMs interleaved, power-capped clocks): sustained peak
+               "tensor_frac": tfl / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
                "attn_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
                "intensity": wk["attn_flops"] / wk["attn_bytes"], "forward_ms": fwd,
                # effective prompt tokens/s of a 32-layer forward, extrapolated from n_layers
