@@ -334,7 +334,7 @@ static glmx_graph* finish_graph(HostGraph&& h, int device) {
 
 int glmx_graph_load_jsonl(const char* path, int32_t device, glmx_graph** out) {
   return guarded([&] {
-    *out = finish_graph(load_graph_jsonl(path), device);
+    *out = finish_graph(load_graph_jsonl(path, device < 0), device);
     return GLMX_OK;
   });
 }
@@ -342,7 +342,7 @@ int glmx_graph_load_jsonl(const char* path, int32_t device, glmx_graph** out) {
 int glmx_graph_synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed,
                               int32_t device, glmx_graph** out) {
   return guarded([&] {
-    *out = finish_graph(synth_powerlaw(n_nodes, edges_per_node, seed), device);
+    *out = finish_graph(synth_powerlaw(n_nodes, edges_per_node, seed, device < 0), device);
     return GLMX_OK;
   });
 }

@@ -1,6 +1,9 @@
 #include "graph.hpp"
 
 #include <algorithm>
+#include <iterator>
+#include <exception>
+#include <thread>
 #include <charconv>
 #include <cmath>
 #include <cstring>
@@ -238,7 +241,7 @@ std::string render_scalar(const JVal& v, JParser& jp) {
   }
 }
 
-HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges) {
+HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges, bool host_csr) {
   HostGraph g;
   std::sort(nodes.begin(), nodes.end(),
             [](const RawNode& a, const RawNode& b) { return a.id < b.id; });
@@ -286,7 +289,7 @@ HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges) {
     g.dst.push_back(d->second);
     g.etype.push_back(ti);
   }
-  g.finalize();
+  g.finalize(host_csr);
   return g;
 }
 
@@ -318,29 +321,44 @@ void json_escape(std::string& out, const std::string& s) {
 
 }  // namespace
 
-void HostGraph::finalize() {
+void HostGraph::finalize(bool host_csr) {
   const uint64_t N = n();
   // Entries: "<id> {k:v, ...}" with ("type", node_type) added and pairs sorted by (key, value)
-  // (retriever.cpp:34-41, render_chunk retriever.cpp:10-20).
+  // (retriever.cpp:34-41, render_chunk retriever.cpp:10-20); rendered on up to 16 threads.
+  std::vector<std::string> ent(N);
+  {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint64_t n_thr = std::max<uint64_t>(1, std::min<uint64_t>(hw, N / 8192 + 1));
+    std::vector<std::thread> th;
+    for (uint64_t t = 0; t < n_thr; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t v = N * t / n_thr; v < N * (t + 1) / n_thr; ++v) {
+          std::vector<std::pair<std::string, std::string>> pairs = attrs[v];
+          pairs.emplace_back("type", types[v]);
+          std::sort(pairs.begin(), pairs.end());
+          std::string s = ids[v] + " {";
+          for (size_t i = 0; i < pairs.size(); ++i) {
+            if (i) s += ", ";
+            s += pairs[i].first;
+            s += ':';
+            s += pairs[i].second;
+          }
+          s += '}';
+          ent[v] = std::move(s);
+        }
+      });
+    for (auto& x : th) x.join();
+  }
   entry_off.assign(N + 1, 0);
   entry_bytes.clear();
   for (uint64_t v = 0; v < N; ++v) {
-    std::vector<std::pair<std::string, std::string>> pairs = attrs[v];
-    pairs.emplace_back("type", types[v]);
-    std::sort(pairs.begin(), pairs.end());
-    std::string s = ids[v] + " {";
-    for (size_t i = 0; i < pairs.size(); ++i) {
-      if (i) s += ", ";
-      s += pairs[i].first;
-      s += ':';
-      s += pairs[i].second;
-    }
-    s += '}';
     entry_off[v] = static_cast<uint32_t>(entry_bytes.size());
-    entry_bytes.insert(entry_bytes.end(), s.begin(), s.end());
+    entry_bytes.insert(entry_bytes.end(), ent[v].begin(), ent[v].end());
     if (entry_bytes.size() > 0xFFFFFFF0ULL) throw Error(GLMX_ERR_ARG, "graph text exceeds 4 GiB");
   }
   entry_off[N] = static_cast<uint32_t>(entry_bytes.size());
+  // the neighbour CSRs and weights are built on the GPU (kernels/ingest.cu) for device graphs
+  if (!host_csr) return;
 
   // total_degree (graph_store.cpp:116-121): every edge counts once at each endpoint.
   w_total.assign(N, 0);
@@ -423,17 +441,19 @@ std::string HostGraph::serialize_jsonl() const {
   return out;
 }
 
-HostGraph load_graph_jsonl(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) throw Error(GLMX_ERR_GLM, "cannot open graph file: " + path);
-  std::vector<RawNode> nodes;
-  std::vector<RawEdge> edges;
-  std::string line;
-  size_t line_no = 0;
-  while (std::getline(in, line)) {
-    ++line_no;
-    if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
-    JParser jp{line.data(), line.data() + line.size(), line_no};
+namespace {
+
+// Parses lines [first, last) of the file (line_no = first + 1, ...) into nodes/edges.
+void parse_lines(const std::vector<std::pair<const char*, const char*>>& lines, size_t first,
+                 size_t last, std::vector<RawNode>& nodes, std::vector<RawEdge>& edges) {
+  for (size_t li = first; li < last; ++li) {
+    const char* lb = lines[li].first;
+    const char* le = lines[li].second;
+    const size_t line_no = li + 1;
+    bool blank = true;
+    for (const char* c = lb; c < le && blank; ++c) blank = *c == ' ' || *c == '\t' || *c == '\r';
+    if (blank) continue;
+    JParser jp{lb, le, line_no};
     JVal j = jp.value();
     if (j.kind != JVal::Obj || !j.get("kind")) jp.fail("expected object with \"kind\"");
     const JVal* kind = j.get("kind");
@@ -477,12 +497,57 @@ HostGraph load_graph_jsonl(const std::string& path) {
       jp.fail("kind must be node or edge");
     }
   }
-  return build(std::move(nodes), std::move(edges));
 }
+
+}  // namespace
+
+// Reads the whole file, then parses it on up to 16 host threads (line ranges of ~equal bytes);
+// nodes and edges are merged in file order, and the first malformed line (lowest line number)
+// is the one reported, as with a sequential parse.
+HostGraph load_graph_jsonl(const std::string& path, bool host_csr) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(GLMX_ERR_GLM, "cannot open graph file: " + path);
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  std::vector<std::pair<const char*, const char*>> lines;
+  const char* p = text.data();
+  const char* end = p + text.size();
+  while (p < end) {
+    const char* nl = static_cast<const char*>(std::memchr(p, '\n', end - p));
+    const char* le = nl ? nl : end;
+    lines.emplace_back(p, le);
+    p = nl ? nl + 1 : end;
+  }
+  const size_t n_lines = lines.size();
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t n_thr = std::max<size_t>(1, std::min<size_t>(hw, n_lines / 4096 + 1));
+  std::vector<std::vector<RawNode>> tn(n_thr);
+  std::vector<std::vector<RawEdge>> te(n_thr);
+  std::vector<std::exception_ptr> err(n_thr);
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < n_thr; ++t)
+    th.emplace_back([&, t] {
+      try {
+        parse_lines(lines, n_lines * t / n_thr, n_lines * (t + 1) / n_thr, tn[t], te[t]);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);  // earliest range first = lowest line number
+  std::vector<RawNode> nodes;
+  std::vector<RawEdge> edges;
+  for (size_t t = 0; t < n_thr; ++t) {
+    for (auto& n : tn[t]) nodes.push_back(std::move(n));
+    for (auto& e : te[t]) edges.push_back(std::move(e));
+  }
+  return build(std::move(nodes), std::move(edges), host_csr);
+}
+
 
 // Seeded power-law property graph: out-edge targets dst = floor(n*u^3) concentrate in-degree on
 // low indices (hub degree ~ n^(2/3)), ids zero-padded so byte order == numeric order.
-HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed) {
+HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed, bool host_csr) {
   static const char* adj[] = {"umber", "cobalt", "ivory", "sable", "viridian", "amber",
                               "russet", "pewter", "indigo", "maroon", "ochre", "teal",
                               "slate", "coral", "fawn", "lilac"};
@@ -525,7 +590,7 @@ HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t see
       edges.push_back({nodes[i].id, nodes[d].id, (x & 3) == 3 ? "viewed" : "linked"});
     }
   }
-  return build(std::move(nodes), std::move(edges));
+  return build(std::move(nodes), std::move(edges), host_csr);
 }
 
 }  // namespace glmx

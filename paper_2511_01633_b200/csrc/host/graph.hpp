@@ -39,12 +39,14 @@ struct HostGraph {
   std::vector<int32_t> w_total, w_by_type;
 
   uint64_t n() const { return ids.size(); }
-  void finalize();  // validates, sorts, builds entries/CSRs/weights
+  // entries always; CSRs and weights on the host unless host_csr = false (GPU ingest)
+  void finalize(bool host_csr = true);
   std::string serialize_jsonl() const;
 };
 
-HostGraph load_graph_jsonl(const std::string& path);
-HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed);
+HostGraph load_graph_jsonl(const std::string& path, bool host_csr = true);
+HostGraph synth_powerlaw(uint64_t n_nodes, uint32_t edges_per_node, uint64_t seed,
+                         bool host_csr = true);
 
 // attr.hpp:19-24 shortest round-trip double rendering (std::to_chars).
 std::string format_double(double d);

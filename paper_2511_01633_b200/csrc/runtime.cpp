@@ -6,6 +6,7 @@
 
 #include "kernels/common.cuh"
 #include "kernels/retrieve.cuh"
+#include "kernels/ingest.cuh"
 #include "host/workload_gen.hpp"
 
 using namespace glmx;
@@ -93,14 +94,28 @@ void glmx_graph::upload() {
   };
   dev.entry_bytes = static_cast<const char*>(put(host.entry_bytes.data(), host.entry_bytes.size()));
   dev.entry_off = static_cast<const uint32_t*>(put(host.entry_off.data(), host.entry_off.size() * 4));
-  dev.und_off = static_cast<const uint32_t*>(put(host.und_off.data(), host.und_off.size() * 4));
-  dev.und_idx = static_cast<const int32_t*>(put(host.und_idx.data(), host.und_idx.size() * 4));
-  dev.dir_off = static_cast<const uint32_t*>(put(host.dir_off.data(), host.dir_off.size() * 4));
-  dev.dir_idx = static_cast<const int32_t*>(put(host.dir_idx.data(), host.dir_idx.size() * 4));
-  dev.w_total = static_cast<const int32_t*>(put(host.w_total.data(), host.w_total.size() * 4));
-  dev.w_by_type = static_cast<const int32_t*>(put(host.w_by_type.data(), host.w_by_type.size() * 4));
-  dev.n = static_cast<uint32_t>(host.n());
   GLMX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  if (host.und_off.empty()) {
+    // GPU ingest (kernels/ingest.cu): CSRs and weights built on the device from the edge list
+    DeviceCsr dc;
+    build_graph_device(host.src.data(), host.dst.data(), host.etype.data(), host.src.size(),
+                       static_cast<uint32_t>(host.n()), dc, host.w_total, stream);
+    for (void* p : dc.allocs) allocs.push_back(p);
+    dev.und_off = dc.und_off;
+    dev.und_idx = dc.und_idx;
+    dev.dir_off = dc.dir_off;
+    dev.dir_idx = dc.dir_idx;
+    dev.w_total = dc.w_total;
+    dev.w_by_type = dc.w_by_type;
+  } else {
+    dev.und_off = static_cast<const uint32_t*>(put(host.und_off.data(), host.und_off.size() * 4));
+    dev.und_idx = static_cast<const int32_t*>(put(host.und_idx.data(), host.und_idx.size() * 4));
+    dev.dir_off = static_cast<const uint32_t*>(put(host.dir_off.data(), host.dir_off.size() * 4));
+    dev.dir_idx = static_cast<const int32_t*>(put(host.dir_idx.data(), host.dir_idx.size() * 4));
+    dev.w_total = static_cast<const int32_t*>(put(host.w_total.data(), host.w_total.size() * 4));
+    dev.w_by_type = static_cast<const int32_t*>(put(host.w_by_type.data(), host.w_by_type.size() * 4));
+  }
+  dev.n = static_cast<uint32_t>(host.n());
   GLMX_CUDA(cudaEventCreate(&ev0));
   GLMX_CUDA(cudaEventCreate(&ev1));
   // K1 / K5 scratch for batches of up to 512 chunks of k <= 64 (~8 KB each) without reallocation
