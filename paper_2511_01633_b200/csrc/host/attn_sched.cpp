@@ -93,7 +93,9 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
   }
   std::vector<int> n_pieces_of(n_items, 0);
   const int64_t max_tiles = *std::max_element(tiles.begin(), tiles.end());
-  if (n_items * 2 > n_sm) {
+  // split only long items: below ~8 key tiles the partial traffic + combine pass costs more
+  // than the idle SMs (decode steps over short contexts)
+  if (n_items * 2 > n_sm || max_tiles < 8) {
     // Enough items to occupy the SMs: whole items, longest first, each to the least-loaded of
     // min(n_items, n_sm) persistent CTAs (LPT; equal items reduce to round-robin).
     std::vector<int> order(n_items);

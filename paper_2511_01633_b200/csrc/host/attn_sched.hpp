@@ -6,7 +6,8 @@
 // (makespan > 1.3 x total / n_sm, e.g. 168 long items on 148 SMs), in which case the flattened
 // tile sequence is cut into n_sm equal ranges (stream-K).  With fewer items (a single
 // long-context query has only 8-16), each item's key range is split into up to n_sm / n_items
-// pieces.  Split pieces write an unnormalised partial (O, m, l) and a combine pass merges them.
+// pieces (only when the longest item has >= 8 key tiles: shorter ones run whole).  Split pieces
+// write an unnormalised partial (O, m, l) and a combine pass merges them.
 #pragma once
 
 #include <cstddef>

@@ -41,12 +41,12 @@ def check(reqs, n_kv=8, n_sm=148, tpi=64):
             assert sorted(parts) == list(range(min(parts), min(parts) + len(parts)))
     assert s["n_partials"] <= 2 * n_sm and s["grid"] <= n_sm
     share = -(-s["total_tiles"] // s["grid"])
-    if n_items * 2 > n_sm and not s["combine"]:  # LPT of whole items, longest first
+    if (n_items * 2 > n_sm or max(need) < 8) and not s["combine"]:  # LPT of whole items
         firsts = [s["pieces"][s["cta_off"][c]] for c in range(s["grid"])]
         lens = [p[2] for p in firsts]
         assert lens == sorted(lens, reverse=True)
         assert max(loads) - min(loads) <= max(need)
-        assert max(loads) <= 1.3 * s["total_tiles"] / n_sm or max(need) < 16
+        assert max(loads) <= 1.3 * s["total_tiles"] / n_sm or max(need) < 16 or n_items * 2 <= n_sm
     elif n_items * 2 > n_sm:  # stream-K cut: equal ranges, edges snapped by <= share/8
         assert s["grid"] == min(n_sm, s["total_tiles"])
         assert max(loads) <= share + 2 * max(1, share // 8) + 1
@@ -95,6 +95,11 @@ def test_ragged_random_batches():
 def test_fewer_tiles_than_sms():
     s = check([(1, 1)])
     assert s["grid"] == 8 and len(s["pieces"]) == 8
+
+
+def test_short_items_are_not_split_even_when_few():
+    s = check([(300, 1)] * 8)  # decode step: 64 items of 3 key tiles
+    assert not s["combine"] and s["grid"] == 64
 
 
 @pytest.mark.parametrize("n_sm", [1, 2, 148])
