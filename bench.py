@@ -377,27 +377,35 @@ def main():
     # last staged batch)
     dq_fin = dq_dec = 0
     dq_ms = 0.0
-    if args.decode_steps > 0 and ws == 1:
+    if args.decode_steps > 0:
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         d0 = torch.cuda.Event(enable_timing=True)
         d1 = torch.cuda.Event(enable_timing=True)
         d0.record()
         for _ in range(args.decode_steps):
+            if px is not None:
+                px.epoch_begin()
             rr = wl.rotation_with_decode(8)
+            if px is not None:
+                px.epoch_end()
             dq_fin += rr.finished
             dq_dec += rr.decoded_tokens
         d1.record()
         torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
         dq_ms = d0.elapsed_time(d1)
     peer_blocks = float(kv.peer_hits() - peer0) if px is not None else 0.0
-    vals = torch.tensor([tokens, computed, cached, calls, finished, peer_blocks],
+    vals = torch.tensor([tokens, computed, cached, calls, finished, peer_blocks, dq_fin, dq_dec],
                         dtype=torch.float64, device=red_dev)
-    times = torch.tensor([fwd_ms, wall_ms], dtype=torch.float64, device=red_dev)
+    times = torch.tensor([fwd_ms, wall_ms, dq_ms], dtype=torch.float64, device=red_dev)
     if ws > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.SUM)
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    tokens, computed, cached, calls, finished, peer_blocks = vals.tolist()
-    fwd_ms, wall_ms = times.tolist()
+    tokens, computed, cached, calls, finished, peer_blocks, dq_fin, dq_dec = vals.tolist()
+    fwd_ms, wall_ms, dq_ms = times.tolist()
     if rank != 0:
         dist.destroy_process_group() if ws > 1 else None
         return
@@ -486,7 +494,8 @@ def main():
         "graph_cot_queries_per_s": (
             {"value": dq_fin / (dq_ms * 1e-3), "unit": "queries/s", "rotations": args.decode_steps,
              "queries_finished": dq_fin, "decoded_tokens": dq_dec, "ms": dq_ms,
-             "step": "prefill + greedy reply decode per call (call_llm), wall with CUDA events"}
+             "step": "prefill + greedy reply decode per call (call_llm), CUDA events, max over ranks",
+             "n_gpus": ws}
             if dq_ms > 0 else None),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
