@@ -329,11 +329,13 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
  * work_xy[i] = (request, first token) are flattened into 128-key tiles and cut into <= n_sm
  * equal CTA ranges.  out_pieces [(n_work*n_kv_heads + n_sm) x 4] = (item, j0, j1, partial slot or
  * -1), out_cta_off [n_sm + 1], out_combine [n_sm x 4] = (item, first slot, n slots, 0);
+ * out_partners (nullable; same shape as out_pieces) = the single-query-tile item paired with
+ * piece i on the CTA's second softmax warpgroup (item -1: none; nullptr disables pairing);
  * out_counts = {pieces, grid, combines, partial slots, total tiles}. */
 int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
                        int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
-                       int32_t* out_combine, int64_t out_counts[5]);
+                       int32_t* out_combine, int32_t* out_partners, int64_t out_counts[5]);
 /* K2 gather on caller-owned DEVICE buffers: one layer's K (kv = 0) or V (kv = 1) of the pages
  * pages[0..n) (host array, a request's block table) into out [n * block_tokens][n_kv_heads]
  * [head_dim] bf16 — the dense view the attention core reads through TMA; used to export a

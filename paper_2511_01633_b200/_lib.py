@@ -157,7 +157,7 @@ _SIGS = {
                                      C.c_uint32, C.c_uint32, C.c_uint32, i32p, C.c_uint64,
                                      C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, f32p]),
     "glmx_attn_schedule": (C.c_int, [i32p, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
-                                     C.c_int32, i32p, i32p, i32p, i64p]),
+                                     C.c_int32, i32p, i32p, i32p, i32p, i64p]),
     "glmx_index_build": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
     "glmx_index_size": (C.c_uint64, [C.c_void_p]),
     "glmx_workload_generate": (C.c_int64, [C.c_void_p, C.c_uint64, C.c_int32, C.c_double,

@@ -71,21 +71,25 @@ def reference_attention(q, pool, q_start, q_len, ctx_len, block_table, layer=0):
     return out
 
 
-def schedule(work, q_len, ctx_len, n_kv_heads=8, tokens_per_item=64, n_sm=148):
+def schedule(work, q_len, ctx_len, n_kv_heads=8, tokens_per_item=64, n_sm=148, pair=True):
     """K3's stream-K schedule (host C++ build_attn_schedule) for inspection/tests.
 
     work: list of (request, first token).  Returns dict(pieces=[(item, j0, j1, part)],
-    cta_off=[...], combine=[(item, part0, n_part)], grid, n_partials, total_tiles)."""
+    partners=[(item or -1, j0, j1, part)] (one per piece), cta_off=[...],
+    combine=[(item, part0, n_part)], grid, n_partials, total_tiles)."""
     n_items = len(work) * n_kv_heads
     flat = [int(v) for xy in work for v in xy]
     pieces = (C.c_int32 * (4 * (n_items + n_sm)))()
     cta = (C.c_int32 * (n_sm + 1))()
     comb = (C.c_int32 * (4 * n_sm))()
+    partners = (C.c_int32 * (4 * (n_items + n_sm)))() if pair else None
     cnt = (C.c_int64 * 5)()
     check(lib().glmx_attn_schedule(_i32(flat), len(work), n_kv_heads, _i32(q_len), _i32(ctx_len),
-                                   tokens_per_item, n_sm, pieces, cta, comb, cnt))
+                                   tokens_per_item, n_sm, pieces, cta, comb, partners, cnt))
     n_p, grid, n_c, n_part, total = list(cnt)
     return {"pieces": [tuple(pieces[4 * i:4 * i + 4]) for i in range(n_p)],
+            "partners": [tuple(partners[4 * i:4 * i + 4]) if pair else (-1, 0, 0, -1)
+                         for i in range(n_p)],
             "cta_off": list(cta[:grid + 1]),
             "combine": [tuple(comb[4 * i:4 * i + 3]) for i in range(n_c)],
             "grid": grid, "n_partials": n_part, "total_tiles": total}

@@ -595,7 +595,7 @@ int glmx_kv_gather_run(void* pool, uint64_t n_pages, uint32_t n_layers, uint32_t
 int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_heads,
                        const int32_t* q_len, const int32_t* ctx_len, int32_t tokens_per_item,
                        int32_t n_sm, int32_t* out_pieces, int32_t* out_cta_off,
-                       int32_t* out_combine, int64_t out_counts[5]) {
+                       int32_t* out_combine, int32_t* out_partners, int64_t out_counts[5]) {
   return guarded([&] {
     if (n_work < 0 || n_kv_heads < 1 || tokens_per_item < 1 || n_sm < 1)
       throw Error(GLMX_ERR_ARG, "bad schedule arguments");
@@ -603,6 +603,7 @@ int glmx_attn_schedule(const int32_t* work_xy, int32_t n_work, int32_t n_kv_head
     sc.pieces = reinterpret_cast<AttnPiece*>(out_pieces);
     sc.cta_off = out_cta_off;
     sc.combine = reinterpret_cast<AttnCombine*>(out_combine);
+    sc.partners = reinterpret_cast<AttnPiece*>(out_partners);
     build_attn_schedule(work_xy, n_work, n_kv_heads, q_len, ctx_len, tokens_per_item, 128, n_sm, sc);
     out_counts[0] = sc.n_pieces;
     out_counts[1] = sc.grid;

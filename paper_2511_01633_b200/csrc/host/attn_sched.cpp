@@ -61,9 +61,11 @@ void stream_k_cut(const int32_t* work_xy, int Hkv, const std::vector<int>& tiles
 }  // namespace
 
 size_t attn_sched_bytes(int max_items, int n_sm, size_t* off_pieces, size_t* off_cta,
-                        size_t* off_combine) {
+                        size_t* off_combine, size_t* off_partners) {
   size_t o = 0;
   if (off_pieces) *off_pieces = o;
+  o = align16(o + static_cast<size_t>(max_items + n_sm) * sizeof(AttnPiece));
+  if (off_partners) *off_partners = o;
   o = align16(o + static_cast<size_t>(max_items + n_sm) * sizeof(AttnPiece));
   if (off_cta) *off_cta = o;
   o = align16(o + static_cast<size_t>(n_sm + 1) * sizeof(int32_t));
@@ -92,28 +94,74 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     s.total_tiles += tiles[w];
   }
   std::vector<int> n_pieces_of(n_items, 0);
+  bool paired = false;
   const int64_t max_tiles = *std::max_element(tiles.begin(), tiles.end());
   // split only long items: below ~8 key tiles the partial traffic + combine pass costs more
   // than the idle SMs (decode steps over short contexts)
   if (n_items * 2 > n_sm || max_tiles < 8) {
     // Enough items to occupy the SMs: whole items, longest first, each to the least-loaded of
-    // min(n_items, n_sm) persistent CTAs (LPT; equal items reduce to round-robin).
-    std::vector<int> order(n_items);
-    for (int w = 0; w < n_items; ++w) order[w] = w;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tiles[a] > tiles[b]; });
-    const int grid = std::min(n_items, n_sm);
-    std::vector<std::vector<int>> mine(grid);
-    std::vector<int64_t> load(grid, 0);
-    using Slot = std::pair<int64_t, int>;  // (load, cta): min-heap, ties to the lower CTA
-    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
-    for (int c = 0; c < grid; ++c) heap.push({0, c});
-    for (int w : order) {
-      auto [l, c] = heap.top();
-      heap.pop();
-      mine[c].push_back(w);
-      load[c] = l + tiles[w];
-      heap.push({load[c], c});
+    // min(units, n_sm) persistent CTAs (LPT; equal items reduce to round-robin).  A unit is a
+    // two-tile item, or two single-tile items of similar length paired into one piece.
+    std::vector<int> single, twin;
+    for (int w = 0; w < n_items; ++w) {
+      const int r = work_xy[2 * (w / Hkv)], t0 = work_xy[2 * (w / Hkv) + 1];
+      (!s.partners || q_len[r] - t0 > tokens_per_item / 2 ? twin : single).push_back(w);
     }
+    auto longer = [&](int a, int b) { return tiles[a] > tiles[b]; };
+    std::stable_sort(single.begin(), single.end(), longer);
+    using Unit = std::pair<int, int>;  // (item, partner or -1)
+    // Cost model per key tile, in quarter tiles of a two-query-tile step: a lone single-tile item
+    // runs its softmax/MMA chain unoverlapped at ~3/4 of a full step; a pair costs a full step.
+    std::vector<char> is_single(n_items, 0);
+    for (int w : single) is_single[w] = 1;
+    auto cost = [&](const Unit& u) -> int64_t {
+      if (u.second >= 0) return 4 * std::max(tiles[u.first], tiles[u.second]);
+      return (is_single[u.first] ? 3 : 4) * static_cast<int64_t>(tiles[u.first]);
+    };
+    struct Plan {
+      std::vector<std::vector<Unit>> mine;
+      std::vector<int64_t> load;
+      int64_t makespan = 0;
+    };
+    // the shortest n_pair single-tile items are paired with their length neighbours, the rest
+    // run alone (a long lone item may set the makespan, pairing it would only lengthen it)
+    auto lpt = [&](size_t n_pair) {
+      std::vector<Unit> units;
+      for (int w : twin) units.push_back({w, -1});
+      const size_t n_alone = single.size() - n_pair;
+      for (size_t i = 0; i < n_alone; ++i) units.push_back({single[i], -1});
+      for (size_t i = n_alone; i < single.size(); i += 2)
+        units.push_back({single[i], i + 1 < single.size() ? single[i + 1] : -1});
+      std::stable_sort(units.begin(), units.end(),
+                       [&](const Unit& a, const Unit& b) { return cost(a) > cost(b); });
+      Plan pl;
+      const int grid = std::min(static_cast<int>(units.size()), n_sm);
+      pl.mine.resize(grid);
+      pl.load.assign(grid, 0);
+      using Slot = std::pair<int64_t, int>;  // (load, cta): min-heap, ties to the lower CTA
+      std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+      for (int c = 0; c < grid; ++c) heap.push({0, c});
+      for (const auto& u : units) {
+        auto [l, c] = heap.top();
+        heap.pop();
+        pl.mine[c].push_back(u);
+        pl.load[c] = l + cost(u);
+        heap.push({pl.load[c], c});
+      }
+      pl.makespan = *std::max_element(pl.load.begin(), pl.load.end());
+      return pl;
+    };
+    Plan plan = lpt(0);
+    if (single.size() >= 2) {
+      for (int f = 4; f >= 1; --f) {  // all, 3/4, 1/2, 1/4 of them paired (even counts)
+        Plan pp = lpt(single.size() * f / 4 & ~size_t(1));
+        if (pp.makespan <= plan.makespan) plan = std::move(pp);
+      }
+    }
+    const int grid = static_cast<int>(plan.mine.size());
+    auto& mine = plan.mine;
+    std::vector<int64_t> load(grid);
+    for (int c = 0; c < grid; ++c) load[c] = plan.load[c] / 4;
     const int64_t makespan = *std::max_element(load.begin(), load.end());
     const double ideal = static_cast<double>(s.total_tiles) / n_sm;
     if (makespan > 1.3 * ideal && max_tiles >= 16) {
@@ -123,16 +171,19 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
       // time; boundaries within share/8 tiles of an item edge snap to it.
       stream_k_cut(work_xy, Hkv, tiles, n_sm, s, n_pieces_of);
     } else {
+      paired = s.partners != nullptr;
       s.grid = grid;
       for (int c = 0; c < grid; ++c) {
         s.cta_off[c] = s.n_pieces;
-        for (int w : mine[c]) {
+        for (const auto& u : mine[c]) {
+          if (paired) s.partners[s.n_pieces] = AttnPiece{u.second, 0, u.second < 0 ? 0 : tiles[u.second], -1};
           AttnPiece& p = s.pieces[s.n_pieces++];
-          p.item = w;
+          p.item = u.first;
           p.j0 = 0;
-          p.j1 = tiles[w];
+          p.j1 = tiles[u.first];
           p.part = -1;
-          n_pieces_of[w] = 1;
+          n_pieces_of[u.first] = 1;
+          if (u.second >= 0) n_pieces_of[u.second] = 1;
         }
       }
       s.cta_off[grid] = s.n_pieces;
@@ -157,6 +208,8 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     s.grid = c;
     s.cta_off[c] = s.n_pieces;
   }
+  if (s.partners && !paired)
+    for (int i = 0; i < s.n_pieces; ++i) s.partners[i] = AttnPiece{-1, 0, 0, -1};
   // partial slots for split items, consecutive per item in sequence order
   int last_item = -1;
   for (int i = 0; i < s.n_pieces; ++i) {

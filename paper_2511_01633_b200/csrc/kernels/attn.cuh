@@ -44,6 +44,7 @@ struct AttnTcSched {
   int grid, n_combine;
   float* part_o;
   float2* part_ml;
+  const int4* partners;  // nullptr: no paired pieces
 };
 int attn_tc_partial_rows();  // rows per partial slot (256)
 // trace build only (-DGLMX_ATTN_TRACE): copy + clear CTA 0's pipeline stamps; -1 otherwise

@@ -244,6 +244,7 @@ struct TcParams {
   const int* cta_off;   // pieces of CTA c: [cta_off[c], cta_off[c+1])
   float* part_o;        // [part][256 rows][128] unnormalised O of split items
   float2* part_ml;      // [part][256 rows] (reference max, row sum)
+  const int4* partners; // per piece: the paired single-tile item for warpgroup 1 (x = -1: none)
 };
 
 struct Item {
@@ -362,6 +363,38 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
         const int4 pz = tp.pieces[pc];
         const Item it = item_of(p, pz.x);
         const int32_t* bt = p.block_table + static_cast<int64_t>(it.req) * p.bt_stride;
+        const int4 pb = tp.partners ? tp.partners[pc] : make_int4(-1, 0, 0, -1);
+        if (pb.x >= 0) {
+          // paired single-tile items A (warpgroup 0) and B (warpgroup 1): their key tiles are
+          // interleaved A(0) B(0) A(1) B(1) ..., the shorter one dropping out when it ends
+          const Item ib = item_of(p, pb.x);
+          const int32_t* btb = p.block_table + static_cast<int64_t>(ib.req) * p.bt_stride;
+          const int na = pz.z - pz.y, nb = pb.z - pb.y;
+          int32_t ca[8], cb[8], xa[8], xb[8];
+          fetch(bt, pz.y, ca);
+          fetch(btb, pb.y, cb);
+          for (int j = 0; j < max(na, nb); ++j) {
+            if (j + 1 < na) fetch(bt, pz.y + j + 1, xa);
+            if (j + 1 < nb) fetch(btb, pb.y + j + 1, xb);
+            if (j < na) load_tile(it, ca, pz.y + j);
+            if (kv == 0 && j == 0) {
+              if (it_local > 0) mbar_wait(b_qempty, (it_local - 1) & 1, 1);
+              mbar_expect_tx(b_qfull, 2 * kTile);
+              for (int hf = 0; hf < 2; ++hf) {
+                tma_load_3d(sbase + kOffQ + hf * kHalf, &q_map, hf * 64, it.kvh * G, it.qs + it.tok0, b_qfull);
+                tma_load_3d(sbase + kOffQ + kTile + hf * kHalf, &q_map, hf * 64, ib.kvh * G,
+                            ib.qs + ib.tok0, b_qfull);
+              }
+            }
+            if (j < nb) load_tile(ib, cb, pb.y + j);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              ca[q] = xa[q];
+              cb[q] = xb[q];
+            }
+          }
+          continue;
+        }
         int32_t cur[8], nxt[8];
         fetch(bt, pz.y, cur);
         for (int j = pz.y; j < pz.z; ++j) {
@@ -418,6 +451,54 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       int c0 = 0, c1 = 0;  // tiles consumed by softmax warpgroup 0 / 1 (pfull phases)
       for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc, ++it_local) {
         const int4 pz = tp.pieces[pc];
+        const int4 pb = tp.partners ? tp.partners[pc] : make_int4(-1, 0, 0, -1);
+        if (pb.x >= 0) {
+          // paired items: side 0 = A on S0/O0 (K/V loads gA(j)), side 1 = B on S1/O1 (gB(j));
+          // the producers interleave A(j) B(j), so with n_x = tiles of side x
+          //   gA(j) = g + min(j, na) + min(j, nb),  gB(j) = gA(j) + (j < na)
+          const int na = pz.z - pz.y, nb = pb.z - pb.y, n = max(na, nb);
+          auto ga = [&](int j) { return g + min(j, na) + min(j, nb); };
+          auto gb = [&](int j) { return g + min(j, na) + min(j, nb) + (j < na ? 1 : 0); };
+          mbar_wait(b_qfull, it_local & 1, 12);
+          wait_k(ga(0), 13);
+          issue_s(0, ga(0));
+          tc_commit(b_kempty + 8 * (ga(0) % kKSlots));
+          wait_k(gb(0), 13);
+          issue_s(1, gb(0));
+          tc_commit(b_kempty + 8 * (gb(0) % kKSlots));
+          if (n == 1) tc_commit(b_qempty);
+          for (int j = 0; j < n; ++j) {
+            if (j < na) {
+              mbar_wait(b_pfull, c0 & 1, 10);
+              ++c0;
+              wait_v(ga(j), 11);
+              issue_pv(0, ga(j), j == 0);
+              tc_commit(b_vempty + 8 * (ga(j) % kVSlots));
+              if (j == na - 1) tc_commit(b_ofull);
+              if (j + 1 < na) {
+                wait_k(ga(j + 1), 13);
+                issue_s(0, ga(j + 1));
+                tc_commit(b_kempty + 8 * (ga(j + 1) % kKSlots));
+              }
+            }
+            if (j < nb) {
+              mbar_wait(b_pfull + 8, c1 & 1, 15);
+              ++c1;
+              wait_v(gb(j), 11);
+              issue_pv(1, gb(j), j == 0);
+              tc_commit(b_vempty + 8 * (gb(j) % kVSlots));
+              if (j == nb - 1) tc_commit(b_ofull + 8);
+              if (j + 1 < nb) {
+                wait_k(gb(j + 1), 13);
+                issue_s(1, gb(j + 1));
+                tc_commit(b_kempty + 8 * (gb(j + 1) % kKSlots));
+              }
+            }
+            if (j + 2 == n) tc_commit(b_qempty);  // the last S of the pair was issued above
+          }
+          g += na + nb;
+          continue;
+        }
         const int n = pz.z - pz.y;
         const bool two = item_of(p, pz.x).nqt == 2;  // single-tile items leave WG1 out
         const int g0 = g;  // global tile count of this piece's first key tile
@@ -477,13 +558,21 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
     uint32_t v[kN];
     int g = 0, it_local = 0;
     for (int pc = tp.cta_off[blockIdx.x]; pc < tp.cta_off[blockIdx.x + 1]; ++pc) {
-      const int4 pz = tp.pieces[pc];
+      int4 pz = tp.pieces[pc];
+      int qi = qt;  // query tile of the item this warpgroup works on
+      if (qt == 1 && tp.partners) {
+        const int4 pb = tp.partners[pc];
+        if (pb.x >= 0) {  // paired piece: warpgroup 1 runs the partner's (single) query tile
+          pz = pb;
+          qi = 0;
+        }
+      }
       const Item it = item_of(p, pz.x);
-      if (qt >= it.nqt) continue;  // single-tile item: this warpgroup has no rows in it
-      const int t_row = it.tok0 + qt * (kM / G) + r / G;  // query token of this row
+      if (qi >= it.nqt) continue;  // single-tile item: this warpgroup has no rows in it
+      const int t_row = it.tok0 + qi * (kM / G) + r / G;  // query token of this row
       const int tq = min(t_row, it.qlen - 1);
       const int pos = it.ctx - it.qlen + tq;
-      const int pos_lo = it.ctx - it.qlen + it.tok0 + qt * (kM / G);  // smallest in the tile
+      const int pos_lo = it.ctx - it.qlen + it.tok0 + qi * (kM / G);  // smallest in the tile
       float m_used = -INFINITY, l = 0.f;
       for (int j = pz.y; j < pz.z; ++j, ++g) {
         if ((threadIdx.x & 127) == 0) ATTN_TRACE(5 + 3 * qt, g);
@@ -566,7 +655,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
       tc_fence_after();
       if (pz.w >= 0) {
         // split item: unnormalised O + (reference max, row sum) for the combine pass
-        const int64_t prow = static_cast<int64_t>(pz.w) * (kQT * kM) + qt * kM + r;
+        const int64_t prow = static_cast<int64_t>(pz.w) * (kQT * kM) + qi * kM + r;
         float4* dst = reinterpret_cast<float4*>(tp.part_o + prow * kHD);
         for (int cc = 0; cc < 4; ++cc) {
           uint32_t o[32];
@@ -715,7 +804,7 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
     GLMX_CUDA(cudaFuncSetAttribute(paged_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     attr[dev & 63].store(true, std::memory_order_release);
   }
-  TcParams tp{p, rows_total, sc.pieces, sc.cta_off, sc.part_o, sc.part_ml};
+  TcParams tp{p, rows_total, sc.pieces, sc.cta_off, sc.part_o, sc.part_ml, sc.partners};
   paged_attn_tc_kernel<<<sc.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
                                                         *reinterpret_cast<const CUtensorMap*>(q_map), tp);
   GLMX_CHECK_LAUNCH();

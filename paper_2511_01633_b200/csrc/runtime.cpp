@@ -374,6 +374,15 @@ int model_export_impl(const glmx_model* m, int which, int layer, uint16_t* out, 
 // ======================================================================== engine
 namespace {
 
+// K3 pairs single-query-tile items two per CTA pass (GLMX_ATTN_PAIR=0 disables, for A/B runs)
+bool attn_pairing() {
+  static const bool on = [] {
+    const char* v = std::getenv("GLMX_ATTN_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // Y[T][out] (+)= X[T][in] * W[out][in]^T  (column-major: C(out x T) = W^T' * X)
 void gemm(cublasHandle_t h, cudaStream_t s, const __nv_bfloat16* X, const __nv_bfloat16* W,
           void* Y, bool y_fp32, bool accumulate, int T, int in, int out) {
@@ -474,7 +483,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->o_last = o; o = align_up(o + R * 4, 256);
   e->o_sched = o;
   o = align_up(o + attn_sched_bytes(static_cast<int>(max_work * Hkv), kNumSMs, &e->o_sc_pieces,
-                                    &e->o_sc_cta, &e->o_sc_comb), 256);
+                                    &e->o_sc_cta, &e->o_sc_comb, &e->o_sc_part), 256);
   e->part_o.reserve(static_cast<size_t>(2 * kNumSMs) * attn_tc_partial_rows() * hd * 4);
   e->part_ml.reserve(static_cast<size_t>(2 * kNumSMs) * attn_tc_partial_rows() * 8);
   e->max_copies = T / B + R + 16;  // peer page copies per batch (src, dst int32 each)
@@ -497,6 +506,7 @@ void stage_attn_schedule(glmx_engine* e, uint8_t* hm, const int2* work, int n_wo
   sc.pieces = reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_pieces);
   sc.cta_off = reinterpret_cast<int32_t*>(hm + e->o_sched + e->o_sc_cta);
   sc.combine = reinterpret_cast<AttnCombine*>(hm + e->o_sched + e->o_sc_comb);
+  sc.partners = attn_pairing() ? reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_part) : nullptr;
   build_attn_schedule(reinterpret_cast<const int32_t*>(work), n_work,
                       static_cast<int>(e->m->cfg.n_kv_heads), q_len, ctx_len, e->tpt, 128,
                       kNumSMs, sc);
@@ -533,7 +543,8 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   AttnTcSched sc{reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_pieces),
                  reinterpret_cast<const int*>(meta + e->o_sched + e->o_sc_cta),
                  reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_comb),
-                 e->sc_grid, e->sc_ncomb, e->part_o.as<float>(), e->part_ml.as<float2>()};
+                 e->sc_grid, e->sc_ncomb, e->part_o.as<float>(), e->part_ml.as<float2>(),
+                 attn_pairing() ? reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_part) : nullptr};
   Prof all(e, kCatAll);
   {
     Prof p(e, kCatOther);
@@ -972,8 +983,9 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t o_ql = a16(nr), o_ctx = o_ql + a16(nr), o_bt = o_ctx + a16(nr);
   const size_t o_wk = o_bt + a16(nbt);
-  size_t o_pc = 0, o_cta = 0, o_cb = 0;
-  const size_t sched_bytes = attn_sched_bytes(static_cast<int>(work.size()) * Hkv, kNumSMs, &o_pc, &o_cta, &o_cb);
+  size_t o_pc = 0, o_cta = 0, o_cb = 0, o_pp = 0;
+  const size_t sched_bytes =
+      attn_sched_bytes(static_cast<int>(work.size()) * Hkv, kNumSMs, &o_pc, &o_cta, &o_cb, &o_pp);
   const size_t o_sched = (o_wk + work.size() * 8 + 255) & ~size_t(255);
   const size_t bytes = o_sched + sched_bytes;
   std::vector<uint8_t> h(bytes);
@@ -986,6 +998,7 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   hs.pieces = reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pc);
   hs.cta_off = reinterpret_cast<int32_t*>(h.data() + o_sched + o_cta);
   hs.combine = reinterpret_cast<AttnCombine*>(h.data() + o_sched + o_cb);
+  hs.partners = attn_pairing() ? reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pp) : nullptr;
   if (!impl)
     build_attn_schedule(reinterpret_cast<const int32_t*>(work.data()), static_cast<int>(work.size()),
                         Hkv, q_len, ctx_len, tpt, 128, kNumSMs, hs);
@@ -1000,7 +1013,8 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   AttnTcSched sc{reinterpret_cast<const int4*>(dm + o_sched + o_pc),
                  reinterpret_cast<const int*>(dm + o_sched + o_cta),
                  reinterpret_cast<const int4*>(dm + o_sched + o_cb), hs.grid, hs.n_combine,
-                 part_o.as<float>(), part_ml.as<float2>()};
+                 part_o.as<float>(), part_ml.as<float2>(),
+                 hs.partners ? reinterpret_cast<const int4*>(dm + o_sched + o_pp) : nullptr};
   AttnParams ap{};
   ap.q = static_cast<const __nv_bfloat16*>(q);
   ap.o = static_cast<__nv_bfloat16*>(o);

@@ -135,7 +135,7 @@ struct glmx_engine {
   size_t o_tok = 0, o_pos = 0, o_slot = 0, o_qs = 0, o_ql = 0, o_ctx = 0, o_bt = 0, o_work = 0,
          o_last = 0;
   // K3 stream-K schedule (packed in meta) + partial workspace
-  size_t o_sched = 0, o_sc_pieces = 0, o_sc_cta = 0, o_sc_comb = 0;
+  size_t o_sched = 0, o_sc_pieces = 0, o_sc_cta = 0, o_sc_comb = 0, o_sc_part = 0;
   int sc_grid = 0, sc_ncomb = 0;
   DBuf part_o, part_ml;
 

@@ -90,3 +90,21 @@ def test_single_long_query_split_and_combined():
     # 16 items < 148 / 2: every item's key range is split over ~9 CTAs, partials merged
     _check(0, [(6000 + 100, 100)], seed=6)
     _check(0, [(3000, 1)], seed=7)  # decode-like: one row, 8 items
+
+
+def test_paired_single_tile_items():
+    # > 148 single-query-tile blocks (<= 32 tokens each): the schedule pairs them two per CTA
+    # pass (one per softmax warpgroup, separate K/V streams of different lengths)
+    rnd = random.Random(8)
+    reqs = []
+    for _ in range(48):
+        ql = rnd.randrange(1, 33)
+        reqs.append((ql + rnd.choice([0, rnd.randrange(0, 3000)]), ql))
+    _check(0, reqs, seed=8)
+
+
+def test_paired_items_mixed_with_two_tile_items():
+    rnd = random.Random(9)
+    reqs = [(rnd.randrange(100, 2500), 0) for _ in range(40)]
+    reqs = [(c, min(c, rnd.choice([1, 7, 32, 33, 64, 96, 150]))) for c, _ in reqs]
+    _check(0, reqs, seed=9)
