@@ -296,14 +296,14 @@ def main():
             px.epoch_end()
         return r
 
-    # single-GPU runs pipeline the rotations (host work of r+1 under the forward of r); with peer
-    # exchange every rotation is an epoch whose directory must describe completed pages, so the
-    # rotations stay sequential there
-    pipelined = px is None and not args.no_pipeline
+    # rotations are pipelined (host work of r+1 under the forward of r); with peer exchange the
+    # directory is published one rotation later, once the pages it names are complete
+    # (PeerExchange.before_bookkeeping / after_wait)
+    pipelined = not args.no_pipeline
 
     def rotations(k):
         if pipelined:
-            yield from wl.rotations(k)
+            yield from wl.rotations(k, peer=px)
         else:
             for _ in range(k):
                 yield step()

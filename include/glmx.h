@@ -121,6 +121,11 @@ uint64_t glmx_kv_chain_ids(const char* tok_bytes, const uint64_t* tok_offsets, u
 /* Pages of blocks evicted since the last call become reusable.  Only safe once no enqueued
  * device work reads them (the engine calls this itself, stream-ordered). */
 int glmx_kv_release_deferred(glmx_kv* kv);
+/* Pipelined epochs (host work of rotation r+1 overlaps the forward of r): deferred pages are
+ * numbered in eviction order; glmx_kv_defer_mark = how many were deferred so far, and
+ * glmx_kv_release_deferred_before(mark) frees only those deferred before the mark. */
+uint64_t glmx_kv_defer_mark(const glmx_kv* kv);
+int glmx_kv_release_deferred_before(glmx_kv* kv, uint64_t mark);
 uint64_t glmx_kv_pool_pages(const glmx_kv* kv);
 uint64_t glmx_kv_free_pages(const glmx_kv* kv);
 /* Device address of the pool (for tests / peer mapping); bytes per page. */

@@ -97,6 +97,8 @@ _SIGS = {
     "glmx_kv_snapshot_json": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_uint64]),
     "glmx_kv_chain_ids": (C.c_uint64, [C.c_char_p, u64p, C.c_uint64, C.c_uint32, u64p]),
     "glmx_kv_release_deferred": (C.c_int, [C.c_void_p]),
+    "glmx_kv_defer_mark": (C.c_uint64, [C.c_void_p]),
+    "glmx_kv_release_deferred_before": (C.c_int, [C.c_void_p, C.c_uint64]),
     "glmx_kv_pool_pages": (C.c_uint64, [C.c_void_p]),
     "glmx_kv_free_pages": (C.c_uint64, [C.c_void_p]),
     "glmx_kv_pool_ptr": (C.c_void_p, [C.c_void_p]),
@@ -191,6 +193,15 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def safe_del(self):
+    """__del__ for handle owners: close(), ignoring failures at interpreter shutdown (module
+    globals such as the loaded library may already be torn down)."""
+    try:
+        self.close()
+    except Exception:  # noqa: BLE001
+        pass
 
 
 class GlmxError(RuntimeError):

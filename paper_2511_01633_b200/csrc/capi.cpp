@@ -233,6 +233,11 @@ int glmx_kv_release_deferred(glmx_kv* kv) {
   kv->bk->pool().release_deferred();
   return GLMX_OK;
 }
+uint64_t glmx_kv_defer_mark(const glmx_kv* kv) { return kv->bk->pool().mark(); }
+int glmx_kv_release_deferred_before(glmx_kv* kv, uint64_t mark) {
+  kv->bk->pool().release_before(mark);
+  return GLMX_OK;
+}
 uint64_t glmx_kv_pool_pages(const glmx_kv* kv) { return kv->bk->pool().total(); }
 uint64_t glmx_kv_free_pages(const glmx_kv* kv) { return kv->bk->pool().free_count(); }
 void* glmx_kv_pool_ptr(const glmx_kv* kv) { return kv->geom.base; }

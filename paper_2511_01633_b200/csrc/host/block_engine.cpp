@@ -9,6 +9,7 @@ void PagePool::reset(uint64_t n) {
   total_ = n;
   free_.clear();
   deferred_.clear();
+  deferred_base_ = 0;
   free_.reserve(n);
   // LIFO: page 0 is handed out first.
   for (uint64_t i = n; i-- > 0;) free_.push_back(static_cast<int32_t>(i));
@@ -32,7 +33,17 @@ int32_t PagePool::alloc() {
 
 void PagePool::release_deferred() {
   free_.insert(free_.end(), deferred_.rbegin(), deferred_.rend());
+  deferred_base_ += deferred_.size();
   deferred_.clear();
+}
+
+void PagePool::release_before(uint64_t m) {
+  if (m <= deferred_base_) return;
+  const size_t n = static_cast<size_t>(std::min<uint64_t>(m - deferred_base_, deferred_.size()));
+  free_.insert(free_.end(), std::make_reverse_iterator(deferred_.begin() + n),
+               std::make_reverse_iterator(deferred_.begin()));
+  deferred_.erase(deferred_.begin(), deferred_.begin() + n);
+  deferred_base_ += n;
 }
 
 BlockEngine::BlockEngine(uint64_t capacity, uint32_t block_tokens, int policy,

@@ -39,6 +39,10 @@ class PagePool {
   void defer(int32_t p) { if (p >= 0) deferred_.push_back(p); }
   void free_now(int32_t p) { if (p >= 0) free_.push_back(p); }
   void release_deferred();
+  // deferred pages are numbered in order; mark() = number deferred so far.  release_before(m)
+  // frees the ones deferred before mark m (pipelined epochs release with a lag)
+  uint64_t mark() const { return deferred_base_ + deferred_.size(); }
+  void release_before(uint64_t m);
   uint64_t total() const { return total_; }
   uint64_t free_count() const { return free_.size(); }
   uint64_t deferred_count() const { return deferred_.size(); }
@@ -47,6 +51,7 @@ class PagePool {
   uint64_t total_ = 0;
   std::vector<int32_t> free_;
   std::vector<int32_t> deferred_;
+  uint64_t deferred_base_ = 0;  // number of deferred pages released so far
 };
 
 struct PrefillResult {        // PrefillReport (cache.hpp:33-39) + block table

@@ -82,7 +82,7 @@ class KvCacheState:
             lib().glmx_kv_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    __del__ = _lib.safe_del
 
     def prefill(self, tokens, tiers, session) -> PrefillReport:
         blob, offs = pack_tokens(tokens)
@@ -210,6 +210,13 @@ class KvCacheState:
 
     def release_deferred(self):
         check(lib().glmx_kv_release_deferred(self.h))
+
+    def defer_mark(self) -> int:
+        """Number of pages deferred so far (pipelined epochs release with a lag)."""
+        return lib().glmx_kv_defer_mark(self.h)
+
+    def release_deferred_before(self, mark: int):
+        check(lib().glmx_kv_release_deferred_before(self.h, mark))
 
     def peer_hits(self):
         return lib().glmx_kv_peer_hits(self.h)

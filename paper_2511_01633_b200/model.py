@@ -67,7 +67,7 @@ class Model:
             lib().glmx_model_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    __del__ = _lib.safe_del
 
     def export(self, name, layer=0, shape=None) -> np.ndarray:
         """bf16 weights as float32 (for the CPU oracle)."""
@@ -118,7 +118,7 @@ class Engine:
             lib().glmx_engine_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    __del__ = _lib.safe_del
 
     def set_profiling(self, on=True):
         lib().glmx_engine_set_profiling(self.h, int(on))

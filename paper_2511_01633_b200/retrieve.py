@@ -44,7 +44,7 @@ class PropertyGraph:
             lib().glmx_graph_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    __del__ = _lib.safe_del
 
     def node_count(self):
         return lib().glmx_graph_node_count(self.h)

@@ -81,3 +81,34 @@ class PeerExchange:
         pages evicted during the epoch may be reused."""
         self.dist.barrier(group=self.group)
         self.kv.release_deferred()
+        self._pending = None
+        self._marks = []
+
+    # ---- pipelined epochs (GraphCoTWorkload.rotations: the bookkeeping of rotation r+1 runs
+    # while the forward of rotation r is on the GPU).  Residents at the moment a rotation's
+    # bookkeeping starts (snapshot S_e, rotations < e) are only complete on the device once
+    # forward e-1 has finished, so S_e is published after that wait and serves the bookkeeping
+    # of rotation e+1 (one rotation later than the sequential protocol).  A page evicted after
+    # S_e was taken may still be named by S_e: it stays deferred until every rank has finished
+    # the forward that consumed S_e's directory (rotation e+1), i.e. it is released at the
+    # exchange after wait(e+1).  Cache decisions do not depend on the directory (peer hits only
+    # change computed -> copied), so the lag changes no counter.
+    def before_bookkeeping(self):
+        """Call right before a rotation's prefill bookkeeping: snapshot + deferral mark."""
+        self._pending = (self.kv.resident_ids_pages(), self.kv.defer_mark())
+
+    def after_wait(self):
+        """Call after the oldest in-flight rotation's forward completed: publish the snapshot
+        taken before the next rotation's bookkeeping (now complete on the device), install the
+        merged directory, release the pages deferred before the previous snapshot's mark."""
+        snap, mark = self._pending if getattr(self, "_pending", None) else (
+            (np.zeros(0, np.uint64), np.zeros(0, np.int32)), self.kv.defer_mark())
+        snaps = [None] * self.world
+        self.dist.all_gather_object(snaps, snap, group=self.group)  # also a barrier
+        ids, peers, pages = merge_directories(snaps, self.rank)
+        self.kv.set_peer_directory(ids, peers, pages)
+        marks = getattr(self, "_marks", [])
+        if marks:
+            self.kv.release_deferred_before(marks[-1])
+        self._marks = [mark]
+        return len(ids)

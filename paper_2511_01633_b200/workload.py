@@ -249,17 +249,22 @@ class GraphCoTWorkload:
             th.start()
         return th, built
 
-    def rotations(self, count):
+    def rotations(self, count, peer=None):
         """`count` rotations, pipelined: the host work of rotation r+1 (its calls, the
         bookkeeping and staging of its prefill, its RetrieveNode/K1 thread) runs while rotation
         r's forward is on the GPU.  Nothing host-side depends on a forward's output (replies are
         scripted), and the engine stream orders the forwards, so the cache decisions and the
         results are those of the sequential loop.  Yields each rotation's RotationResult after its
-        forward completed (engine timings/work then describe that rotation)."""
+        forward completed (engine timings/work then describe that rotation).
+
+        peer: a sharding.PeerExchange running the pipelined epoch protocol (before_bookkeeping
+        ahead of every prefill, after_wait behind every completed forward) for multi-GPU runs."""
         if count <= 0:
             return
         calls = self.next_calls()
         th, built = self._start_retrieval(calls)
+        if peer is not None:
+            peer.before_bookkeeping()
         reps = self.prefill_async(calls)
         for r in range(count):
             if th is not None:
@@ -269,8 +274,12 @@ class GraphCoTWorkload:
             if r + 1 < count:
                 calls_n = self.next_calls()
                 th_n, built_n = self._start_retrieval(calls_n)
+                if peer is not None:
+                    peer.before_bookkeeping()
                 nxt = (calls_n, th_n, built_n, self.prefill_async(calls_n))
             res.first_tokens = self.wait(len(calls))
+            if peer is not None:
+                peer.after_wait()
             yield res
             if nxt is not None:
                 calls, th, built, reps = nxt

@@ -61,3 +61,14 @@ def test_ipc_two_processes_one_gpu():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "peer_ipc_check ok" in out.stdout
+
+
+def test_pipelined_epochs_match_sequential():
+    # rotation r+1's bookkeeping overlaps forward r: the directory is published one rotation
+    # later and evicted pages stay deferred until every rank finished the forward that used it
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29519",
+           os.path.join(ROOT, "scripts", "peer_pipeline_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "peer_pipeline_check ok" in out.stdout
