@@ -88,13 +88,25 @@ void glmx_graph::upload() {
   auto put = [&](const void* src, size_t bytes) -> void* {
     void* p = nullptr;
     GLMX_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
-    if (bytes) GLMX_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+    if (bytes && src) GLMX_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
     allocs.push_back(p);
     return p;
   };
-  dev.entry_bytes = static_cast<const char*>(put(host.entry_bytes.data(), host.entry_bytes.size()));
+  {
+    // K1 reads entries as 16-byte words: pad the allocation past the last word
+    std::vector<char> eb(host.entry_bytes.size() + 32, 0);
+    std::memcpy(eb.data(), host.entry_bytes.data(), host.entry_bytes.size());
+    dev.entry_bytes = static_cast<const char*>(put(eb.data(), eb.size()));
+  }
   dev.entry_off = static_cast<const uint32_t*>(put(host.entry_off.data(), host.entry_off.size() * 4));
+  for (size_t i = 0; i + 1 < host.entry_off.size(); ++i)
+    max_entry = std::max(max_entry, host.entry_off[i + 1] - host.entry_off[i]);
   GLMX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {
+    uint32_t* st = static_cast<uint32_t*>(put(nullptr, host.n() * 4));
+    entry_stats(dev.entry_bytes, dev.entry_off, static_cast<uint32_t>(host.n()), st, stream);
+    dev.ent_stat = st;
+  }
   if (host.und_off.empty()) {
     // GPU ingest (kernels/ingest.cu): CSRs and weights built on the device from the edge list
     DeviceCsr dc;
@@ -177,27 +189,34 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   GLMX_CUDA(cudaMemsetAsync(g->d_tidx.as<uint32_t>() + n, 0, 4, s));
   GLMX_CUDA(cudaEventRecord(g->ev0, s));
   chunk_select(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), g->d_flag.as<int32_t>(), big_count, s);
+               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), g->d_tidx.as<uint32_t>(),
+               g->d_flag.as<int32_t>(), big_count, s);
   scan_u64(g->d_temp.p, t64, g->d_len.as<uint64_t>(), g->d_off.as<uint64_t>(),
            static_cast<int>(n + 1), s);
+  scan_u32(g->d_temp.p, t32, g->d_tidx.as<uint32_t>(), g->d_toff.as<uint32_t>(), n + 1, s);
+  // output buffers: sized from a bound when it is small (no host round trip before the render),
+  // else from the scanned totals
+  const uint64_t bound = n * (21 + static_cast<uint64_t>(k + 1) * (g->max_entry + 3));
   uint64_t total = 0;
-  GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
-  GLMX_CUDA(cudaStreamSynchronize(s));
+  uint32_t ntok32 = 0;
+  if (bound > (64ull << 20)) {
+    GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaStreamSynchronize(s));
+  } else {
+    total = bound;
+  }
   // a token has >= 1 byte and is followed by a space or the chunk end: <= total/2 + n tokens
   const uint64_t tok_bound = total / 2 + n + 1;
   g->d_bytes.reserve(total + 16);
   g->d_tid.reserve(tok_bound * 4);
   g->d_tbeg.reserve(tok_bound * 8);
   g->d_tend.reserve(tok_bound * 8);
-  chunk_render(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-               g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_bytes.as<char>(),
-               g->d_tidx.as<uint32_t>(), s);
-  scan_u32(g->d_temp.p, t32, g->d_tidx.as<uint32_t>(), g->d_toff.as<uint32_t>(), n + 1, s);
-  chunk_emit(g->d_bytes.as<char>(), g->d_off.as<uint64_t>(), static_cast<int>(n),
-             g->d_toff.as<uint32_t>(), cfg->vocab, g->d_tid.as<int32_t>(), g->d_tbeg.as<uint64_t>(),
-             g->d_tend.as<uint64_t>(), s);
+  chunk_render_emit(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
+                    g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_toff.as<uint32_t>(),
+                    cfg->vocab, g->d_bytes.as<char>(), g->d_tid.as<int32_t>(),
+                    g->d_tbeg.as<uint64_t>(), g->d_tend.as<uint64_t>(), s);
   GLMX_CUDA(cudaEventRecord(g->ev1, s));
-  uint32_t ntok32 = 0;
+  GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_toff.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaStreamSynchronize(s));
   GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));

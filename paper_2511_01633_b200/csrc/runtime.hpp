@@ -61,6 +61,7 @@ struct glmx_graph {
   glmx::HostGraph host;
   int device = -1;
   glmx::DevGraph dev{};
+  uint32_t max_entry = 0;  // longest pre-rendered entry (K1 output bound)
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
