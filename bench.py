@@ -334,6 +334,7 @@ def main():
     k5_launches = 0
     k5_ms = 0.0
     k1_rotations = 0
+    k2_big_ms = k2_big_bytes = 0.0
     for r in rotations(args.steps):
         tm = eng.last_timings()
         fwd_ms += tm["forward"]
@@ -355,6 +356,9 @@ def main():
         wk = eng.last_work()
         for k in work:
             work[k] += wk[k]
+        if wk["computed_tokens"] >= 2048:  # K2 in its bandwidth regime (large prefill batches)
+            k2_big_ms += tm["kv_append"]
+            k2_big_bytes += wk["append_bytes"]
         # host->device per step: packed batch metadata + chunk node ids; device->host: greedy ids
         # + chunk bytes/tokens
         h2d += int(wk["computed_tokens"]) * 16 + r.calls * (16 + 8 * 520) + r.chunks * 4
@@ -436,6 +440,13 @@ def main():
                  "latency-bound items; the tensor-bound regime is C5 (scripts/bench_attn.py)"},
         {"kernel": "K2 rope_kv_append (fused RoPE + paged KV append)", "bound": "hbm",
          "share_of_forward": tm["kv_append"] / fwd, "achieved": append_gbs, "peak": hbm,
+         # rotations whose batch computes >= 2048 tokens; the rest are small batches (~500
+         # tokens, ~12 MB per launch) where launch latency dominates; in-step times also carry
+         # the write-back of the QKV GEMM output that K2's traffic evicts from L2
+         "achieved_batches_ge_2048_tokens": (k2_big_bytes / (k2_big_ms * 1e-3) / 1e9
+                                             if k2_big_ms > 0 else None),
+         "frac_batches_ge_2048_tokens": (k2_big_bytes / (k2_big_ms * 1e-3) / 1e9 / hbm
+                                         if k2_big_ms > 0 else None),
          "unit": "GB/s", "frac": append_gbs / hbm,
          "ms_per_launch": tm["kv_append"] / n_launch_layers},
     ]
@@ -503,7 +514,7 @@ def main():
         "kernels": kernels,
         # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
         # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
-        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations + k5_launches),
+        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 3 * k1_rotations + k5_launches),
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:

@@ -43,7 +43,7 @@ def emit(row):
 
 H, Hkv, hd, B, L = 32, 8, 128, 16, 32
 if "K2" not in args.skip:
-    for T in [512, 4096, 16384]:
+    for T in [520, 2750, 4965, 16384]:
         n_pages = (T + B - 1) // B + 8
         pool = torch.zeros((n_pages, L, 2, Hkv, B, hd), dtype=torch.bfloat16, device="cuda")
         qkv = torch.randn((T, (H + 2 * Hkv) * hd), device="cuda").to(torch.bfloat16)
