@@ -359,7 +359,8 @@ int32_t glmx_attn_trace_read(int64_t* out, int32_t n);
  * [n_layers][K|V][n_kv_heads][block_tokens][head_dim] bf16.  Host arrays per request: q_start,
  * q_len (suffix rows), ctx_len (cached + suffix keys), block_table [n_req][bt_stride] pages.
  * Causal over absolute positions (query t of request r sits at ctx_len - q_len + t).
- * impl 0 = tcgen05/TMEM/TMA kernel, 1 = mma.sync baseline.  Launches `reps` times on `stream`;
+ * impl 0 = tcgen05/TMEM/TMA kernel, 1 = mma.sync baseline, 2 = CUDA-core decode kernel (every
+ * q_len == 1; the engine uses it for decode steps).  Launches `reps` times on `stream`;
  * out_ms = mean device time per launch (CUDA events). */
 int glmx_attention_run(int32_t impl, const void* q, void* o, uint64_t n_q_rows, int32_t n_heads,
                        int32_t n_kv_heads, int32_t head_dim, void* pool, uint64_t n_pages,

@@ -12,6 +12,7 @@ from ._lib import check, lib
 
 TC = 0   # tcgen05 / TMEM / TMA kernel (the product path)
 MMA = 1  # mma.sync baseline (A/B only)
+DECODE = 2  # CUDA-core flash-decoding kernel for one-token rows (the engine's decode steps)
 
 
 def _i32(xs):

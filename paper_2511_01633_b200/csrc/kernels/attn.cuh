@@ -53,3 +53,13 @@ int attn_trace_read(long long* out, int n);
 void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_total,
                         const void* q_map, const AttnTcSched& sc, cudaStream_t s);
 }  // namespace glmx
+
+namespace glmx {
+// Decode rows (q_len == 1 for every request) on CUDA cores (attn_decode.cu): flash-decoding over
+// the block table, n_split CTAs per (request, kv head); partials (n_split > 1) in part_o /
+// part_ml ([item * n_split + split][4 heads] rows), merged by a combine kernel.
+bool decode_attention_supported(const AttnParams& p);
+int decode_attention_splits(int n_items, int max_ctx, int max_rows);
+void paged_attention_decode(const AttnParams& p, int n_req, int n_split, float* part_o,
+                            float2* part_ml, cudaStream_t s);
+}  // namespace glmx

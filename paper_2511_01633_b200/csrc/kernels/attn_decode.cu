@@ -1,0 +1,262 @@
+// K3d — paged attention for decode rows (one query token per request, q_len == 1) on CUDA cores.
+//
+// A decode row of a GQA group is 4 query heads x 128 dims against the request's cached keys: a
+// GEMV-shaped, HBM-bound read of the K and V pages (4 KB per page per kv head each).  The tcgen05
+// kernel (attn_tc.cu) would fill 4 of its 128 MMA rows and serialise softmax -> PV -> S per key
+// tile, so decode batches take this path instead (flash-decoding):
+//   grid (request x kv head, split): a CTA walks pages [pg0, pg1) of its item's block table, its
+//   4 warps taking half pages (8 keys) round robin.  Lane (half = lane / 16, slice = lane % 16)
+//   loads 16 bytes (8 dims) of 4 key rows of K and of V (all 8 loads issued together), computes
+//   partial dot products for the 4 heads, and a 4-step butterfly reduce-scatter over the 16
+//   lanes of its half leaves every lane one full score (key, head).  Online softmax in base 2
+//   per head (running max / sum in lanes 0-3, probabilities through shared memory), PV
+//   accumulated in fp32 registers (4 heads x 8 dims per lane); the halves and the 4 warps merge
+//   at the end.  Splits > 1 write unnormalised partials (O, m, l) that decode_combine_kernel
+//   merges.
+#include <cfloat>
+
+#include "attn.cuh"
+#include "common.cuh"
+
+namespace glmx {
+
+namespace {
+
+constexpr int kG = 4;     // query heads per kv head
+constexpr int kHd = 128;  // head dim
+constexpr int kB = 16;    // tokens per page
+constexpr int kWarps = 4;
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void bf8(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
+                   float2* __restrict__ part_ml) {
+  __shared__ float4 s_p[kWarps][8];  // probabilities of the current half page: [key][head]
+  __shared__ float s_mx[kWarps][kG], s_alpha[kWarps][kG];
+  __shared__ float s_m[kWarps][kG], s_l[kWarps][kG];
+  __shared__ float s_acc[kWarps][kG][kHd];
+  const int item = blockIdx.x, split = blockIdx.y;
+  const int req = item / p.Hkv, kvh = item % p.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, sl = lane & 15;
+  const int ctx = p.ctx_len[req];
+  const int n_units = (ctx + 7) / 8;  // half pages
+  const int per = (n_units + n_split - 1) / n_split;
+  const int u0 = split * per, u1 = min(n_units, u0 + per);
+  const int qrow = p.q_start[req] + p.q_len[req] - 1;
+  const float scale = p.scale_log2;
+  float q[kG][8];
+#pragma unroll
+  for (int h = 0; h < kG; ++h) {
+    const uint4 u = *reinterpret_cast<const uint4*>(
+        p.q + (static_cast<int64_t>(qrow) * p.H + kvh * kG + h) * kHd + sl * 8);
+    float f[8];
+    bf8(u, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) q[h][j] = f[j] * scale;
+  }
+  float acc[kG][8];
+#pragma unroll
+  for (int h = 0; h < kG; ++h)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[h][j] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;  // head = lane, lanes 0-3
+  const int32_t* bt = p.block_table + static_cast<int64_t>(req) * p.bt_stride;
+  const uint64_t kv_stride = p.pool.tile_off(0, p.layer, 1, kvh) - p.pool.tile_off(0, p.layer, 0, kvh);
+  // half pages u0 + warp, u0 + warp + kWarps, ...  (a register double buffer of the next half
+  // page's loads was measured slower: 188 registers halve the resident warps)
+  auto load = [&](int u, uint4 (&kr)[4], uint4 (&vr)[4]) {
+    const int page = bt[u >> 1];
+    const __nv_bfloat16* kt = p.pool.base + p.pool.tile_off(page, p.layer, 0, kvh) +
+                              static_cast<int64_t>((u & 1) * 8) * kHd + sl * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int key = 2 * i + half;  // within the half page
+      kr[i] = __ldcs(reinterpret_cast<const uint4*>(kt + key * kHd));
+      vr[i] = __ldcs(reinterpret_cast<const uint4*>(kt + kv_stride + key * kHd));
+    }
+  };
+  auto process = [&](int u, const uint4 (&kr)[4], const uint4 (&vr)[4]) {
+    // partial dots of this lane's 8 dims: v[i * 4 + h]
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float f[8];
+      bf8(kr[i], f);
+#pragma unroll
+      for (int h = 0; h < kG; ++h) {
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s = fmaf(q[h][j], f[j], s);
+        v[i * 4 + h] = s;
+      }
+    }
+    // reduce-scatter over the 16 lanes of this half: lane bit b keeps the half of the values
+    // whose index bit matches; afterwards lane sl holds value index sl (i = sl >> 2, h = sl & 3)
+#pragma unroll
+    for (int step = 0; step < 4; ++step) {
+      const int m = 8 >> step, c = 16 >> step;  // partner mask, values still held
+      const bool up = sl & m;
+#pragma unroll
+      for (int j = 0; j < c / 2; ++j) {
+        const float send = up ? v[j] : v[j + c / 2];
+        const float keep = up ? v[j + c / 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    const int my_i = sl >> 2, my_h = sl & 3;
+    const int key_abs = u * 8 + 2 * my_i + half;
+    const float sc = key_abs < ctx ? v[0] : -INFINITY;
+    // per-head max over the 8 keys: lanes with the same my_h (xor over bits 2, 3 and 4)
+    float mx = sc;
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    if (lane < kG) {  // lane == my_h here
+      const float m_new = fmaxf(m_run, mx);
+      s_alpha[warp][lane] = ex2f(m_run - m_new);  // m_run = -inf -> 0
+      s_mx[warp][lane] = m_new;
+      m_run = m_new;
+    }
+    __syncwarp();
+    const float pr = ex2f(sc - s_mx[warp][my_h]);
+    reinterpret_cast<float*>(&s_p[warp][2 * my_i + half])[my_h] = pr;
+    float ps = pr;  // per-head sum over the 8 keys
+    ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+    ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+    if (lane < kG) l_run = l_run * s_alpha[warp][lane] + ps;
+    __syncwarp();
+    float al[kG];
+#pragma unroll
+    for (int h = 0; h < kG; ++h) al[h] = s_alpha[warp][h];
+#pragma unroll
+    for (int h = 0; h < kG; ++h)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[h][j] *= al[h];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 pp = s_p[warp][2 * i + half];
+      const float ph[kG] = {pp.x, pp.y, pp.z, pp.w};
+      float f[8];
+      bf8(vr[i], f);
+#pragma unroll
+      for (int h = 0; h < kG; ++h)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[h][j] = fmaf(ph[h], f[j], acc[h][j]);
+    }
+    __syncwarp();  // s_p / s_alpha reuse by the next half page
+  };
+  for (int u = u0 + warp; u < u1; u += kWarps) {
+    uint4 kr[4], vr[4];
+    load(u, kr, vr);
+    process(u, kr, vr);
+  }
+  // merge the two key halves, then the warps
+#pragma unroll
+  for (int h = 0; h < kG; ++h)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[h][j] += __shfl_xor_sync(0xffffffffu, acc[h][j], 16);
+  if (lane < kG) {
+    s_m[warp][lane] = m_run;
+    s_l[warp][lane] = l_run;
+  }
+  if (half == 0) {
+#pragma unroll
+    for (int h = 0; h < kG; ++h)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s_acc[warp][h][sl * 8 + j] = acc[h][j];
+  }
+  __syncthreads();
+  const int d = threadIdx.x;  // 128 threads = 128 dims
+#pragma unroll
+  for (int h = 0; h < kG; ++h) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w][h]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float wt = s_m[w][h] == -INFINITY ? 0.f : ex2f(s_m[w][h] - M);
+      L += wt * s_l[w][h];
+      O += wt * s_acc[w][h][d];
+    }
+    if (n_split == 1) {
+      p.o[(static_cast<int64_t>(qrow) * p.H + kvh * kG + h) * kHd + d] = __float2bfloat16_rn(O / L);
+    } else {
+      const int64_t row = (static_cast<int64_t>(item) * n_split + split) * kG + h;
+      part_o[row * kHd + d] = O;
+      if (d == 0) part_ml[row] = make_float2(M, L);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kHd)
+decode_combine_kernel(AttnParams p, int n_split, const float* __restrict__ part_o,
+                      const float2* __restrict__ part_ml) {
+  const int item = blockIdx.x;
+  const int req = item / p.Hkv, kvh = item % p.Hkv;
+  const int qrow = p.q_start[req] + p.q_len[req] - 1;
+  const int d = threadIdx.x;
+#pragma unroll
+  for (int h = 0; h < kG; ++h) {
+    float M = -INFINITY;
+    for (int s = 0; s < n_split; ++s)
+      M = fmaxf(M, part_ml[(static_cast<int64_t>(item) * n_split + s) * kG + h].x);
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < n_split; ++s) {
+      const int64_t row = (static_cast<int64_t>(item) * n_split + s) * kG + h;
+      const float2 ml = part_ml[row];
+      const float wt = ml.x == -INFINITY ? 0.f : ex2f(ml.x - M);
+      L += wt * ml.y;
+      O += wt * part_o[row * kHd + d];
+    }
+    p.o[(static_cast<int64_t>(qrow) * p.H + kvh * kG + h) * kHd + d] = __float2bfloat16_rn(O / L);
+  }
+}
+
+}  // namespace
+
+bool decode_attention_supported(const AttnParams& p) {
+  return p.H == kG * p.Hkv && p.pool.head_dim == kHd && p.pool.block_tokens == kB;
+}
+
+// Splits per item so that ~2 CTAs per SM are in flight (a 64-request decode step, 512 items,
+// needs no split and no combine pass), bounded by the partial workspace rows (max_rows) and by
+// one split per 4 half pages.
+int decode_attention_splits(int n_items, int max_ctx, int max_rows) {
+  const int units = (max_ctx + 7) / 8;
+  int s = std::max(1, (2 * kNumSMs + n_items - 1) / std::max(1, n_items));
+  s = std::min(s, std::max(1, units / 4));
+  s = std::min(s, std::max(1, max_rows / std::max(1, n_items * kG)));
+  return s;
+}
+
+void paged_attention_decode(const AttnParams& p, int n_req, int n_split, float* part_o,
+                            float2* part_ml, cudaStream_t s) {
+  if (n_req <= 0) return;
+  if (!decode_attention_supported(p)) throw Error(GLMX_ERR_ARG, "decode attention: unsupported geometry");
+  const int items = n_req * p.Hkv;
+  decode_attn_kernel<<<dim3(items, n_split), kWarps * 32, 0, s>>>(p, n_split, part_o, part_ml);
+  GLMX_CHECK_LAUNCH();
+  if (n_split > 1) {
+    decode_combine_kernel<<<items, kHd, 0, s>>>(p, n_split, part_o, part_ml);
+    GLMX_CHECK_LAUNCH();
+  }
+}
+
+}  // namespace glmx

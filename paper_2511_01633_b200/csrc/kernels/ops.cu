@@ -299,6 +299,47 @@ swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ff, __nv_bfloat16
   }
 }
 
+// Greedy argmax over the vocabulary, split across CTAs: grid (slices, rows); a CTA reduces its
+// slice with 16-byte loads to one 64-bit key (orderable value << 32 | ~index: the max key is the
+// first maximal index) and atomicMax-es it into keys[row]; argmax_finalize turns keys into ids.
+// Values must exceed -FLT_MAX (NaN never wins); a row without one yields 0x7fffffff as before.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int i) {
+  if (!(v > -FLT_MAX)) return 0ull;
+  const uint32_t b = v == 0.f ? 0u : __float_as_uint(v);  // -0 == +0, as the float compare
+  const uint32_t o = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(o) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(i));
+}
+
+__global__ void __launch_bounds__(256)
+argmax_slice_kernel(const float* __restrict__ logits, int V, int slice,
+                    unsigned long long* __restrict__ keys) {
+  const int row = blockIdx.y;
+  const float* r = logits + static_cast<int64_t>(row) * V;
+  const int lo = blockIdx.x * slice, hi = min(V, lo + slice);
+  unsigned long long best = 0;
+  if ((V & 3) == 0) {  // rows 16-byte aligned: float4 loads
+    for (int i = lo + 4 * threadIdx.x; i < hi; i += 4 * blockDim.x) {
+      const float4 x = *reinterpret_cast<const float4*>(r + i);
+      const unsigned long long k0 = argmax_key(x.x, i), k1 = argmax_key(x.y, i + 1);
+      const unsigned long long k2 = argmax_key(x.z, i + 2), k3 = argmax_key(x.w, i + 3);
+      best = max(best, max(max(k0, k1), max(k2, k3)));
+    }
+  } else {
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) best = max(best, argmax_key(r[i], i));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(keys + row, best);
+}
+
+__global__ void argmax_finalize_kernel(const unsigned long long* __restrict__ keys, int n,
+                                       int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long k = keys[i];
+  out[i] = k ? static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k)) : 0x7fffffff;
+}
+
 // First maximal index per row (greedy decode; ties -> lowest id like a first-max scan).
 __global__ void __launch_bounds__(1024)
 argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
@@ -413,10 +454,19 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
   if (T <= 0) return;
   if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
   if (hd == 128) {
-    constexpr int kPassU = 4;  // 16 heads per warp
-    const int groups = static_cast<int>(ceil_div(ceil_div(H + 2 * Hkv, 4), kPassU));
-    rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, 8)), groups), 256, 0, s>>>(
-        qkv, pos, slot, T, H, Hkv, inv_freq, pool, layer, q_out);
+    // 16 heads per warp; decode-sized batches (< 1024 tokens) 4 heads per warp and 2 warps per
+    // CTA, so a 64-token step still spreads over ~380 CTAs with one load round trip each
+    const int passes = static_cast<int>(ceil_div(H + 2 * Hkv, 4));
+    if (T < 1024) {
+      rope_kv_append_warp_kernel<1><<<dim3(static_cast<int>(ceil_div(T, 2)), passes), 64, 0, s>>>(
+          qkv, pos, slot, T, H, Hkv, inv_freq, pool, layer, q_out);
+    } else {
+      constexpr int kPassU = 4;
+      rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, 8)),
+                                                static_cast<int>(ceil_div(passes, kPassU))),
+                                           256, 0, s>>>(qkv, pos, slot, T, H, Hkv, inv_freq, pool,
+                                                        layer, q_out);
+    }
     GLMX_CHECK_LAUNCH();
     return;
   }
@@ -435,9 +485,22 @@ void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStre
   GLMX_CHECK_LAUNCH();
 }
 
-void argmax_rows(const float* logits, int n, int V, int32_t* out, cudaStream_t s) {
+void argmax_rows(const float* logits, int n, int V, int32_t* out, void* keys, cudaStream_t s) {
   if (n <= 0) return;
-  argmax_kernel<<<n, 1024, 0, s>>>(logits, V, out);
+  if (!keys) {  // one CTA per row
+    argmax_kernel<<<n, 1024, 0, s>>>(logits, V, out);
+    GLMX_CHECK_LAUNCH();
+    return;
+  }
+  // ~2 CTAs per SM over all rows, slices a multiple of 1024 elements
+  const int slices = std::max(1, std::min(static_cast<int>(ceil_div(V, 1024)),
+                                          static_cast<int>(ceil_div(2 * kNumSMs, n))));
+  const int slice = static_cast<int>(ceil_div(ceil_div(V, slices), 1024) * 1024);
+  unsigned long long* k = static_cast<unsigned long long*>(keys);
+  GLMX_CUDA(cudaMemsetAsync(k, 0, static_cast<size_t>(n) * 8, s));
+  argmax_slice_kernel<<<dim3(static_cast<int>(ceil_div(V, slice)), n), 256, 0, s>>>(logits, V, slice, k);
+  GLMX_CHECK_LAUNCH();
+  argmax_finalize_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(k, n, out);
   GLMX_CHECK_LAUNCH();
 }
 

@@ -474,6 +474,10 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->bt_stride = static_cast<int>(align_up((cfg->max_context + B - 1) / B + 1, 8));
   const char* impl = std::getenv("GLMX_ATTN");
   e->attn_impl = (impl && std::string(impl) == "mma") ? 1 : 0;
+  {
+    const char* dv = std::getenv("GLMX_DECODE_ATTN");
+    e->decode_cc = !(dv && std::string(dv) == "tc");
+  }
   e->tpt = e->attn_impl ? attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv))
                         : attn_tc_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
   make_pool_tensor_map(kv->geom, kv->bk->pool().total(), e->kv_map, &e->kv_rows);
@@ -488,6 +492,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->hl.reserve(R * d * 2);
   e->logits.reserve(R * c.vocab * 4);
   e->next_tok.reserve((R * (cfg->max_decode + 1) + 16) * 4);
+  e->amax_keys.reserve(R * 8 + 64);
   // metadata layout (one pinned block, one H2D)
   const uint64_t max_work = T / 1 + R;  // upper bound on attention tiles
   size_t o = 0;
@@ -517,6 +522,18 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
 }
 
 namespace {
+
+// One-token batches (decode steps) take the CUDA-core decode kernel: returns its split count, or
+// 0 when the batch has a longer row (prefill) or the path is off / unsupported.
+int choose_decode_split(glmx_engine* e, int R, int T, const int32_t* ctx_len) {
+  if (e->attn_impl || !e->decode_cc || R <= 0 || T != R) return 0;
+  const auto& c = e->m->cfg;
+  if (c.n_heads != 4 * c.n_kv_heads || c.head_dim != 128 || e->kv->cfg.block_tokens != 16) return 0;
+  int max_ctx = 0;
+  for (int r = 0; r < R; ++r) max_ctx = std::max(max_ctx, ctx_len[r]);
+  return decode_attention_splits(R * static_cast<int>(c.n_kv_heads), max_ctx,
+                                 2 * kNumSMs * attn_tc_partial_rows());
+}
 
 // Packs the K3 stream-K schedule of the staged work list into the host metadata block.
 void stage_attn_schedule(glmx_engine* e, uint8_t* hm, const int2* work, int n_work,
@@ -587,7 +604,9 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     {
       Prof p(e, kCatAttn);
       ap.layer = l;
-      if (e->attn_impl)
+      if (e->dec_split)
+        paged_attention_decode(ap, R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
+      else if (e->attn_impl)
         paged_attention(ap, s);
       else
         paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, sc, s);
@@ -754,7 +773,8 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     int ka = h_ctx[a.x] - h_ql[a.x] + a.y, kb = h_ctx[b.x] - h_ql[b.x] + b.y;
     return ka > kb;
   });
-  if (!e->attn_impl) stage_attn_schedule(e, hm, h_work, n_work, h_ql, h_ctx);
+  e->dec_split = choose_decode_split(e, R, T, h_ctx);
+  if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n_work, h_ql, h_ctx);
   e->last_T = T;
   e->last_R = R;
   e->last_work = n_work;
@@ -817,7 +837,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     }
   }
   forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
-  argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), s);
+  argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), e->amax_keys.p, s);
   const int slot = static_cast<int>(e->batch_seq & 1);
   {
     Prof p(e, kCatD2H);
@@ -877,7 +897,8 @@ int engine_replay_impl(glmx_engine* e) {
   DeviceGuard dg(e->m->device);
   forward(e, e->last_T, e->last_R, e->last_work, e->last_R,
           reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
-  argmax_rows(e->logits.as<float>(), e->last_R, e->m->cfg.vocab, e->next_tok.as<int32_t>(), e->stream);
+  argmax_rows(e->logits.as<float>(), e->last_R, e->m->cfg.vocab, e->next_tok.as<int32_t>(),
+              e->amax_keys.p, e->stream);
   GLMX_CUDA(cudaStreamSynchronize(e->stream));
   collect_profile(e);
   return GLMX_OK;
@@ -940,12 +961,13 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
       h_last[j] = j;
       rq.ctx_len = p + 1;
     }
-    if (!e->attn_impl) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
+    e->dec_split = choose_decode_split(e, n, n, h_ctx);
+    if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
     GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
     GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
     const int32_t* in_tok = st == 0 ? d_prev : d_seq + static_cast<size_t>(st - 1) * R;
     forward(e, n, n, n, n, in_tok);
-    argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R, s);
+    argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R, e->amax_keys.p, s);
   }
   std::vector<int32_t> seq(static_cast<size_t>(max_steps) * R);
   GLMX_CUDA(cudaMemcpyAsync(seq.data(), d_seq, seq.size() * 4, cudaMemcpyDeviceToHost, s));
@@ -977,6 +999,13 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
                        int bt_stride, int reps, cudaStream_t s, float* out_ms) {
   if (n_req == 0) return GLMX_OK;
   if (H % Hkv != 0 || reps < 1) throw Error(GLMX_ERR_ARG, "bad attention arguments");
+  // impl 2: the CUDA-core decode kernel (every request one query token)
+  const bool dec = impl == 2;
+  if (dec) {
+    for (uint64_t r = 0; r < n_req; ++r)
+      if (q_len[r] != 1) throw Error(GLMX_ERR_ARG, "decode attention needs q_len == 1");
+    impl = 1;
+  }
   PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, static_cast<uint32_t>(Hkv),
                 block_tokens, static_cast<uint32_t>(hd)};
   const int tpt = impl ? attn_tokens_per_tile(H, Hkv) : attn_tc_tokens_per_tile(H, Hkv);
@@ -1055,6 +1084,15 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
     make_pool_tensor_map(geom, n_pages, kv_map, &rows);
     make_q_tensor_map(q, T, H, Hkv, q_map);
   }
+  int dec_split = 0;
+  if (dec) {
+    if (!decode_attention_supported(ap)) throw Error(GLMX_ERR_ARG, "decode attention: unsupported geometry");
+    int max_ctx = 0;
+    for (uint64_t r = 0; r < n_req; ++r) max_ctx = std::max(max_ctx, ctx_len[r]);
+    dec_split = decode_attention_splits(static_cast<int>(n_req) * Hkv, max_ctx, 1 << 20);
+    part_o.reserve(static_cast<size_t>(n_req) * Hkv * dec_split * 4 * hd * 4);
+    part_ml.reserve(static_cast<size_t>(n_req) * Hkv * dec_split * 4 * 8);
+  }
   cudaEvent_t e0, e1;
   GLMX_CUDA(cudaEventCreate(&e0));
   GLMX_CUDA(cudaEventCreate(&e1));
@@ -1062,7 +1100,10 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   try {
     GLMX_CUDA(cudaEventRecord(e0, s));
     for (int i = 0; i < reps; ++i) {
-      if (impl)
+      if (dec)
+        paged_attention_decode(ap, static_cast<int>(n_req), dec_split, part_o.as<float>(),
+                               part_ml.as<float2>(), s);
+      else if (impl)
         paged_attention(ap, s);
       else
         paged_attention_tc(ap, kv_map, rows, q_map, sc, s);

@@ -110,7 +110,7 @@ struct glmx_engine {
   uint32_t kv_rows = 0;
 
   // activations
-  DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok;
+  DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok, amax_keys;
   // batch metadata (device) + pinned host staging (single H2D)
   DBuf meta;
   void* h_meta = nullptr;
@@ -138,6 +138,8 @@ struct glmx_engine {
   // K3 stream-K schedule (packed in meta) + partial workspace
   size_t o_sched = 0, o_sc_pieces = 0, o_sc_cta = 0, o_sc_comb = 0, o_sc_part = 0;
   int sc_grid = 0, sc_ncomb = 0;
+  bool decode_cc = true;  // one-token batches on the CUDA-core decode kernel (GLMX_DECODE_ATTN=tc: off)
+  int dec_split = 0;      // > 0: the staged batch is all one-token rows -> K3d with this many splits
   DBuf part_o, part_ml;
 
   // profiling

@@ -108,3 +108,26 @@ def test_paired_items_mixed_with_two_tile_items():
     reqs = [(rnd.randrange(100, 2500), 0) for _ in range(40)]
     reqs = [(c, min(c, rnd.choice([1, 7, 32, 33, 64, 96, 150]))) for c, _ in reqs]
     _check(0, reqs, seed=9)
+
+
+@pytest.mark.parametrize("n_req", [1, 8, 64, 200])
+def test_decode_kernel_one_token_rows(n_req):
+    # K3d (CUDA-core flash-decoding, impl 2): one query token per request, contexts from a single
+    # key to several thousand (one split per item for large batches, many for small ones)
+    rnd = random.Random(n_req)
+    reqs = [(rnd.choice([1, 15, 16, 17, 31, rnd.randrange(2, 400), rnd.randrange(400, 4000)]), 1)
+            for _ in range(n_req)]
+    _check(2, reqs, seed=10 + n_req)
+
+
+def test_decode_kernel_matches_tc_kernel():
+    import paper_2511_01633_b200.attention as A
+
+    reqs = [(c, 1) for c in (5, 100, 333, 1024, 2049)]
+    q, pool, qs, ql, ctx, bt, layer = _case(reqs, seed=21)
+    o2 = torch.empty_like(q)
+    o0 = torch.empty_like(q)
+    A.paged_attention(q, o2, pool, qs, ql, ctx, bt, layer=layer, impl=2)
+    A.paged_attention(q, o0, pool, qs, ql, ctx, bt, layer=layer, impl=0)
+    torch.cuda.synchronize()
+    assert (o2.float() - o0.float()).abs().max().item() < 2e-2
