@@ -330,6 +330,13 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
                             int32_t head_dim, float rope_theta, void* pool, uint32_t n_layers,
                             uint32_t layer, uint32_t block_tokens, void* q_out, int32_t reps,
                             void* stream, float* out_ms);
+/* Decode GEMM hook (kernel level, caller-owned DEVICE buffers): y[n][n_out] (+)= x[n][k] .
+ * w[n_out][k]^T, bf16 inputs, on the tcgen05 weight-streaming kernel the engine uses for decode
+ * steps (n <= 64, k % 64 == 0, n_out % 128 == 0).  mode 0: y bf16, 1: y fp32, 2: y fp32 += .
+ * Launches `reps` times on `stream`; out_ms = mean device ms per launch.  Replaces cuBLAS for
+ * the provider step's decode forwards (no reference counterpart). */
+int glmx_gemv_run(const void* w, const void* x, void* y, int32_t n, int32_t k, int32_t n_out,
+                  int32_t mode, int32_t reps, void* stream, float* out_ms);
 /* K3's persistent-CTA schedule (host only, no device): items w = i * n_kv_heads + h of work entries
  * work_xy[i] = (request, first token) are flattened into 128-key tiles and cut into <= n_sm
  * equal CTA ranges.  out_pieces [(n_work*n_kv_heads + n_sm) x 4] = (item, j0, j1, partial slot or

@@ -169,6 +169,8 @@ _SIGS = {
     "glmx_retriever_stats": (None, [C.c_void_p, i64p]),
     "glmx_retrieve_last_kernel_ms": (C.c_float, [C.c_void_p]),
     "glmx_embed_text": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, f32p]),
+    "glmx_gemv_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int32, C.c_int32, C.c_void_p, f32p]),
     "glmx_attention_run": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                                      C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_uint64, i32p, i32p, i32p, i32p,

@@ -35,6 +35,7 @@ int retrieve_impl(glmx_graph*, const char*, const uint64_t*, uint64_t, int32_t*,
 int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
                          float, void*, uint32_t, uint32_t, uint32_t, void*, int, cudaStream_t,
                          float*);
+int gemv_run_impl(const void*, const void*, void*, int, int, int, int, int, cudaStream_t, float*);
 int attention_run_impl(int, const void*, void*, uint64_t, int, int, int, void*, uint64_t, uint32_t,
                        uint32_t, uint32_t, uint64_t, const int32_t*, const int32_t*,
                        const int32_t*, const int32_t*, int, int, cudaStream_t, float*);
@@ -575,6 +576,13 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
     return rope_append_run_impl(qkv, pos, slot, n_tokens, n_heads, n_kv_heads, head_dim,
                                 rope_theta, pool, n_layers, layer, block_tokens, q_out, reps,
                                 static_cast<cudaStream_t>(stream), out_ms);
+  });
+}
+
+int glmx_gemv_run(const void* w, const void* x, void* y, int32_t n, int32_t k, int32_t n_out,
+                  int32_t mode, int32_t reps, void* stream, float* out_ms) {
+  return guarded([&] {
+    return gemv_run_impl(w, x, y, n, k, n_out, mode, reps, static_cast<cudaStream_t>(stream), out_ms);
   });
 }
 

@@ -7,6 +7,7 @@
 #include "kernels/common.cuh"
 #include "kernels/retrieve.cuh"
 #include "kernels/ingest.cuh"
+#include "kernels/gemv_tc.cuh"
 #include "host/workload_gen.hpp"
 
 using namespace glmx;
@@ -1348,6 +1349,36 @@ int kv_gather_run_impl(void* pool_base, uint64_t n_pages_pool, uint32_t n_layers
     cudaEventDestroy(e1);
     throw;
   }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (out_ms) *out_ms = ms / static_cast<float>(reps);
+  return GLMX_OK;
+}
+
+// ======================================================================== decode GEMM hook
+// Y[n][N] (+)= X[n][K] . W[N][K]^T on caller-owned device buffers through the tcgen05 decode GEMM
+// (mode 0 bf16 out, 1 fp32 out, 2 fp32 accumulate); `reps` launches, mean ms per launch.
+int gemv_run_impl(const void* w, const void* x, void* y, int n, int K, int N, int mode, int reps,
+                  cudaStream_t s, float* out_ms) {
+  if (!gemv_tc_supported(n, K, N) || mode < 0 || mode > 2 || reps < 1)
+    throw Error(GLMX_ERR_ARG, "gemv: unsupported shape (n <= 64, K % 64 == 0, N % 128 == 0)");
+  alignas(64) uint8_t w_map[128], x_map[128];
+  make_gemv_map(w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), 128, w_map);
+  make_gemv_map(x, static_cast<uint64_t>(n), static_cast<uint64_t>(K), 64, x_map);
+  DBuf part, cnt;
+  part.reserve(gemv_tc_part_floats(K, N) * 4);
+  cnt.reserve(static_cast<size_t>(N / 128) * 4);
+  GLMX_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(N / 128) * 4, s));
+  cudaEvent_t e0, e1;
+  GLMX_CUDA(cudaEventCreate(&e0));
+  GLMX_CUDA(cudaEventCreate(&e1));
+  float ms = 0.f;
+  GLMX_CUDA(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i)
+    gemv_tc(w_map, x_map, n, K, N, mode, y, part.as<float>(), cnt.as<int>(), s);
+  GLMX_CUDA(cudaEventRecord(e1, s));
+  GLMX_CUDA(cudaEventSynchronize(e1));
+  GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (out_ms) *out_ms = ms / static_cast<float>(reps);

@@ -53,3 +53,22 @@ def kv_gather(pool, pages, layer, kv, out, impl=0, reps=1, stream=None):
     check(lib().glmx_kv_gather_run(pool.data_ptr(), n_pages, L, Hkv, B, hd, layer, kv, arr,
                                    len(pages), out.data_ptr(), impl, reps, s, C.byref(ms)))
     return ms.value
+
+
+def gemv(x, w, y, mode=0, reps=1, stream=None):
+    """Decode GEMM on the tcgen05 weight-streaming kernel: y (+)= x @ w.T (glmx_gemv_run).
+
+    x [n <= 64][K] bf16, w [N][K] bf16, y [n][N] bf16 (mode 0) or fp32 (1 store, 2 accumulate).
+    Returns the mean device ms per launch."""
+    import torch
+
+    n, K = x.shape
+    N = w.shape[0]
+    assert x.is_cuda and w.is_cuda and y.is_cuda and w.shape[1] == K and tuple(y.shape) == (n, N)
+    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+    assert y.dtype == (torch.bfloat16 if mode == 0 else torch.float32)
+    ms = C.c_float(0.0)
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(lib().glmx_gemv_run(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, K, N,
+                              mode, reps, s, C.byref(ms)))
+    return ms.value
