@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--routing", default="mod", choices=["mod", "affinity"],
                    help="query -> GPU: i mod N (reference sharding) or prefix affinity "
                         "(fnv1a(question) mod N: repeated questions stay on one GPU)")
+    p.add_argument("--no-standalone", action="store_true",
+                   help="skip the standalone K1 / K3 measurements reported beside the in-step ones")
     p.add_argument("--no-pipeline", action="store_true",
                    help="run the rotations back to back instead of pipelining the host work")
     p.add_argument("--decode-steps", type=int, default=8,
@@ -231,6 +233,45 @@ def run_reference(args, ws, rank):
 
 
 # ------------------------------------------------------------------------------------------
+def standalone_kernels(glmx, g, ret, peaks, tc_peak_burst):
+    """K1 and K3 timed alone on synthetic inputs of their large-batch / long-context regimes."""
+    import random
+
+    import torch
+
+    import paper_2511_01633_b200.attention as A
+    out = {}
+    rnd = random.Random(65536)
+    nodes = [rnd.randrange(g.node_count()) for _ in range(65536)]
+    ret.chunk_build_device(nodes)
+    tb, tt, ms = ret.chunk_build_device(nodes)
+    deg = sum(g.total_degree(i) for i in nodes)
+    by = 8 * len(nodes) + 8 * deg + 2 * tb + 20 * tt
+    out["K1"] = {"workload": "65536 chunks (k=16) of the bench graph", "ms": ms,
+                 "achieved": by / ms / 1e6, "unit": "GB/s", "frac": by / ms / 1e6 / peaks["hbm_gbs"],
+                 "note": "issue-bound byte work (render, whitespace mask, fnv1a): ncu in profiles/"}
+    H, Hkv, hd, B, P, s, nb = 32, 8, 128, 16, 8192, 128, 8
+    ctx = P + s
+    per = (ctx + B - 1) // B
+    pool = torch.empty((nb * per, 4, 2, Hkv, B, hd), dtype=torch.bfloat16, device="cuda").normal_()
+    q = torch.empty((nb * s, H, hd), dtype=torch.bfloat16, device="cuda").normal_()
+    o = torch.empty_like(q)
+    perm = list(range(nb * per))
+    random.Random(P).shuffle(perm)
+    bt = [perm[i * per:(i + 1) * per] for i in range(nb)]
+    qs, ql, cl = [i * s for i in range(nb)], [s] * nb, [ctx] * nb
+    A.paged_attention(q, o, pool, qs, ql, cl, bt, reps=3)
+    ms = A.paged_attention(q, o, pool, qs, ql, cl, bt, reps=20)
+    flops = nb * sum(4.0 * H * hd * (P + t + 1) for t in range(s))
+    out["K3"] = {"workload": "C5 shape: 8 requests x (8192 cached + 128 suffix), one layer",
+                 "ms": ms, "achieved": flops / ms / 1e9, "unit": "TFLOP/s",
+                 "peak": tc_peak_burst, "frac": flops / ms / 1e9 / tc_peak_burst,
+                 "peak_kind": "measured burst bf16 (kernel timed alone)"}
+    del pool, q, o
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
@@ -471,6 +512,14 @@ def main():
                         "overlapped_with_prefill": True,
                         "retrieval_stats": dict(zip(("cache_hits", "cache_misses", "index_probes"),
                                                     nidx.stats()))})
+    if not args.no_standalone:
+        # the same kernels alone in their bandwidth / tensor regimes (untimed region, GPU idle):
+        # K1 over a 65536-chunk batch of this graph, K3 at the C5 shape (8 x 8192 cached + 128)
+        sa = standalone_kernels(glmx, g, ret, peaks, tc_peak_burst=peaks["bf16_tflops"])
+        for kd in kernels:
+            tag = kd["kernel"].split()[0]
+            if tag in sa:
+                kd["standalone"] = sa[tag]
     # dominant kernel of the step by device time: the cuBLAS GEMMs (Llama-3-8B linears)
     roof = {"bound": "tensor", "achieved": gemm_tflops, "peak": tc_peak, "unit": "TFLOP/s",
             "frac": gemm_tflops / tc_peak,

@@ -107,6 +107,16 @@ class Retriever:
             spans.append([(tbeg[j], tend[j]) for j in range(toff[i], toff[i + 1])])
         return ChunkBatch(texts, ids, spans, lib().glmx_chunk_last_kernel_ms(self.graph.h))
 
+    def chunk_build_device(self, node_idx):
+        """K1 over a batch without copying the outputs back: (total bytes, total tokens, device ms
+        of select -> scans -> render+tokenize).  For measurements."""
+        n = len(node_idx)
+        nodes = (C.c_int32 * max(1, n))(*node_idx)
+        tb, tt = C.c_uint64(), C.c_uint64()
+        check(lib().glmx_chunk_build(self.graph.h, C.byref(self.cfg), nodes, n, None, 0, None,
+                                     None, None, None, 0, None, C.byref(tb), C.byref(tt)))
+        return tb.value, tt.value, lib().glmx_chunk_last_kernel_ms(self.graph.h)
+
 
 def embed(text: str, dim: int = 64):
     """embed(text, dim) of the reference (embedder.cpp:19-36), host C++: list of padded floats."""
