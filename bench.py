@@ -421,7 +421,7 @@ def main():
     # decode of each reply — for Graph-CoT queries/s; rotations sequential (decode continues the
     # last staged batch)
     dq_fin = dq_dec = 0
-    dq_ms = dq_dec_ms = 0.0
+    dq_ms = dq_dec_ms = dq_pre_ms = 0.0
     if args.decode_steps > 0:
         if ws > 1:
             dist.barrier()
@@ -430,16 +430,27 @@ def main():
         d1 = torch.cuda.Event(enable_timing=True)
         d0.record()
         eng.set_profiling(1)  # one event pair per forward: the decode forwards' device time
-        for _ in range(args.decode_steps):
-            if px is not None:
-                px.epoch_begin()
-            rr = wl.rotation_with_decode(8)
-            if px is not None:
-                px.epoch_end()
+
+        def account(rr):
+            nonlocal dq_fin, dq_dec, dq_dec_ms, dq_pre_ms
             dq_fin += rr.finished
             dq_dec += rr.decoded_tokens
             if rr.decoded_tokens:  # device time of this rotation's decode forwards
                 dq_dec_ms += eng.last_timings()["forward"]
+            dq_pre_ms += getattr(wl, "last_prefill_forward_ms", 0.0)
+
+        if px is None and pipelined:
+            # rotation r+1's host work (advance, calls, RetrieveNode/K1) under r's decode steps
+            for rr in wl.rotations_with_decode(args.decode_steps, 8):
+                account(rr)
+        else:
+            for _ in range(args.decode_steps):
+                if px is not None:
+                    px.epoch_begin()
+                rr = wl.rotation_with_decode(8)
+                if px is not None:
+                    px.epoch_end()
+                account(rr)
         d1.record()
         torch.cuda.synchronize()
         eng.set_profiling(0)
@@ -558,7 +569,7 @@ def main():
         "graph_cot_queries_per_s": (
             {"value": dq_fin / (dq_ms * 1e-3), "unit": "queries/s", "rotations": args.decode_steps,
              "queries_finished": dq_fin, "decoded_tokens": dq_dec, "ms": dq_ms,
-             "decode_forward_ms": dq_dec_ms,
+             "decode_forward_ms": dq_dec_ms, "prefill_forward_ms": dq_pre_ms,
              "step": "prefill + greedy reply decode per call (call_llm), CUDA events, max over ranks",
              "n_gpus": ws}
             if dq_ms > 0 else None),

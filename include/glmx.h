@@ -302,6 +302,11 @@ int32_t glmx_engine_in_flight(const glmx_engine* e);
  * out_tokens host [n_req][max_steps], -1 past a request's count. */
 int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens,
                        float* last_logits);
+/* The same decode split in two: _async stages and launches every step of the last staged batch
+ * without waiting for the GPU (a prefill may still be in flight; the next prefill may be staged
+ * before the collect), _collect waits and writes out_tokens [n_req][max_steps] as above. */
+int glmx_engine_decode_async(glmx_engine* e, const uint32_t* steps);
+int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens);
 /* Re-run the device forward of the last prefill batch (inputs already resident in HBM) —
  * used to time the device part alone; KV writes are idempotent. */
 int glmx_engine_replay_forward(glmx_engine* e);

@@ -485,6 +485,18 @@ void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStre
   GLMX_CHECK_LAUNCH();
 }
 
+__global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                                  int n, int32_t* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+void gather_i32(const int32_t* src, const int32_t* idx, int n, int32_t* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  gather_i32_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(src, idx, n, dst);
+  GLMX_CHECK_LAUNCH();
+}
+
 void argmax_rows(const float* logits, int n, int V, int32_t* out, void* keys, cudaStream_t s) {
   if (n <= 0) return;
   if (!keys) {  // one CTA per row

@@ -37,6 +37,8 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
                     int H, int Hkv, int hd, const float* inv_freq, const PoolGeom& pool,
                     uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s);
 void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStream_t s);
+// dst[i] = src[idx[i]] (decode: first tokens into decode row order)
+void gather_i32(const int32_t* src, const int32_t* idx, int n, int32_t* dst, cudaStream_t s);
 // keys: n x 8 bytes of device scratch (split over CTAs), or nullptr (one CTA per row)
 void argmax_rows(const float* logits, int n, int V, int32_t* out, void* keys, cudaStream_t s);
 // K4: copy whole pages (all layers) pool_src[src[i]] -> pool_dst[dst[i]]; peer pointers allowed.

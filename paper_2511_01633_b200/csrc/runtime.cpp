@@ -69,7 +69,12 @@ glmx_model::~glmx_model() {
 }
 
 glmx_engine::~glmx_engine() {
-  if (h_meta) cudaFreeHost(h_meta);
+  for (auto& hp : h_ring)
+    if (hp) cudaFreeHost(hp);
+  for (auto& ev : ring_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h_dec) cudaFreeHost(h_dec);
+  if (dec_done) cudaEventDestroy(dec_done);
   if (h_out) cudaFreeHost(h_out);
   if (h2d_done) cudaEventDestroy(h2d_done);
   if (fwd_done) cudaEventDestroy(fwd_done);
@@ -440,7 +445,7 @@ struct Prof {
     if (a) {
       cudaEvent_t b = next_event(e);
       cudaEventRecord(b, e->stream);
-      e->spans.push_back({a, b, cat, e->batch_seq});
+      e->spans.push_back({a, b, cat, e->prof_tag ? e->prof_tag : e->batch_seq});
     }
   }
 };
@@ -506,6 +511,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->o_bt = o; o = align_up(o + R * e->bt_stride * 4, 256);
   e->o_work = o; o = align_up(o + max_work * 8, 256);
   e->o_last = o; o = align_up(o + R * 4, 256);
+  e->o_perm = o; o = align_up(o + R * 4, 256);
   e->o_sched = o;
   o = align_up(o + attn_sched_bytes(static_cast<int>(max_work * Hkv), kNumSMs, &e->o_sc_pieces,
                                     &e->o_sc_cta, &e->o_sc_comb, &e->o_sc_part), 256);
@@ -515,7 +521,14 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->o_copy = o; o = align_up(o + e->max_copies * 8, 256);
   e->meta_bytes = o;
   e->meta.reserve(o);
-  GLMX_CUDA(cudaMallocHost(&e->h_meta, o));
+  for (int i = 0; i < glmx_engine::kMetaRing; ++i) {
+    GLMX_CUDA(cudaMallocHost(&e->h_ring[i], o));
+    GLMX_CUDA(cudaEventCreateWithFlags(&e->ring_ev[i], cudaEventDisableTiming));
+  }
+  e->h_meta = e->h_ring[0];
+  GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_dec), (R * (cfg->max_decode + 1) + 16) * 4));
+  GLMX_CUDA(cudaEventCreateWithFlags(&e->dec_done, cudaEventDisableTiming));
+  e->dec_in.reserve(R * 4 + 64);
   e->h_out_stride = R * (cfg->max_decode + 1) + 16;
   GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_out), 2 * e->h_out_stride * 4));
   for (auto& ev : e->done_ev) GLMX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -534,6 +547,21 @@ int choose_decode_split(glmx_engine* e, int R, int T, const int32_t* ctx_len) {
   for (int r = 0; r < R; ++r) max_ctx = std::max(max_ctx, ctx_len[r]);
   return decode_attention_splits(R * static_cast<int>(c.n_kv_heads), max_ctx,
                                  2 * kNumSMs * attn_tc_partial_rows());
+}
+
+// Next pinned staging slot (waits until that slot's previous upload has been consumed).
+uint8_t* meta_acquire(glmx_engine* e) {
+  e->ring_slot = (e->ring_slot + 1) % glmx_engine::kMetaRing;
+  GLMX_CUDA(cudaEventSynchronize(e->ring_ev[e->ring_slot]));
+  e->h_meta = e->h_ring[e->ring_slot];
+  return static_cast<uint8_t*>(e->h_meta);
+}
+// Uploads the current slot to the device metadata buffer (stream-ordered after the previous
+// batch's kernels that read it).
+void meta_commit(glmx_engine* e, cudaStream_t s) {
+  GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
+  GLMX_CUDA(cudaEventRecord(e->ring_ev[e->ring_slot], s));
+  GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
 }
 
 // Packs the K3 stream-K schedule of the staged work list into the host metadata block.
@@ -687,15 +715,14 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   const uint32_t B = kv->cfg.block_tokens;
   if (n_req > e->cfg.max_requests) throw Error(GLMX_ERR_ARG, "too many requests in batch");
   DeviceGuard dg(m->device);
-  // The previous batch's host staging must have been consumed before it is rewritten; its
-  // scratch pages become free (device reuse is stream-ordered after its forward).
-  GLMX_CUDA(cudaEventSynchronize(e->h2d_done));
+  // The previous batch's scratch pages become free (device reuse is stream-ordered after its
+  // forward and decode steps); its staging slot stays untouched until its upload was consumed.
   for (auto& r : e->reqs)
     for (int32_t p : r.scratch) bk.pool().free_now(p);
   e->reqs.clear();
   e->has_batch = false;
 
-  uint8_t* hm = static_cast<uint8_t*>(e->h_meta);
+  uint8_t* hm = meta_acquire(e);
   int32_t* h_tok = reinterpret_cast<int32_t*>(hm + e->o_tok);
   int32_t* h_pos = reinterpret_cast<int32_t*>(hm + e->o_pos);
   int64_t* h_slot = reinterpret_cast<int64_t*>(hm + e->o_slot);
@@ -818,9 +845,8 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   cudaStream_t s = e->stream;
   {
     Prof p(e, kCatH2D);
-    GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
+    meta_commit(e, s);
   }
-  GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
   if (!e->copies.empty()) {
     Prof p(e, kCatOther);
     const int32_t* d_cp = reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_copy);
@@ -907,9 +933,14 @@ int engine_replay_impl(glmx_engine* e) {
 
 // Greedy decode.  Requests are re-ordered by step count (descending) so the active set of every
 // step is a row prefix and step s+1 consumes step s's argmax rows in place on the device.
-int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens, float* last_logits) {
+// engine_decode_enqueue stages and launches all steps of the staged batch without waiting for
+// the GPU (the prefill that produced the first tokens may still be in flight: the first-token
+// row order is a device gather); engine_decode_collect waits and returns the tokens.  The next
+// prefill may be staged in between (its staging uses the next pinned slots; the decode's pages
+// and device buffers are stream-ordered before it).
+int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
-  while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
+  if (e->dec_pending) throw Error(GLMX_ERR_ARG, "a decode is already enqueued: collect it first");
   glmx_model* m = e->m;
   const auto& c = m->cfg;
   const uint32_t B = e->kv->cfg.block_tokens;
@@ -919,28 +950,28 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
     if (steps[i] > e->cfg.max_decode) throw Error(GLMX_ERR_ARG, "steps exceed max_decode");
     max_steps = std::max(max_steps, steps[i]);
   }
-  for (int i = 0; i < R; ++i)
-    for (uint32_t s = 0; s < max_steps; ++s) out_tokens[static_cast<size_t>(i) * max_steps + s] = -1;
+  e->dec_steps.assign(steps, steps + R);
+  e->dec_max = max_steps;
+  e->dec_R = R;
+  e->dec_order.resize(R);
+  for (int i = 0; i < R; ++i) e->dec_order[i] = i;
+  std::stable_sort(e->dec_order.begin(), e->dec_order.end(),
+                   [&](int a, int b) { return steps[a] > steps[b]; });
+  e->dec_pending = true;
   if (max_steps == 0) return GLMX_OK;
   DeviceGuard dg(m->device);
-  std::vector<int> order(R);
-  for (int i = 0; i < R; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return steps[a] > steps[b]; });
   cudaStream_t s = e->stream;
-  GLMX_CUDA(cudaEventSynchronize(e->fwd_done));
-  // the prefill's greedy tokens, rows permuted into decode order
-  int32_t* d_prev = e->next_tok.as<int32_t>();
-  std::vector<int32_t> first(R);
-  GLMX_CUDA(cudaMemcpy(first.data(), d_prev, R * 4, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> toks(R);
-  for (int j = 0; j < R; ++j) toks[j] = first[order[j]];
-  int32_t* d_seq = d_prev + R;  // [max_steps][R] generated tokens
-  GLMX_CUDA(cudaMemcpy(d_prev, toks.data(), R * 4, cudaMemcpyHostToDevice));
-  uint8_t* hm = static_cast<uint8_t*>(e->h_meta);
+  const std::vector<int>& order = e->dec_order;
+  int32_t* d_first = e->next_tok.as<int32_t>();      // the prefill's greedy tokens, request rows
+  int32_t* d_seq = d_first + R;                      // [max_steps][R] generated tokens
+  int32_t* d_in = e->dec_in.as<int32_t>();           // step 0 input, decode row order
+  static constexpr uint64_t kDecTag = 1ull << 63;
+  e->dec_tag_batch = e->batch_seq;
+  e->prof_tag = kDecTag | e->batch_seq;
   for (uint32_t st = 0; st < max_steps; ++st) {
     int n = 0;
     while (n < R && steps[order[n]] > st) ++n;
-    GLMX_CUDA(cudaEventSynchronize(e->h2d_done));
+    uint8_t* hm = meta_acquire(e);
     int32_t* h_pos = reinterpret_cast<int32_t*>(hm + e->o_pos);
     int64_t* h_slot = reinterpret_cast<int64_t*>(hm + e->o_slot);
     int32_t* h_qs = reinterpret_cast<int32_t*>(hm + e->o_qs);
@@ -949,6 +980,7 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
     int32_t* h_bt = reinterpret_cast<int32_t*>(hm + e->o_bt);
     int2* h_work = reinterpret_cast<int2*>(hm + e->o_work);
     int32_t* h_last = reinterpret_cast<int32_t*>(hm + e->o_last);
+    int32_t* h_perm = reinterpret_cast<int32_t*>(hm + e->o_perm);
     for (int j = 0; j < n; ++j) {
       glmx_engine::Req& rq = e->reqs[order[j]];
       const int32_t p = rq.ctx_len;  // position of the token being fed
@@ -960,33 +992,60 @@ int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_token
       std::memcpy(h_bt + static_cast<size_t>(j) * e->bt_stride, rq.pages.data(), rq.pages.size() * 4);
       h_work[j] = make_int2(j, 0);
       h_last[j] = j;
+      h_perm[j] = order[j];
       rq.ctx_len = p + 1;
     }
     e->dec_split = choose_decode_split(e, n, n, h_ctx);
     if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
-    GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
-    GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
-    const int32_t* in_tok = st == 0 ? d_prev : d_seq + static_cast<size_t>(st - 1) * R;
+    meta_commit(e, s);
+    if (st == 0)
+      gather_i32(d_first, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_perm), R,
+                 d_in, s);
+    const int32_t* in_tok = st == 0 ? d_in : d_seq + static_cast<size_t>(st - 1) * R;
     forward(e, n, n, n, n, in_tok);
-    argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R, e->amax_keys.p, s);
+    argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R,
+                e->amax_keys.p, s);
   }
-  std::vector<int32_t> seq(static_cast<size_t>(max_steps) * R);
-  GLMX_CUDA(cudaMemcpyAsync(seq.data(), d_seq, seq.size() * 4, cudaMemcpyDeviceToHost, s));
-  GLMX_CUDA(cudaStreamSynchronize(s));
-  collect_profile(e);
+  e->prof_tag = 0;
+  GLMX_CUDA(cudaMemcpyAsync(e->h_dec, d_seq, static_cast<size_t>(max_steps) * R * 4,
+                            cudaMemcpyDeviceToHost, s));
+  GLMX_CUDA(cudaEventRecord(e->dec_done, s));
+  return GLMX_OK;
+}
+
+int engine_decode_collect(glmx_engine* e, int32_t* out_tokens, float* last_logits) {
+  if (!e->dec_pending) throw Error(GLMX_ERR_ARG, "no decode enqueued");
+  e->dec_pending = false;
+  const int R = e->dec_R;
+  const uint32_t max_steps = e->dec_max;
+  for (int i = 0; i < R; ++i)
+    for (uint32_t st = 0; st < max_steps; ++st) out_tokens[static_cast<size_t>(i) * max_steps + st] = -1;
+  if (max_steps == 0) return GLMX_OK;
+  DeviceGuard dg(e->m->device);
+  GLMX_CUDA(cudaEventSynchronize(e->dec_done));
+  collect_profile(e, (1ull << 63) | e->dec_tag_batch);
+  const std::vector<int>& order = e->dec_order;
   for (int j = 0; j < R; ++j)
-    for (uint32_t st = 0; st < steps[order[j]]; ++st)
-      out_tokens[static_cast<size_t>(order[j]) * max_steps + st] = seq[static_cast<size_t>(st) * R + j];
+    for (uint32_t st = 0; st < e->dec_steps[order[j]]; ++st)
+      out_tokens[static_cast<size_t>(order[j]) * max_steps + st] = e->h_dec[static_cast<size_t>(st) * R + j];
   if (last_logits) {
-    // logits of the final step for the requests still active in it (others untouched)
+    // logits of the final step for the requests still active in it (valid only while no later
+    // batch has run: the synchronous decode path)
+    const int V = static_cast<int>(e->m->cfg.vocab);
     int n = 0;
-    while (n < R && steps[order[n]] >= max_steps) ++n;
+    while (n < R && e->dec_steps[order[n]] >= max_steps) ++n;
     for (int j = 0; j < n; ++j)
-      GLMX_CUDA(cudaMemcpy(last_logits + static_cast<size_t>(order[j]) * c.vocab,
-                           e->logits.as<float>() + static_cast<size_t>(j) * c.vocab, c.vocab * 4,
+      GLMX_CUDA(cudaMemcpy(last_logits + static_cast<size_t>(order[j]) * V,
+                           e->logits.as<float>() + static_cast<size_t>(j) * V, V * 4,
                            cudaMemcpyDeviceToHost));
   }
   return GLMX_OK;
+}
+
+int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens, float* last_logits) {
+  while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
+  engine_decode_enqueue(e, steps);
+  return engine_decode_collect(e, out_tokens, last_logits);
 }
 
 // ======================================================================== K3 kernel-level hook

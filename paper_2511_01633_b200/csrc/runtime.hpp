@@ -110,10 +110,27 @@ struct glmx_engine {
   uint32_t kv_rows = 0;
 
   // activations
-  DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok, amax_keys;
+  DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok, amax_keys, dec_in;
   // batch metadata (device) + pinned host staging (single H2D)
   DBuf meta;
-  void* h_meta = nullptr;
+  void* h_meta = nullptr;  // the staging slot in use (one of h_ring)
+  // pinned staging ring: the host stages batch / decode-step metadata up to kMetaRing copies
+  // ahead of the GPU (slot reuse waits on the event of that slot's previous upload)
+  static constexpr int kMetaRing = 8;
+  void* h_ring[kMetaRing] = {};
+  cudaEvent_t ring_ev[kMetaRing] = {};
+  int ring_slot = 0;
+  // asynchronous decode: enqueued steps of the staged batch, collected by engine_decode_collect
+  bool dec_pending = false;
+  std::vector<int> dec_order;
+  std::vector<uint32_t> dec_steps;
+  uint32_t dec_max = 0;
+  int dec_R = 0;
+  int32_t* h_dec = nullptr;
+  cudaEvent_t dec_done = nullptr;
+  size_t o_perm = 0;  // meta: decode row order (first-token gather)
+  uint64_t prof_tag = 0;       // != 0: profiling spans tagged with this instead of batch_seq
+  uint64_t dec_tag_batch = 0;  // batch_seq when the pending decode was enqueued
   size_t meta_bytes = 0;
   int32_t* h_out = nullptr;  // pinned: tokens out
   cudaEvent_t h2d_done = nullptr, fwd_done = nullptr;

@@ -172,6 +172,21 @@ class Engine:
         toks = [[out[i * m + s] for s in range(steps[i])] for i in range(n)]
         return (toks, logits) if want_logits else toks
 
+    def decode_async(self, steps):
+        """Enqueue the greedy decode of the last staged batch (see decode); collect with
+        decode_collect().  The next prefill may be staged in between."""
+        self._dec_steps = list(steps)
+        st = (C.c_uint32 * max(1, len(steps)))(*steps)
+        check(lib().glmx_engine_decode_async(self.h, st))
+
+    def decode_collect(self):
+        steps = self._dec_steps
+        n = len(steps)
+        m = max(steps) if steps else 0
+        out = (C.c_int32 * max(1, n * m))()
+        check(lib().glmx_engine_decode_collect(self.h, out))
+        return [[out[i * m + s] for s in range(steps[i])] for i in range(n)]
+
     def replay_forward(self):
         check(lib().glmx_engine_replay_forward(self.h))
 

@@ -299,11 +299,55 @@ class GraphCoTWorkload:
         finally:
             if th is not None:
                 th.join()
+        self.last_prefill_forward_ms = self.engine.last_timings()["forward"]
         if any(steps):
             self.engine.decode(steps)
         res = self.advance(calls, reps, first, chunks=built.get("b") if acting else None)
         res.decoded_tokens = sum(steps)
         return res
+
+    def rotations_with_decode(self, count, max_decode):
+        """`count` rotations of rotation_with_decode, pipelined on one engine stream: the GPU
+        runs prefill r, decode r, prefill r+1, decode r+1, ... back to back while the host
+        advances the state machines with r's (scripted) replies and stages rotation r+1's prefill
+        (bookkeeping, staging, RetrieveNode/K1) before r's decode has finished
+        (glmx_engine_decode_async / _collect; the engine stages decode steps and prefills in a
+        ring of pinned slots).  Cache decisions and tokens are those of the sequential loop.
+        Yields each rotation's RotationResult after its decode completed; engine.last_timings()
+        then holds the decode and self.last_prefill_forward_ms the prefill."""
+        if count <= 0:
+            return
+
+        def steps_of(calls):
+            return [max(0, min(max_decode, count_tokens(c.reply) - 1)) for c in calls]
+
+        calls = self.next_calls()
+        th, built = self._start_retrieval(calls) if self.overlap_retrieval else (None, {})
+        reps = self.prefill_async(calls)
+        steps = steps_of(calls)
+        if any(steps):
+            self.engine.decode_async(steps)
+        for r in range(count):
+            if th is not None:
+                th.join()
+            acting = [c for c in calls if c.agent == "action"]
+            res = self.advance(calls, reps, None, chunks=built.get("b") if acting else None)
+            res.decoded_tokens = sum(steps)
+            nxt = None
+            if r + 1 < count:
+                calls_n = self.next_calls()
+                th_n, built_n = (self._start_retrieval(calls_n) if self.overlap_retrieval
+                                 else (None, {}))
+                nxt = (calls_n, th_n, built_n, self.prefill_async(calls_n), steps_of(calls_n))
+            res.first_tokens = self.wait(len(calls))
+            self.last_prefill_forward_ms = self.engine.last_timings()["forward"]
+            if any(steps):
+                self.engine.decode_collect()
+            yield res
+            if nxt is not None:
+                calls, th, built, reps, steps = nxt
+                if any(steps):
+                    self.engine.decode_async(steps)
 
     def rotation(self) -> RotationResult:
         """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on

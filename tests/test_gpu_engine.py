@@ -161,6 +161,36 @@ def test_pipelined_rotations_match_sequential():
     assert out[0] == out[1]
 
 
+def test_overlapped_decode_rotations_match_sequential():
+    """Graph-CoT rotations with reply decode, overlapped (rotation r+1's host work under r's decode
+    steps in a second thread) == the sequential rotation_with_decode loop: reports, first tokens,
+    decoded counts, cache counters and snapshot."""
+    from paper_2511_01633_b200.workload import GraphCoTWorkload
+
+    cfg = glmx.TINY
+    g = glmx.PropertyGraph.synth_powerlaw(3000, 6, seed=4, device=0)
+    out = []
+    for mode in ("seq", "overlap"):
+        model = glmx.Model(cfg, device=0)
+        kv = glmx.KvCacheState(256, 16, glmx.PRIORITY, device=0, n_layers=cfg.n_layers,
+                               n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
+                               headroom_pages=512)
+        eng = glmx.Engine(model, kv, max_requests=16, max_batch_tokens=16 * 1024, max_decode=8,
+                          max_context=4096)
+        ret = glmx.Retriever(g, chunk_k=8, vocab=cfg.vocab)
+        wl = GraphCoTWorkload(eng, ret, n_queries=40, lanes=16, seed=5, question_pool=20,
+                              node_index=glmx.NodeIndex(g))
+        rows = []
+        it = ((wl.rotation_with_decode(8) for _ in range(12)) if mode == "seq"
+              else wl.rotations_with_decode(12, 8))
+        for r in it:
+            rows.append(([(x.cached_tokens, x.computed_tokens, x.tail_tokens) for x in r.reports],
+                         r.first_tokens, r.finished, r.decoded_tokens))
+        out.append((rows, kv.counters(), kv.snapshot_json()))
+    assert out[0] == out[1]
+    assert sum(r[3] for r in out[0][0]) > 0
+
+
 def test_c3_shaped_run_bookkeeping_matches_reference():
     """C3 in miniature: 96 concurrent Graph-CoT queries on a 96-block pool with four-tier
     priority eviction (pipelined rotations, RetrieveNode, K1); every prefill and set_tier replayed
