@@ -219,13 +219,12 @@ rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t*
   const int pass_lo = blockIdx.y * kPassU, pass_hi = min((heads + kHeadsPerPass - 1) / kHeadsPerPass,
                                                         pass_lo + kPassU);
   if (pass_lo >= pass_hi) return;
-  const float p = static_cast<float>(pos[t]);
-  float cs[8], sn[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) sincosf(p * inv_freq[c * 8 + j], &sn[j], &cs[j]);
   const int64_t sl = slot[t];
   const __nv_bfloat16* row = qkv + static_cast<int64_t>(t) * heads * kHd + c * 8;
-  for (int p0 = pass_lo; p0 < pass_hi; p0 += kPassU) {
+  // the grid's y dimension covers kPassU passes per warp: one group, loads issued before the
+  // cos/sin of the rotation pairs are computed (V-only groups skip them)
+  const int p0 = pass_lo;
+  {
     uint4 av[kPassU], bv[kPassU];
 #pragma unroll
     for (int i = 0; i < kPassU; ++i) {
@@ -234,6 +233,12 @@ rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t*
         av[i] = __ldcs(reinterpret_cast<const uint4*>(row + h * kHd));
         bv[i] = __ldcs(reinterpret_cast<const uint4*>(row + h * kHd + kHalf));
       }
+    }
+    float cs[8], sn[8];
+    if (p0 * kHeadsPerPass < H + Hkv) {
+      const float p = static_cast<float>(pos[t]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sincosf(p * inv_freq[c * 8 + j], &sn[j], &cs[j]);
     }
 #pragma unroll
     for (int i = 0; i < kPassU; ++i) {
