@@ -439,9 +439,10 @@ def main():
                 dq_dec_ms += eng.last_timings()["forward"]
             dq_pre_ms += getattr(wl, "last_prefill_forward_ms", 0.0)
 
-        if px is None and pipelined:
-            # rotation r+1's host work (advance, calls, RetrieveNode/K1) under r's decode steps
-            for rr in wl.rotations_with_decode(args.decode_steps, 8):
+        if pipelined:
+            # rotation r+1's host work (advance, calls, RetrieveNode/K1) under r's decode steps;
+            # with peer exchange the directory follows the pipelined epoch protocol
+            for rr in wl.rotations_with_decode(args.decode_steps, 8, peer=px):
                 account(rr)
         else:
             for _ in range(args.decode_steps):

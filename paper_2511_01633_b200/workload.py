@@ -306,7 +306,7 @@ class GraphCoTWorkload:
         res.decoded_tokens = sum(steps)
         return res
 
-    def rotations_with_decode(self, count, max_decode):
+    def rotations_with_decode(self, count, max_decode, peer=None):
         """`count` rotations of rotation_with_decode, pipelined on one engine stream: the GPU
         runs prefill r, decode r, prefill r+1, decode r+1, ... back to back while the host
         advances the state machines with r's (scripted) replies and stages rotation r+1's prefill
@@ -314,7 +314,9 @@ class GraphCoTWorkload:
         (glmx_engine_decode_async / _collect; the engine stages decode steps and prefills in a
         ring of pinned slots).  Cache decisions and tokens are those of the sequential loop.
         Yields each rotation's RotationResult after its decode completed; engine.last_timings()
-        then holds the decode and self.last_prefill_forward_ms the prefill."""
+        then holds the decode and self.last_prefill_forward_ms the prefill.
+
+        peer: a sharding.PeerExchange running the pipelined epoch protocol (as in rotations())."""
         if count <= 0:
             return
 
@@ -323,6 +325,8 @@ class GraphCoTWorkload:
 
         calls = self.next_calls()
         th, built = self._start_retrieval(calls) if self.overlap_retrieval else (None, {})
+        if peer is not None:
+            peer.before_bookkeeping()
         reps = self.prefill_async(calls)
         steps = steps_of(calls)
         if any(steps):
@@ -338,8 +342,12 @@ class GraphCoTWorkload:
                 calls_n = self.next_calls()
                 th_n, built_n = (self._start_retrieval(calls_n) if self.overlap_retrieval
                                  else (None, {}))
+                if peer is not None:
+                    peer.before_bookkeeping()
                 nxt = (calls_n, th_n, built_n, self.prefill_async(calls_n), steps_of(calls_n))
             res.first_tokens = self.wait(len(calls))
+            if peer is not None:
+                peer.after_wait()
             self.last_prefill_forward_ms = self.engine.last_timings()["forward"]
             if any(steps):
                 self.engine.decode_collect()

@@ -29,6 +29,24 @@ perm = list(range(nb * pp))
 random.Random(0).shuffle(perm)
 bt = [perm[i * pp:(i + 1) * pp] for i in range(nb)]
 args = (q, o, pool, [i * s for i in range(nb)], [s] * nb, [ctx] * nb, bt)
+if os.environ.get("GLMX_TRACE_SHAPES"):  # "file.json:index": one ragged batch [[ctx, q_len], ...]
+    import json
+    fn, idx = os.environ["GLMX_TRACE_SHAPES"].rsplit(":", 1)
+    reqs = json.load(open(fn))[int(idx)]
+    pages = [(c + B - 1) // B for c, _ in reqs]
+    pool = torch.randn((sum(pages), 1, 2, Hkv, B, hd), device="cuda").to(torch.bfloat16)
+    rows = sum(n for _, n in reqs)
+    q = torch.randn((rows, H, hd), device="cuda").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    perm = list(range(sum(pages)))
+    random.Random(0).shuffle(perm)
+    bt, qs, p0, r0 = [], [], 0, 0
+    for (c, n), k in zip(reqs, pages):
+        bt.append(perm[p0:p0 + k])
+        qs.append(r0)
+        p0 += k
+        r0 += n
+    args = (q, o, pool, qs, [n for _, n in reqs], [c for c, _ in reqs], bt)
 A.paged_attention(*args, reps=2)
 buf = (C.c_int64 * (16 * 1024))()
 lib().glmx_attn_trace_read(buf, 16 * 1024)  # clear

@@ -32,7 +32,7 @@ ret = glmx.Retriever(g, chunk_k=16, vocab=cfg.vocab)
 model = glmx.Model(cfg, dev)
 
 
-def run(pipelined):
+def run(pipelined, decode=False):
     kv = glmx.KvCacheState(CAP, 16, glmx.PRIORITY, device=dev, n_layers=cfg.n_layers,
                            n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim, headroom_pages=1024)
     eng = glmx.Engine(model, kv, max_requests=16, max_batch_tokens=16 * 1024, max_decode=4,
@@ -42,13 +42,14 @@ def run(pipelined):
     px = PeerExchange(kv)
     firsts, peer = [], []
     if pipelined:
-        for r in wl.rotations(ROT, peer=px):
+        it = wl.rotations_with_decode(ROT, 4, peer=px) if decode else wl.rotations(ROT, peer=px)
+        for r in it:
             firsts += r.first_tokens
             peer.append(kv.peer_hits())
     else:
         for _ in range(ROT):
             px.epoch_begin()
-            r = wl.rotation()
+            r = wl.rotation_with_decode(4) if decode else wl.rotation()
             px.epoch_end()
             firsts += r.first_tokens
             peer.append(kv.peer_hits())
@@ -61,12 +62,11 @@ def run(pipelined):
     return out
 
 
-seq = run(False)
-pip = run(True)
+results = [(run(False), run(True)), (run(False, decode=True), run(True, decode=True))]
 res = [None] * world
-dist.all_gather_object(res, (seq, pip))
+dist.all_gather_object(res, results)
 if rank == 0:
-    for q, (s, p) in enumerate(res):
+    for q, (s, p) in [(q, sp) for q, rr in enumerate(res) for sp in rr]:
         assert s[0] == p[0], (q, s[0], p[0])
         if CAP <= 224:
             assert sum(s[0]["evictions_by_tier"]) > 0, s[0]
