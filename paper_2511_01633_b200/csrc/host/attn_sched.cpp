@@ -102,10 +102,16 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     // Enough items to occupy the SMs: whole items, longest first, each to the least-loaded of
     // min(units, n_sm) persistent CTAs (LPT; equal items reduce to round-robin).  A unit is a
     // two-tile item, or two single-tile items of similar length paired into one piece.
-    std::vector<int> single, twin;
+    // Pairs are formed only from short single-tile items (<= kPairMaxTiles key tiles): there the
+    // per-tile softmax -> PV -> S chain is latency-bound; a pair of long items streams two K/V
+    // sequences per CTA and hits the L2 throughput limit that one shared stream avoids.
+    constexpr int kPairMaxTiles = 16;
+    std::vector<int> single, twin, lone;
     for (int w = 0; w < n_items; ++w) {
       const int r = work_xy[2 * (w / Hkv)], t0 = work_xy[2 * (w / Hkv) + 1];
-      (!s.partners || q_len[r] - t0 > tokens_per_item / 2 ? twin : single).push_back(w);
+      if (!s.partners || q_len[r] - t0 > tokens_per_item / 2) twin.push_back(w);
+      else if (tiles[w] <= kPairMaxTiles) single.push_back(w);
+      else lone.push_back(w);
     }
     auto longer = [&](int a, int b) { return tiles[a] > tiles[b]; };
     std::stable_sort(single.begin(), single.end(), longer);
@@ -114,6 +120,7 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     // runs its softmax/MMA chain unoverlapped at ~3/4 of a full step; a pair costs a full step.
     std::vector<char> is_single(n_items, 0);
     for (int w : single) is_single[w] = 1;
+    for (int w : lone) is_single[w] = 1;
     auto cost = [&](const Unit& u) -> int64_t {
       if (u.second >= 0) return 4 * std::max(tiles[u.first], tiles[u.second]);
       return (is_single[u.first] ? 3 : 4) * static_cast<int64_t>(tiles[u.first]);
@@ -128,6 +135,7 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     auto lpt = [&](size_t n_pair) {
       std::vector<Unit> units;
       for (int w : twin) units.push_back({w, -1});
+      for (int w : lone) units.push_back({w, -1});
       const size_t n_alone = single.size() - n_pair;
       for (size_t i = 0; i < n_alone; ++i) units.push_back({single[i], -1});
       for (size_t i = n_alone; i < single.size(); i += 2)
@@ -153,9 +161,9 @@ void build_attn_schedule(const int32_t* work_xy, int n_work, int Hkv, const int3
     };
     Plan plan = lpt(0);
     if (single.size() >= 2) {
-      for (int f = 4; f >= 1; --f) {  // all, 3/4, 1/2, 1/4 of them paired (even counts)
+      for (int f = 1; f <= 4; ++f) {  // 1/4, 1/2, 3/4, all of them paired (even counts)
         Plan pp = lpt(single.size() * f / 4 & ~size_t(1));
-        if (pp.makespan <= plan.makespan) plan = std::move(pp);
+        if (pp.makespan < plan.makespan) plan = std::move(pp);  // ties: fewer pairs
       }
     }
     const int grid = static_cast<int>(plan.mine.size());
