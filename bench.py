@@ -548,7 +548,7 @@ def main():
     value = tokens / (fwd_ms * 1e-3)
     e2e = tokens / (wall_ms * 1e-3)
     n_layers = cfg.n_layers
-    launches_per_fwd = 1 + 5 * n_layers + 2
+    launches_per_fwd = 1 + 5 * n_layers + 3  # embed, 5 per layer, final norm + split argmax (2)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
