@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--routing", default="mod", choices=["mod", "affinity"],
                    help="query -> GPU: i mod N (reference sharding) or prefix affinity "
                         "(fnv1a(question) mod N: repeated questions stay on one GPU)")
+    p.add_argument("--decode-merge", action="store_true",
+                   help="batch two rotations' decode rows into one decode (continuous batching); "
+                        "measured slower on this workload: the long contexts make decode KV-bound")
     p.add_argument("--no-standalone", action="store_true",
                    help="skip the standalone K1 / K3 measurements reported beside the in-step ones")
     p.add_argument("--no-pipeline", action="store_true",
@@ -422,6 +425,7 @@ def main():
     # last staged batch)
     dq_fin = dq_dec = 0
     dq_ms = dq_dec_ms = dq_pre_ms = 0.0
+    dq_n_dec = [0]
     if args.decode_steps > 0:
         if ws > 1:
             dist.barrier()
@@ -435,14 +439,16 @@ def main():
             nonlocal dq_fin, dq_dec, dq_dec_ms, dq_pre_ms
             dq_fin += rr.finished
             dq_dec += rr.decoded_tokens
-            if rr.decoded_tokens:  # device time of this rotation's decode forwards
+            if rr.decoded_tokens and rr.decode_collected:  # device time of the decode forwards
                 dq_dec_ms += eng.last_timings()["forward"]
+            dq_n_dec[0] += 1 if rr.decode_collected else 0
             dq_pre_ms += getattr(wl, "last_prefill_forward_ms", 0.0)
 
         if pipelined:
             # rotation r+1's host work (advance, calls, RetrieveNode/K1) under r's decode steps;
             # with peer exchange the directory follows the pipelined epoch protocol
-            for rr in wl.rotations_with_decode(args.decode_steps, 8, peer=px):
+            for rr in wl.rotations_with_decode(args.decode_steps, 8, peer=px,
+                                               merge=args.decode_merge):
                 account(rr)
         else:
             for _ in range(args.decode_steps):
@@ -571,6 +577,7 @@ def main():
             {"value": dq_fin / (dq_ms * 1e-3), "unit": "queries/s", "rotations": args.decode_steps,
              "queries_finished": dq_fin, "decoded_tokens": dq_dec, "ms": dq_ms,
              "decode_forward_ms": dq_dec_ms, "prefill_forward_ms": dq_pre_ms,
+             "decode_launches": dq_n_dec[0],
              "step": "prefill + greedy reply decode per call (call_llm), CUDA events, max over ranks",
              "n_gpus": ws}
             if dq_ms > 0 else None),

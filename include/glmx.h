@@ -304,9 +304,13 @@ int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_token
                        float* last_logits);
 /* The same decode split in two: _async stages and launches every step of the last staged batch
  * without waiting for the GPU (a prefill may still be in flight; the next prefill may be staged
- * before the collect), _collect waits and writes out_tokens [n_req][max_steps] as above. */
+ * before the collect), _collect waits and writes out_tokens [n_req][max_steps] as above.
+ * Continuous batching across rotations: _defer(steps) sets the staged batch's decode aside (its
+ * pages are kept); the next batch's _async then runs both sets of rows in one decode (one weight
+ * stream per step) and _collect also writes out_prev [deferred n_req][max_steps]. */
 int glmx_engine_decode_async(glmx_engine* e, const uint32_t* steps);
-int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens);
+int glmx_engine_decode_defer(glmx_engine* e, const uint32_t* steps);
+int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out_prev);
 /* Re-run the device forward of the last prefill batch (inputs already resident in HBM) —
  * used to time the device part alone; KV writes are idempotent. */
 int glmx_engine_replay_forward(glmx_engine* e);

@@ -145,7 +145,8 @@ _SIGS = {
     "glmx_engine_in_flight": (C.c_int32, [C.c_void_p]),
     "glmx_engine_decode": (C.c_int, [C.c_void_p, u32p, i32p, f32p]),
     "glmx_engine_decode_async": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
-    "glmx_engine_decode_collect": (C.c_int, [C.c_void_p, i32p]),
+    "glmx_engine_decode_collect": (C.c_int, [C.c_void_p, i32p, i32p]),
+    "glmx_engine_decode_defer": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
     "glmx_engine_replay_forward": (C.c_int, [C.c_void_p]),
     "glmx_engine_last_timings": (C.c_int, [C.c_void_p, f32p]),
     "glmx_engine_last_work": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),

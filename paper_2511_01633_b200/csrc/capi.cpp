@@ -27,7 +27,8 @@ int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefil
 int engine_wait_impl(glmx_engine*, int32_t*, uint64_t);
 int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_decode_enqueue(glmx_engine*, const uint32_t*);
-int engine_decode_collect(glmx_engine*, int32_t*, float*);
+int engine_decode_collect(glmx_engine*, int32_t*, int32_t*, float*);
+int engine_decode_defer(glmx_engine*, const uint32_t*);
 int engine_replay_impl(glmx_engine*);
 int index_build_impl(glmx_graph*, int, uint64_t);
 int kv_gather_run_impl(void*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
@@ -549,8 +550,11 @@ int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_token
 int glmx_engine_decode_async(glmx_engine* e, const uint32_t* steps) {
   return guarded([&] { return engine_decode_enqueue(e, steps); });
 }
-int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens) {
-  return guarded([&] { return engine_decode_collect(e, out_tokens, nullptr); });
+int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out_prev) {
+  return guarded([&] { return engine_decode_collect(e, out_tokens, out_prev, nullptr); });
+}
+int glmx_engine_decode_defer(glmx_engine* e, const uint32_t* steps) {
+  return guarded([&] { return engine_decode_defer(e, steps); });
 }
 int glmx_engine_replay_forward(glmx_engine* e) {
   return guarded([&] { return engine_replay_impl(e); });

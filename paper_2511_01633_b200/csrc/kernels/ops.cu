@@ -496,6 +496,22 @@ __global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int32_t
   if (i < n) dst[i] = src[idx[i]];
 }
 
+__global__ void gather2_i32_kernel(const int32_t* __restrict__ a, int na, const int32_t* __restrict__ b,
+                                   const int32_t* __restrict__ idx, int n, int32_t* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int k = idx[i];
+    dst[i] = k < na ? a[k] : b[k - na];
+  }
+}
+
+void gather2_i32(const int32_t* a, int na, const int32_t* b, const int32_t* idx, int n, int32_t* dst,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  gather2_i32_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(a, na, b, idx, n, dst);
+  GLMX_CHECK_LAUNCH();
+}
+
 void gather_i32(const int32_t* src, const int32_t* idx, int n, int32_t* dst, cudaStream_t s) {
   if (n <= 0) return;
   gather_i32_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(src, idx, n, dst);

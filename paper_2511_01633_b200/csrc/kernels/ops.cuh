@@ -39,6 +39,9 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
 void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStream_t s);
 // dst[i] = src[idx[i]] (decode: first tokens into decode row order)
 void gather_i32(const int32_t* src, const int32_t* idx, int n, int32_t* dst, cudaStream_t s);
+// dst[i] = idx[i] < na ? a[idx[i]] : b[idx[i] - na] (a merged decode's two first-token sets)
+void gather2_i32(const int32_t* a, int na, const int32_t* b, const int32_t* idx, int n, int32_t* dst,
+                 cudaStream_t s);
 // keys: n x 8 bytes of device scratch (split over CTAs), or nullptr (one CTA per row)
 void argmax_rows(const float* logits, int n, int V, int32_t* out, void* keys, cudaStream_t s);
 // K4: copy whole pages (all layers) pool_src[src[i]] -> pool_dst[dst[i]]; peer pointers allowed.

@@ -471,8 +471,9 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   GLMX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   GLMX_CUDA(cudaEventCreateWithFlags(&e->h2d_done, cudaEventDisableTiming));
   GLMX_CUDA(cudaEventCreateWithFlags(&e->fwd_done, cudaEventDisableTiming));
-  const uint64_t T = std::max<uint32_t>(cfg->max_batch_tokens, cfg->max_requests);
-  const uint64_t R = cfg->max_requests;
+  // decode steps may merge two batches' rows (deferred decode): row buffers hold 2 x max_requests
+  const uint64_t T = std::max<uint32_t>(cfg->max_batch_tokens, 2 * cfg->max_requests);
+  const uint64_t R = 2ull * cfg->max_requests;
   const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
   const uint32_t B = kv->cfg.block_tokens;
   // block-table rows padded to a multiple of 8 pages: K3 reads a key tile's 8 entries with two
@@ -529,6 +530,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_dec), (R * (cfg->max_decode + 1) + 16) * 4));
   GLMX_CUDA(cudaEventCreateWithFlags(&e->dec_done, cudaEventDisableTiming));
   e->dec_in.reserve(R * 4 + 64);
+  e->def_first.reserve(R * 4 + 64);
   e->h_out_stride = R * (cfg->max_decode + 1) + 16;
   GLMX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->h_out), 2 * e->h_out_stride * 4));
   for (auto& ev : e->done_ev) GLMX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -938,39 +940,77 @@ int engine_replay_impl(glmx_engine* e) {
 // row order is a device gather); engine_decode_collect waits and returns the tokens.  The next
 // prefill may be staged in between (its staging uses the next pinned slots; the decode's pages
 // and device buffers are stream-ordered before it).
+// Defers the decode of the staged batch so it runs merged with the next batch's decode (one
+// weight stream per step for both sets of rows): the batch's requests keep their pages (the next
+// prefill's staging will not free them) and its first tokens are copied aside on the stream.
+int engine_decode_defer(glmx_engine* e, const uint32_t* steps) {
+  if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
+  if (e->def_R) throw Error(GLMX_ERR_ARG, "a decode is already deferred");
+  if (e->dec_pending) throw Error(GLMX_ERR_ARG, "a decode is already enqueued: collect it first");
+  const int R = e->last_R;
+  for (int i = 0; i < R; ++i)
+    if (steps[i] > e->cfg.max_decode) throw Error(GLMX_ERR_ARG, "steps exceed max_decode");
+  DeviceGuard dg(e->m->device);
+  e->def_reqs = std::move(e->reqs);
+  e->reqs.clear();
+  e->def_steps.assign(steps, steps + R);
+  e->def_R = R;
+  e->has_batch = false;
+  GLMX_CUDA(cudaMemcpyAsync(e->def_first.p, e->next_tok.p, static_cast<size_t>(R) * 4,
+                            cudaMemcpyDeviceToDevice, e->stream));
+  return GLMX_OK;
+}
+
+// Greedy decode.  Rows (the deferred batch's first, then the staged batch's) are re-ordered by
+// step count (descending) so the active set of every step is a row prefix and step s+1 consumes
+// step s's argmax rows in place on the device.  engine_decode_enqueue stages and launches all
+// steps without waiting for the GPU (the prefill that produced the first tokens may still be in
+// flight: the first-token row order is a device gather); engine_decode_collect waits and returns
+// the tokens.  The next prefill may be staged in between (its staging uses the next pinned
+// slots; the decode's pages and device buffers are stream-ordered before it).
 int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
   if (e->dec_pending) throw Error(GLMX_ERR_ARG, "a decode is already enqueued: collect it first");
   glmx_model* m = e->m;
   const auto& c = m->cfg;
   const uint32_t B = e->kv->cfg.block_tokens;
-  const int R = e->last_R;
+  const int Rc = e->last_R, Rd = e->def_R, R = Rc + Rd;
   uint32_t max_steps = 0;
-  for (int i = 0; i < R; ++i) {
+  e->dec_steps.assign(e->def_steps.begin(), e->def_steps.begin() + Rd);
+  for (int i = 0; i < Rc; ++i) {
     if (steps[i] > e->cfg.max_decode) throw Error(GLMX_ERR_ARG, "steps exceed max_decode");
-    max_steps = std::max(max_steps, steps[i]);
+    e->dec_steps.push_back(steps[i]);
   }
-  e->dec_steps.assign(steps, steps + R);
+  for (uint32_t st : e->dec_steps) max_steps = std::max(max_steps, st);
   e->dec_max = max_steps;
   e->dec_R = R;
+  e->dec_R_def = Rd;
   e->dec_order.resize(R);
   for (int i = 0; i < R; ++i) e->dec_order[i] = i;
+  const std::vector<uint32_t>& all_steps = e->dec_steps;
   std::stable_sort(e->dec_order.begin(), e->dec_order.end(),
-                   [&](int a, int b) { return steps[a] > steps[b]; });
+                   [&](int a, int b) { return all_steps[a] > all_steps[b]; });
   e->dec_pending = true;
+  // the deferred requests' scratch pages are freed at the collect (after their last step)
+  e->dec_free = std::move(e->def_reqs);
+  std::vector<glmx_engine::Req>& dreqs = e->dec_free;
+  // row i < Rd: deferred request i; else staged request i - Rd
+  auto row_req = [&](int i) -> glmx_engine::Req& { return i < Rd ? dreqs[i] : e->reqs[i - Rd]; };
+  e->def_R = 0;
+  e->def_reqs.clear();
+  e->def_steps.clear();
   if (max_steps == 0) return GLMX_OK;
   DeviceGuard dg(m->device);
   cudaStream_t s = e->stream;
   const std::vector<int>& order = e->dec_order;
-  int32_t* d_first = e->next_tok.as<int32_t>();      // the prefill's greedy tokens, request rows
-  int32_t* d_seq = d_first + R;                      // [max_steps][R] generated tokens
-  int32_t* d_in = e->dec_in.as<int32_t>();           // step 0 input, decode row order
+  int32_t* d_seq = e->next_tok.as<int32_t>() + R;  // [max_steps][R] generated tokens
+  int32_t* d_in = e->dec_in.as<int32_t>();         // step 0 input, decode row order
   static constexpr uint64_t kDecTag = 1ull << 63;
   e->dec_tag_batch = e->batch_seq;
   e->prof_tag = kDecTag | e->batch_seq;
   for (uint32_t st = 0; st < max_steps; ++st) {
     int n = 0;
-    while (n < R && steps[order[n]] > st) ++n;
+    while (n < R && all_steps[order[n]] > st) ++n;
     uint8_t* hm = meta_acquire(e);
     int32_t* h_pos = reinterpret_cast<int32_t*>(hm + e->o_pos);
     int64_t* h_slot = reinterpret_cast<int64_t*>(hm + e->o_slot);
@@ -982,7 +1022,7 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
     int32_t* h_last = reinterpret_cast<int32_t*>(hm + e->o_last);
     int32_t* h_perm = reinterpret_cast<int32_t*>(hm + e->o_perm);
     for (int j = 0; j < n; ++j) {
-      glmx_engine::Req& rq = e->reqs[order[j]];
+      glmx_engine::Req& rq = row_req(order[j]);
       const int32_t p = rq.ctx_len;  // position of the token being fed
       h_pos[j] = p;
       h_slot[j] = static_cast<int64_t>(rq.pages[p / B]) * B + (p % B);
@@ -999,8 +1039,8 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
     if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
     meta_commit(e, s);
     if (st == 0)
-      gather_i32(d_first, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_perm), R,
-                 d_in, s);
+      gather2_i32(e->def_first.as<int32_t>(), Rd, e->next_tok.as<int32_t>(),
+                  reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_perm), R, d_in, s);
     const int32_t* in_tok = st == 0 ? d_in : d_seq + static_cast<size_t>(st - 1) * R;
     forward(e, n, n, n, n, in_tok);
     argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R,
@@ -1013,39 +1053,57 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   return GLMX_OK;
 }
 
-int engine_decode_collect(glmx_engine* e, int32_t* out_tokens, float* last_logits) {
+// out_tokens [staged rows][max_steps]; out_prev (nullable) [deferred rows][max_steps] for the
+// rows of a batch whose decode was deferred into this one.
+int engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out_prev, float* last_logits) {
   if (!e->dec_pending) throw Error(GLMX_ERR_ARG, "no decode enqueued");
   e->dec_pending = false;
-  const int R = e->dec_R;
+  const int R = e->dec_R, Rd = e->dec_R_def;
   const uint32_t max_steps = e->dec_max;
-  for (int i = 0; i < R; ++i)
-    for (uint32_t st = 0; st < max_steps; ++st) out_tokens[static_cast<size_t>(i) * max_steps + st] = -1;
-  if (max_steps == 0) return GLMX_OK;
   DeviceGuard dg(e->m->device);
-  GLMX_CUDA(cudaEventSynchronize(e->dec_done));
-  collect_profile(e, (1ull << 63) | e->dec_tag_batch);
+  if (max_steps > 0) {
+    GLMX_CUDA(cudaEventSynchronize(e->dec_done));
+    collect_profile(e, (1ull << 63) | e->dec_tag_batch);
+  }
+  for (auto& rq : e->dec_free)
+    for (int32_t pg : rq.scratch) e->kv->bk->pool().free_now(pg);
+  e->dec_free.clear();
+  for (int i = 0; i < R; ++i) {
+    int32_t* dst = i < Rd ? out_prev : out_tokens;
+    if (!dst) continue;
+    const int row = i < Rd ? i : i - Rd;
+    for (uint32_t st = 0; st < max_steps; ++st) dst[static_cast<size_t>(row) * max_steps + st] = -1;
+  }
+  if (max_steps == 0) return GLMX_OK;
   const std::vector<int>& order = e->dec_order;
-  for (int j = 0; j < R; ++j)
-    for (uint32_t st = 0; st < e->dec_steps[order[j]]; ++st)
-      out_tokens[static_cast<size_t>(order[j]) * max_steps + st] = e->h_dec[static_cast<size_t>(st) * R + j];
+  for (int j = 0; j < R; ++j) {
+    const int i = order[j];
+    int32_t* dst = i < Rd ? out_prev : out_tokens;
+    if (!dst) continue;
+    const int row = i < Rd ? i : i - Rd;
+    for (uint32_t st = 0; st < e->dec_steps[i]; ++st)
+      dst[static_cast<size_t>(row) * max_steps + st] = e->h_dec[static_cast<size_t>(st) * R + j];
+  }
   if (last_logits) {
-    // logits of the final step for the requests still active in it (valid only while no later
-    // batch has run: the synchronous decode path)
+    // logits of the final step for the staged requests still active in it (synchronous path)
     const int V = static_cast<int>(e->m->cfg.vocab);
     int n = 0;
     while (n < R && e->dec_steps[order[n]] >= max_steps) ++n;
-    for (int j = 0; j < n; ++j)
-      GLMX_CUDA(cudaMemcpy(last_logits + static_cast<size_t>(order[j]) * V,
+    for (int j = 0; j < n; ++j) {
+      if (order[j] < Rd) continue;
+      GLMX_CUDA(cudaMemcpy(last_logits + static_cast<size_t>(order[j] - Rd) * V,
                            e->logits.as<float>() + static_cast<size_t>(j) * V, V * 4,
                            cudaMemcpyDeviceToHost));
+    }
   }
   return GLMX_OK;
 }
 
 int engine_decode_impl(glmx_engine* e, const uint32_t* steps, int32_t* out_tokens, float* last_logits) {
   while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
+  if (e->def_R) throw Error(GLMX_ERR_ARG, "a decode is deferred: use the async decode to merge it");
   engine_decode_enqueue(e, steps);
-  return engine_decode_collect(e, out_tokens, last_logits);
+  return engine_decode_collect(e, out_tokens, nullptr, last_logits);
 }
 
 // ======================================================================== K3 kernel-level hook

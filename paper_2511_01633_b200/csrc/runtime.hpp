@@ -142,6 +142,14 @@ struct glmx_engine {
     std::vector<int32_t> scratch;
   };
   std::vector<Req> reqs;
+  // a batch whose decode is deferred to run merged with the next batch's decode (continuous
+  // batching of decode rows across rotations): its requests (pages kept), steps, first tokens
+  std::vector<Req> def_reqs;
+  std::vector<uint32_t> def_steps;
+  DBuf def_first;
+  int def_R = 0;            // rows of the deferred batch (0: none)
+  int dec_R_def = 0;        // rows of the deferred batch merged into the pending decode
+  std::vector<Req> dec_free;  // requests whose scratch pages are freed at the next collect
   int last_T = 0, last_R = 0, last_work = 0;
   bool has_batch = false;
   // offsets into meta

@@ -173,19 +173,32 @@ class Engine:
         return (toks, logits) if want_logits else toks
 
     def decode_async(self, steps):
-        """Enqueue the greedy decode of the last staged batch (see decode); collect with
-        decode_collect().  The next prefill may be staged in between."""
+        """Enqueue the greedy decode of the last staged batch (see decode), merged with a
+        deferred batch's rows if decode_defer() set one aside; collect with decode_collect().
+        The next prefill may be staged in between."""
         self._dec_steps = list(steps)
+        self._dec_prev = getattr(self, "_def_steps", None)
+        self._def_steps = None
         st = (C.c_uint32 * max(1, len(steps)))(*steps)
         check(lib().glmx_engine_decode_async(self.h, st))
 
+    def decode_defer(self, steps):
+        """Set the staged batch's decode aside: it runs merged with the next decode_async."""
+        self._def_steps = list(steps)
+        st = (C.c_uint32 * max(1, len(steps)))(*steps)
+        check(lib().glmx_engine_decode_defer(self.h, st))
+
     def decode_collect(self):
-        steps = self._dec_steps
-        n = len(steps)
-        m = max(steps) if steps else 0
-        out = (C.c_int32 * max(1, n * m))()
-        check(lib().glmx_engine_decode_collect(self.h, out))
-        return [[out[i * m + s] for s in range(steps[i])] for i in range(n)]
+        """Tokens of the collected decode: (tokens of the staged batch, tokens of the merged
+        deferred batch or None)."""
+        steps, prev = self._dec_steps, self._dec_prev
+        m = max(steps + (prev or [])) if (steps or prev) else 0
+        out = (C.c_int32 * max(1, len(steps) * m))()
+        outp = (C.c_int32 * max(1, len(prev) * m))() if prev else None
+        check(lib().glmx_engine_decode_collect(self.h, out, outp))
+        cur = [[out[i * m + s] for s in range(steps[i])] for i in range(len(steps))]
+        old = [[outp[i * m + s] for s in range(prev[i])] for i in range(len(prev))] if prev else None
+        return cur, old
 
     def replay_forward(self):
         check(lib().glmx_engine_replay_forward(self.h))

@@ -64,6 +64,7 @@ class RotationResult:
     retrieve_ms: float = 0.0     # K5 device time (0 when every RetrieveNode hit the LRU)
     retrieve_probes: int = 0     # index probes (LRU misses) of this rotation
     decoded_tokens: int = 0      # reply tokens decoded after the prefill (rotation_with_decode)
+    decode_collected: bool = True  # False: this rotation's decode was deferred into the next
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
 
@@ -306,16 +307,19 @@ class GraphCoTWorkload:
         res.decoded_tokens = sum(steps)
         return res
 
-    def rotations_with_decode(self, count, max_decode, peer=None):
+    def rotations_with_decode(self, count, max_decode, peer=None, merge=False):
         """`count` rotations of rotation_with_decode, pipelined on one engine stream: the GPU
         runs prefill r, decode r, prefill r+1, decode r+1, ... back to back while the host
         advances the state machines with r's (scripted) replies and stages rotation r+1's prefill
         (bookkeeping, staging, RetrieveNode/K1) before r's decode has finished
         (glmx_engine_decode_async / _collect; the engine stages decode steps and prefills in a
         ring of pinned slots).  Cache decisions and tokens are those of the sequential loop.
-        Yields each rotation's RotationResult after its decode completed; engine.last_timings()
-        then holds the decode and self.last_prefill_forward_ms the prefill.
+        Yields each rotation's RotationResult; engine.last_timings() then holds the last
+        collected decode and self.last_prefill_forward_ms the prefill.
 
+        merge: continuous batching of the decode rows of two consecutive rotations (even
+        rotations defer their decode into the next one's: one weight stream per decode step for
+        both; replies are scripted, so no call waits on them).
         peer: a sharding.PeerExchange running the pipelined epoch protocol (as in rotations())."""
         if count <= 0:
             return
@@ -323,14 +327,28 @@ class GraphCoTWorkload:
         def steps_of(calls):
             return [max(0, min(max_decode, count_tokens(c.reply) - 1)) for c in calls]
 
+        state = {"deferred": False}
+        self.decode_log = []  # (rotation, per-call decoded tokens) in collect order
+
+        def launch_decode(r, steps):
+            """Right after rotation r's prefill is staged; True if a decode was enqueued."""
+            if merge and not state["deferred"] and r + 1 < count and any(steps):
+                self.engine.decode_defer(steps)
+                state["deferred"] = True
+                return False
+            if any(steps) or state["deferred"]:
+                self.engine.decode_async(steps)
+                state["deferred"] = False
+                return True
+            return False
+
         calls = self.next_calls()
         th, built = self._start_retrieval(calls) if self.overlap_retrieval else (None, {})
         if peer is not None:
             peer.before_bookkeeping()
         reps = self.prefill_async(calls)
         steps = steps_of(calls)
-        if any(steps):
-            self.engine.decode_async(steps)
+        enq = launch_decode(0, steps)
         for r in range(count):
             if th is not None:
                 th.join()
@@ -349,13 +367,16 @@ class GraphCoTWorkload:
             if peer is not None:
                 peer.after_wait()
             self.last_prefill_forward_ms = self.engine.last_timings()["forward"]
-            if any(steps):
-                self.engine.decode_collect()
+            res.decode_collected = enq
+            if enq:
+                cur, prev = self.engine.decode_collect()
+                if prev is not None:
+                    self.decode_log.append((r - 1, prev))
+                self.decode_log.append((r, cur))
             yield res
             if nxt is not None:
                 calls, th, built, reps, steps = nxt
-                if any(steps):
-                    self.engine.decode_async(steps)
+                enq = launch_decode(r + 1, steps)
 
     def rotation(self) -> RotationResult:
         """One round-robin rotation.  The actions' RetrieveNode -> NodeInfo chunks depend only on

@@ -10,7 +10,7 @@ import paper_2511_01633_b200 as glmx  # noqa: E402
 cfg = glmx.ModelConfig(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=128,
                        d_ff=14336, vocab=128256, seed=0)
 model = glmx.Model(cfg, device=0)
-for R in (8, 64):
+for R in (8, 64, 128):
     kv = glmx.KvCacheState(8192, 16, glmx.PRIORITY, device=0, n_layers=32, n_kv_heads=8,
                            head_dim=128, headroom_pages=2048)
     eng = glmx.Engine(model, kv, max_requests=R, max_batch_tokens=R * 400, max_decode=16,

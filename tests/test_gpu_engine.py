@@ -191,6 +191,40 @@ def test_overlapped_decode_rotations_match_sequential():
     assert sum(r[3] for r in out[0][0]) > 0
 
 
+def test_merged_decode_matches_separate_decode():
+    """Continuous batching of two rotations' decode rows (decode_defer + decode_async) gives the
+    same bookkeeping and the same greedy reply tokens as decoding each rotation alone."""
+    from paper_2511_01633_b200.workload import GraphCoTWorkload
+
+    cfg = glmx.TINY
+    g = glmx.PropertyGraph.synth_powerlaw(3000, 6, seed=4, device=0)
+    out = []
+    for merge in (False, True):
+        model = glmx.Model(cfg, device=0)
+        kv = glmx.KvCacheState(256, 16, glmx.PRIORITY, device=0, n_layers=cfg.n_layers,
+                               n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
+                               headroom_pages=512)
+        eng = glmx.Engine(model, kv, max_requests=16, max_batch_tokens=16 * 1024, max_decode=8,
+                          max_context=4096)
+        ret = glmx.Retriever(g, chunk_k=8, vocab=cfg.vocab)
+        wl = GraphCoTWorkload(eng, ret, n_queries=40, lanes=16, seed=5, question_pool=20,
+                              node_index=glmx.NodeIndex(g))
+        rows = []
+        for r in wl.rotations_with_decode(11, 8, merge=merge):
+            rows.append(([(x.cached_tokens, x.computed_tokens, x.tail_tokens) for x in r.reports],
+                         r.first_tokens, r.finished, r.decoded_tokens))
+        toks = dict(wl.decode_log)
+        out.append((rows, kv.counters(), kv.snapshot_json(), toks))
+    assert out[0][:3] == out[1][:3]
+    a, b = out[0][3], out[1][3]
+    assert sorted(a) == sorted(b)
+    flat_a = [t for r in sorted(a) for call in a[r] for t in call]
+    flat_b = [t for r in sorted(b) for call in b[r] for t in call]
+    assert len(flat_a) == len(flat_b) and len(flat_a) > 0
+    agree = sum(x == y for x, y in zip(flat_a, flat_b)) / len(flat_a)
+    assert agree >= 0.99, agree
+
+
 def test_c3_shaped_run_bookkeeping_matches_reference():
     """C3 in miniature: 96 concurrent Graph-CoT queries on a 96-block pool with four-tier
     priority eviction (pipelined rotations, RetrieveNode, K1); every prefill and set_tier replayed
