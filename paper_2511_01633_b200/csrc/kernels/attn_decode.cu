@@ -26,6 +26,19 @@ constexpr int kG = 4;     // query heads per kv head
 constexpr int kHd = 128;  // head dim
 constexpr int kB = 16;    // tokens per page
 constexpr int kWarps = 4;
+constexpr int kStage = 2;  // half pages in flight per warp (cp.async ring, 32 KB per CTA)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -49,6 +62,9 @@ decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
   __shared__ float s_mx[kWarps][kG], s_alpha[kWarps][kG];
   __shared__ float s_m[kWarps][kG], s_l[kWarps][kG];
   __shared__ float s_acc[kWarps][kG][kHd];
+  // cp.async staging of the next half page: [warp][slot][K|V][row i][lane] 16-byte chunks (each
+  // lane reads back exactly the chunks it copied)
+  __shared__ uint4 s_kv[kWarps][kStage][2][4][32];
   const int item = blockIdx.x, split = blockIdx.y;
   const int req = item / p.Hkv, kvh = item % p.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -77,19 +93,9 @@ decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
   float m_run = -INFINITY, l_run = 0.f;  // head = lane, lanes 0-3
   const int32_t* bt = p.block_table + static_cast<int64_t>(req) * p.bt_stride;
   const uint64_t kv_stride = p.pool.tile_off(0, p.layer, 1, kvh) - p.pool.tile_off(0, p.layer, 0, kvh);
-  // half pages u0 + warp, u0 + warp + kWarps, ...  (a register double buffer of the next half
-  // page's loads was measured slower: 188 registers halve the resident warps)
-  auto load = [&](int u, uint4 (&kr)[4], uint4 (&vr)[4]) {
-    const int page = bt[u >> 1];
-    const __nv_bfloat16* kt = p.pool.base + p.pool.tile_off(page, p.layer, 0, kvh) +
-                              static_cast<int64_t>((u & 1) * 8) * kHd + sl * 8;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int key = 2 * i + half;  // within the half page
-      kr[i] = __ldcs(reinterpret_cast<const uint4*>(kt + key * kHd));
-      vr[i] = __ldcs(reinterpret_cast<const uint4*>(kt + kv_stride + key * kHd));
-    }
-  };
+  // half pages u0 + warp, u0 + warp + kWarps, ...; the next one is staged in shared memory by
+  // cp.async while this one is processed (a register double buffer was slower: 188 registers
+  // halve the resident warps)
   auto process = [&](int u, const uint4 (&kr)[4], const uint4 (&vr)[4]) {
     // partial dots of this lane's 8 dims: v[i * 4 + h]
     float v[16];
@@ -161,11 +167,36 @@ decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
     }
     __syncwarp();  // s_p / s_alpha reuse by the next half page
   };
-  for (int u = u0 + warp; u < u1; u += kWarps) {
+  // the loads of kStage - 1 half pages are in flight while one is processed
+  auto issue = [&](int u, int slot) {
+    if (u < u1) {
+      const int page = bt[u >> 1];
+      const __nv_bfloat16* kt = p.pool.base + p.pool.tile_off(page, p.layer, 0, kvh) +
+                                static_cast<int64_t>((u & 1) * 8) * kHd + sl * 8;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int key = 2 * i + half;
+        cp_async16(&s_kv[warp][slot][0][i][lane], kt + key * kHd);
+        cp_async16(&s_kv[warp][slot][1][i][lane], kt + kv_stride + key * kHd);
+      }
+    }
+    cp_async_commit();  // possibly empty: keeps the group count uniform
+  };
+#pragma unroll
+  for (int k = 0; k < kStage - 1; ++k) issue(u0 + warp + k * kWarps, k);
+  for (int k = 0, u = u0 + warp; u < u1; ++k, u += kWarps) {
+    issue(u + (kStage - 1) * kWarps, (k + kStage - 1) % kStage);
+    cp_async_wait<kStage - 1>();
+    const int slot = k % kStage;
     uint4 kr[4], vr[4];
-    load(u, kr, vr);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      kr[i] = s_kv[warp][slot][0][i][lane];
+      vr[i] = s_kv[warp][slot][1][i][lane];
+    }
     process(u, kr, vr);
   }
+  cp_async_wait<0>();
   // merge the two key halves, then the warps
 #pragma unroll
   for (int h = 0; h < kG; ++h)
