@@ -22,6 +22,10 @@ __device__ __forceinline__ uint32_t orderable(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  return static_cast<uint64_t>(__float_as_uint(lo)) | (static_cast<uint64_t>(__float_as_uint(hi)) << 32);
+}
+
 template <int DPAD>
 __global__ void __launch_bounds__(256)
 nearest_kernel(const float* __restrict__ emb, int n_rows, const float* __restrict__ queries, int n_q,
@@ -48,12 +52,27 @@ nearest_kernel(const float* __restrict__ emb, int n_rows, const float* __restric
 #pragma unroll
     for (int q = 0; q < kQB; ++q) {
       if (q >= nq) break;
-      const float* b = sq + q * DPAD;
-      float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // the 8 lanes of dot.hpp as 4 packed fp32 pairs: mul.rn.f32x2 / add.rn.f32x2 round every
+      // element exactly like __fmul_rn / __fadd_rn (no FMA contraction), two per instruction
+      const float2* b2 = reinterpret_cast<const float2*>(sq + q * DPAD);
+      uint64_t l2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
       for (int i = 0; i < DPAD; i += 8)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) l[j] = __fadd_rn(l[j], __fmul_rn(row[i + j], b[i + j]));
+        for (int j = 0; j < 4; ++j) {
+          const float2 bb = b2[i / 2 + j];
+          const uint64_t x = pack2(row[i + 2 * j], row[i + 2 * j + 1]);
+          const uint64_t y = pack2(bb.x, bb.y);
+          uint64_t m;
+          asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(x), "l"(y));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(l2[j]) : "l"(l2[j]), "l"(m));
+        }
+      float l[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        l[2 * j] = __uint_as_float(static_cast<uint32_t>(l2[j]));
+        l[2 * j + 1] = __uint_as_float(static_cast<uint32_t>(l2[j] >> 32));
+      }
       const float even = __fadd_rn(__fadd_rn(l[0], l[4]), __fadd_rn(l[2], l[6]));
       const float odd = __fadd_rn(__fadd_rn(l[1], l[5]), __fadd_rn(l[3], l[7]));
       const float score = __fadd_rn(even, odd);
