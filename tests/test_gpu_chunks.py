@@ -69,3 +69,51 @@ def test_hub_rows_stream_through_window(ref, tmp_path):
         r = glmx.Retriever(g, chunk_k=k)
         for v in (0, 1, 2):
             assert r.node_info_rendered(g.node_id(v)) == rg.node_info_rendered(g.node_id(v), k)
+
+
+def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
+    """Attribute values with tabs, newlines, runs of spaces, leading/trailing blanks, no blanks at
+    all and non-ASCII bytes: chunk text and whitespace tokens (spans + fnv1a ids) fused across
+    entry boundaries exactly as the reference tokenizer splits them; includes chunks larger than
+    the 8 KB shared-memory staging buffer (built and tokenised in place in global memory)."""
+    import json
+
+    rnd = random.Random(11)
+    tab, nl, cr = chr(9), chr(10), chr(13)
+    vals = ["plain", "two words", "  lead", "trail  ", "tab" + tab + "sep", "new" + nl + "line",
+            "cr" + cr + "lf" + nl, "multi   space", "", " ", "caf" + chr(233), "x" * 40, "abc",
+            "end,", "(paren)", "}{"]
+    lines = []
+    n_nodes = 400
+    for i in range(n_nodes):
+        attrs = {f"k{j}": rnd.choice(vals) for j in range(rnd.randrange(0, 4))}
+        if i % 7 == 0:
+            attrs["blob"] = " ".join(rnd.choice(vals) for _ in range(60))  # long entries
+        lines.append(json.dumps({"kind": "node", "id": f"v{i:04d}",
+                                 "type": rnd.choice(["a", "b c"]), "attrs": attrs}))
+    for i in range(n_nodes):
+        for _ in range(rnd.randrange(1, 6)):
+            lines.append(json.dumps({"kind": "edge", "src": f"v{i:04d}",
+                                     "dst": f"v{rnd.randrange(10):04d}", "etype": "e"}))
+    path = str(tmp_path / "ws.jsonl")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    g = glmx.PropertyGraph.load(path, device=0)
+    rg = oracle.RefGraph(path=path)
+    V = 128256
+    nodes = list(range(g.node_count()))
+    for k in (3, 16, 64, 200):
+        r = glmx.Retriever(g, chunk_k=k, vocab=V)
+        batch = r.chunk_build(nodes)
+        big = 0
+        for i, v in enumerate(nodes):
+            want = rg.node_info_rendered(g.node_id(v), k)
+            assert batch.texts[i] == want, (k, v)
+            big += len(want.encode()) > 8192
+            toks = oracle.tokenize(want)
+            raw = batch.texts[i].encode()
+            got = [raw[b:e].decode() for b, e in batch.token_spans[i]]
+            assert got == toks, (k, v)
+            assert batch.token_ids[i] == [fnv1a(t.encode()) % V for t in toks]
+        if k == 200:
+            assert big > 0  # the unstaged path ran
