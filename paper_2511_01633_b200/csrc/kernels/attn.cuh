@@ -62,4 +62,15 @@ bool decode_attention_supported(const AttnParams& p);
 int decode_attention_splits(int n_items, int max_ctx, int max_rows);
 void paged_attention_decode(const AttnParams& p, int n_req, int n_split, float* part_o,
                             float2* part_ml, cudaStream_t s);
+// Same, fused with K2 for the decode rows: q, k are RoPE'd from the qkv rows inside the kernel
+// (k and v appended to the pool page at slot[row] by the CTA that owns the last key), so no
+// separate rope_kv_append launch and no q buffer round trip.
+struct DecodeRope {
+  const __nv_bfloat16* qkv;  // [rows][(H + 2 Hkv) * hd]
+  const int32_t* pos;        // [rows]
+  const int64_t* slot;       // [rows] pool slot (page * B + offset) of the new key
+  const float* inv_freq;     // [hd / 2]
+};
+void paged_attention_decode_rope(const AttnParams& p, const DecodeRope& r, int n_req, int n_split,
+                                 float* part_o, float2* part_ml, cudaStream_t s);
 }  // namespace glmx

@@ -55,8 +55,9 @@ __device__ __forceinline__ void bf8(const uint4& u, float (&f)[8]) {
   }
 }
 
+template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32)
-decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
+decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__ part_o,
                    float2* __restrict__ part_ml) {
   __shared__ float4 s_p[kWarps][8];  // probabilities of the current half page: [key][head]
   __shared__ float s_mx[kWarps][kG], s_alpha[kWarps][kG];
@@ -76,14 +77,65 @@ decode_attn_kernel(AttnParams p, int n_split, float* __restrict__ part_o,
   const int qrow = p.q_start[req] + p.q_len[req] - 1;
   const float scale = p.scale_log2;
   float q[kG][8];
+  if constexpr (kFused) {
+    // RoPE of this lane's 8 dims (rotation partner dims are in lane sl ^ 8 of the same half),
+    // rounded to bf16 like the separate K2 kernel's q / pool writes
+    const int heads = p.H + 2 * p.Hkv;
+    const __nv_bfloat16* row = rp.qkv + static_cast<int64_t>(qrow) * heads * kHd + sl * 8;
+    const float ps = static_cast<float>(rp.pos[qrow]);
+    float cs[8], sn[8];
 #pragma unroll
-  for (int h = 0; h < kG; ++h) {
-    const uint4 u = *reinterpret_cast<const uint4*>(
-        p.q + (static_cast<int64_t>(qrow) * p.H + kvh * kG + h) * kHd + sl * 8);
-    float f[8];
-    bf8(u, f);
+    for (int j = 0; j < 8; ++j) sincosf(ps * rp.inv_freq[(sl & 7) * 8 + j], &sn[j], &cs[j]);
+    auto rope8 = [&](const uint4& u, float (&out)[8]) {
+      float f[8], o[8];
+      bf8(u, f);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) q[h][j] = f[j] * scale;
+      for (int j = 0; j < 8; ++j) o[j] = __shfl_xor_sync(0xffffffffu, f[j], 8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        // first half: x1 c - x2 s; second half: x2 c + x1 s (own = x2, partner = x1)
+        const float v = sl < 8 ? f[j] * cs[j] - o[j] * sn[j] : f[j] * cs[j] + o[j] * sn[j];
+        out[j] = __bfloat162float(__float2bfloat16_rn(v));
+      }
+    };
+#pragma unroll
+    for (int h = 0; h < kG; ++h) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + (kvh * kG + h) * kHd);
+      float f[8];
+      rope8(u, f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[h][j] = f[j] * scale;
+    }
+    // the new key / value: appended by the CTA whose range holds the last key, before its loop
+    const uint4 ku = *reinterpret_cast<const uint4*>(row + (p.H + kvh) * kHd);
+    const uint4 vu = *reinterpret_cast<const uint4*>(row + (p.H + p.Hkv + kvh) * kHd);
+    float kf[8];
+    rope8(ku, kf);
+    if (u1 == n_units && half == 0 && warp == 0) {
+      const int64_t slt = rp.slot[qrow];
+      __nv_bfloat16* kd = p.pool.base + p.pool.tile_off(slt / p.pool.block_tokens, p.layer, 0, kvh) +
+                          static_cast<int64_t>(slt % p.pool.block_tokens) * kHd + sl * 8;
+      __nv_bfloat16* vd = p.pool.base + p.pool.tile_off(slt / p.pool.block_tokens, p.layer, 1, kvh) +
+                          static_cast<int64_t>(slt % p.pool.block_tokens) * kHd + sl * 8;
+      uint4 kb;
+      __nv_bfloat162* k2 = reinterpret_cast<__nv_bfloat162*>(&kb);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k2[j] = __floats2bfloat162_rn(kf[2 * j], kf[2 * j + 1]);
+      *reinterpret_cast<uint4*>(kd) = kb;
+      *reinterpret_cast<uint4*>(vd) = vu;
+      __threadfence();
+    }
+    __syncthreads();  // the appended key is read through L2 by the cp.async loads below
+  } else {
+#pragma unroll
+    for (int h = 0; h < kG; ++h) {
+      const uint4 u = *reinterpret_cast<const uint4*>(
+          p.q + (static_cast<int64_t>(qrow) * p.H + kvh * kG + h) * kHd + sl * 8);
+      float f[8];
+      bf8(u, f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[h][j] = f[j] * scale;
+    }
   }
   float acc[kG][8];
 #pragma unroll
@@ -282,7 +334,21 @@ void paged_attention_decode(const AttnParams& p, int n_req, int n_split, float* 
   if (n_req <= 0) return;
   if (!decode_attention_supported(p)) throw Error(GLMX_ERR_ARG, "decode attention: unsupported geometry");
   const int items = n_req * p.Hkv;
-  decode_attn_kernel<<<dim3(items, n_split), kWarps * 32, 0, s>>>(p, n_split, part_o, part_ml);
+  decode_attn_kernel<false><<<dim3(items, n_split), kWarps * 32, 0, s>>>(p, DecodeRope{}, n_split,
+                                                                       part_o, part_ml);
+  GLMX_CHECK_LAUNCH();
+  if (n_split > 1) {
+    decode_combine_kernel<<<items, kHd, 0, s>>>(p, n_split, part_o, part_ml);
+    GLMX_CHECK_LAUNCH();
+  }
+}
+
+void paged_attention_decode_rope(const AttnParams& p, const DecodeRope& r, int n_req, int n_split,
+                                 float* part_o, float2* part_ml, cudaStream_t s) {
+  if (n_req <= 0) return;
+  if (!decode_attention_supported(p)) throw Error(GLMX_ERR_ARG, "decode attention: unsupported geometry");
+  const int items = n_req * p.Hkv;
+  decode_attn_kernel<true><<<dim3(items, n_split), kWarps * 32, 0, s>>>(p, r, n_split, part_o, part_ml);
   GLMX_CHECK_LAUNCH();
   if (n_split > 1) {
     decode_combine_kernel<<<items, kHd, 0, s>>>(p, n_split, part_o, part_ml);

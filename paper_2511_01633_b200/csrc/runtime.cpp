@@ -484,6 +484,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   {
     const char* dv = std::getenv("GLMX_DECODE_ATTN");
     e->decode_cc = !(dv && std::string(dv) == "tc");
+    e->decode_fuse = !(dv && std::string(dv) == "unfused");
   }
   e->tpt = e->attn_impl ? attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv))
                         : attn_tc_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
@@ -627,7 +628,9 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
       Prof p(e, kCatGemm);
       gemm(m->blas, s, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
     }
-    {
+    // decode rows with the fused kernel: RoPE + K/V append happen inside the decode attention
+    const bool fuse = e->dec_split && e->decode_fuse;
+    if (!fuse) {
       Prof p(e, kCatAppend);
       rope_kv_append(e->qkv.as<__nv_bfloat16>(), pos, slot, T, H, Hkv, hd, m->inv_freq,
                      e->kv->geom, l, e->q.as<__nv_bfloat16>(), s);
@@ -635,7 +638,10 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     {
       Prof p(e, kCatAttn);
       ap.layer = l;
-      if (e->dec_split)
+      if (fuse)
+        paged_attention_decode_rope(ap, DecodeRope{e->qkv.as<__nv_bfloat16>(), pos, slot, m->inv_freq},
+                                    R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
+      else if (e->dec_split)
         paged_attention_decode(ap, R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
       else if (e->attn_impl)
         paged_attention(ap, s);

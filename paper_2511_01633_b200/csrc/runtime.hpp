@@ -164,6 +164,7 @@ struct glmx_engine {
   size_t o_sched = 0, o_sc_pieces = 0, o_sc_cta = 0, o_sc_comb = 0, o_sc_part = 0;
   int sc_grid = 0, sc_ncomb = 0;
   bool decode_cc = true;  // one-token batches on the CUDA-core decode kernel (GLMX_DECODE_ATTN=tc: off)
+  bool decode_fuse = true;  // ... with RoPE + K/V append fused in (GLMX_DECODE_ATTN=unfused: off)
   int dec_split = 0;      // > 0: the staged batch is all one-token rows -> K3d with this many splits
   DBuf part_o, part_ml;
 
