@@ -26,7 +26,7 @@ __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
   return static_cast<uint64_t>(__float_as_uint(lo)) | (static_cast<uint64_t>(__float_as_uint(hi)) << 32);
 }
 
-template <int DPAD>
+template <int DPAD, bool kPacked>
 __global__ void __launch_bounds__(256)
 nearest_kernel(const float* __restrict__ emb, int n_rows, const float* __restrict__ queries, int n_q,
                unsigned long long* __restrict__ best) {
@@ -52,26 +52,34 @@ nearest_kernel(const float* __restrict__ emb, int n_rows, const float* __restric
 #pragma unroll
     for (int q = 0; q < kQB; ++q) {
       if (q >= nq) break;
-      // the 8 lanes of dot.hpp as 4 packed fp32 pairs: mul.rn.f32x2 / add.rn.f32x2 round every
-      // element exactly like __fmul_rn / __fadd_rn (no FMA contraction), two per instruction
-      const float2* b2 = reinterpret_cast<const float2*>(sq + q * DPAD);
-      uint64_t l2[4] = {0ull, 0ull, 0ull, 0ull};
+      float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if constexpr (kPacked) {
+        // the 8 lanes of dot.hpp as 4 packed fp32 pairs: mul.rn.f32x2 / add.rn.f32x2 round every
+        // element exactly like __fmul_rn / __fadd_rn (no FMA contraction), two per instruction
+        const float2* b2 = reinterpret_cast<const float2*>(sq + q * DPAD);
+        uint64_t l2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int i = 0; i < DPAD; i += 8)
+        for (int i = 0; i < DPAD; i += 8)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 bb = b2[i / 2 + j];
+            const uint64_t x = pack2(row[i + 2 * j], row[i + 2 * j + 1]);
+            const uint64_t y = pack2(bb.x, bb.y);
+            uint64_t m;
+            asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(x), "l"(y));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(l2[j]) : "l"(l2[j]), "l"(m));
+          }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float2 bb = b2[i / 2 + j];
-          const uint64_t x = pack2(row[i + 2 * j], row[i + 2 * j + 1]);
-          const uint64_t y = pack2(bb.x, bb.y);
-          uint64_t m;
-          asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(m) : "l"(x), "l"(y));
-          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(l2[j]) : "l"(l2[j]), "l"(m));
+          l[2 * j] = __uint_as_float(static_cast<uint32_t>(l2[j]));
+          l[2 * j + 1] = __uint_as_float(static_cast<uint32_t>(l2[j] >> 32));
         }
-      float l[8];
+      } else {
+        const float* b = sq + q * DPAD;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        l[2 * j] = __uint_as_float(static_cast<uint32_t>(l2[j]));
-        l[2 * j + 1] = __uint_as_float(static_cast<uint32_t>(l2[j] >> 32));
+        for (int i = 0; i < DPAD; i += 8)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) l[j] = __fadd_rn(l[j], __fmul_rn(row[i + j], b[i + j]));
       }
       const float even = __fadd_rn(__fadd_rn(l[0], l[4]), __fadd_rn(l[2], l[6]));
       const float odd = __fadd_rn(__fadd_rn(l[1], l[5]), __fadd_rn(l[3], l[7]));
@@ -96,14 +104,23 @@ nearest_kernel(const float* __restrict__ emb, int n_rows, const float* __restric
 }  // namespace
 
 void nearest_top1(const float* emb, int n_rows, int dpad, const float* queries, int n_q,
-                  unsigned long long* best, cudaStream_t s) {
+                  unsigned long long* best, cudaStream_t s, bool packed) {
   if (n_q <= 0 || n_rows <= 0) return;
   const int blocks_x = static_cast<int>(std::min<uint64_t>(ceil_div(n_rows, 256), kNumSMs * 2));
   dim3 grid(blocks_x, static_cast<unsigned>(ceil_div(n_q, kQB)));
   switch (dpad) {
-    case 64: nearest_kernel<64><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best); break;
-    case 32: nearest_kernel<32><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best); break;
-    case 128: nearest_kernel<128><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best); break;
+    case 64:
+      if (packed) nearest_kernel<64, true><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      else nearest_kernel<64, false><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      break;
+    case 32:
+      if (packed) nearest_kernel<32, true><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      else nearest_kernel<32, false><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      break;
+    case 128:
+      if (packed) nearest_kernel<128, true><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      else nearest_kernel<128, false><<<grid, 256, 0, s>>>(emb, n_rows, queries, n_q, best);
+      break;
     default: throw Error(GLMX_ERR_ARG, "embedding dim must pad to 32, 64 or 128");
   }
   GLMX_CHECK_LAUNCH();

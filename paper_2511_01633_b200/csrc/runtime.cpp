@@ -1420,7 +1420,7 @@ int workload_generate_impl(glmx_graph* g, uint64_t seed, int n, double ratio, st
     GLMX_CUDA(cudaMemsetAsync(g->d_best.p, 0, static_cast<size_t>(nq) * 8, s));
     GLMX_CUDA(cudaEventRecord(g->ev0, s));
     nearest_top1(g->d_emb.as<float>(), static_cast<int>(g->idx_node.size()), dpad,
-                 g->d_qemb.as<float>(), nq, g->d_best.as<unsigned long long>(), s);
+                 g->d_qemb.as<float>(), nq, g->d_best.as<unsigned long long>(), s, /*packed=*/true);
     GLMX_CUDA(cudaEventRecord(g->ev1, s));
     best.resize(nq);
     GLMX_CUDA(cudaMemcpyAsync(best.data(), g->d_best.p, nq * 8, cudaMemcpyDeviceToHost, s));
