@@ -396,7 +396,7 @@ chunk_select_hub_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ n
 // per lane are in flight before any byte is scattered.  Chunks longer than the buffer are built
 // in place in global memory by the same code.
 constexpr int kRW = 4;         // warps (chunks) per CTA
-constexpr int kBuf = 8192;     // staged chunk bytes per warp
+constexpr int kBuf = 6144;     // staged chunk bytes per warp
 constexpr int kSeg = 1024;     // bytes per token-start compaction segment
 constexpr int kWordsU = 4;     // 16-byte loads in flight per lane
 
@@ -559,7 +559,7 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kRW * 32, 6)
+__global__ void __launch_bounds__(kRW * 32, 7)
 chunk_render_emit_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ node_idx,
                          int n_req, const int32_t* __restrict__ sel,
                          const int32_t* __restrict__ sel_count,
