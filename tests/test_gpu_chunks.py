@@ -75,7 +75,7 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
     """Attribute values with tabs, newlines, runs of spaces, leading/trailing blanks, no blanks at
     all and non-ASCII bytes: chunk text and whitespace tokens (spans + fnv1a ids) fused across
     entry boundaries exactly as the reference tokenizer splits them; includes chunks larger than
-    the 8 KB shared-memory staging buffer (built and tokenised in place in global memory)."""
+    the 6 KB shared-memory staging buffer (built and tokenised in place in global memory)."""
     import json
 
     rnd = random.Random(11)
@@ -109,7 +109,7 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
         for i, v in enumerate(nodes):
             want = rg.node_info_rendered(g.node_id(v), k)
             assert batch.texts[i] == want, (k, v)
-            big += len(want.encode()) > 8192
+            big += len(want.encode()) > 6144
             toks = oracle.tokenize(want)
             raw = batch.texts[i].encode()
             got = [raw[b:e].decode() for b, e in batch.token_spans[i]]
