@@ -85,19 +85,23 @@ rmsnorm_reg_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows
   const int64_t src = rows ? rows[t] : t;
   const float4* xr = reinterpret_cast<const float4*>(x + src * D);
   float4 v[kV];
+  uint2 wr[kV];  // the weights are loaded together with x, not after the reduction
+  const uint2* w4 = reinterpret_cast<const uint2*>(w);
 #pragma unroll
-  for (int k = 0; k < kV; ++k) v[k] = __ldcs(xr + threadIdx.x + k * NT);
+  for (int k = 0; k < kV; ++k) {
+    v[k] = __ldcs(xr + threadIdx.x + k * NT);
+    wr[k] = __ldg(w4 + threadIdx.x + k * NT);
+  }
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < kV; ++k) ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
   ss = block_sum<NT>(ss, red);
   const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
-  const uint2* w4 = reinterpret_cast<const uint2*>(w);
   uint2* o = reinterpret_cast<uint2*>(out + static_cast<int64_t>(t) * D);
 #pragma unroll
   for (int k = 0; k < kV; ++k) {
     const int i = threadIdx.x + k * NT;
-    const uint2 wv = w4[i];
+    const uint2 wv = wr[k];
     const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.x));
     const float2 wb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv.y));
     __nv_bfloat162 a = __floats2bfloat162_rn(v[k].x * inv * wa.x, v[k].y * inv * wa.y);
