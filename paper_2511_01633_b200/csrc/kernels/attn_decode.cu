@@ -46,6 +46,29 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// packed fp32 pairs (FFMA2 / FMUL2 on sm_100): two lanes of the 8-dim slice per instruction
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  return static_cast<uint64_t>(__float_as_uint(lo)) | (static_cast<uint64_t>(__float_as_uint(hi)) << 32);
+}
+__device__ __forceinline__ float f2lo(uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x)); }
+__device__ __forceinline__ float f2hi(uint64_t x) { return __uint_as_float(static_cast<uint32_t>(x >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 8 bf16 -> 4 packed fp32 pairs
+__device__ __forceinline__ void bf8x2(const uint4& u, uint64_t (&f)[4]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) f[i] = f2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+}
+
 __device__ __forceinline__ void bf8(const uint4& u, float (&f)[8]) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -137,11 +160,16 @@ decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__
       for (int j = 0; j < 8; ++j) q[h][j] = f[j] * scale;
     }
   }
-  float acc[kG][8];
+  uint64_t q2[kG][4];
 #pragma unroll
   for (int h = 0; h < kG; ++h)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[h][j] = 0.f;
+    for (int jj = 0; jj < 4; ++jj) q2[h][jj] = f2(q[h][2 * jj], q[h][2 * jj + 1]);
+  uint64_t acc2[kG][4];
+#pragma unroll
+  for (int h = 0; h < kG; ++h)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc2[h][jj] = 0ull;
   float m_run = -INFINITY, l_run = 0.f;  // head = lane, lanes 0-3
   const int32_t* bt = p.block_table + static_cast<int64_t>(req) * p.bt_stride;
   const uint64_t kv_stride = p.pool.tile_off(0, p.layer, 1, kvh) - p.pool.tile_off(0, p.layer, 0, kvh);
@@ -153,14 +181,14 @@ decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__
     float v[16];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      float f[8];
-      bf8(kr[i], f);
+      uint64_t kf[4];
+      bf8x2(kr[i], kf);
 #pragma unroll
       for (int h = 0; h < kG; ++h) {
-        float s = 0.f;
+        uint64_t s2 = 0ull;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s = fmaf(q[h][j], f[j], s);
-        v[i * 4 + h] = s;
+        for (int jj = 0; jj < 4; ++jj) s2 = ffma2(q2[h][jj], kf[jj], s2);
+        v[i * 4 + h] = f2lo(s2) + f2hi(s2);
       }
     }
     // reduce-scatter over the 16 lanes of this half: lane bit b keeps the half of the values
@@ -203,19 +231,23 @@ decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__
 #pragma unroll
     for (int h = 0; h < kG; ++h) al[h] = s_alpha[warp][h];
 #pragma unroll
-    for (int h = 0; h < kG; ++h)
+    for (int h = 0; h < kG; ++h) {
+      const uint64_t a2 = f2(al[h], al[h]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[h][j] *= al[h];
+      for (int jj = 0; jj < 4; ++jj) acc2[h][jj] = fmul2(acc2[h][jj], a2);
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float4 pp = s_p[warp][2 * i + half];
       const float ph[kG] = {pp.x, pp.y, pp.z, pp.w};
-      float f[8];
-      bf8(vr[i], f);
+      uint64_t vf[4];
+      bf8x2(vr[i], vf);
 #pragma unroll
-      for (int h = 0; h < kG; ++h)
+      for (int h = 0; h < kG; ++h) {
+        const uint64_t p2 = f2(ph[h], ph[h]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[h][j] = fmaf(ph[h], f[j], acc[h][j]);
+        for (int jj = 0; jj < 4; ++jj) acc2[h][jj] = ffma2(p2, vf[jj], acc2[h][jj]);
+      }
     }
     __syncwarp();  // s_p / s_alpha reuse by the next half page
   };
@@ -250,6 +282,14 @@ decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__
   }
   cp_async_wait<0>();
   // merge the two key halves, then the warps
+  float acc[kG][8];
+#pragma unroll
+  for (int h = 0; h < kG; ++h)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      acc[h][2 * jj] = f2lo(acc2[h][jj]);
+      acc[h][2 * jj + 1] = f2hi(acc2[h][jj]);
+    }
 #pragma unroll
   for (int h = 0; h < kG; ++h)
 #pragma unroll
