@@ -75,6 +75,31 @@ def test_decode_matches_greedy_oracle(tiny):
         dec.check_greedy(ids, [first[i]] + out[i])
 
 
+G4 = glmx.ModelConfig(n_layers=2, d_model=512, n_heads=8, n_kv_heads=2, head_dim=128, d_ff=1024,
+                      vocab=32000)
+
+
+@pytest.mark.parametrize("mode", ["fused", "unfused", "tc"])
+def test_decode_gqa4_matches_greedy_oracle(mode, monkeypatch):
+    """GQA 4:1 (the Llama-3 ratio): decode steps run the CUDA-core decode kernel (K3d) with RoPE +
+    K/V append fused in (default), the unfused K2 + K3d pair, or the tcgen05 kernel; greedy tokens
+    follow the fp32 oracle and the three paths agree."""
+    if mode != "fused":
+        monkeypatch.setenv("GLMX_DECODE_ATTN", mode)
+    model, kv, eng = make(G4)
+    dec = Decoder(G4, model.export_all())
+    reqs = [glmx.Request(words(40, "q"), [(0, 40, 3)], "s"),
+            glmx.Request(words(17, "r"), [(0, 17, 3)], "t"),
+            glmx.Request(words(300, "p"), [(0, 300, 3)], "u")]
+    _, first = eng.prefill(reqs)
+    out, last = eng.decode([6, 3, 5], want_logits=True)
+    assert [len(o) for o in out] == [6, 3, 5]
+    for i, r in enumerate(reqs):
+        dec.check_greedy(token_ids(r.tokens, G4.vocab), [first[i]] + out[i])
+    ref_last = dec.forward(token_ids(reqs[0].tokens, G4.vocab) + [first[0]] + out[0][:-1])[0]
+    check_logits(last[0], ref_last)
+
+
 def test_bookkeeping_matches_reference_under_pressure(ref):
     """Same request stream through the engine (device pool) and the reference KvCacheState:
     identical reports, eviction order and residents, including self-eviction + orphans."""
