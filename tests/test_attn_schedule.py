@@ -148,3 +148,17 @@ def test_two_tile_items_are_not_paired():
 @pytest.mark.parametrize("n_sm", [1, 2, 148])
 def test_single_long_item(n_sm):
     check([(32768, 1)], n_kv=1, n_sm=n_sm)
+
+
+def test_pairing_boundaries():
+    # a block of 32 tokens (= tokens_per_item / 2) uses one query tile and may pair; 33 tokens
+    # need two tiles and never pair; single-tile items longer than 16 key tiles never pair
+    reqs = [(100, 32)] * 300  # 2400 single-tile items of 1 key tile: two waves alone
+    s = check(reqs)
+    assert any(b >= 0 for b, _, _, _ in s["partners"])
+    s = check([(100, 33)] * 300)
+    assert all(b == -1 for b, _, _, _ in s["partners"])
+    s = check([(128 * 17, 32)] * 40)  # 17 key tiles each
+    assert all(b == -1 for b, _, _, _ in s["partners"])
+    s = check([(128 * 16, 32)] * 40)  # 16 key tiles each: pairable
+    assert s["grid"] <= 148
