@@ -61,6 +61,10 @@ def parse():
                         "(Graph-CoT queries/s with the full call_llm step); 0 skips it")
     p.add_argument("--no-peer", action="store_true",
                    help="N>1: disable cross-GPU prefix hits (per-epoch directory + K4 peer copies)")
+    p.add_argument("--gemm-tune-tokens", type=int, default=12288,
+                   help="before timing, pick cuBLAS algorithms for the projection GEMMs per M "
+                        "bucket up to this many batch tokens (glmx_model_tune_gemms); 0 keeps "
+                        "cublasGemmEx's default choice")
     return p.parse_args()
 
 
@@ -303,6 +307,9 @@ def main():
     g = glmx.PropertyGraph.synth_powerlaw(args.nodes, 8, seed=args.seed, device=local)
     ret = glmx.Retriever(g, chunk_k=args.k, vocab=cfg.vocab)
     model = glmx.Model(cfg, device=local)
+    t_tune = time.perf_counter()
+    gemm_tuned = model.tune_gemms(args.gemm_tune_tokens) if args.gemm_tune_tokens > 0 else 0
+    t_tune = time.perf_counter() - t_tune
     kv = glmx.KvCacheState(args.capacity, 16, glmx.PRIORITY, device=local, n_layers=cfg.n_layers,
                            n_kv_heads=cfg.n_kv_heads, head_dim=cfg.head_dim,
                            headroom_pages=4096)
@@ -567,7 +574,10 @@ def main():
                    "kv_capacity_blocks": args.capacity, "block_tokens": 16,
                    "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
                    "parallelism": f"query-sharded x{ws}", "routing": args.routing,
-                   "host_pipelining": pipelined},
+                   "host_pipelining": pipelined,
+                   "gemm_algorithms": {"tuned_up_to_tokens": args.gemm_tune_tokens,
+                                       "buckets_with_winner": gemm_tuned,
+                                       "tune_s": round(t_tune, 2)}},
         "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
         "cache_hit_token_frac": cached / max(1.0, tokens),
         "calls": calls, "queries_finished": finished,

@@ -242,6 +242,15 @@ void glmx_model_destroy(glmx_model* m);
 int glmx_model_export_weight(const glmx_model* m, int32_t which, int32_t layer, uint16_t* out,
                              uint64_t n);
 
+/* Times cuBLAS's algorithm candidates for the four per-layer projections (QKV, O, gate/up,
+ * down) at every M bucket up to max_tokens (128-row buckets to 2048, 256-row above) against the
+ * default cublasGemmEx choice, on layer 0's weights, and records the winners; later forwards of
+ * every engine on this model launch them.  Takes seconds and synchronises the device: call it
+ * once at start-up, before any engine work is in flight.  No reference counterpart (the
+ * reference's model step is a cost model, orchestrator.cpp:131-132); untuned models keep
+ * cublasGemmEx.  *out_entries (nullable) = buckets with a recorded winner. */
+int glmx_model_tune_gemms(glmx_model* m, int32_t max_tokens, int32_t* out_entries);
+
 /* ================================================================== engine: prefill / decode step
  * The seam at orchestrator.cpp:131-132 (span = c_prefill*computed + c_decode*tokens_out) becomes
  * a real forward: bookkeeping prefill per request in caller order (sequential semantics, exactly

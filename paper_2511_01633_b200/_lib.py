@@ -131,6 +131,7 @@ _SIGS = {
     "glmx_model_destroy": (None, [C.c_void_p]),
     "glmx_model_export_weight": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32,
                                            C.POINTER(C.c_uint16), C.c_uint64]),
+    "glmx_model_tune_gemms": (C.c_int, [C.c_void_p, C.c_int32, i32p]),
     "glmx_engine_create": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(EngineConfig),
                                      C.POINTER(C.c_void_p)]),
     "glmx_engine_destroy": (None, [C.c_void_p]),

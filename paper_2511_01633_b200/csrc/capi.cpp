@@ -21,6 +21,7 @@ glmx_kv* kv_create_impl(const glmx_kv_config*);
 void pool_copy_impl(glmx_kv*, glmx_kv*, const int32_t*, const int32_t*, uint64_t, cudaStream_t);
 glmx_model* model_create_impl(const glmx_model_config*, int);
 int model_export_impl(const glmx_model*, int, int, uint16_t*, uint64_t);
+int model_tune_gemms_impl(glmx_model*, int);
 glmx_engine* engine_create_impl(glmx_model*, glmx_kv*, const glmx_engine_config*);
 int engine_prefill_impl(glmx_engine*, uint64_t, const glmx_request*, glmx_prefill_report*,
                         int32_t*, float*, bool);
@@ -463,6 +464,14 @@ void glmx_model_destroy(glmx_model* m) {
 int glmx_model_export_weight(const glmx_model* m, int32_t which, int32_t layer, uint16_t* out,
                              uint64_t n) {
   return guarded([&] { return model_export_impl(m, which, layer, out, n); });
+}
+
+int glmx_model_tune_gemms(glmx_model* m, int32_t max_tokens, int32_t* out_entries) {
+  return guarded([&] {
+    const int n = model_tune_gemms_impl(m, max_tokens);
+    if (out_entries) *out_entries = n;
+    return GLMX_OK;
+  });
 }
 
 int glmx_engine_create(glmx_model* m, glmx_kv* kv, const glmx_engine_config* cfg,

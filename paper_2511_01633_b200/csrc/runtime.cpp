@@ -12,6 +12,10 @@
 
 using namespace glmx;
 
+namespace {
+constexpr size_t kBlasWsBytes = 64ull << 20;  // cuBLAS / cuBLASLt workspace per model
+}
+
 #define GLMX_BLAS(call)                                                                   \
   do {                                                                                    \
     cublasStatus_t s_ = (call);                                                           \
@@ -364,8 +368,8 @@ glmx_model* model_create_impl(const glmx_model_config* c, int device) {
   GLMX_CUDA(cudaMalloc(&m->inv_freq, inv.size() * 4));
   GLMX_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
   GLMX_BLAS(cublasCreate(&m->blas));
-  GLMX_CUDA(cudaMalloc(&m->blas_ws, 64 << 20));
-  GLMX_BLAS(cublasSetWorkspace(m->blas, m->blas_ws, 64 << 20));
+  GLMX_CUDA(cudaMalloc(&m->blas_ws, kBlasWsBytes));
+  GLMX_BLAS(cublasSetWorkspace(m->blas, m->blas_ws, kBlasWsBytes));
   GLMX_CUDA(cudaDeviceSynchronize());
   return m.release();
 }
@@ -396,6 +400,60 @@ int model_export_impl(const glmx_model* m, int which, int layer, uint16_t* out, 
   return GLMX_OK;
 }
 
+// Times the projection GEMMs' algorithm candidates per M bucket (host/gemm_tune.hpp) on layer
+// 0's weights and random activations; T <= 128 (decode rows) stays with cublasGemmEx.
+int model_tune_gemms_impl(glmx_model* m, int max_tokens) {
+  if (max_tokens <= 128) return 0;
+  DeviceGuard g(m->device);
+  const auto& c = m->cfg;
+  const uint64_t d = c.d_model, hd = c.head_dim, H = c.n_heads, Hkv = c.n_kv_heads, ff = c.d_ff;
+  struct P {
+    int shape;
+    const __nv_bfloat16* w;
+    int in, out;
+    bool fp32, acc;
+  };
+  const LayerW& w = m->layers.at(0);
+  const P ps[kGemmShapes] = {
+      {kGemmQKV, w.wqkv, int(d), int((H + 2 * Hkv) * hd), false, false},
+      {kGemmO, w.wo, int(H * hd), int(d), true, true},
+      {kGemmGU, w.wgu, int(d), int(2 * ff), false, false},
+      {kGemmDown, w.wdown, int(ff), int(d), true, true}};
+  const int nb = GemmTuner::bucket(max_tokens) + 1;
+  const uint64_t T = static_cast<uint64_t>(GemmTuner::bucket_hi(nb - 1));
+  uint64_t x_elems = 0, y_bytes = 0;
+  for (const P& p : ps) {
+    x_elems = std::max<uint64_t>(x_elems, T * p.in);
+    y_bytes = std::max<uint64_t>(y_bytes, T * p.out * (p.fp32 ? 4 : 2));
+  }
+  __nv_bfloat16* X = nullptr;
+  void* Y = nullptr;
+  GLMX_CUDA(cudaMalloc(&X, x_elems * 2));
+  cudaError_t ye = cudaMalloc(&Y, y_bytes);
+  if (ye != cudaSuccess) {
+    cudaFree(X);
+    GLMX_CUDA(ye);
+  }
+  int n = 0;
+  try {
+    // random operands: all-zero inputs draw less power and would favour the wrong candidates
+    init_normal_bf16(X, x_elems, 0x7e57u, 1.0f, 0);
+    GLMX_CUDA(cudaMemset(Y, 0, y_bytes));
+    for (int b = 1; b < nb; ++b)
+      for (const P& p : ps)
+        n += m->tuner.tune(p.shape, b, m->blas, 0, X, p.w, Y, p.fp32, p.acc, p.in, p.out,
+                           m->blas_ws, kBlasWsBytes);
+    GLMX_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    cudaFree(X);
+    cudaFree(Y);
+    throw;
+  }
+  cudaFree(X);
+  cudaFree(Y);
+  return n;
+}
+
 // ======================================================================== engine
 namespace {
 
@@ -408,10 +466,15 @@ bool attn_pairing() {
   return on;
 }
 
-// Y[T][out] (+)= X[T][in] * W[out][in]^T  (column-major: C(out x T) = W^T' * X)
-void gemm(cublasHandle_t h, cudaStream_t s, const __nv_bfloat16* X, const __nv_bfloat16* W,
-          void* Y, bool y_fp32, bool accumulate, int T, int in, int out) {
+// Y[T][out] (+)= X[T][in] * W[out][in]^T  (column-major: C(out x T) = W^T' * X); `shape` names
+// the projection for the tuned algorithm table (host/gemm_tune.hpp), -1 = always cublasGemmEx
+void gemm(glmx_model* m, int shape, cudaStream_t s, const __nv_bfloat16* X,
+          const __nv_bfloat16* W, void* Y, bool y_fp32, bool accumulate, int T, int in, int out) {
   if (T <= 0) return;
+  if (shape >= 0 && m->tuner.run(shape, s, X, W, Y, y_fp32, accumulate, T, in, out, m->blas_ws,
+                                 kBlasWsBytes))
+    return;
+  cublasHandle_t h = m->blas;
   GLMX_BLAS(cublasSetStream(h, s));
   const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
   GLMX_BLAS(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, out, T, in, &alpha, W, CUDA_R_16BF, in, X,
@@ -626,7 +689,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m->blas, s, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
+      gemm(m, kGemmQKV, s, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
     }
     // decode rows with the fused kernel: RoPE + K/V append happen inside the decode attention
     const bool fuse = e->dec_split && e->decode_fuse;
@@ -650,7 +713,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m->blas, s, e->attn.as<__nv_bfloat16>(), w.wo, e->x.p, true, true, T, H * hd, d);
+      gemm(m, kGemmO, s, e->attn.as<__nv_bfloat16>(), w.wo, e->x.p, true, true, T, H * hd, d);
     }
     {
       Prof p(e, kCatOther);
@@ -658,7 +721,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m->blas, s, e->h.as<__nv_bfloat16>(), w.wgu, e->gu.p, false, false, T, d, 2 * ff);
+      gemm(m, kGemmGU, s, e->h.as<__nv_bfloat16>(), w.wgu, e->gu.p, false, false, T, d, 2 * ff);
     }
     {
       Prof p(e, kCatOther);
@@ -666,7 +729,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m->blas, s, e->act.as<__nv_bfloat16>(), w.wdown, e->x.p, true, true, T, ff, d);
+      gemm(m, kGemmDown, s, e->act.as<__nv_bfloat16>(), w.wdown, e->x.p, true, true, T, ff, d);
     }
   }
   {
@@ -676,7 +739,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   }
   {
     Prof p(e, kCatGemm);
-    gemm(m->blas, s, e->hl.as<__nv_bfloat16>(), m->lm_head, e->logits.p, true, false, n_last, d,
+    gemm(m, -1, s, e->hl.as<__nv_bfloat16>(), m->lm_head, e->logits.p, true, false, n_last, d,
          c.vocab);
   }
 }

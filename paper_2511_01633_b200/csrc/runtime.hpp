@@ -13,6 +13,7 @@
 
 #include "host/attn_sched.hpp"
 #include "host/block_engine.hpp"
+#include "host/gemm_tune.hpp"
 #include "host/vindex.hpp"
 #include "host/graph.hpp"
 #include "kernels/attn.cuh"
@@ -94,6 +95,7 @@ struct glmx_model {
   float* inv_freq = nullptr;
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
+  glmx::GemmTuner tuner;  // per-(projection, M bucket) cuBLASLt algorithms; empty = cublasGemmEx
   ~glmx_model();
 };
 

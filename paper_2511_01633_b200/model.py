@@ -69,6 +69,14 @@ class Model:
 
     __del__ = _lib.safe_del
 
+    def tune_gemms(self, max_tokens: int) -> int:
+        """Pick cuBLAS algorithms for the per-layer projections per M bucket up to max_tokens
+        (glmx_model_tune_gemms); seconds of device time, call before any engine work. Returns
+        the number of buckets where a candidate beat the default cublasGemmEx choice."""
+        n = C.c_int32()
+        check(lib().glmx_model_tune_gemms(self.h, int(max_tokens), C.byref(n)))
+        return n.value
+
     def export(self, name, layer=0, shape=None) -> np.ndarray:
         """bf16 weights as float32 (for the CPU oracle)."""
         c = self.cfg
