@@ -28,6 +28,8 @@ ap.add_argument("--nodes", type=int, default=5000)
 ap.add_argument("--policy", type=int, default=glmx.PRIORITY)
 ap.add_argument("--sequential", action="store_true", help="no host pipelining")
 ap.add_argument("--dump", default=None, help="write the bookkeeping op log (pickle) here")
+ap.add_argument("--gemm-tune-tokens", type=int, default=12288,
+                help="cuBLAS algorithm table up to this many batch tokens (0 = cublasGemmEx default)")
 args = ap.parse_args()
 
 cfg = glmx.ModelConfig(n_layers=args.layers, d_model=4096, n_heads=32, n_kv_heads=8,
@@ -35,6 +37,8 @@ cfg = glmx.ModelConfig(n_layers=args.layers, d_model=4096, n_heads=32, n_kv_head
 g = glmx.PropertyGraph.synth_powerlaw(args.nodes, 8, seed=7, device=0)
 ret = glmx.Retriever(g, chunk_k=16, vocab=cfg.vocab)
 model = glmx.Model(cfg, device=0)
+if args.gemm_tune_tokens > 0:
+    model.tune_gemms(args.gemm_tune_tokens)
 kv = glmx.KvCacheState(args.cap, 16, args.policy, device=0, n_layers=cfg.n_layers, n_kv_heads=8,
                        head_dim=128, headroom_pages=args.lanes * 48)
 eng = glmx.Engine(model, kv, max_requests=args.lanes, max_batch_tokens=args.lanes * 600,

@@ -22,6 +22,8 @@ ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--prefix", type=int, nargs="+", default=[2048, 4096, 8192, 16384, 32768])
 ap.add_argument("--k", type=int, nargs="+", default=[8, 16, 32, 64])
 ap.add_argument("--replays", type=int, default=5)
+ap.add_argument("--gemm-tune-tokens", type=int, default=12288,
+                help="cuBLAS algorithm table up to this many batch tokens (0 = cublasGemmEx default)")
 args = ap.parse_args()
 
 peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -30,6 +32,8 @@ cfg = glmx.ModelConfig(n_layers=args.layers, d_model=4096, n_heads=32, n_kv_head
                        d_ff=14336, vocab=128256)
 g = glmx.PropertyGraph.synth_powerlaw(100000, 8, seed=0, device=0)
 model = glmx.Model(cfg, device=0)
+if args.gemm_tune_tokens > 0:
+    model.tune_gemms(args.gemm_tune_tokens)
 max_ctx = max(args.prefix) + 4096
 t = TemplateSet()
 rows = []
