@@ -548,7 +548,7 @@ def main():
     # dominant kernel of the step by device time: the cuBLAS GEMMs (Llama-3-8B linears)
     roof = {"bound": "tensor", "achieved": gemm_tflops, "peak": tc_peak, "unit": "TFLOP/s",
             "frac": gemm_tflops / tc_peak,
-            "kernel": "cuBLAS bf16 GEMM (cublasGemmEx, library; QKV/O/gate-up/down/lm_head)",
+            "kernel": "cuBLAS bf16 GEMM (library: cublasLtMatmul with the tuned per-bucket algorithm, else cublasGemmEx; QKV/O/gate-up/down/lm_head)",
             "traffic": traffic.get("gemm"), "traffic_unit": "bytes per launch (ncu, profiles/)",
             "peak_kind": peak_kind + " sustained bf16",
             "share_of_forward": tm["gemm"] / fwd,
