@@ -243,7 +243,7 @@ int glmx_model_export_weight(const glmx_model* m, int32_t which, int32_t layer, 
                              uint64_t n);
 
 /* Times cuBLAS's algorithm candidates for the four per-layer projections (QKV, O, gate/up,
- * down) at every M bucket up to max_tokens (128-row buckets to 2048, 256-row above) against the
+ * down) at every M bucket up to max_tokens (128-row buckets to 2048, 256-row to 16384, 2048-row above) against the
  * default cublasGemmEx choice, on layer 0's weights, and records the winners; later forwards of
  * every engine on this model launch them.  Takes seconds and synchronises the device: call it
  * once at start-up, before any engine work is in flight.  No reference counterpart (the

@@ -40,10 +40,15 @@ GemmTuner::~GemmTuner() {
 
 int GemmTuner::bucket(int T) {
   if (T <= 2048) return (T + 127) / 128 - 1;
-  return 16 + (T - 2048 + 255) / 256 - 1;
+  if (T <= 16384) return 16 + (T - 2048 + 255) / 256 - 1;
+  return 72 + (T - 16384 + 2047) / 2048 - 1;
 }
 
-int GemmTuner::bucket_hi(int b) { return b < 16 ? (b + 1) * 128 : 2048 + (b - 15) * 256; }
+int GemmTuner::bucket_hi(int b) {
+  if (b < 16) return (b + 1) * 128;
+  if (b < 72) return 2048 + (b - 15) * 256;
+  return 16384 + (b - 71) * 2048;
+}
 
 int GemmTuner::entries() const {
   int n = 0;

@@ -27,8 +27,9 @@ class GemmTuner {
   GemmTuner& operator=(const GemmTuner&) = delete;
   ~GemmTuner();
 
-  // M buckets: 128 wide up to 2048, 256 wide above (aligned to the 128/256-row tiles cuBLAS
-  // uses, so a bucket's tile count is that of its upper edge).
+  // M buckets: 128 wide up to 2048, 256 wide up to 16384 (aligned to the 128/256-row tiles
+  // cuBLAS uses, so a bucket's tile count is that of its upper edge), 2048 wide above (tens of
+  // waves: the tail wave no longer matters).
   static int bucket(int T);
   static int bucket_hi(int b);
 

@@ -28,7 +28,7 @@ ap.add_argument("--nodes", type=int, default=5000)
 ap.add_argument("--policy", type=int, default=glmx.PRIORITY)
 ap.add_argument("--sequential", action="store_true", help="no host pipelining")
 ap.add_argument("--dump", default=None, help="write the bookkeeping op log (pickle) here")
-ap.add_argument("--gemm-tune-tokens", type=int, default=12288,
+ap.add_argument("--gemm-tune-tokens", type=int, default=32768,
                 help="cuBLAS algorithm table up to this many batch tokens (0 = cublasGemmEx default)")
 args = ap.parse_args()
 
