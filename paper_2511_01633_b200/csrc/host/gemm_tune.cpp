@@ -1,7 +1,10 @@
 #include "host/gemm_tune.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "host/common.hpp"
 
@@ -94,10 +97,16 @@ int GemmTuner::tune(int shape, int b, cublasHandle_t blas, cudaStream_t s, const
   check_lt(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
                                                 &ws_bytes, sizeof(ws_bytes)),
            "pref workspace");
-  cublasLtMatmulHeuristicResult_t res[kCandidates];
+  // GLMX_GEMM_TUNE="candidates,rounds" overrides the defaults (dev A/B only)
+  static const std::pair<int, int> knobs = [] {
+    int c = kCandidates, r = 3;
+    if (const char* v = std::getenv("GLMX_GEMM_TUNE")) std::sscanf(v, "%d,%d", &c, &r);
+    return std::make_pair(std::clamp(c, 1, kMaxCandidates), std::max(1, r));
+  }();
+  cublasLtMatmulHeuristicResult_t res[kMaxCandidates];
   int got = 0;
   const cublasStatus_t hs = cublasLtMatmulAlgoGetHeuristic(lt_, desc_, l.A(), l.B(), l.C(), l.C(),
-                                                           pref, kCandidates, res, &got);
+                                                           pref, knobs.first, res, &got);
   cublasLtMatmulPreferenceDestroy(pref);
   if (hs != CUBLAS_STATUS_SUCCESS || got <= 0) return 0;
 
@@ -116,7 +125,8 @@ int GemmTuner::tune(int shape, int b, cublasHandle_t blas, cudaStream_t s, const
   };
   // candidate -1 = cublasGemmEx; rounds interleave the candidates so that clock drift under the
   // power cap falls on all of them alike
-  constexpr int kRounds = 3, kIters = 2;
+  const int kRounds = knobs.second;
+  constexpr int kIters = 2;
   std::vector<bool> ok(got + 1, true);
   for (int i = -1; i < got; ++i) ok[i + 1] = launch(i);  // warm-up (and validity)
   cudaEvent_t e0, e1;

@@ -48,7 +48,7 @@ class GemmTuner {
   int entries() const;
 
  private:
-  static constexpr int kCandidates = 6;
+  static constexpr int kCandidates = 6, kMaxCandidates = 16;
   struct Entry {
     bool has = false;
     cublasLtMatmulAlgo_t algo{};
