@@ -129,9 +129,16 @@ int GemmTuner::tune(int shape, int b, cublasHandle_t blas, cudaStream_t s, const
   constexpr int kIters = 2;
   std::vector<bool> ok(got + 1, true);
   for (int i = -1; i < got; ++i) ok[i + 1] = launch(i);  // warm-up (and validity)
-  cudaEvent_t e0, e1;
-  check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
-  check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+  struct Events {  // released on every exit path (check_* throw)
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~Events() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } ev;
+  check_cuda(cudaEventCreate(&ev.a), "cudaEventCreate");
+  check_cuda(cudaEventCreate(&ev.b), "cudaEventCreate");
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   std::vector<std::vector<float>> t(got + 1);
   for (int r = 0; r < kRounds; ++r)
     for (int i = -1; i < got; ++i) {
@@ -144,8 +151,6 @@ int GemmTuner::tune(int shape, int b, cublasHandle_t blas, cudaStream_t s, const
       check_cuda(cudaEventElapsedTime(&ms, e0, e1), "cudaEventElapsedTime");
       t[i + 1].push_back(ms);
     }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   auto median = [](std::vector<float> v) {
     std::sort(v.begin(), v.end());
     return v[v.size() / 2];
