@@ -108,7 +108,9 @@ int glmx_kv_force_insert(glmx_kv* kv, uint64_t id, int32_t tier, uint64_t last_u
                          const char* session);
 /* CacheCounters (cache.hpp:41-49): hits, misses, evictions_by_tier[4] */
 int glmx_kv_counters(const glmx_kv* kv, int64_t out6[6]);
-/* resident_snapshot (cache.cpp:160-165), sorted by id; returns the resident count */
+/* resident_snapshot (cache.cpp:160-165), sorted by id; returns the resident count.  pages[i] is
+ * the block's page in the device pool, or -1 (device pools) when the page holds no KV for it (stale: inserted
+ * by a bookkeeping-only prefill, force_insert, or a batch that failed before its forward). */
 uint64_t glmx_kv_resident(const glmx_kv* kv, uint64_t* ids, int32_t* tiers, uint64_t* last_used,
                           int32_t* pages, uint64_t cap);
 /* CacheBlock::session of a resident block (cache.hpp:17-23); -1 when not resident */
@@ -145,6 +147,7 @@ int glmx_kv_ipc_handle(const glmx_kv* kv, uint8_t out[64]);
 int glmx_kv_attach_peer(glmx_kv* kv, int32_t peer, const uint8_t handle[64]);
 /* same-process variant: another pool (possibly on another device) as peer `peer` */
 int glmx_kv_attach_peer_local(glmx_kv* kv, int32_t peer, const glmx_kv* other);
+/* (entries with page < 0 are skipped) */
 int glmx_kv_set_peer_directory(glmx_kv* kv, uint64_t n, const uint64_t* block_ids,
                                const int32_t* peers, const int32_t* pages);
 int glmx_kv_set_epoch_mode(glmx_kv* kv, int32_t on);
@@ -300,7 +303,7 @@ int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
  * caller can stage batch r+1 while batch r runs (at most two batches in flight).
  * glmx_engine_wait completes the OLDEST in-flight batch: writes its greedy first tokens
  * (first_token[cap], -1 for empty prompts) and publishes its timings/work; returns its request
- * count, or -status.  The synchronous entry points, decode and replay wait for in-flight batches
+ * count, or -status.  The synchronous entry points and decode wait for in-flight batches
  * first. */
 int glmx_engine_prefill_segments_async(glmx_engine* e, uint64_t n_req,
                                        const glmx_segment_request* reqs,
@@ -320,9 +323,6 @@ int glmx_engine_decode(glmx_engine* e, const uint32_t* steps, int32_t* out_token
 int glmx_engine_decode_async(glmx_engine* e, const uint32_t* steps);
 int glmx_engine_decode_defer(glmx_engine* e, const uint32_t* steps);
 int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out_prev);
-/* Re-run the device forward of the last prefill batch (inputs already resident in HBM) —
- * used to time the device part alone; KV writes are idempotent. */
-int glmx_engine_replay_forward(glmx_engine* e);
 /* Per-phase device times of the last forward (CUDA events on the compute stream), ms:
  * [0] whole forward, [1] attention kernels (sum), [2] KV append (sum), [3] GEMMs (sum),
  * [4] other elementwise, [5] H2D, [6] D2H */
@@ -331,6 +331,11 @@ int glmx_engine_last_timings(const glmx_engine* e, float out7[7]);
  * Q in + O out), [2] K2 bytes (qkv read + q write + K/V page writes), [3] linear FLOPs, [4] computed tokens, [5] context tokens */
 int glmx_engine_last_work(const glmx_engine* e, double out6[6]);
 void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
+/* Bytes the engine moved between host and device since it was created: out2[0] host->device
+ * (batch and decode-step metadata: token ids, positions, slots, block tables, the attention
+ * schedule, peer-copy lists — the used part of each section only), out2[1] device->host
+ * (greedy tokens, requested logits). */
+int glmx_engine_io_bytes(const glmx_engine* e, uint64_t out2[2]);
 
 /* ================================================================== kernel-level test hooks */
 /* K4: copy pages (all layers) src_pages[i] -> dst_pages[i] between two pools (same or peer
@@ -348,13 +353,6 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
                             int32_t head_dim, float rope_theta, void* pool, uint32_t n_layers,
                             uint32_t layer, uint32_t block_tokens, void* q_out, int32_t reps,
                             void* stream, float* out_ms);
-/* Decode GEMM hook (kernel level, caller-owned DEVICE buffers): y[n][n_out] (+)= x[n][k] .
- * w[n_out][k]^T, bf16 inputs, on the tcgen05 weight-streaming kernel the engine uses for decode
- * steps (n <= 64, k % 64 == 0, n_out % 128 == 0).  mode 0: y bf16, 1: y fp32, 2: y fp32 += .
- * Launches `reps` times on `stream`; out_ms = mean device ms per launch.  Replaces cuBLAS for
- * the provider step's decode forwards (no reference counterpart). */
-int glmx_gemv_run(const void* w, const void* x, void* y, int32_t n, int32_t k, int32_t n_out,
-                  int32_t mode, int32_t reps, void* stream, float* out_ms);
 /* K3's persistent-CTA schedule (host only, no device): items w = i * n_kv_heads + h of work entries
  * work_xy[i] = (request, first token) are flattened into 128-key tiles and cut into <= n_sm
  * equal CTA ranges.  out_pieces [(n_work*n_kv_heads + n_sm) x 4] = (item, j0, j1, partial slot or
@@ -384,8 +382,8 @@ int32_t glmx_attn_trace_read(int64_t* out, int32_t n);
  * [n_layers][K|V][n_kv_heads][block_tokens][head_dim] bf16.  Host arrays per request: q_start,
  * q_len (suffix rows), ctx_len (cached + suffix keys), block_table [n_req][bt_stride] pages.
  * Causal over absolute positions (query t of request r sits at ctx_len - q_len + t).
- * impl 0 = tcgen05/TMEM/TMA kernel, 1 = mma.sync baseline, 2 = CUDA-core decode kernel (every
- * q_len == 1; the engine uses it for decode steps).  Launches `reps` times on `stream`;
+ * impl 0 = the tcgen05/TMEM/TMA prefill kernel, 2 = the CUDA-core decode kernel (every q_len == 1;
+ * the engine uses it for decode steps); any other value is GLMX_ERR_ARG.  Launches `reps` times on `stream`;
  * out_ms = mean device time per launch (CUDA events). */
 int glmx_attention_run(int32_t impl, const void* q, void* o, uint64_t n_q_rows, int32_t n_heads,
                        int32_t n_kv_heads, int32_t head_dim, void* pool, uint64_t n_pages,

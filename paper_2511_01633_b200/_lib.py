@@ -148,7 +148,7 @@ _SIGS = {
     "glmx_engine_decode_async": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
     "glmx_engine_decode_collect": (C.c_int, [C.c_void_p, i32p, i32p]),
     "glmx_engine_decode_defer": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
-    "glmx_engine_replay_forward": (C.c_int, [C.c_void_p]),
+    "glmx_engine_io_bytes": (C.c_int, [C.c_void_p, u64p]),
     "glmx_engine_last_timings": (C.c_int, [C.c_void_p, f32p]),
     "glmx_engine_last_work": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "glmx_engine_set_profiling": (None, [C.c_void_p, C.c_int32]),
@@ -173,8 +173,6 @@ _SIGS = {
     "glmx_retriever_stats": (None, [C.c_void_p, i64p]),
     "glmx_retrieve_last_kernel_ms": (C.c_float, [C.c_void_p]),
     "glmx_embed_text": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, f32p]),
-    "glmx_gemv_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                                C.c_int32, C.c_int32, C.c_void_p, f32p]),
     "glmx_attention_run": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                                      C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_uint64, i32p, i32p, i32p, i32p,

@@ -11,7 +11,6 @@ import ctypes as C
 from ._lib import check, lib
 
 TC = 0   # tcgen05 / TMEM / TMA kernel (the product path)
-MMA = 1  # mma.sync baseline (A/B only)
 DECODE = 2  # CUDA-core flash-decoding kernel for one-token rows (the engine's decode steps)
 
 
@@ -44,32 +43,6 @@ def paged_attention(q, o, pool, q_start, q_len, ctx_len, block_table, layer=0, i
                                    _i32(q_len), _i32(ctx_len), _i32(bt), stride, reps, s,
                                    C.byref(ms)))
     return ms.value
-
-
-def reference_attention(q, pool, q_start, q_len, ctx_len, block_table, layer=0):
-    """Plain PyTorch fp32 restatement (causal GQA over absolute positions) for the tests."""
-    import torch
-
-    n_pages, L, _, Hkv, B, hd = pool.shape
-    H = q.shape[1]
-    G = H // Hkv
-    out = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
-    scale = hd ** -0.5
-    for r in range(len(q_len)):
-        ctx, ql, qs = int(ctx_len[r]), int(q_len[r]), int(q_start[r])
-        pages = torch.tensor(block_table[r][:(ctx + B - 1) // B], device=pool.device,
-                             dtype=torch.long)
-        k = pool[pages, layer, 0].float().permute(1, 0, 2, 3).reshape(Hkv, -1, hd)[:, :ctx]
-        v = pool[pages, layer, 1].float().permute(1, 0, 2, 3).reshape(Hkv, -1, hd)[:, :ctx]
-        qq = q[qs:qs + ql].float().permute(1, 0, 2)                     # [H][ql][hd]
-        kk = k.repeat_interleave(G, dim=0)                               # [H][ctx][hd]
-        vv = v.repeat_interleave(G, dim=0)
-        s = torch.matmul(qq, kk.transpose(1, 2)) * scale                 # [H][ql][ctx]
-        pos = torch.arange(ctx - ql, ctx, device=q.device)[:, None]
-        key = torch.arange(ctx, device=q.device)[None, :]
-        s = s.masked_fill(key > pos, float("-inf"))
-        out[qs:qs + ql] = torch.matmul(torch.softmax(s, dim=-1), vv).permute(1, 0, 2)
-    return out
 
 
 def schedule(work, q_len, ctx_len, n_kv_heads=8, tokens_per_item=64, n_sm=148, pair=True):

@@ -30,7 +30,6 @@ int engine_decode_impl(glmx_engine*, const uint32_t*, int32_t*, float*);
 int engine_decode_enqueue(glmx_engine*, const uint32_t*);
 int engine_decode_collect(glmx_engine*, int32_t*, int32_t*, float*);
 int engine_decode_defer(glmx_engine*, const uint32_t*);
-int engine_replay_impl(glmx_engine*);
 int index_build_impl(glmx_graph*, int, uint64_t);
 int kv_gather_run_impl(void*, uint64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                        const int32_t*, uint64_t, void*, int, int, cudaStream_t, float*);
@@ -39,7 +38,6 @@ int retrieve_impl(glmx_graph*, const char*, const uint64_t*, uint64_t, int32_t*,
 int rope_append_run_impl(const void*, const int32_t*, const int64_t*, uint64_t, int, int, int,
                          float, void*, uint32_t, uint32_t, uint32_t, void*, int, cudaStream_t,
                          float*);
-int gemv_run_impl(const void*, const void*, void*, int, int, int, int, int, cudaStream_t, float*);
 int attention_run_impl(int, const void*, void*, uint64_t, int, int, int, void*, uint64_t, uint32_t,
                        uint32_t, uint32_t, uint64_t, const int32_t*, const int32_t*,
                        const int32_t*, const int32_t*, int, int, cudaStream_t, float*);
@@ -210,7 +208,7 @@ uint64_t glmx_kv_resident(const glmx_kv* kv, uint64_t* ids, int32_t* tiers, uint
     if (ids) ids[i] = v[i]->id;
     if (tiers) tiers[i] = v[i]->tier;
     if (last_used) last_used[i] = v[i]->last_used;
-    if (pages) pages[i] = v[i]->page;
+    if (pages) pages[i] = (kv->has_pool() && v[i]->stale) ? -1 : v[i]->page;  // -1: no KV (yet)
   }
   return v.size();
 }
@@ -303,8 +301,8 @@ int glmx_kv_set_peer_directory(glmx_kv* kv, uint64_t n, const uint64_t* block_id
     kv->peer_dir.reserve(n);
     const uint64_t total = kv->bk->pool().total();
     for (uint64_t i = 0; i < n; ++i) {
-      if (pages[i] < 0 || static_cast<uint64_t>(pages[i]) >= total)
-        throw Error(GLMX_ERR_ARG, "directory page out of range");
+      if (pages[i] < 0) continue;  // a stale block (no KV in its page): not servable
+      if (static_cast<uint64_t>(pages[i]) >= total) throw Error(GLMX_ERR_ARG, "directory page out of range");
       kv->peer_dir.emplace(block_ids[i], std::make_pair(peers[i], pages[i]));  // first wins
     }
     return GLMX_OK;
@@ -565,9 +563,6 @@ int glmx_engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out
 int glmx_engine_decode_defer(glmx_engine* e, const uint32_t* steps) {
   return guarded([&] { return engine_decode_defer(e, steps); });
 }
-int glmx_engine_replay_forward(glmx_engine* e) {
-  return guarded([&] { return engine_replay_impl(e); });
-}
 int glmx_engine_last_timings(const glmx_engine* e, float out7[7]) {
   std::memcpy(out7, e->timings, sizeof(e->timings));
   return GLMX_OK;
@@ -577,6 +572,11 @@ int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {  // of the las
   return GLMX_OK;
 }
 void glmx_engine_set_profiling(glmx_engine* e, int32_t level) { e->profiling = level; }
+int glmx_engine_io_bytes(const glmx_engine* e, uint64_t out2[2]) {
+  out2[0] = e->h2d_bytes;
+  out2[1] = e->d2h_bytes;
+  return GLMX_OK;
+}
 
 // ------------------------------------------------------------------ kernel test hooks
 int glmx_pool_copy(glmx_kv* src, glmx_kv* dst, const int32_t* src_pages,
@@ -597,13 +597,6 @@ int glmx_rope_kv_append_run(const void* qkv, const int32_t* pos, const int64_t* 
     return rope_append_run_impl(qkv, pos, slot, n_tokens, n_heads, n_kv_heads, head_dim,
                                 rope_theta, pool, n_layers, layer, block_tokens, q_out, reps,
                                 static_cast<cudaStream_t>(stream), out_ms);
-  });
-}
-
-int glmx_gemv_run(const void* w, const void* x, void* y, int32_t n, int32_t k, int32_t n_out,
-                  int32_t mode, int32_t reps, void* stream, float* out_ms) {
-  return guarded([&] {
-    return gemv_run_impl(w, x, y, n, k, n_out, mode, reps, static_cast<cudaStream_t>(stream), out_ms);
   });
 }
 

@@ -131,6 +131,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
   out.tail = toks.n - full * B_;
   out.pages.resize(full, -1);
   out.fresh.assign(full, 0);
+  out.stale.assign(full, 0);
 
   // Maximal resident chain prefix counts as cached (cache.cpp:70-81).
   uint64_t hit = 0;
@@ -138,6 +139,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
     auto it = resident_.find(out.ids[hit]);
     if (it == resident_.end()) break;
     out.pages[hit] = it->second.page;
+    out.stale[hit] = it->second.stale;
     ++hit;
   }
   out.hit_blocks = hit;
@@ -157,6 +159,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
       // Orphaned descendant of an evicted block: recomputed, stamp refreshed, tier upgraded.
       touch(it->second, ++clock_, tier);
       out.pages[b] = it->second.page;
+      out.stale[b] = it->second.stale;
       continue;
     }
     if (resident_.size() >= cap_) {
@@ -174,6 +177,7 @@ void BlockEngine::prefill(const TokenSpans& toks, const glmx_tier_range* tiers,
     blk.page = pool_.alloc();
     out.pages[b] = blk.page;
     out.fresh[b] = 1;
+    out.stale[b] = 1;
     order_insert(blk);
     owned_[blk.session].insert(blk.id);
     resident_.emplace(blk.id, blk);
@@ -232,9 +236,11 @@ void BlockEngine::set_tier(const std::string& session, int from, int to) {
 void BlockEngine::force_insert(uint64_t id, int tier, uint64_t last_used,
                                const std::string& session) {
   int32_t page = -1;
+  bool stale = true;  // a new block's page holds no KV
   auto it = resident_.find(id);
   if (it != resident_.end()) {
     page = it->second.page;
+    stale = it->second.stale;
     order_erase(it->second);
     auto o = owned_.find(it->second.session);
     if (o != owned_.end()) o->second.erase(id);
@@ -248,10 +254,22 @@ void BlockEngine::force_insert(uint64_t id, int tier, uint64_t last_used,
   b.last_used = last_used;
   b.session = intern(session);
   b.page = page;
+  b.stale = stale;
   order_insert(b);
   owned_[b.session].insert(id);
   resident_.emplace(id, b);
   clock_ = std::max(clock_, last_used);
+}
+
+void BlockEngine::set_stale(uint64_t id, bool stale) {
+  auto it = resident_.find(id);
+  if (it != resident_.end()) it->second.stale = stale;
+}
+
+int32_t BlockEngine::ensure_page(uint64_t id) {
+  Block& b = resident_.at(id);
+  if (b.page < 0) b.page = pool_.alloc();
+  return b.page;
 }
 
 const Block* BlockEngine::block(uint64_t id) const {

@@ -27,6 +27,10 @@ struct Block {                // CacheBlock (cache.hpp:17-23) + physical page
   uint64_t last_used = 0;
   int32_t session = 0;        // interned owner; 0 == "" (shared)
   int32_t page = -1;          // physical page in the device pool, -1 = none (force_insert)
+  // the page does not hold this block's KV yet: inserted by a prefill whose forward has not been
+  // enqueued (or never was: a failed batch, a bookkeeping-only prefill, force_insert).  The
+  // engine recomputes a stale block on its next use instead of attending over the page.
+  bool stale = true;
 };
 
 // Deterministic physical-page allocator (LIFO free list).
@@ -60,6 +64,7 @@ struct PrefillResult {        // PrefillReport (cache.hpp:33-39) + block table
   std::vector<uint64_t> ids;     // chain ids of the full blocks
   std::vector<int32_t> pages;    // physical page per full block
   std::vector<uint8_t> fresh;    // 1 = inserted by this call (new page, KV not yet present)
+  std::vector<uint8_t> stale;    // per full block: Block::stale at the end of the call
   uint64_t hit_blocks = 0;
 };
 
@@ -81,6 +86,10 @@ class BlockEngine {
   static void chain_ids(const TokenSpans& toks, uint32_t B, std::vector<uint64_t>& out);
 
   const Block* block(uint64_t id) const;
+  // KV-presence flag of a resident block (no-op for absent ids); ensure_page gives a resident
+  // block without a page (force_insert on a full pool) one, returning it
+  void set_stale(uint64_t id, bool stale);
+  int32_t ensure_page(uint64_t id);
   std::vector<const Block*> resident_sorted() const;
   uint64_t resident() const { return resident_.size(); }
   uint64_t capacity() const { return cap_; }

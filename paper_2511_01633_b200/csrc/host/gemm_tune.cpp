@@ -97,12 +97,8 @@ int GemmTuner::tune(int shape, int b, cublasHandle_t blas, cudaStream_t s, const
   check_lt(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
                                                 &ws_bytes, sizeof(ws_bytes)),
            "pref workspace");
-  // GLMX_GEMM_TUNE="candidates,rounds" overrides the defaults (dev A/B only)
-  static const std::pair<int, int> knobs = [] {
-    int c = kCandidates, r = 3;
-    if (const char* v = std::getenv("GLMX_GEMM_TUNE")) std::sscanf(v, "%d,%d", &c, &r);
-    return std::make_pair(std::clamp(c, 1, kMaxCandidates), std::max(1, r));
-  }();
+  // candidates, interleaved rounds (a wider search, 12 x 5, measured no better: DESIGN.md §5)
+  static constexpr std::pair<int, int> knobs{kCandidates, 3};
   cublasLtMatmulHeuristicResult_t res[kMaxCandidates];
   int got = 0;
   const cublasStatus_t hs = cublasLtMatmulAlgoGetHeuristic(lt_, desc_, l.A(), l.B(), l.C(), l.C(),

@@ -24,13 +24,6 @@ struct AttnParams {
   float scale_log2;  // softmax scale * log2(e)
 };
 
-// Query rows per CTA tile: 64 / (H / Hkv) tokens x (H / Hkv) heads of one kv head.
-int attn_tokens_per_tile(int H, int Hkv);
-void paged_attention(const AttnParams& p, cudaStream_t s);
-
-}  // namespace glmx
-
-namespace glmx {
 // tcgen05 / TMEM / TMA version (attn_tc.cu): 128 query rows per CTA.
 int attn_tc_tokens_per_tile(int H, int Hkv);
 void make_pool_tensor_map(const PoolGeom& g, uint64_t pages, void* out_map, uint32_t* rows_total);

@@ -43,10 +43,6 @@ constexpr int kHalf = 16384;  // bytes of one [128][64] bf16 SW128 half tile
 constexpr int kTile = 2 * kHalf;
 constexpr int kKSlots = 3;    // K ring depth (32 KB [128 keys][128 dims] tiles)
 constexpr int kVSlots = 2;    // V ring depth
-#ifndef GLMX_POLY_FROM
-#define GLMX_POLY_FROM 8
-#endif
-constexpr int kPolyFrom = GLMX_POLY_FROM;  // of every 8 P pairs, [kPolyFrom, 8) use the polynomial
 constexpr int kSoftmaxThreads = 128 * kQT;
 constexpr int kThreads = kSoftmaxThreads + 96;  // + K producer, MMA, V producer warps
 // registers: up to 3 warps per SM sub-partition (16K regs each) -> <= 168 per thread
@@ -64,18 +60,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-// 2^x (x <= 8) on the FMA pipe: round-to-nearest split by the 1.5 * 2^23 magic (t's low mantissa
-// bits hold n = rint(x)), degree-3 minimax of 2^f on [-0.5, 0.5] (max rel err 7.5e-5), exponent
-// added as an integer; x clamped to -126.  Only used when GLMX_POLY_FROM < 8 (measured slower).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float q = fmaf(f, 0.05517161265015602f, 0.24261116981506348f);
-  q = fmaf(q, f, 0.6932610273361206f);
-  q = fmaf(q, f, 0.9999280571937561f);
-  return __uint_as_float(__float_as_uint(q) + (__float_as_uint(t) << 23));
 }
 // kind::f16 instruction descriptor: D f32, A/B bf16, M=128.
 __host__ __device__ constexpr uint32_t idesc_bf16(int n, bool b_mn_major) {
@@ -476,24 +460,18 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
           m_used = mx;
         }
         // P = 2^(s*scale - m_used) as bf16 pairs into the first 64 columns of S_i (the S values
-        // are already in registers); masked keys are -inf -> 0.
-        // P = 2^(s*scale - m_used) as bf16 pairs into the first 64 columns of S_i (the S values
         // are already in registers); masked keys are -inf -> 0.  The first 32 packed columns
         // are stored while the second half is computed.  (Packed fp32x2 FFMA2/FADD2 and a
         // polynomial exp2 for a quarter of the pairs were measured slower here: the softmax
         // phase went from ~1650 to ~2000 cycles per tile, scripts/attn_trace.py.)
-        const float neg_m = -m_used;
+        // a row with no visible key so far (a split piece that starts past its position) keeps
+        // m_used = -inf: use 0 so 2^(-inf - m) is 0, not 2^(-inf + inf) = NaN
+        const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < kN; i += 2) {
-          float p0, p1;
-          if (((i >> 1) & 7) >= kPolyFrom) {
-            p0 = ex2_poly(fmaf(__uint_as_float(v[i]), scale, neg_m));
-            p1 = ex2_poly(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
-          } else {
-            p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
-            p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
-          }
+          const float p0 = ex2(fmaf(__uint_as_float(v[i]), scale, neg_m));
+          const float p1 = ex2(fmaf(__uint_as_float(v[i + 1]), scale, neg_m));
           ls[(i >> 1) & 3] += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           v[i >> 1] = *reinterpret_cast<uint32_t*>(&b2);
@@ -594,7 +572,8 @@ attn_combine_kernel(AttnParams p, const int4* __restrict__ combine, const float*
   for (int k = 0; k < cb.z; ++k) {
     const int64_t prow = static_cast<int64_t>(cb.y + k) * (kQT * kM) + rr;
     const float2 ml = part_ml[prow];
-    const float wgt = ml.x == -INFINITY ? 0.f : ex2(ml.x - m);
+    if (ml.x == -INFINITY || ml.y == 0.f) continue;  // piece with no visible key for this row
+    const float wgt = ex2(ml.x - m);
     const float4 o = reinterpret_cast<const float4*>(part_o + prow * kHD)[lane];
     acc.x += wgt * o.x;
     acc.y += wgt * o.y;

@@ -7,7 +7,6 @@
 #include "kernels/common.cuh"
 #include "kernels/retrieve.cuh"
 #include "kernels/ingest.cuh"
-#include "kernels/gemv_tc.cuh"
 #include "host/workload_gen.hpp"
 
 using namespace glmx;
@@ -90,6 +89,7 @@ glmx_engine::~glmx_engine() {
   for (auto e : done_ev)
     if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
+  if (m) --m->n_engines;
 }
 
 // ======================================================================== graph upload
@@ -403,6 +403,8 @@ int model_export_impl(const glmx_model* m, int which, int layer, uint16_t* out, 
 // Times the projection GEMMs' algorithm candidates per M bucket (host/gemm_tune.hpp) on layer
 // 0's weights and random activations; T <= 128 (decode rows) stays with cublasGemmEx.
 int model_tune_gemms_impl(glmx_model* m, int max_tokens) {
+  if (m->n_engines > 0)
+    throw Error(GLMX_ERR_ARG, "tune the GEMMs before creating engines (the table is read by every forward)");
   if (max_tokens <= 128) return 0;
   DeviceGuard g(m->device);
   const auto& c = m->cfg;
@@ -457,25 +459,20 @@ int model_tune_gemms_impl(glmx_model* m, int max_tokens) {
 // ======================================================================== engine
 namespace {
 
-// K3 pairs single-query-tile items two per CTA pass (GLMX_ATTN_PAIR=0 disables, for A/B runs)
-bool attn_pairing() {
-  static const bool on = [] {
-    const char* v = std::getenv("GLMX_ATTN_PAIR");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
-
 // Y[T][out] (+)= X[T][in] * W[out][in]^T  (column-major: C(out x T) = W^T' * X); `shape` names
 // the projection for the tuned algorithm table (host/gemm_tune.hpp), -1 = always cublasGemmEx
-void gemm(glmx_model* m, int shape, cudaStream_t s, const __nv_bfloat16* X,
-          const __nv_bfloat16* W, void* Y, bool y_fp32, bool accumulate, int T, int in, int out) {
+// (the workspace is the calling engine's: engines sharing a model run on their own streams)
+void gemm(glmx_engine* e, int shape, const __nv_bfloat16* X, const __nv_bfloat16* W, void* Y,
+          bool y_fp32, bool accumulate, int T, int in, int out) {
   if (T <= 0) return;
-  if (shape >= 0 && m->tuner.run(shape, s, X, W, Y, y_fp32, accumulate, T, in, out, m->blas_ws,
+  glmx_model* m = e->m;
+  cudaStream_t s = e->stream;
+  if (shape >= 0 && m->tuner.run(shape, s, X, W, Y, y_fp32, accumulate, T, in, out, e->blas_ws.p,
                                  kBlasWsBytes))
     return;
   cublasHandle_t h = m->blas;
   GLMX_BLAS(cublasSetStream(h, s));
+  GLMX_BLAS(cublasSetWorkspace(h, e->blas_ws.p, kBlasWsBytes));
   const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
   GLMX_BLAS(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, out, T, in, &alpha, W, CUDA_R_16BF, in, X,
                          CUDA_R_16BF, in, &beta, Y, y_fp32 ? CUDA_R_32F : CUDA_R_16BF, out,
@@ -528,10 +525,12 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
     throw Error(GLMX_ERR_ARG, "kv pool geometry does not match the model");
   auto e = std::make_unique<glmx_engine>();
   e->m = m;
+  ++m->n_engines;  // (the destructor undoes it)
   e->kv = kv;
   e->cfg = *cfg;
   DeviceGuard g(m->device);
   GLMX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  e->blas_ws.reserve(kBlasWsBytes);
   GLMX_CUDA(cudaEventCreateWithFlags(&e->h2d_done, cudaEventDisableTiming));
   GLMX_CUDA(cudaEventCreateWithFlags(&e->fwd_done, cudaEventDisableTiming));
   // decode steps may merge two batches' rows (deferred decode): row buffers hold 2 x max_requests
@@ -542,15 +541,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   // block-table rows padded to a multiple of 8 pages: K3 reads a key tile's 8 entries with two
   // 16-byte loads
   e->bt_stride = static_cast<int>(align_up((cfg->max_context + B - 1) / B + 1, 8));
-  const char* impl = std::getenv("GLMX_ATTN");
-  e->attn_impl = (impl && std::string(impl) == "mma") ? 1 : 0;
-  {
-    const char* dv = std::getenv("GLMX_DECODE_ATTN");
-    e->decode_cc = !(dv && std::string(dv) == "tc");
-    e->decode_fuse = !(dv && std::string(dv) == "unfused");
-  }
-  e->tpt = e->attn_impl ? attn_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv))
-                        : attn_tc_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
+  e->tpt = attn_tc_tokens_per_tile(static_cast<int>(H), static_cast<int>(Hkv));
   make_pool_tensor_map(kv->geom, kv->bk->pool().total(), e->kv_map, &e->kv_rows);
   e->x.reserve(T * d * 4);
   e->h.reserve(T * d * 2);
@@ -565,7 +556,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->next_tok.reserve((R * (cfg->max_decode + 1) + 16) * 4);
   e->amax_keys.reserve(R * 8 + 64);
   // metadata layout (one pinned block, one H2D)
-  const uint64_t max_work = T / 1 + R;  // upper bound on attention tiles
+  const uint64_t max_work = T / e->tpt + R;  // attention work items: sum of ceil(q_len / tpt)
   size_t o = 0;
   e->o_tok = o; o = align_up(o + T * 4, 256);
   e->o_pos = o; o = align_up(o + T * 4, 256);
@@ -604,9 +595,9 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
 namespace {
 
 // One-token batches (decode steps) take the CUDA-core decode kernel: returns its split count, or
-// 0 when the batch has a longer row (prefill) or the path is off / unsupported.
+// 0 when the batch has a longer row (prefill) or the geometry is not the kernel's (G != 4).
 int choose_decode_split(glmx_engine* e, int R, int T, const int32_t* ctx_len) {
-  if (e->attn_impl || !e->decode_cc || R <= 0 || T != R) return 0;
+  if (R <= 0 || T != R) return 0;
   const auto& c = e->m->cfg;
   if (c.n_heads != 4 * c.n_kv_heads || c.head_dim != 128 || e->kv->cfg.block_tokens != 16) return 0;
   int max_ctx = 0;
@@ -622,10 +613,55 @@ uint8_t* meta_acquire(glmx_engine* e) {
   e->h_meta = e->h_ring[e->ring_slot];
   return static_cast<uint8_t*>(e->h_meta);
 }
-// Uploads the current slot to the device metadata buffer (stream-ordered after the previous
-// batch's kernels that read it).
-void meta_commit(glmx_engine* e, cudaStream_t s) {
-  GLMX_CUDA(cudaMemcpyAsync(e->meta.p, e->h_meta, e->meta_bytes, cudaMemcpyHostToDevice, s));
+// Used sizes of the staged sections (rows, requests, work items, schedule, peer copies) and the
+// batch's block-table stride (a multiple of 8 entries: K3 reads a key tile's 8 pages as 2 x 16 B).
+struct MetaCounts {
+  int n_tok = 0;  // token ids (prefill; decode steps read their input tokens on the device)
+  int T = 0, R = 0, n_work = 0, n_perm = 0, n_copy = 0, bt_stride = 8;
+  bool sched = false;  // the K3 schedule was staged (prefill-shaped batch)
+};
+
+// Packs the used part of every section of the current slot in place (sections keep their
+// order, so a section's packed offset never exceeds its staging offset and forward memmoves are
+// safe; block-table rows move from the capacity stride to the batch stride) and uploads exactly
+// those bytes to the device metadata buffer, stream-ordered after the previous batch's kernels.
+void meta_commit(glmx_engine* e, cudaStream_t s, const MetaCounts& n) {
+  uint8_t* hm = static_cast<uint8_t*>(e->h_meta);
+  glmx_engine::MetaLayout L{};
+  size_t o = 0;
+  auto put = [&](size_t src, size_t bytes) {
+    const size_t dst = o;
+    if (bytes && dst != src) std::memmove(hm + dst, hm + src, bytes);
+    o = align_up(o + bytes, 16);
+    return dst;
+  };
+  L.tok = put(e->o_tok, static_cast<size_t>(n.n_tok) * 4);
+  L.pos = put(e->o_pos, static_cast<size_t>(n.T) * 4);
+  L.slot = put(e->o_slot, static_cast<size_t>(n.T) * 8);
+  L.qs = put(e->o_qs, static_cast<size_t>(n.R) * 4);
+  L.ql = put(e->o_ql, static_cast<size_t>(n.R) * 4);
+  L.ctx = put(e->o_ctx, static_cast<size_t>(n.R) * 4);
+  L.bt = o;
+  L.bt_stride = n.bt_stride;
+  const size_t row = static_cast<size_t>(n.bt_stride) * 4;
+  for (int r = 0; r < n.R; ++r) {
+    const size_t src = e->o_bt + static_cast<size_t>(r) * e->bt_stride * 4;
+    if (L.bt + r * row != src) std::memmove(hm + L.bt + r * row, hm + src, row);
+  }
+  o = align_up(o + n.R * row, 16);
+  L.work = put(e->o_work, static_cast<size_t>(n.n_work) * 8);
+  L.last = put(e->o_last, static_cast<size_t>(n.R) * 4);
+  L.perm = put(e->o_perm, static_cast<size_t>(n.n_perm) * 4);
+  const size_t sp = n.sched ? static_cast<size_t>(e->sc_npieces) * sizeof(AttnPiece) : 0;
+  L.pieces = put(e->o_sched + e->o_sc_pieces, sp);
+  L.partners = put(e->o_sched + e->o_sc_part, sp);
+  L.cta = put(e->o_sched + e->o_sc_cta, n.sched ? static_cast<size_t>(e->sc_grid + 1) * 4 : 0);
+  L.comb = put(e->o_sched + e->o_sc_comb, n.sched ? static_cast<size_t>(e->sc_ncomb) * sizeof(AttnCombine) : 0);
+  L.copy = put(e->o_copy, static_cast<size_t>(n.n_copy) * 8);
+  L.bytes = o;
+  e->ml = L;
+  GLMX_CUDA(cudaMemcpyAsync(e->meta.p, hm, o, cudaMemcpyHostToDevice, s));
+  e->h2d_bytes += o;
   GLMX_CUDA(cudaEventRecord(e->ring_ev[e->ring_slot], s));
   GLMX_CUDA(cudaEventRecord(e->h2d_done, s));
 }
@@ -637,12 +673,13 @@ void stage_attn_schedule(glmx_engine* e, uint8_t* hm, const int2* work, int n_wo
   sc.pieces = reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_pieces);
   sc.cta_off = reinterpret_cast<int32_t*>(hm + e->o_sched + e->o_sc_cta);
   sc.combine = reinterpret_cast<AttnCombine*>(hm + e->o_sched + e->o_sc_comb);
-  sc.partners = attn_pairing() ? reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_part) : nullptr;
+  sc.partners = reinterpret_cast<AttnPiece*>(hm + e->o_sched + e->o_sc_part);
   build_attn_schedule(reinterpret_cast<const int32_t*>(work), n_work,
                       static_cast<int>(e->m->cfg.n_kv_heads), q_len, ctx_len, e->tpt, 128,
                       kNumSMs, sc);
   e->sc_grid = sc.grid;
   e->sc_ncomb = sc.n_combine;
+  e->sc_npieces = sc.n_pieces;
 }
 
 // Runs the decoder over the staged batch: T rows (tokens/pos/slot), R requests (attention
@@ -654,28 +691,29 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   const int QKV = (H + 2 * Hkv) * hd;
   cudaStream_t s = e->stream;
   uint8_t* meta = e->meta.as<uint8_t>();
-  const int32_t* pos = reinterpret_cast<const int32_t*>(meta + e->o_pos);
-  const int64_t* slot = reinterpret_cast<const int64_t*>(meta + e->o_slot);
+  const glmx_engine::MetaLayout& ml = e->ml;
+  const int32_t* pos = reinterpret_cast<const int32_t*>(meta + ml.pos);
+  const int64_t* slot = reinterpret_cast<const int64_t*>(meta + ml.slot);
   AttnParams ap{};
   ap.q = e->q.as<__nv_bfloat16>();
   ap.o = e->attn.as<__nv_bfloat16>();
   ap.pool = e->kv->geom;
-  ap.q_start = reinterpret_cast<const int32_t*>(meta + e->o_qs);
-  ap.q_len = reinterpret_cast<const int32_t*>(meta + e->o_ql);
-  ap.ctx_len = reinterpret_cast<const int32_t*>(meta + e->o_ctx);
-  ap.block_table = reinterpret_cast<const int32_t*>(meta + e->o_bt);
-  ap.bt_stride = e->bt_stride;
-  ap.work = reinterpret_cast<const int2*>(meta + e->o_work);
+  ap.q_start = reinterpret_cast<const int32_t*>(meta + ml.qs);
+  ap.q_len = reinterpret_cast<const int32_t*>(meta + ml.ql);
+  ap.ctx_len = reinterpret_cast<const int32_t*>(meta + ml.ctx);
+  ap.block_table = reinterpret_cast<const int32_t*>(meta + ml.bt);
+  ap.bt_stride = ml.bt_stride;
+  ap.work = reinterpret_cast<const int2*>(meta + ml.work);
   ap.n_work = n_work;
   ap.H = H;
   ap.Hkv = Hkv;
   ap.scale_log2 = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)) * 1.4426950408889634);
   (void)R;
-  AttnTcSched sc{reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_pieces),
-                 reinterpret_cast<const int*>(meta + e->o_sched + e->o_sc_cta),
-                 reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_comb),
+  AttnTcSched sc{reinterpret_cast<const int4*>(meta + ml.pieces),
+                 reinterpret_cast<const int*>(meta + ml.cta),
+                 reinterpret_cast<const int4*>(meta + ml.comb),
                  e->sc_grid, e->sc_ncomb, e->part_o.as<float>(), e->part_ml.as<float2>(),
-                 attn_pairing() ? reinterpret_cast<const int4*>(meta + e->o_sched + e->o_sc_part) : nullptr};
+                 reinterpret_cast<const int4*>(meta + ml.partners)};
   Prof all(e, kCatAll);
   {
     Prof p(e, kCatOther);
@@ -689,10 +727,10 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m, kGemmQKV, s, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
+      gemm(e, kGemmQKV, e->h.as<__nv_bfloat16>(), w.wqkv, e->qkv.p, false, false, T, d, QKV);
     }
     // decode rows with the fused kernel: RoPE + K/V append happen inside the decode attention
-    const bool fuse = e->dec_split && e->decode_fuse;
+    const bool fuse = e->dec_split > 0;
     if (!fuse) {
       Prof p(e, kCatAppend);
       rope_kv_append(e->qkv.as<__nv_bfloat16>(), pos, slot, T, H, Hkv, hd, m->inv_freq,
@@ -704,16 +742,12 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
       if (fuse)
         paged_attention_decode_rope(ap, DecodeRope{e->qkv.as<__nv_bfloat16>(), pos, slot, m->inv_freq},
                                     R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
-      else if (e->dec_split)
-        paged_attention_decode(ap, R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
-      else if (e->attn_impl)
-        paged_attention(ap, s);
       else
         paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, sc, s);
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m, kGemmO, s, e->attn.as<__nv_bfloat16>(), w.wo, e->x.p, true, true, T, H * hd, d);
+      gemm(e, kGemmO, e->attn.as<__nv_bfloat16>(), w.wo, e->x.p, true, true, T, H * hd, d);
     }
     {
       Prof p(e, kCatOther);
@@ -721,7 +755,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m, kGemmGU, s, e->h.as<__nv_bfloat16>(), w.wgu, e->gu.p, false, false, T, d, 2 * ff);
+      gemm(e, kGemmGU, e->h.as<__nv_bfloat16>(), w.wgu, e->gu.p, false, false, T, d, 2 * ff);
     }
     {
       Prof p(e, kCatOther);
@@ -729,17 +763,17 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     }
     {
       Prof p(e, kCatGemm);
-      gemm(m, kGemmDown, s, e->act.as<__nv_bfloat16>(), w.wdown, e->x.p, true, true, T, ff, d);
+      gemm(e, kGemmDown, e->act.as<__nv_bfloat16>(), w.wdown, e->x.p, true, true, T, ff, d);
     }
   }
   {
     Prof p(e, kCatOther);
-    rmsnorm(e->x.as<float>(), reinterpret_cast<const int32_t*>(meta + e->o_last), n_last, d,
+    rmsnorm(e->x.as<float>(), reinterpret_cast<const int32_t*>(meta + ml.last), n_last, d,
             m->final_norm, c.norm_eps, e->hl.as<__nv_bfloat16>(), s);
   }
   {
     Prof p(e, kCatGemm);
-    gemm(m, -1, s, e->hl.as<__nv_bfloat16>(), m->lm_head, e->logits.p, true, false, n_last, d,
+    gemm(e, -1, e->hl.as<__nv_bfloat16>(), m->lm_head, e->logits.p, true, false, n_last, d,
          c.vocab);
   }
 }
@@ -785,6 +819,10 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   const auto& c = m->cfg;
   const uint32_t B = kv->cfg.block_tokens;
   if (n_req > e->cfg.max_requests) throw Error(GLMX_ERR_ARG, "too many requests in batch");
+  // engine limits that do not depend on cache state are checked before any bookkeeping
+  for (uint64_t i = 0; i < n_req; ++i)
+    if (reqs[i].n_tok > 0 && reqs[i].n_tok + e->cfg.max_decode > e->cfg.max_context)
+      throw Error(GLMX_ERR_ARG, "request exceeds max_context");
   DeviceGuard dg(m->device);
   // The previous batch's scratch pages become free (device reuse is stream-ordered after its
   // forward and decode steps); its staging slot stays untouched until its upload was consumed.
@@ -792,6 +830,9 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     for (int32_t p : r.scratch) bk.pool().free_now(p);
   e->reqs.clear();
   e->has_batch = false;
+  // Pages evicted by earlier batches: every batch that may read them is enqueued by now, unless
+  // the last batch's decode is deferred (it still reads that batch's self-evicted pages).
+  if (!kv->epoch_mode && !e->def_R) bk.pool().release_before(e->rel_mark);
 
   uint8_t* hm = meta_acquire(e);
   int32_t* h_tok = reinterpret_cast<int32_t*>(hm + e->o_tok);
@@ -806,66 +847,104 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
 
   PrefillResult pr;
   int T = 0, R = 0, n_work = 0;
+  size_t max_pages = 0;
   std::vector<int> req_row(n_req, -1);
   e->copies.clear();
+  e->batch_written.clear();
   double attn_flops = 0, attn_bytes = 0, ctx_tokens = 0;
   const double kv_tok_bytes = 2.0 * c.n_kv_heads * c.head_dim * 2;  // per layer
-  for (uint64_t i = 0; i < n_req; ++i) {
-    const glmx_request& rq = reqs[i];
-    TokenSpans ts{rq.tok_bytes, rq.tok_offsets, rq.n_tok};
-    bk.prefill(ts, rq.tiers, rq.n_tiers, rq.session ? rq.session : "", pr);  // may throw
-    glmx_prefill_report& rep = reports[i];
-    rep.cached_tokens = pr.cached;
-    rep.computed_tokens = pr.computed;
-    rep.tail_tokens = pr.tail;
-    rep.n_evicted = pr.evicted.size();
-    rep.n_blocks = pr.pages.size();
-    if (first_token) first_token[i] = -1;
-    if (rq.n_tok == 0) continue;
-    glmx_engine::Req st;
-    st.pages = pr.pages;
-    const uint64_t full_tok = pr.pages.size() * B;
-    const uint64_t need = rq.n_tok + e->cfg.max_decode;
-    if (need > e->cfg.max_context) throw Error(GLMX_ERR_ARG, "request exceeds max_context");
-    for (uint64_t t = full_tok; t < need; t += B) {
-      int32_t p = bk.pool().alloc();
-      st.scratch.push_back(p);
-      st.pages.push_back(p);
-    }
-    // Cross-GPU prefix hit: the run of freshly inserted blocks that directly extends the local
-    // hit prefix and is resident on a peer is copied instead of computed (bookkeeping already
-    // counted them as misses, like independent per-GPU caches).
-    uint64_t reuse_blocks = pr.hit_blocks;
-    if (!kv->peer_dir.empty()) {
-      for (uint64_t b = pr.hit_blocks; b < pr.pages.size() && pr.fresh[b]; ++b) {
-        auto it = kv->peer_dir.find(pr.ids[b]);
-        if (it == kv->peer_dir.end()) break;
-        e->copies.push_back({it->second.first, it->second.second, pr.pages[b]});
-        ++reuse_blocks;
+  try {
+    for (uint64_t i = 0; i < n_req; ++i) {
+      const glmx_request& rq = reqs[i];
+      TokenSpans ts{rq.tok_bytes, rq.tok_offsets, rq.n_tok};
+      // may throw with partial state, exactly like the reference; the blocks it inserted stay
+      // stale, so their KV is recomputed on first use
+      bk.prefill(ts, rq.tiers, rq.n_tiers, rq.session ? rq.session : "", pr);
+      glmx_prefill_report& rep = reports[i];
+      rep.cached_tokens = pr.cached;
+      rep.computed_tokens = pr.computed;
+      rep.tail_tokens = pr.tail;
+      rep.n_evicted = pr.evicted.size();
+      rep.n_blocks = pr.pages.size();
+      if (first_token) first_token[i] = -1;
+      if (rq.n_tok == 0) continue;
+      e->reqs.emplace_back();
+      glmx_engine::Req& st = e->reqs.back();
+      st.pages = pr.pages;
+      const uint64_t full = pr.pages.size();
+      const uint64_t need = rq.n_tok + e->cfg.max_decode;
+      for (uint64_t t = full * B; t < need; t += B) {
+        int32_t p = bk.pool().alloc();
+        st.scratch.push_back(p);
+        st.pages.push_back(p);
       }
+      // KV reuse = the leading cached blocks whose pages hold their KV; a stale cached block
+      // (its batch failed, or it was inserted without the engine) is recomputed from there on
+      uint64_t reuse_blocks = 0;
+      while (reuse_blocks < pr.hit_blocks && !pr.stale[reuse_blocks]) ++reuse_blocks;
+      // Cross-GPU prefix hit: the run of freshly inserted blocks that directly extends the local
+      // hit prefix and is resident on a peer is copied instead of computed (bookkeeping already
+      // counted them as misses, like independent per-GPU caches).
+      if (reuse_blocks == pr.hit_blocks && !kv->peer_dir.empty()) {
+        for (uint64_t b = pr.hit_blocks; b < full && pr.fresh[b]; ++b) {
+          auto it = kv->peer_dir.find(pr.ids[b]);
+          if (it == kv->peer_dir.end()) break;
+          e->copies.push_back({it->second.first, it->second.second, pr.pages[b]});
+          ++reuse_blocks;
+        }
+      }
+      const uint64_t q0 = std::min<uint64_t>(reuse_blocks * B, rq.n_tok - 1);  // always >= 1 row
+      const int ql = static_cast<int>(rq.n_tok - q0);
+      if (T + ql > static_cast<int>(e->cfg.max_batch_tokens))
+        throw Error(GLMX_ERR_ARG, "batch exceeds max_batch_tokens");
+      // every block from reuse_blocks on is written by this batch (peer copy or K2 append):
+      // no longer stale for the requests staged after this one (the append of a layer precedes
+      // its attention); re-marked if the batch fails before its forward is enqueued
+      for (uint64_t b = std::min(pr.hit_blocks, reuse_blocks); b < full; ++b) {
+        if (st.pages[b] < 0) {  // a force_insert'ed block without a page
+          if (bk.block(pr.ids[b])) {
+            st.pages[b] = bk.ensure_page(pr.ids[b]);
+          } else {  // ... already evicted again by this request: a scratch page serves it
+            st.pages[b] = bk.pool().alloc();
+            st.scratch.push_back(st.pages[b]);
+          }
+        }
+        const Block* blk = bk.block(pr.ids[b]);
+        if (blk && blk->stale) {
+          bk.set_stale(pr.ids[b], false);
+          e->batch_written.push_back(pr.ids[b]);
+        }
+      }
+      h_qs[R] = T;
+      h_ql[R] = ql;
+      h_ctx[R] = static_cast<int32_t>(rq.n_tok);
+      std::memcpy(h_bt + static_cast<size_t>(R) * e->bt_stride, st.pages.data(), st.pages.size() * 4);
+      max_pages = std::max(max_pages, st.pages.size());
+      for (uint64_t t = q0; t < rq.n_tok; ++t, ++T) {
+        h_tok[T] = token_id(rq.tok_bytes + rq.tok_offsets[t], rq.tok_offsets[t + 1] - rq.tok_offsets[t], c.vocab);
+        h_pos[T] = static_cast<int32_t>(t);
+        h_slot[T] = static_cast<int64_t>(st.pages[t / B]) * B + (t % B);
+      }
+      for (int t0 = 0; t0 < ql; t0 += e->tpt) h_work[n_work++] = make_int2(R, t0);
+      h_last[R] = T - 1;
+      req_row[i] = R;
+      for (uint64_t qi = q0; qi < rq.n_tok; ++qi) attn_flops += 4.0 * c.n_heads * c.head_dim * (qi + 1);
+      attn_bytes += kv_tok_bytes * rq.n_tok + 2.0 * ql * c.n_heads * c.head_dim * 2;
+      ctx_tokens += rq.n_tok;
+      st.ctx_len = static_cast<int32_t>(rq.n_tok);
+      ++R;
     }
-    const uint64_t q0 = std::min<uint64_t>(reuse_blocks * B, rq.n_tok - 1);  // always >= 1 row
-    const int ql = static_cast<int>(rq.n_tok - q0);
-    if (T + ql > static_cast<int>(e->cfg.max_batch_tokens))
-      throw Error(GLMX_ERR_ARG, "batch exceeds max_batch_tokens");
-    h_qs[R] = T;
-    h_ql[R] = ql;
-    h_ctx[R] = static_cast<int32_t>(rq.n_tok);
-    std::memcpy(h_bt + static_cast<size_t>(R) * e->bt_stride, st.pages.data(), st.pages.size() * 4);
-    for (uint64_t t = q0; t < rq.n_tok; ++t, ++T) {
-      h_tok[T] = token_id(rq.tok_bytes + rq.tok_offsets[t], rq.tok_offsets[t + 1] - rq.tok_offsets[t], c.vocab);
-      h_pos[T] = static_cast<int32_t>(t);
-      h_slot[T] = static_cast<int64_t>(st.pages[t / B]) * B + (t % B);
-    }
-    for (int t0 = 0; t0 < ql; t0 += e->tpt) h_work[n_work++] = make_int2(R, t0);
-    h_last[R] = T - 1;
-    req_row[i] = R;
-    for (uint64_t qi = q0; qi < rq.n_tok; ++qi) attn_flops += 4.0 * c.n_heads * c.head_dim * (qi + 1);
-    attn_bytes += kv_tok_bytes * rq.n_tok + 2.0 * ql * c.n_heads * c.head_dim * 2;
-    ctx_tokens += rq.n_tok;
-    st.ctx_len = static_cast<int32_t>(rq.n_tok);
-    e->reqs.push_back(std::move(st));
-    ++R;
+    if (e->copies.size() > e->max_copies) throw Error(GLMX_ERR_ARG, "too many peer copies in batch");
+  } catch (...) {
+    // No forward will write this batch's blocks: they become stale again (recomputed on their
+    // next use), and its scratch pages go back to the pool.
+    for (uint64_t id : e->batch_written) bk.set_stale(id, true);
+    e->batch_written.clear();
+    for (auto& r : e->reqs)
+      for (int32_t p : r.scratch) bk.pool().free_now(p);
+    e->reqs.clear();
+    e->copies.clear();
+    throw;
   }
   // longest tiles first (LPT over the 148 SMs)
   std::sort(h_work, h_work + n_work, [&](const int2& a, const int2& b) {
@@ -873,7 +952,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     return ka > kb;
   });
   e->dec_split = choose_decode_split(e, R, T, h_ctx);
-  if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n_work, h_ql, h_ctx);
+  if (!e->dec_split) stage_attn_schedule(e, hm, h_work, n_work, h_ql, h_ctx);
   e->last_T = T;
   e->last_R = R;
   e->last_work = n_work;
@@ -889,8 +968,8 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   e->work[3] = lin * T * c.n_layers + 2.0 * c.d_model * c.vocab * R;
   e->work[4] = T;
   e->work[5] = ctx_tokens;
+  e->rel_mark = bk.pool().mark();
   if (R == 0) {  // nothing to compute (empty prompts): a completed pseudo-batch keeps wait() in order
-    if (!kv->epoch_mode) bk.pool().release_deferred();
     glmx_engine::Pending pd;
     pd.req_row.assign(n_req, -1);
     pd.batch = e->batch_seq++;
@@ -900,8 +979,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
     if (!async) engine_wait_impl(e, nullptr, 0);
     return GLMX_OK;
   }
-  // peer copies, grouped by source pool: src pages then dst pages per group in o_copy
-  if (e->copies.size() > e->max_copies) throw Error(GLMX_ERR_ARG, "too many peer copies in batch");
+  // peer copies, grouped by source pool: src pages then dst pages per group in the copy section
   std::stable_sort(e->copies.begin(), e->copies.end(),
                    [](const glmx_engine::Copy& a, const glmx_engine::Copy& b) { return a.peer < b.peer; });
   {
@@ -916,11 +994,19 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   cudaStream_t s = e->stream;
   {
     Prof p(e, kCatH2D);
-    meta_commit(e, s);
+    MetaCounts mc;
+    mc.n_tok = T;
+    mc.T = T;
+    mc.R = R;
+    mc.n_work = n_work;
+    mc.n_copy = static_cast<int>(e->copies.size());
+    mc.bt_stride = static_cast<int>(align_up(std::max<size_t>(max_pages, 1), 8));
+    mc.sched = !e->dec_split;
+    meta_commit(e, s, mc);
   }
   if (!e->copies.empty()) {
     Prof p(e, kCatOther);
-    const int32_t* d_cp = reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_copy);
+    const int32_t* d_cp = reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->ml.copy);
     const size_t nc = e->copies.size();
     for (size_t a = 0; a < nc;) {
       size_t b = a;
@@ -934,19 +1020,17 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
       a = b;
     }
   }
-  forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
+  forward(e, T, R, n_work, R, reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->ml.tok));
   argmax_rows(e->logits.as<float>(), R, c.vocab, e->next_tok.as<int32_t>(), e->amax_keys.p, s);
   const int slot = static_cast<int>(e->batch_seq & 1);
   {
     Prof p(e, kCatD2H);
     GLMX_CUDA(cudaMemcpyAsync(e->h_out + slot * e->h_out_stride, e->next_tok.p, R * 4,
                               cudaMemcpyDeviceToHost, s));
+    e->d2h_bytes += static_cast<uint64_t>(R) * 4;
   }
   GLMX_CUDA(cudaEventRecord(e->fwd_done, s));
   GLMX_CUDA(cudaEventRecord(e->done_ev[slot], s));
-  // evicted pages were read by this batch; any later writer is stream-ordered after it.  In
-  // epoch mode peers may still copy them: the caller releases after its epoch barrier.
-  if (!kv->epoch_mode) bk.pool().release_deferred();
   glmx_engine::Pending pd;
   pd.req_row = std::move(req_row);
   pd.batch = e->batch_seq;
@@ -964,9 +1048,11 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
   for (uint64_t i = 0; i < n_req; ++i) {
     if (rows[i] < 0) continue;
     if (first_token) first_token[i] = h[rows[i]];
-    if (logits_out)
+    if (logits_out) {
       GLMX_CUDA(cudaMemcpy(logits_out + i * c.vocab, e->logits.as<float>() + static_cast<size_t>(rows[i]) * c.vocab,
                            c.vocab * 4, cudaMemcpyDeviceToHost));
+      e->d2h_bytes += static_cast<uint64_t>(c.vocab) * 4;
+    }
   }
   return GLMX_OK;
 }
@@ -987,19 +1073,6 @@ int engine_wait_impl(glmx_engine* e, int32_t* first_token, uint64_t cap) {
     for (size_t i = 0; i < pd.req_row.size(); ++i) first_token[i] = pd.req_row[i] < 0 ? -1 : h[pd.req_row[i]];
   }
   return static_cast<int>(pd.req_row.size());
-}
-
-int engine_replay_impl(glmx_engine* e) {
-  if (!e->has_batch) throw Error(GLMX_ERR_ARG, "no staged batch");
-  while (!e->pending.empty()) engine_wait_impl(e, nullptr, 0);
-  DeviceGuard dg(e->m->device);
-  forward(e, e->last_T, e->last_R, e->last_work, e->last_R,
-          reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_tok));
-  argmax_rows(e->logits.as<float>(), e->last_R, e->m->cfg.vocab, e->next_tok.as<int32_t>(),
-              e->amax_keys.p, e->stream);
-  GLMX_CUDA(cudaStreamSynchronize(e->stream));
-  collect_profile(e);
-  return GLMX_OK;
 }
 
 // Greedy decode.  Requests are re-ordered by step count (descending) so the active set of every
@@ -1024,6 +1097,7 @@ int engine_decode_defer(glmx_engine* e, const uint32_t* steps) {
   e->reqs.clear();
   e->def_steps.assign(steps, steps + R);
   e->def_R = R;
+  e->def_mark = e->rel_mark;  // pages this batch evicted stay deferred until its decode is enqueued
   e->has_batch = false;
   GLMX_CUDA(cudaMemcpyAsync(e->def_first.p, e->next_tok.p, static_cast<size_t>(R) * 4,
                             cudaMemcpyDeviceToDevice, e->stream));
@@ -1048,8 +1122,12 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   e->dec_steps.assign(e->def_steps.begin(), e->def_steps.begin() + Rd);
   for (int i = 0; i < Rc; ++i) {
     if (steps[i] > e->cfg.max_decode) throw Error(GLMX_ERR_ARG, "steps exceed max_decode");
+    // the request's pages cover its prompt + max_decode positions (scratch allocated at prefill)
+    if (static_cast<uint64_t>(e->reqs[i].ctx_len) + steps[i] > e->reqs[i].pages.size() * B)
+      throw Error(GLMX_ERR_ARG, "decode steps exceed the request's pages");
     e->dec_steps.push_back(steps[i]);
   }
+  e->has_batch = false;  // one decode per prefill batch
   for (uint32_t st : e->dec_steps) max_steps = std::max(max_steps, st);
   e->dec_max = max_steps;
   e->dec_R = R;
@@ -1068,7 +1146,13 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   e->def_R = 0;
   e->def_reqs.clear();
   e->def_steps.clear();
-  if (max_steps == 0) return GLMX_OK;
+  // the deferred batch's self-evicted pages are released once the merged decode that reads them
+  // is enqueued (any later writer, the next prefill, is stream-ordered after it)
+  const bool release_def = Rd > 0 && !e->kv->epoch_mode;
+  if (max_steps == 0) {
+    if (release_def) e->kv->bk->pool().release_before(e->def_mark);
+    return GLMX_OK;
+  }
   DeviceGuard dg(m->device);
   cudaStream_t s = e->stream;
   const std::vector<int>& order = e->dec_order;
@@ -1090,6 +1174,7 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
     int2* h_work = reinterpret_cast<int2*>(hm + e->o_work);
     int32_t* h_last = reinterpret_cast<int32_t*>(hm + e->o_last);
     int32_t* h_perm = reinterpret_cast<int32_t*>(hm + e->o_perm);
+    size_t max_pages = 1;
     for (int j = 0; j < n; ++j) {
       glmx_engine::Req& rq = row_req(order[j]);
       const int32_t p = rq.ctx_len;  // position of the token being fed
@@ -1099,17 +1184,26 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
       h_ql[j] = 1;
       h_ctx[j] = p + 1;
       std::memcpy(h_bt + static_cast<size_t>(j) * e->bt_stride, rq.pages.data(), rq.pages.size() * 4);
+      max_pages = std::max(max_pages, rq.pages.size());
       h_work[j] = make_int2(j, 0);
       h_last[j] = j;
-      h_perm[j] = order[j];
       rq.ctx_len = p + 1;
     }
+    if (st == 0)  // first-token gather: every decode row (rows with 0 steps are never fed)
+      for (int j = 0; j < R; ++j) h_perm[j] = order[j];
     e->dec_split = choose_decode_split(e, n, n, h_ctx);
-    if (!e->attn_impl && !e->dec_split) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
-    meta_commit(e, s);
+    if (!e->dec_split) stage_attn_schedule(e, hm, h_work, n, h_ql, h_ctx);
+    MetaCounts mc;
+    mc.T = n;
+    mc.R = n;
+    mc.n_work = n;
+    mc.n_perm = st == 0 ? R : 0;
+    mc.bt_stride = static_cast<int>(align_up(max_pages, 8));
+    mc.sched = !e->dec_split;
+    meta_commit(e, s, mc);
     if (st == 0)
       gather2_i32(e->def_first.as<int32_t>(), Rd, e->next_tok.as<int32_t>(),
-                  reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->o_perm), R, d_in, s);
+                  reinterpret_cast<const int32_t*>(e->meta.as<uint8_t>() + e->ml.perm), R, d_in, s);
     const int32_t* in_tok = st == 0 ? d_in : d_seq + static_cast<size_t>(st - 1) * R;
     forward(e, n, n, n, n, in_tok);
     argmax_rows(e->logits.as<float>(), n, c.vocab, d_seq + static_cast<size_t>(st) * R,
@@ -1118,7 +1212,9 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
   e->prof_tag = 0;
   GLMX_CUDA(cudaMemcpyAsync(e->h_dec, d_seq, static_cast<size_t>(max_steps) * R * 4,
                             cudaMemcpyDeviceToHost, s));
+  e->d2h_bytes += static_cast<uint64_t>(max_steps) * R * 4;
   GLMX_CUDA(cudaEventRecord(e->dec_done, s));
+  if (release_def) e->kv->bk->pool().release_before(e->def_mark);
   return GLMX_OK;
 }
 
@@ -1186,16 +1282,15 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
                        int bt_stride, int reps, cudaStream_t s, float* out_ms) {
   if (n_req == 0) return GLMX_OK;
   if (H % Hkv != 0 || reps < 1) throw Error(GLMX_ERR_ARG, "bad attention arguments");
-  // impl 2: the CUDA-core decode kernel (every request one query token)
+  // impl 0: the tcgen05 kernel; impl 2: the CUDA-core decode kernel (every request one token)
+  if (impl != 0 && impl != 2) throw Error(GLMX_ERR_ARG, "attention impl must be 0 (tcgen05) or 2 (decode)");
   const bool dec = impl == 2;
-  if (dec) {
+  if (dec)
     for (uint64_t r = 0; r < n_req; ++r)
       if (q_len[r] != 1) throw Error(GLMX_ERR_ARG, "decode attention needs q_len == 1");
-    impl = 1;
-  }
   PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, static_cast<uint32_t>(Hkv),
                 block_tokens, static_cast<uint32_t>(hd)};
-  const int tpt = impl ? attn_tokens_per_tile(H, Hkv) : attn_tc_tokens_per_tile(H, Hkv);
+  const int tpt = attn_tc_tokens_per_tile(H, Hkv);
   std::vector<int2> work;
   for (uint64_t r = 0; r < n_req; ++r) {
     if (q_len[r] < 1 || ctx_len[r] < q_len[r] ||
@@ -1233,14 +1328,14 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   hs.pieces = reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pc);
   hs.cta_off = reinterpret_cast<int32_t*>(h.data() + o_sched + o_cta);
   hs.combine = reinterpret_cast<AttnCombine*>(h.data() + o_sched + o_cb);
-  hs.partners = attn_pairing() ? reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pp) : nullptr;
-  if (!impl)
+  hs.partners = reinterpret_cast<AttnPiece*>(h.data() + o_sched + o_pp);
+  if (!dec)
     build_attn_schedule(reinterpret_cast<const int32_t*>(work.data()), static_cast<int>(work.size()),
                         Hkv, q_len, ctx_len, tpt, 128, kNumSMs, hs);
   DBuf meta, part_o, part_ml;
   meta.reserve(bytes);
   GLMX_CUDA(cudaMemcpyAsync(meta.p, h.data(), bytes, cudaMemcpyHostToDevice, s));
-  if (!impl && hs.n_combine > 0) {
+  if (!dec && hs.n_combine > 0) {
     part_o.reserve(static_cast<size_t>(hs.n_partials) * attn_tc_partial_rows() * hd * 4);
     part_ml.reserve(static_cast<size_t>(hs.n_partials) * attn_tc_partial_rows() * 8);
   }
@@ -1249,7 +1344,7 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
                  reinterpret_cast<const int*>(dm + o_sched + o_cta),
                  reinterpret_cast<const int4*>(dm + o_sched + o_cb), hs.grid, hs.n_combine,
                  part_o.as<float>(), part_ml.as<float2>(),
-                 hs.partners ? reinterpret_cast<const int4*>(dm + o_sched + o_pp) : nullptr};
+                 reinterpret_cast<const int4*>(dm + o_sched + o_pp)};
   AttnParams ap{};
   ap.q = static_cast<const __nv_bfloat16*>(q);
   ap.o = static_cast<__nv_bfloat16*>(o);
@@ -1267,7 +1362,7 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
   ap.scale_log2 = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)) * 1.4426950408889634);
   alignas(64) uint8_t kv_map[128], q_map[128];
   uint32_t rows = 0;
-  if (!impl) {
+  if (!dec) {
     make_pool_tensor_map(geom, n_pages, kv_map, &rows);
     make_q_tensor_map(q, T, H, Hkv, q_map);
   }
@@ -1290,8 +1385,6 @@ int attention_run_impl(int impl, const void* q, void* o, uint64_t T, int H, int 
       if (dec)
         paged_attention_decode(ap, static_cast<int>(n_req), dec_split, part_o.as<float>(),
                                part_ml.as<float2>(), s);
-      else if (impl)
-        paged_attention(ap, s);
       else
         paged_attention_tc(ap, kv_map, rows, q_map, sc, s);
     }
@@ -1541,32 +1634,3 @@ int kv_gather_run_impl(void* pool_base, uint64_t n_pages_pool, uint32_t n_layers
   return GLMX_OK;
 }
 
-// ======================================================================== decode GEMM hook
-// Y[n][N] (+)= X[n][K] . W[N][K]^T on caller-owned device buffers through the tcgen05 decode GEMM
-// (mode 0 bf16 out, 1 fp32 out, 2 fp32 accumulate); `reps` launches, mean ms per launch.
-int gemv_run_impl(const void* w, const void* x, void* y, int n, int K, int N, int mode, int reps,
-                  cudaStream_t s, float* out_ms) {
-  if (!gemv_tc_supported(n, K, N) || mode < 0 || mode > 2 || reps < 1)
-    throw Error(GLMX_ERR_ARG, "gemv: unsupported shape (n <= 64, K % 64 == 0, N % 128 == 0)");
-  alignas(64) uint8_t w_map[128], x_map[128];
-  make_gemv_map(w, static_cast<uint64_t>(N), static_cast<uint64_t>(K), 128, w_map);
-  make_gemv_map(x, static_cast<uint64_t>(n), static_cast<uint64_t>(K), 64, x_map);
-  DBuf part, cnt;
-  part.reserve(gemv_tc_part_floats(K, N) * 4);
-  cnt.reserve(static_cast<size_t>(N / 128) * 4);
-  GLMX_CUDA(cudaMemsetAsync(cnt.p, 0, static_cast<size_t>(N / 128) * 4, s));
-  cudaEvent_t e0, e1;
-  GLMX_CUDA(cudaEventCreate(&e0));
-  GLMX_CUDA(cudaEventCreate(&e1));
-  float ms = 0.f;
-  GLMX_CUDA(cudaEventRecord(e0, s));
-  for (int i = 0; i < reps; ++i)
-    gemv_tc(w_map, x_map, n, K, N, mode, y, part.as<float>(), cnt.as<int>(), s);
-  GLMX_CUDA(cudaEventRecord(e1, s));
-  GLMX_CUDA(cudaEventSynchronize(e1));
-  GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (out_ms) *out_ms = ms / static_cast<float>(reps);
-  return GLMX_OK;
-}

@@ -96,6 +96,7 @@ struct glmx_model {
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
   glmx::GemmTuner tuner;  // per-(projection, M bucket) cuBLASLt algorithms; empty = cublasGemmEx
+  int n_engines = 0;      // live engines: the algorithm table is immutable while any exists
   ~glmx_model();
 };
 
@@ -106,7 +107,6 @@ struct glmx_engine {
   cudaStream_t stream = nullptr;
   int bt_stride = 0;
   int tpt = 0;  // attention tokens per tile
-  int attn_impl = 0;  // 0 = tcgen05 (attn_tc.cu), 1 = mma.sync baseline (dev A/B only)
   alignas(64) uint8_t kv_map[128];  // CUtensorMap over the KV pool (TMA)
   alignas(64) uint8_t q_map[128];   // CUtensorMap over the q activation buffer
   uint32_t kv_rows = 0;
@@ -162,11 +162,26 @@ struct glmx_engine {
   size_t max_copies = 0, o_copy = 0;
   size_t o_tok = 0, o_pos = 0, o_slot = 0, o_qs = 0, o_ql = 0, o_ctx = 0, o_bt = 0, o_work = 0,
          o_last = 0;
+  // The host stages a batch at the fixed capacity offsets above; meta_commit packs the used part
+  // of every section (block-table rows at the batch's own stride) in place and uploads only
+  // those bytes.  ml = the packed layout of the last upload (what the kernels read).
+  struct MetaLayout {
+    size_t tok, pos, slot, qs, ql, ctx, bt, work, last, perm, pieces, partners, cta, comb, copy;
+    size_t bytes;
+    int bt_stride;
+  };
+  MetaLayout ml{};
+  int sc_npieces = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // cumulative host<->device bytes moved by the engine
+  DBuf blas_ws;                           // this engine's cuBLAS / cuBLASLt workspace
+  // deferred (evicted) pages: released at the next prefill's start (rel_mark = the pool's defer
+  // mark after the last batch), or, for a batch whose decode is deferred, only once that merged
+  // decode is enqueued (def_mark)
+  uint64_t rel_mark = 0, def_mark = 0;
+  std::vector<uint64_t> batch_written;  // stale blocks this batch recomputes (rollback on error)
   // K3 stream-K schedule (packed in meta) + partial workspace
   size_t o_sched = 0, o_sc_pieces = 0, o_sc_cta = 0, o_sc_comb = 0, o_sc_part = 0;
   int sc_grid = 0, sc_ncomb = 0;
-  bool decode_cc = true;  // one-token batches on the CUDA-core decode kernel (GLMX_DECODE_ATTN=tc: off)
-  bool decode_fuse = true;  // ... with RoPE + K/V append fused in (GLMX_DECODE_ATTN=unfused: off)
   int dec_split = 0;      // > 0: the staged batch is all one-token rows -> K3d with this many splits
   DBuf part_o, part_ml;
 

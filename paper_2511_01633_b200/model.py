@@ -208,8 +208,11 @@ class Engine:
         old = [[outp[i * m + s] for s in range(prev[i])] for i in range(len(prev))] if prev else None
         return cur, old
 
-    def replay_forward(self):
-        check(lib().glmx_engine_replay_forward(self.h))
+    def io_bytes(self):
+        """(host->device, device->host) bytes moved by the engine since creation."""
+        out = (C.c_uint64 * 2)()
+        check(lib().glmx_engine_io_bytes(self.h, out))
+        return int(out[0]), int(out[1])
 
     def last_timings(self):
         out = (C.c_float * 7)()

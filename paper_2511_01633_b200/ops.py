@@ -26,21 +26,6 @@ def rope_kv_append(qkv, pos, slot, pool, q_out, n_heads, n_kv_heads, layer=0,
     return ms.value
 
 
-def reference_rope(x, pos, rope_theta=500000.0):
-    """fp32 rotate-half RoPE, angles as in oracle/decoder.py:rope (fp32 pos * fp32 inv_freq, then
-    cos/sin in fp64): x [T][heads][hd]."""
-    import torch
-
-    hd = x.shape[-1]
-    inv = (1.0 / (float(torch.tensor(rope_theta, dtype=torch.float32)) **
-                  (torch.arange(0, hd // 2, dtype=torch.float64) * 2.0 / hd))).float()
-    ang = (pos.cpu().float()[:, None] * inv[None, :]).double()
-    cos = torch.cos(ang).float().to(x.device)[:, None, :]
-    sin = torch.sin(ang).float().to(x.device)[:, None, :]
-    a, b = x[..., :hd // 2].float(), x[..., hd // 2:].float()
-    return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
-
-
 def kv_gather(pool, pages, layer, kv, out, impl=0, reps=1, stream=None):
     """K2 gather: out [len(pages)*B][Hkv][hd] <- pool[pages][layer][kv] (TMA-staged when impl=0).
     Returns the mean device ms per launch."""
@@ -54,21 +39,3 @@ def kv_gather(pool, pages, layer, kv, out, impl=0, reps=1, stream=None):
                                    len(pages), out.data_ptr(), impl, reps, s, C.byref(ms)))
     return ms.value
 
-
-def gemv(x, w, y, mode=0, reps=1, stream=None):
-    """Decode GEMM on the tcgen05 weight-streaming kernel: y (+)= x @ w.T (glmx_gemv_run).
-
-    x [n <= 64][K] bf16, w [N][K] bf16, y [n][N] bf16 (mode 0) or fp32 (1 store, 2 accumulate).
-    Returns the mean device ms per launch."""
-    import torch
-
-    n, K = x.shape
-    N = w.shape[0]
-    assert x.is_cuda and w.is_cuda and y.is_cuda and w.shape[1] == K and tuple(y.shape) == (n, N)
-    assert x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
-    assert y.dtype == (torch.bfloat16 if mode == 0 else torch.float32)
-    ms = C.c_float(0.0)
-    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-    check(lib().glmx_gemv_run(w.data_ptr(), x.data_ptr(), y.data_ptr(), n, K, N,
-                              mode, reps, s, C.byref(ms)))
-    return ms.value

@@ -10,7 +10,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("T", [1, 7, 64, 1000, 1024, 2501])  # both launch configs (< and >= 1024)
 def test_append_matches_reference(T):
-    from paper_2511_01633_b200.ops import reference_rope, rope_kv_append
+    from paper_2511_01633_b200.ops import rope_kv_append
+    from torch_refs import reference_rope
 
     H, Hkv, hd, B, L, layer = 32, 8, 128, 16, 3, 2
     g = torch.Generator().manual_seed(T)

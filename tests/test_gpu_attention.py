@@ -7,6 +7,8 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
+from torch_refs import reference_attention
+
 pytestmark = pytest.mark.gpu
 
 ATOL, RTOL = 2e-2, 1e-2
@@ -42,7 +44,7 @@ def _check(impl, reqs, **kw):
     o = torch.full_like(q, float("nan"))
     A.paged_attention(q, o, pool, qs, ql, ctx, bt, layer=layer, impl=impl)
     torch.cuda.synchronize()
-    ref = A.reference_attention(q, pool, qs, ql, ctx, bt, layer=layer)
+    ref = reference_attention(q, pool, qs, ql, ctx, bt, layer=layer)
     err = (o.float() - ref).abs()
     bound = ATOL + RTOL * ref.abs()
     assert torch.isfinite(o.float()).all(), "unwritten or non-finite output rows"
@@ -55,9 +57,8 @@ MIXED = [(1, 1), (16, 16), (37, 37), (200, 5), (300, 33), (129, 64), (1000, 130)
          (2050, 1), (513, 97)]
 
 
-@pytest.mark.parametrize("impl", [0, 1], ids=["tcgen05", "mma_sync"])
-def test_mixed_requests(impl):
-    _check(impl, MIXED)
+def test_mixed_requests():
+    _check(0, MIXED)
 
 
 def test_long_prefix_short_suffix():
@@ -90,6 +91,47 @@ def test_single_long_query_split_and_combined():
     # 16 items < 148 / 2: every item's key range is split over ~9 CTAs, partials merged
     _check(0, [(6000 + 100, 100)], seed=6)
     _check(0, [(3000, 1)], seed=7)  # decode-like: one row, 8 items
+
+
+# Split pieces that start past some rows' positions (few items: every item's key range is cut
+# into ~148 / items pieces).  ctx = 2060, q = 20: the piece of key tile 16 (keys 2048..2059) holds
+# no visible key for the rows at positions 2040..2047, whose partial must be (m=-inf, l=0, O=0),
+# not NaN, and must drop out of the combine.
+SPLIT_EDGE = [(c, q) for c in (900, 1025, 1064, 1500, 2049, 2060, 2100, 2400)
+              for q in (1, 8, 20, 33, 64)]
+
+
+@pytest.mark.parametrize("ctx,ql", SPLIT_EDGE, ids=[f"{c}x{q}" for c, q in SPLIT_EDGE])
+def test_split_pieces_with_invisible_rows(ctx, ql):
+    _check(0, [(ctx, ql)], seed=ctx * 100 + ql)
+
+
+def test_split_pieces_few_requests_unaligned():
+    # 3 and 9 requests (24 / 72 items <= 74): still the split path, several items per request
+    _check(0, [(2060, 20), (1064, 64), (1300, 37)], seed=31)
+    _check(0, [(1000 + 131 * i, 5 + 7 * i) for i in range(9)], seed=32)
+
+
+def test_split_schedule_reaches_invisible_rows():
+    """The schedule really produces a piece whose first key lies past some rows (the case the
+    tests above must cover): item rows at 2040..2059, a piece starting at key 2048."""
+    import paper_2511_01633_b200.attention as A
+
+    sc = A.schedule([(0, 0)], [20], [2060], n_kv_heads=8, tokens_per_item=64)
+    starts = {j0 for _, j0, _, _ in sc["pieces"]}
+    assert 16 in starts and sc["combine"], sc["pieces"][:20]
+
+
+def test_stream_k_cut_unaligned_rows():
+    # 21 requests x 8 kv heads = 168 long items on 148 SMs: the LPT makespan has a long tail, so
+    # the flattened tile sequence is cut into equal ranges (stream-K) with partials + combine
+    import paper_2511_01633_b200.attention as A
+
+    reqs = [(2060 + 37 * i, 40 + (i % 5)) for i in range(21)]
+    sc = A.schedule([(i, 0) for i in range(21)], [q for _, q in reqs], [c for c, _ in reqs],
+                    n_kv_heads=8, tokens_per_item=64)
+    assert sc["combine"] and sc["grid"] == 148  # the stream-K path, with split items
+    _check(0, reqs, seed=33)
 
 
 def test_paired_single_tile_items():
