@@ -296,7 +296,7 @@ def test_overlapped_decode_rotations_match_sequential():
     assert sum(r[3] for r in out[0][0]) > 0
 
 
-@pytest.mark.parametrize("cap,policy", [(256, glmx.PRIORITY), (40, glmx.LRU)],
+@pytest.mark.parametrize("cap,policy", [(256, glmx.PRIORITY), (40, glmx.PLAIN_LRU)],
                          ids=["roomy", "self_evicting"])
 def test_merged_decode_matches_separate_decode(cap, policy):
     """Continuous batching of two rotations' decode rows (decode_defer + decode_async) gives the
