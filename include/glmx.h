@@ -238,6 +238,7 @@ typedef struct {
 } glmx_model_config;
 
 int glmx_model_create(const glmx_model_config* cfg, int32_t device, glmx_model** out);
+/* frees the weights; with engines still alive the release is deferred to the last engine's destroy */
 void glmx_model_destroy(glmx_model* m);
 /* test hook: copy one bf16 weight tensor to host (raw uint16 bits).  which: 0 embed [V,d],
  * 1 attn_norm [d], 2 wqkv [(H+2Hkv)*hd, d], 3 wo [d, H*hd], 4 mlp_norm [d], 5 w_gate_up

@@ -226,6 +226,8 @@ def ref():
                                             C.c_uint64]
         L.ref_nearest.restype = C.c_int64
         L.ref_nearest.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_char_p, C.c_uint64]
+        L.ref_tokenize.restype = C.c_uint64
+        L.ref_tokenize.argtypes = [C.c_char_p, C.c_uint64, u64p, u64p, C.c_uint64]
         L.ref_render.restype = C.c_int64
         L.ref_render.argtypes = [C.c_char_p] * 4 + [C.c_char_p, C.c_uint64]
         L.ref_trace_len.restype = C.c_uint64
@@ -404,6 +406,19 @@ def ref_render(name, a0="", a1="", a2=""):
     if n < 0:
         raise ValueError(L.ref_last_error().decode())
     return [(t, txt) for t, txt in json.loads(buf.raw[:n].decode())]
+
+
+def ref_tokenize(text):
+    """The reference's own glm::tokenize (tokenizer.hpp:14-25) through oracle/_ref: the tokens of
+    `text` (str or bytes) as the same type."""
+    L = ref()
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    cap = len(raw) // 2 + 2
+    b, e = (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
+    n = L.ref_tokenize(raw, len(raw), b, e, cap)
+    assert n <= cap
+    toks = [raw[b[i]:e[i]] for i in range(n)]
+    return [t.decode() for t in toks] if isinstance(text, str) else toks
 
 
 def tokenize(text: str):

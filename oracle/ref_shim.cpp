@@ -79,6 +79,11 @@ PrefillReport glmref_real_prefill(KvCacheState* kv, const TokenSeq& p, const Tie
 void glmref_real_set_tier(KvCacheState* kv, const std::string& s, Tier from, Tier to) {
   kv->set_tier(s, from, to);
 }
+// segment texts kv_prefill tokenized since the last recorded prefill (rec_tokenize.hpp)
+thread_local std::vector<std::string> g_seg_texts;
+void glmref_record_segment_text(std::string_view text) {
+  if (g_recording) g_seg_texts.emplace_back(text);
+}
 void glmref_record_prefill(const TokenSeq& p, const TierMap& t, const std::string& s,
                            const PrefillReport* rep, const char* error) {
   if (!g_recording) return;
@@ -87,6 +92,24 @@ void glmref_record_prefill(const TokenSeq& p, const TierMap& t, const std::strin
   j["session"] = s;
   j["tokens"] = p;
   j["tiers"] = tiers_json(t);
+  // the PromptSegments behind this call: (text, tier) per part.  A part's tier is the TierMap
+  // tier at its first token (kv_prefill gave all its tokens that tier); empty parts (skipped by
+  // kv_prefill) carry the previous part's tier.
+  json segs = json::array();
+  std::size_t at = 0;
+  int last_tier = 0;
+  for (const auto& text : g_seg_texts) {
+    const std::size_t n = glm::tokenize(text).size();
+    int tier = last_tier;
+    if (n > 0)
+      for (const auto& r : t)
+        if (r.begin <= at && at < r.end) tier = static_cast<int>(r.tier);
+    segs.push_back(json::array({text, tier}));
+    at += n;
+    last_tier = tier;
+  }
+  g_seg_texts.clear();
+  if (at == p.size()) j["segments"] = segs;
   if (rep) {
     j["cached"] = rep->cached_tokens;
     j["computed"] = rep->computed_tokens;

@@ -456,6 +456,10 @@ int glmx_model_create(const glmx_model_config* cfg, int32_t device, glmx_model**
 }
 void glmx_model_destroy(glmx_model* m) {
   if (!m) return;
+  if (m->n_engines > 0) {  // engines still run on its weights: freed when the last one goes
+    m->destroy_pending = true;
+    return;
+  }
   DeviceGuard g(m->device);
   delete m;
 }

@@ -89,7 +89,7 @@ glmx_engine::~glmx_engine() {
   for (auto e : done_ev)
     if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
-  if (m) --m->n_engines;
+  if (m && --m->n_engines == 0 && m->destroy_pending) delete m;  // the model outlived its handle
 }
 
 // ======================================================================== graph upload

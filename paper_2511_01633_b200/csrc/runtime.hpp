@@ -97,6 +97,7 @@ struct glmx_model {
   void* blas_ws = nullptr;
   glmx::GemmTuner tuner;  // per-(projection, M bucket) cuBLASLt algorithms; empty = cublasGemmEx
   int n_engines = 0;      // live engines: the algorithm table is immutable while any exists
+  bool destroy_pending = false;  // glmx_model_destroy with live engines: freed with the last one
   ~glmx_model();
 };
 

@@ -36,6 +36,34 @@ def test_fixture_chunks_match_reference(ref):
         "[neighbours:(n3 {brand:Y, price:11, title:gamma widget, type:item}),(u1 {name:u, type:user})]")
 
 
+def test_attribute_rendering_matches_reference(ref):
+    """attr.hpp:19-48 + retriever.cpp:34-41 (SURVEY trap A11): doubles in shortest round-trip form
+    (1e+21, 0.1, -0, 1e-07, 5e-324, DBL_MAX, integers beyond int64 as doubles, 100.0 -> 100),
+    uint64 values wrapped to int64, bools, lists (empty, mixed), an attribute literally named
+    `type` (two type pairs, sorted by value), non-ASCII / escaped / whitespace-bearing strings,
+    multi-edges and a self-loop: chunk bytes, token spans and token ids per node, every k /
+    weight mode / direction, against the compiled reference."""
+    path = os.path.join(GOLDEN, "attrs.jsonl")
+    g = glmx.PropertyGraph.load(path, device=0)
+    rg = oracle.RefGraph(path=path)
+    ids = rg.node_ids()
+    assert [g.node_id(i) for i in range(g.node_count())] == ids
+    V = 32000
+    for k in (0, 1, 2, 8):
+        for wm in (0, 1):
+            for directed in (False, True):
+                r = glmx.Retriever(g, chunk_k=k, weight_mode=wm, directed=directed, vocab=V)
+                batch = r.chunk_build(list(range(len(ids))))
+                for i, nid in enumerate(ids):
+                    want = rg.node_info_rendered(nid, k, wm, directed)
+                    assert r.node_info_rendered(nid) == want
+                    assert batch.texts[i] == want
+                    raw = want.encode()
+                    toks = oracle.ref_tokenize(raw)
+                    assert [raw[b:e] for b, e in batch.token_spans[i]] == toks
+                    assert batch.token_ids[i] == [fnv1a(t) % V for t in toks]
+
+
 def test_batched_chunks_and_tokens_match_reference(ref, tmp_path):
     g = glmx.PropertyGraph.synth_powerlaw(20000, 8, seed=3, device=0)
     path = str(tmp_path / "g.jsonl")
@@ -52,7 +80,7 @@ def test_batched_chunks_and_tokens_match_reference(ref, tmp_path):
             for i, v in enumerate(nodes):
                 want = rg.node_info_rendered(g.node_id(v), k, wm, directed)
                 assert batch.texts[i] == want, (k, wm, directed, v)
-                toks = oracle.tokenize(want)
+                toks = oracle.ref_tokenize(want)  # the reference's glm::tokenize
                 got = [batch.texts[i].encode()[b:e].decode() for b, e in batch.token_spans[i]]
                 assert got == toks
                 assert batch.token_ids[i] == [fnv1a(t.encode()) % V for t in toks]
@@ -110,7 +138,7 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
             want = rg.node_info_rendered(g.node_id(v), k)
             assert batch.texts[i] == want, (k, v)
             big += len(want.encode()) > 6144
-            toks = oracle.tokenize(want)
+            toks = oracle.ref_tokenize(want)  # the reference's glm::tokenize
             raw = batch.texts[i].encode()
             got = [raw[b:e].decode() for b, e in batch.token_spans[i]]
             assert got == toks, (k, v)

@@ -179,6 +179,46 @@ def replay_trace(trace, cap, B=16, policy=0):
     return kv
 
 
+def replay_segments(trace, cap, B=16, policy=0):
+    """The same recorded call sequence, but each prefill fed as the PromptSegments the reference
+    orchestrator tokenized (recorded inside Orchestrator::kv_prefill, oracle/rec_tokenize.hpp)
+    through glmx_kv_prefill_segments -- tokenisation per segment, empty parts skipped, same-tier
+    ranges merged -- instead of the already-flattened (tokens, TierMap)."""
+    kv = glmx.KvCacheState(cap, B, policy)
+    n = 0
+    for i, op in enumerate(trace):
+        if op["op"] == "set_tier":
+            kv.set_tier(op["session"], op["from"], op["to"])
+            continue
+        segs = [(tier, text) for text, tier in op["segments"]]
+        # the Python restatement (oracle.kv_prefill_inputs) is pinned to the same records
+        toks, tiers = oracle.kv_prefill_inputs(segs)
+        assert toks == op["tokens"] and [list(t) for t in tiers] == op["tiers"], i
+        if "error" in op:
+            with pytest.raises(glmx.CacheExhausted):
+                kv.prefill_segments(segs, op["session"])
+            return kv, n
+        r = kv.prefill_segments(segs, op["session"])
+        assert (r.cached_tokens, r.computed_tokens, r.tail_tokens) == (
+            op["cached"], op["computed"], op["tail"]), i
+        assert [str(e) for e in r.evicted] == [str(e) for e in op["evicted"]], i
+        n += 1
+    return kv, n
+
+
+def test_recorded_prompt_segments_replay(golden):
+    """a2/a3 pinned to the reference: every prefill the reference orchestrator made (Fig. 6
+    scripted run and three run_bench runs, incl. eviction pressure), replayed from its segments."""
+    f = golden["fig6"]
+    kv, n = replay_segments(f["trace"], 4096)
+    assert n == 10 and kv.snapshot() == f["kv"]
+    for bt in golden["bench_traces"]:
+        kv_s, n = replay_segments(bt["trace"], bt["cap"], 16, bt["policy"])
+        kv_t = replay_trace(bt["trace"], bt["cap"], 16, bt["policy"])
+        assert n > 0 and kv_s.resident_snapshot() == kv_t.resident_snapshot()
+        assert kv_s.counters() == kv_t.counters()
+
+
 def test_fig6_scripted_trace_c1(golden):
     f = golden["fig6"]
     kv = replay_trace(f["trace"], 4096)

@@ -86,11 +86,24 @@ def test_templates_match_reference(ref):
 
 
 def test_tokenizer_matches_reference_spans(ref):
+    """glmx_tokenize (and the Python restatement) against the reference's glm::tokenize itself
+    (tokenizer.hpp:14-25, std::isspace in the C locale), incl. bytes >= 0x80 and NBSP."""
     rnd = random.Random(0)
-    alphabet = "ab \t\n\r\x0b\x0cxyz{}[](),:"
-    for _ in range(200):
+    alphabet = "ab \t\n\r\x0b\x0cxyz{}[](),:é\xa0"
+    for _ in range(300):
         s = "".join(rnd.choice(alphabet) for _ in range(rnd.randint(0, 40)))
-        assert glmx.tokenize(s) == oracle.tokenize(s)
+        want = oracle.ref_tokenize(s)
+        assert glmx.tokenize(s) == want
+        assert oracle.tokenize(s) == want
+
+
+def test_malformed_attribute_rejected_like_reference(ref):
+    path = os.path.join(ROOT, "tests", "golden", "attrs_nested.jsonl")
+    with pytest.raises(ValueError) as ref_err:
+        oracle.RefGraph(path=path)
+    with pytest.raises(glmx.GlmxError) as err:
+        glmx.PropertyGraph.load(path, device=-1)
+    assert str(ref_err.value) in str(err.value)  # same line, same message
 
 
 # ---------------------------------------------------------------- the C-ABI boundary
