@@ -275,6 +275,11 @@ typedef struct {
   const glmx_tier_range* tiers;
   uint64_t n_tiers;
   const char* session;
+  /* nonzero: this call's reply is a Finish (known ahead for scripted replies), so the session's
+   * Orchestrator::finish -- KvCacheState::set_tier(session, II, III), orchestrator.cpp:147-154 --
+   * is applied right after this request's bookkeeping, before the next request's: the batch then
+   * reproduces run_bench's exact round-robin call order (bench.cpp:65-83). */
+  int32_t finish;
 } glmx_request;
 
 int glmx_engine_create(glmx_model* m, glmx_kv* kv, const glmx_engine_config* cfg,
@@ -295,6 +300,7 @@ typedef struct {
   const int32_t* seg_tier;
   uint64_t n_seg;
   const char* session;
+  int32_t finish; /* as glmx_request::finish */
 } glmx_segment_request;
 int glmx_engine_prefill_segments(glmx_engine* e, uint64_t n_req,
                                  const glmx_segment_request* reqs, glmx_prefill_report* reports,

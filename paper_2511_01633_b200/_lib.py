@@ -67,12 +67,12 @@ class EngineConfig(C.Structure):
 class RequestC(C.Structure):
     _fields_ = [("tok_bytes", C.c_char_p), ("tok_offsets", u64p), ("n_tok", C.c_uint64),
                 ("tiers", C.POINTER(TierRange)), ("n_tiers", C.c_uint64),
-                ("session", C.c_char_p)]
+                ("session", C.c_char_p), ("finish", C.c_int32)]
 
 
 class SegmentRequestC(C.Structure):
     _fields_ = [("seg_text", C.POINTER(C.c_char_p)), ("seg_len", u64p), ("seg_tier", i32p),
-                ("n_seg", C.c_uint64), ("session", C.c_char_p)]
+                ("n_seg", C.c_uint64), ("session", C.c_char_p), ("finish", C.c_int32)]
 
 
 _SIGS = {

@@ -527,7 +527,7 @@ int prefill_segments(glmx_engine* e, uint64_t n_req, const glmx_segment_request*
           t.tiers.push_back({begin, end, s.seg_tier[i], 0});
       }
       rq[r] = {t.bytes.data(), t.offs.data(), t.offs.size() - 1, t.tiers.data(), t.tiers.size(),
-               s.session};
+               s.session, s.finish};
     }
     return engine_prefill_impl(e, n_req, rq.data(), reports, first_token, logits, async);
   });

@@ -860,6 +860,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
       // may throw with partial state, exactly like the reference; the blocks it inserted stay
       // stale, so their KV is recomputed on first use
       bk.prefill(ts, rq.tiers, rq.n_tiers, rq.session ? rq.session : "", pr);
+      if (rq.finish) bk.set_tier(rq.session ? rq.session : "", GLMX_TIER_II, GLMX_TIER_III);
       glmx_prefill_report& rep = reports[i];
       rep.cached_tokens = pr.cached;
       rep.computed_tokens = pr.computed;
