@@ -381,6 +381,17 @@ int64_t glmx_graph_node_id(const glmx_graph* g, uint64_t idx, char* buf, uint64_
   if (idx >= g->host.n()) return -1;
   return copy_str(g->host.ids[idx], buf, cap);
 }
+int64_t glmx_graph_node_attr(const glmx_graph* g, uint64_t idx, const char* key, char* buf,
+                             uint64_t cap, int32_t* kind) {
+  if (idx >= g->host.n() || !key) return -1;
+  const auto& a = g->host.attrs[idx];
+  for (size_t i = 0; i < a.size(); ++i)
+    if (a[i].first == key) {
+      if (kind) *kind = g->host.attr_kind.empty() ? 0 : g->host.attr_kind[idx][i];
+      return copy_str(a[i].second, buf, cap);
+    }
+  return -1;
+}
 int64_t glmx_graph_degree(const glmx_graph* g, uint64_t idx) {
   if (idx >= g->host.n()) return -1;
   return g->host.w_total[idx];

@@ -224,6 +224,7 @@ struct RawNode {
   std::string id, type;
   std::map<std::string, std::string> attrs;  // key -> rendered value (std::map like NodeRecord)
   std::set<std::string> str_attrs;           // keys whose value is a JSON string scalar
+  std::map<std::string, uint8_t> kinds;      // key -> AttrKind (strings: str_attrs)
 };
 struct RawEdge {
   std::string src, dst, etype;
@@ -256,6 +257,15 @@ HostGraph build(std::vector<RawNode> nodes, std::vector<RawEdge> edges, bool hos
     g.ids.push_back(std::move(nodes[i].id));
     g.types.push_back(std::move(nodes[i].type));
     g.attrs.emplace_back(nodes[i].attrs.begin(), nodes[i].attrs.end());
+    std::vector<uint8_t> kinds;
+    kinds.reserve(nodes[i].attrs.size());
+    for (const auto& kv : nodes[i].attrs) {
+      auto k = nodes[i].kinds.find(kv.first);
+      kinds.push_back(nodes[i].str_attrs.count(kv.first) ? kAttrString
+                      : k != nodes[i].kinds.end()         ? k->second
+                                                          : kAttrInt);
+    }
+    g.attr_kind.push_back(std::move(kinds));
     std::string text;
     uint8_t has = 0, is_title = 0;
     for (const char* f : {"title", "name"}) {
@@ -419,12 +429,11 @@ std::string HostGraph::serialize_jsonl() const {
       if (i) out += ',';
       json_escape(out, attrs[v][i].first);
       out += ':';
-      // synthetic graphs only carry strings and integers
+      // scalars round-trip (the canonical renders of ints, doubles and bools are JSON numbers /
+      // literals); a list is written as its rendered string
       const std::string& val = attrs[v][i].second;
-      bool integral = !val.empty() && std::all_of(val.begin(), val.end(), [](char c) {
-        return (c >= '0' && c <= '9') || c == '-';
-      });
-      if (integral && val != "-") out += val;
+      const uint8_t kind = attr_kind.empty() ? kAttrString : attr_kind[v][i];
+      if (kind == kAttrInt || kind == kAttrDouble || kind == kAttrBool) out += val;
       else json_escape(out, val);
     }
     out += "}}\n";
@@ -478,9 +487,14 @@ void parse_lines(const std::vector<std::pair<const char*, const char*>>& lines, 
               s += render_scalar(v.arr[i], jp);
             }
             n.attrs[k] = s + "]";
+            n.kinds[k] = kAttrList;
           } else {
             n.attrs[k] = render_scalar(v, jp);
             if (v.kind == JVal::Str) n.str_attrs.insert(k);
+            n.kinds[k] = v.kind == JVal::Str    ? kAttrString
+                         : v.kind == JVal::Bool ? kAttrBool
+                         : v.kind == JVal::Double ? kAttrDouble
+                                                  : kAttrInt;
           }
         }
       }

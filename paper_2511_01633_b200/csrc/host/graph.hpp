@@ -18,10 +18,14 @@
 
 namespace glmx {
 
+// attribute value kinds (attr.hpp:13-16): Scalar string / int64 / double / bool, or a list
+constexpr uint8_t kAttrString = 0, kAttrInt = 1, kAttrDouble = 2, kAttrBool = 3, kAttrList = 4;
+
 struct HostGraph {
   std::vector<std::string> ids;            // ascending
   std::vector<std::string> types;
   std::vector<std::vector<std::pair<std::string, std::string>>> attrs;  // rendered, key order
+  std::vector<std::vector<uint8_t>> attr_kind;  // per attrs entry: kAttr*
   // VectorIndex text per node (index.cpp:12-25, default Config): the "title" attribute when it is
   // a string, else "name" when it is a string; has_itext[v] = 0 for nodes without one
   std::vector<std::string> itext;

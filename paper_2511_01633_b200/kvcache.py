@@ -56,6 +56,12 @@ def chain_ids(tokens, block_tokens=16):
     return [out[i] for i in range(n)]
 
 
+def count_tokens(text: str) -> int:
+    """count_tokens (tokenizer.hpp:36-46): std::isspace-delimited tokens, through the C-ABI."""
+    b = text.encode()
+    return int(lib().glmx_tokenize(b, len(b), None, None, 0))
+
+
 def tokenize(text: str):
     """tokenizer.hpp:14-25 through the C-ABI."""
     b = text.encode()

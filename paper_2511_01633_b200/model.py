@@ -119,6 +119,7 @@ class Engine:
         check(lib().glmx_engine_create(model.h, kv.h, C.byref(cfg), C.byref(h)))
         self.h = h
         self.max_requests = max_requests
+        self.max_decode = max_decode
         self._keep = None
 
     def close(self):

@@ -60,6 +60,19 @@ class PropertyGraph:
         n = lib().glmx_graph_node_id(self.h, idx, buf, 4096)
         return None if n < 0 else buf.raw[:n].decode()
 
+    def node_attr(self, idx, key):
+        """(rendered value, kind) of node idx's attribute `key` (kinds: 0 string, 1 int,
+        2 double, 3 bool, 4 list), or None when absent."""
+        buf = C.create_string_buffer(4096)
+        kind = C.c_int32()
+        n = lib().glmx_graph_node_attr(self.h, int(idx), key.encode(), buf, 4096, C.byref(kind))
+        if n < 0:
+            return None
+        if n > 4096:
+            buf = C.create_string_buffer(n)
+            lib().glmx_graph_node_attr(self.h, int(idx), key.encode(), buf, n, C.byref(kind))
+        return buf.raw[:n].decode(), kind.value
+
     def total_degree(self, idx):
         return lib().glmx_graph_degree(self.h, idx)
 

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 from . import _lib
 from ._lib import check, lib
-from .kvcache import PrefillReport
+from .kvcache import PrefillReport, count_tokens  # noqa: F401  (count_tokens: tokenizer.hpp:36-46)
 from .templates import TIER_II, TIER_III, TIER_IV, TemplateSet
 
 
@@ -50,6 +50,10 @@ class Call:
     segments: list
     reply: str
 
+    @property
+    def is_finish(self):
+        return self.agent == "reasoning" and self.reply.startswith("Finish:")
+
 
 @dataclass
 class RotationResult:
@@ -67,10 +71,6 @@ class RotationResult:
     decode_collected: bool = True  # False: this rotation's decode was deferred into the next
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
-
-
-def count_tokens(text):
-    return len(text.split())
 
 
 class GraphCoTWorkload:
@@ -149,6 +149,9 @@ class GraphCoTWorkload:
             keep += [texts, ta, la, tr, sb]
             arr[i].seg_text, arr[i].seg_len, arr[i].seg_tier = ta, la, tr
             arr[i].n_seg, arr[i].session = len(texts), sb
+            # a Finish reply: Orchestrator::finish's set_tier(II -> III) follows this call's
+            # bookkeeping inside the batch, before the next lane's (run_bench order)
+            arr[i].finish = int(c.is_finish)
         return arr, keep
 
     def prefill(self, calls, packed=None):
@@ -191,10 +194,8 @@ class GraphCoTWorkload:
             elif c.agent == "action":
                 s.round += 1
                 s.state = "R"
-            elif c.reply.startswith("Finish:"):
+            elif c.is_finish:  # set_tier(II -> III) ran inside the prefill batch (pack)
                 s.state = "done"
-                if self.kv is not None:
-                    self.kv.set_tier(s.sid, TIER_II, TIER_III)
                 res.finished += 1
                 continue
             else:

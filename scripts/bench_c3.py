@@ -49,22 +49,18 @@ wl = W.GraphCoTWorkload(eng, ret, n_queries=args.lanes * 2, lanes=args.lanes, se
 # record every bookkeeping op in order: prefills (via prefill_async) and finish() set_tiers
 log = []
 orig_prefill = wl.prefill_async
-orig_set_tier = kv.set_tier
 
 
 def rec_prefill(calls):
+    # the reference's run_step order: each call's prefill, then finish()'s set_tier for a Finish
     for c in calls:
         log.append(("p", kv_prefill_inputs(c.segments), c.session.sid))
+        if c.is_finish:
+            log.append(("t", c.session.sid, 1, 2))
     return orig_prefill(calls)
 
 
-def rec_set_tier(session, a, b):
-    log.append(("t", session, a, b))
-    return orig_set_tier(session, a, b)
-
-
 wl.prefill_async = rec_prefill
-kv.set_tier = rec_set_tier
 eng.set_profiling(1)
 t0 = time.perf_counter()
 tokens = computed = fwd = 0.0
@@ -76,6 +72,8 @@ if args.sequential:
     def rec_prefill_sync(calls, packed=None):
         for c in calls:
             log.append(("p", kv_prefill_inputs(c.segments), c.session.sid))
+            if c.is_finish:
+                log.append(("t", c.session.sid, 1, 2))
         return orig_rot_prefill(calls, packed)
     wl.prefill = rec_prefill_sync
 for r in rots:

@@ -33,3 +33,11 @@ def port():
     if not os.path.exists(oracle.PORT_SO):
         oracle.build(ref=False)
     return oracle.port()
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    with open(os.path.join(GOLDEN, "golden.json")) as f:
+        return json.load(f)

@@ -212,10 +212,10 @@ def test_bookkeeping_matches_reference_under_pressure(ref):
 
 # bf16 floor at the Llama-3-8B shape (N(0,0.02) weights, 2 layers, 150 tokens), measured on the
 # CPU alone by rounding the fp32 oracle's activations to bf16 at the engine's storage points
-# (scripts/cpu_bf16_sensitivity.py): max |dlogit| 0.074, mean 0.0126 -- a bf16 KV cache alone
-# gives max 0.032.  The 2e-2/1e-2 logit tolerance is therefore unattainable at this shape with
-# any bf16 KV pool; the kernel-level attention check keeps it (test_attention_kernel_*), and the
-# logits are bounded by 1.5x the measured floor.
+# (scripts/cpu_bf16_sensitivity.py): max |dlogit| 0.074, mean 0.0126.  Against the plain fp32
+# oracle the engine is therefore bounded by that floor; against the oracle that rounds at the
+# engine's own storage points (Decoder(emulate_bf16=True): h1, qkv, q, k, v, P, attn, h2, gu, act,
+# hf) it must meet the north star's 2e-2 / 1e-2.
 FLOOR_MAX, FLOOR_MEAN = 0.074, 0.0126
 
 
@@ -225,18 +225,27 @@ def test_llama8b_shape_two_layer_slice():
                            d_ff=14336, vocab=128256)
     model, kv, eng = make(cfg, cap=64, headroom=64, max_req=4, max_tok=1024, max_decode=2,
                           max_ctx=1024)
-    dec = Decoder(cfg, model.export_all())
+    w = model.export_all()
+    dec = Decoder(cfg, w)
+    dec_bf = Decoder(cfg, w, emulate_bf16=True)
     p = words(150)
     reqs = [glmx.Request(p, [(0, 40, 0), (40, 150, 3)], "a"),
             glmx.Request(p[:130] + words(30, "y"), [(0, 160, 1)], "b")]
     reps, first, logits = eng.prefill(reqs, want_logits=True)
     assert reps[1].cached_tokens == 128
-    refs = [dec.forward(token_ids(r.tokens, cfg.vocab))[0] for r in reqs]
-    for i in range(2):
-        err = np.abs(logits[i] - refs[i])
-        assert err.max() <= 1.5 * FLOOR_MAX and err.mean() <= 1.5 * FLOOR_MEAN, (err.max(), err.mean())
+    ties = 0
     for i, r in enumerate(reqs):
-        dec.check_greedy(token_ids(r.tokens, cfg.vocab), [first[i]], atol=FLOOR_MAX, rtol=0.0)
+        ids = token_ids(r.tokens, cfg.vocab)
+        ref_bf = dec_bf.forward(ids)[0]
+        check_logits(logits[i], ref_bf)  # 2e-2 / 1e-2 at the engine's rounding points
+        ref = dec.forward(ids)[0]
+        err = np.abs(logits[i] - ref)
+        assert err.max() <= 1.5 * FLOOR_MAX and err.mean() <= 1.5 * FLOOR_MEAN, (err.max(), err.mean())
+        top = np.sort(ref_bf)[-2:]
+        ties += dec_bf.check_greedy(ids, [first[i]])
+        print(f"req {i}: max|d| vs bf16-emulating oracle {np.abs(logits[i] - ref_bf).max():.4f}, "
+              f"vs fp32 {err.max():.4f}; top1-top2 margin {top[1] - top[0]:.4f}")
+    print("near-tie exemptions:", ties)
 
 
 def test_pipelined_rotations_match_sequential():
