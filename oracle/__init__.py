@@ -239,6 +239,14 @@ def ref():
         L.ref_run_scripted.restype = C.c_int64
         L.ref_run_scripted.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_uint64,
                                        C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_uint64]
+        L.ref_scripted_open.restype = C.c_void_p
+        L.ref_scripted_open.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, C.c_uint64,
+                                        C.c_int, C.c_int]
+        L.ref_scripted_rotation.restype = C.c_int64
+        L.ref_scripted_rotation.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+        L.ref_scripted_snapshot.restype = C.c_int64
+        L.ref_scripted_snapshot.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+        L.ref_scripted_close.argtypes = [C.c_void_p]
         _ref = L
     return _ref
 
@@ -384,6 +392,42 @@ class RefGraph:
         if m < 0:
             raise RuntimeError(L.ref_last_error().decode())
         return json.loads(buf.raw[:m].decode()), (trace_lines() if record else None)
+
+
+class RefScriptedRun:
+    """The reference's Orchestrator + ScriptedProvider + KvCacheState + Retriever (oracle/_ref)
+    over a graph, driven one round-robin rotation at a time (bench.cpp:71-83)."""
+
+    def __init__(self, graph, trace_path, questions, lanes=8, cap=4096, policy=0, chunk_k=8):
+        L = ref()
+        self.L, self.graph = L, graph
+        qs = "\n".join(json.dumps(q) for q in questions)
+        self.h = L.ref_scripted_open(graph.h, trace_path.encode(), qs.encode(), lanes, cap, policy,
+                                     chunk_k)
+        if not self.h:
+            raise RuntimeError(L.ref_last_error().decode())
+        self.done = False
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_scripted_close(self.h)
+            self.h = None
+
+    def rotation(self):
+        """Runs one rotation; returns its calls [(session, actor, cached, computed+tail)]."""
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        m = self.L.ref_scripted_rotation(self.h, buf, cap)
+        if m < 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        out = json.loads(buf.raw[:m].decode())
+        self.done = out["done"]
+        return [tuple(c) for c in out["calls"]]
+
+    def snapshot(self):
+        buf = C.create_string_buffer(4096)
+        n = self.L.ref_scripted_snapshot(self.h, buf, 4096)
+        return json.loads(buf.raw[:n].decode())
 
 
 def trace_lines():

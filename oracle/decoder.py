@@ -64,6 +64,32 @@ class Decoder:
         self.inv = inv_freq(cfg.head_dim, cfg.rope_theta)
         sites = set(self.SITES) if emulate_bf16 is True else set(emulate_bf16 or ())
         self.r = lambda a, site: bf16_round(a) if site in sites else a
+        # with P emulated, the softmax follows the engine's K3 algorithm (attn_tc.cu): 128-key
+        # tiles, base-2 exponent with a lazily raised reference max (only when a tile's row max
+        # exceeds it by > 2^8), P rounded to bf16 for PV while the row sum adds the fp32 P
+        self.lazy_p = "P" in sites
+
+    def _attn_tiled(self, q, k, v, mask):
+        """One head: q [n, hd], k / v [m, hd], mask [n, m] -> [n, hd] (fp32)."""
+        n, hd = q.shape
+        scale = np.float32(1.0 / np.sqrt(hd) * 1.4426950408889634)
+        s_all = (q @ k.T).astype(np.float32)
+        m_used = np.full(n, -np.inf, dtype=np.float32)
+        l = np.zeros(n, dtype=np.float32)
+        o = np.zeros((n, v.shape[1]), dtype=np.float32)
+        for j0 in range(0, k.shape[0], 128):
+            s = np.where(mask[:, j0:j0 + 128], s_all[:, j0:j0 + 128], -np.inf).astype(np.float32)
+            mx = s.max(axis=1) * scale
+            grow = mx > m_used + np.float32(8.0)
+            with np.errstate(invalid="ignore", over="ignore"):
+                alpha = np.where(grow, np.exp2(m_used - mx), np.float32(1.0)).astype(np.float32)
+            alpha = np.where(np.isnan(alpha), np.float32(0.0), alpha)
+            m_used = np.where(grow, mx, m_used)
+            neg_m = np.where(np.isinf(m_used), np.float32(0.0), -m_used).astype(np.float32)
+            p = np.exp2(s * scale + neg_m[:, None]).astype(np.float32)
+            l = l * alpha + p.sum(axis=1, dtype=np.float32)
+            o = o * alpha[:, None] + bf16_round(p) @ v[j0:j0 + 128]
+        return o / l[:, None]
 
     def forward(self, ids, pos=None, past=None, return_all=False):
         """ids [n]; past: per-layer (K [p,Hkv,hd], V) of preceding positions.  Returns logits of
@@ -97,6 +123,9 @@ class Decoder:
             mask = kpos[None, :] <= np.asarray(pos)[:, None]
             for hh in range(H):
                 kh = hh // G
+                if self.lazy_p:
+                    out[:, hh, :] = self._attn_tiled(q[:, hh, :], k[:, kh, :], v[:, kh, :], mask)
+                    continue
                 s = (q[:, hh, :] @ k[:, kh, :].T) / np.sqrt(hd)
                 s = np.where(mask, s, -np.inf)
                 s = s - s.max(axis=1, keepdims=True)

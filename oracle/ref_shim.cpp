@@ -498,4 +498,90 @@ int64_t ref_run_scripted(void* g, const char* trace_path, const char* questions_
   }
 }
 
+// ---------------------------------------------------------------- rotation-granular scripted run
+// The same round-robin as ref_run_scripted, one rotation per call, so a caller can time the
+// reference's CPU path rotation by rotation (bench.py --impl reference).
+struct RefScripted {
+  glm::Config cfg;
+  std::unique_ptr<glm::VectorIndex> index;
+  std::unique_ptr<glm::Retriever> retriever;
+  std::unique_ptr<glm::KvCacheState> kv;
+  glm::TemplateSet templates = glm::TemplateSet::builtin();
+  std::unique_ptr<glm::ScriptedProvider> provider;
+  std::unique_ptr<glm::Orchestrator> orch;
+  std::vector<glm::Session> sessions;
+  std::size_t admitted = 0, lanes = 1;
+  std::vector<std::size_t> active;
+};
+
+void* ref_scripted_open(void* g, const char* trace_path, const char* questions_jsonl,
+                        int concurrency, std::uint64_t cap_blocks, int policy, int chunk_k) {
+  auto* rg = static_cast<RefGraph*>(g);
+  try {
+    auto r = std::make_unique<RefScripted>();
+    r->cfg.kv_capacity_blocks = cap_blocks;
+    r->cfg.kv_policy = policy == 0 ? glm::CachePolicy::Priority : glm::CachePolicy::PlainLru;
+    r->cfg.chunk_k = chunk_k;
+    r->cfg.timing_mode = glm::TimingMode::Simulated;
+    r->index = std::make_unique<glm::VectorIndex>(glm::VectorIndex::build(rg->g, r->cfg));
+    r->retriever = std::make_unique<glm::Retriever>(rg->g, *r->index, r->cfg);
+    r->kv = std::make_unique<glm::KvCacheState>(r->cfg.kv_capacity_blocks, r->cfg.kv_block_tokens,
+                                                r->cfg.kv_policy);
+    r->provider = std::make_unique<glm::ScriptedProvider>(glm::ScriptedProvider::load_jsonl(trace_path));
+    r->orch = std::make_unique<glm::Orchestrator>(*r->retriever, r->templates, *r->provider, *r->kv,
+                                                  r->cfg);
+    std::istringstream qs(questions_jsonl);
+    std::string line;
+    while (std::getline(qs, line)) {
+      if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
+      json j = json::parse(line);
+      r->sessions.push_back(r->orch->make_session(j.at("id").get<std::string>(),
+                                                  j.at("text").get<std::string>(), false));
+    }
+    r->lanes = static_cast<std::size_t>(std::max(1, concurrency));
+    return r.release();
+  } catch (const std::exception& e) {
+    status_of(e);
+    return nullptr;
+  }
+}
+
+// One rotation (bench.cpp:71-83).  Writes {"calls": [[session, actor, cached, computed], ...],
+// "done": bool}: the C / R / A records the rotation's run_steps appended, in call order.
+int64_t ref_scripted_rotation(void* h, char* buf, std::uint64_t cap) {
+  auto* r = static_cast<RefScripted*>(h);
+  try {
+    while (r->active.size() < r->lanes && r->admitted < r->sessions.size())
+      r->active.push_back(r->admitted++);
+    json calls = json::array();
+    for (std::size_t i = 0; i < r->active.size();) {
+      glm::Session& s = r->sessions[r->active[i]];
+      const std::size_t before = s.trace.records.size();
+      r->orch->run_step(s);
+      if (s.state == glm::SessionState::Interrupted) r->orch->resume(s);
+      for (std::size_t k = before; k < s.trace.records.size(); ++k) {
+        const auto& rec = s.trace.records[k];
+        if (rec.actor == 'C' || rec.actor == 'R' || rec.actor == 'A')
+          calls.push_back({s.id, std::string(1, rec.actor), rec.cached_tokens, rec.computed_tokens});
+      }
+      if (s.terminal())
+        r->active.erase(r->active.begin() + static_cast<std::ptrdiff_t>(i));
+      else
+        ++i;
+    }
+    json out;
+    out["calls"] = calls;
+    out["done"] = r->admitted >= r->sessions.size() && r->active.empty();
+    return copy_out(out.dump(), buf, cap);
+  } catch (const std::exception& e) {
+    return -status_of(e);
+  }
+}
+
+int64_t ref_scripted_snapshot(void* h, char* buf, std::uint64_t cap) {
+  return copy_out(static_cast<RefScripted*>(h)->kv->snapshot_json(), buf, cap);
+}
+
+void ref_scripted_close(void* h) { delete static_cast<RefScripted*>(h); }
+
 }  // extern "C"

@@ -25,7 +25,7 @@ import random
 import threading
 from dataclasses import dataclass, field
 
-from . import _lib
+from . import _lib, synth
 from ._lib import check, lib
 from .kvcache import PrefillReport, count_tokens  # noqa: F401  (count_tokens: tokenizer.hpp:36-46)
 from .templates import TIER_II, TIER_III, TIER_IV, TemplateSet
@@ -71,6 +71,7 @@ class RotationResult:
     decode_collected: bool = True  # False: this rotation's decode was deferred into the next
     reports: list = field(default_factory=list)
     first_tokens: list = field(default_factory=list)
+    calls_made: list = field(default_factory=list)  # the rotation's Calls, in lane order
 
 
 class GraphCoTWorkload:
@@ -86,26 +87,17 @@ class GraphCoTWorkload:
         self.retriever = retriever
         self.templates = templates or TemplateSet()
         self.lanes = lanes
-        rnd = random.Random(seed)
         g = retriever.graph
-        n = g.node_count()
-        self.sessions = []
+        # the question stream (synth.graph_cot_questions, shared with bench.py's reference arm);
         # question_pool > 0: questions are drawn WITH replacement from that many candidate source
         # lists, as generate_workload picks clusters (workload.cpp:216-225), so questions recur
         # across sessions (and, sharded i mod N, across GPUs)
-        pool = []
-        for _ in range(question_pool):
-            m = rnd.randint(min_hops, max_hops)
-            pool.append([min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)])
-        for q in range(n_queries):
-            if pool:
-                src = list(pool[rnd.randrange(len(pool))])
-            else:
-                m = rnd.randint(min_hops, max_hops)
-                src = [min(n - 1, int(n * rnd.random() ** skew)) for _ in range(m)]
+        self.sessions = []
+        for sid, src, _ in synth.graph_cot_questions(g.node_count(), n_queries, seed, min_hops,
+                                                     max_hops, skew, question_pool):
             ids = [g.node_id(v) for v in src]
             question = "Which item is linked from all of: " + "; ".join(ids) + "?"
-            self.sessions.append(Session(f"q{q:05d}", src, question))
+            self.sessions.append(Session(sid, src, question))
         self.admitted = 0
         self.active = []
 
@@ -115,18 +107,18 @@ class GraphCoTWorkload:
     def _call_for(self, s: Session) -> Call:
         t = self.templates
         if s.state == "C":
-            return Call(s, "classification", t.render_classification(s.question), "no\n")
+            return Call(s, "classification", t.render_classification(s.question),
+                        synth.classify_reply())
         if s.state == "R":
             if s.round < len(s.sources):
                 nid = self.retriever.graph.node_id(s.sources[s.round])
                 s.task = "vertex chunks for: " + nid
                 return Call(s, "reasoning", t.render_reasoning(s.question, s.notebook),
-                            "Missing: " + s.task + "\n")
+                            synth.missing_reply(nid))
             return Call(s, "reasoning", t.render_reasoning(s.question, s.notebook),
-                        "Finish: " + self.retriever.graph.node_id(s.sources[0]) + "\n")
+                        synth.finish_reply(self.retriever.graph.node_id(s.sources[0])))
         nid = s.task[len("vertex chunks for: "):]
-        code = f'```\nprint(NodeInfo(RetrieveNode("{nid}")))\n```\n'
-        return Call(s, "action", t.render_action(s.task), code)
+        return Call(s, "action", t.render_action(s.task), synth.action_reply(nid))
 
     def next_calls(self):
         """Admission + one call per active lane, in lane order (bench.cpp:71-76)."""
@@ -167,7 +159,7 @@ class GraphCoTWorkload:
         """Apply the replies: state transitions, K1 chunk build for the actions (or the batch
         `chunks` already built for them), finish."""
         res = RotationResult(calls=len(calls), reports=reports or [],
-                             first_tokens=first_tokens or [])
+                             first_tokens=first_tokens or [], calls_made=list(calls))
         for r in res.reports:
             res.cached_tokens += r.cached_tokens
             res.computed_tokens += r.computed_tokens + r.tail_tokens
