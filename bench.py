@@ -43,9 +43,12 @@ def parse():
     p.add_argument("--capacity", type=int, default=16384)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--question-pool", type=int, default=-1,
+    p.add_argument("--question-pool", type=int, default=192,
                    help="draw questions with replacement from this many candidates (reference "
-                        "generate_workload style); -1 = half the total query count, 0 = all unique")
+                        "generate_workload style); 0 = all unique")
+    p.add_argument("--cache-warm", type=int, default=64,
+                   help="untimed rotations before the warm-up steps that bring the prefix cache "
+                        "to its steady state (the value then does not drift with --steps)")
     p.add_argument("--routing", default="mod", choices=["mod", "affinity"],
                    help="query -> GPU: i mod N (reference sharding) or prefix affinity "
                         "(fnv1a(question) mod N: repeated questions stay on one GPU)")
@@ -66,6 +69,43 @@ def parse():
                         "bucket up to this many batch tokens (glmx_model_tune_gemms); 0 keeps "
                         "cublasGemmEx's default choice")
     return p.parse_args()
+
+
+def workload_shape(args, ws):
+    """(queries per rank, question pool, rotations run) -- identical in both arms.  The pool is
+    fixed and the question stream is a prefix-stable draw (synth.graph_cot_questions), so the
+    rotations that are timed do not depend on --steps."""
+    rotations = args.cache_warm + args.warmup + args.steps
+    n_q = args.lanes * (rotations // 6 + 2)
+    return n_q, args.question_pool, rotations
+
+
+def bench_config(args, ws, pipelined=True, pool_n=None):
+    """The `config` object of the JSON line -- the same for `--impl glmx` and `--impl reference`."""
+    return {"workload": "C2: Graph-CoT scripted sessions (classify -> reason/act per hop "
+                        "-> finish), synthetic 100k-node power-law graph, top-k=16 vertex "
+                        "chunks, Llama-3-8B-shaped random-init bf16, paged KV pool",
+            "lanes_per_gpu": args.lanes, "nodes": args.nodes, "k": args.k,
+            "question_pool": args.question_pool if pool_n is None else pool_n,
+            "cache_warm_rotations": args.cache_warm,
+            "kv_capacity_blocks": args.capacity, "block_tokens": 16, "policy": "priority",
+            "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
+            "parallelism": f"query-sharded x{ws}", "routing": args.routing,
+            "host_pipelining": pipelined}
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) without an external launcher: re-exec under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -146,96 +186,174 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_baseline_sample(calls_tokens, chunk_nodes, graph_jsonl, seconds_budget=20.0, reps=None):
-    """The reference's CPU path on a bounded sample: the reference bookkeeping (oracle/_ref,
-    KvCacheState::prefill + Retriever::node_info_rendered) and, because the reference has no
-    tensor math, the builder's fp32 numpy decoder for the computed tokens as a 1-layer
-    Llama-3-8B slice x 32 layers (labelled extrapolation).  Returns (tokens/s, cores, sample)."""
-    import numpy as np
+def load_synth():
+    """paper_2511_01633_b200/synth.py loaded by path: the reference arm builds the same workload
+    without importing the package (no product library is mapped in that process)."""
+    import importlib.util
 
-    import oracle
-    from oracle.decoder import rmsnorm
+    spec = importlib.util.spec_from_file_location(
+        "glmx_synth", os.path.join(ROOT, "paper_2511_01633_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
-    t_book = 0.0
-    ref_graph = oracle.RefGraph(path=graph_jsonl)
-    rk = oracle.RefKv(oracle.ref(), 1 << 20, 16, 0)
-    t0 = time.perf_counter()
-    for nid in chunk_nodes:
-        ref_graph.node_info_rendered(nid, 16)
-    total_tok, comp_tok = 0, []
-    for toks, tiers, sess in calls_tokens:
-        st, rep, _ = rk.prefill(toks, tiers, sess)
-        total_tok += len(toks)
-        comp_tok.append(max(1, rep[1] + rep[2]))
-    t_book = time.perf_counter() - t0
-    # one decoder layer of the 8B shape, fp32, all host threads (numpy BLAS)
-    rng = np.random.default_rng(0)
-    d, H, Hkv, hd, ff = 4096, 32, 8, 128, 14336
-    W = {k: (rng.standard_normal(s, dtype=np.float32) * 0.02) for k, s in
-         {"wqkv": ((H + 2 * Hkv) * hd, d), "wo": (d, H * hd), "wgu": (2 * ff, d),
-          "wd": (d, ff)}.items()}
-    x = rng.standard_normal((sum(comp_tok), d), dtype=np.float32)
-    t1 = time.perf_counter()
-    h = rmsnorm(x, 1.0, 1e-5)
-    qkv = h @ W["wqkv"].T
-    x = x + qkv[:, :H * hd] @ W["wo"].T  # attention core omitted: linear-dominated at this size
-    h = rmsnorm(x, 1.0, 1e-5)
-    gu = h @ W["wgu"].T
-    act = gu[:, :ff] / (1 + np.exp(-gu[:, :ff])) * gu[:, ff:]
-    x = x + act @ W["wd"].T
-    t_layer = time.perf_counter() - t1
-    total = t_book + 32 * t_layer
+
+def host_cpu():
+    """(threads usable, CPU model line) of this host."""
     cores = os.cpu_count() or 1
     try:
         cores = len(os.sched_getaffinity(0))
     except AttributeError:
         pass
-    sample = (f"{len(calls_tokens)} prefill calls ({total_tok} prompt tokens, {sum(comp_tok)} computed) "
-              f"+ {len(chunk_nodes)} vertex chunks: reference bookkeeping {t_book:.3f}s + numpy fp32 "
-              f"1-layer 8B slice {t_layer:.3f}s x32 (extrapolated; attention core omitted)")
-    return total_tok / total, cores, sample
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return cores, model
+
+
+class CpuDecoderSlice:
+    """The tensor math of the prefill step on the host cores -- which the reference does not have
+    (it only costs it, orchestrator.cpp:131-132) -- restated in fp32 numpy: ONE
+    Llama-3-8B decoder layer (RMSNorm, QKV, RoPE-free causal GQA attention over each sampled
+    call's full context, O, RMSNorm, SwiGLU MLP) timed on a bounded sample of the rotation's
+    computed tokens, scaled to all its computed tokens x 32 layers, plus the lm_head rows of the
+    rotation's calls (a 1/16 vocabulary slice, x16).  An extrapolation, labelled as such."""
+
+    SAMPLE_TOKENS = 256
+
+    def __init__(self, seed=0):
+        import numpy as np
+
+        rng = np.random.default_rng(seed)
+        d, self.H, self.Hkv, self.hd, ff = 4096, 32, 8, 128, 14336
+        self.d, self.ff = d, ff
+
+        def w(*shape):
+            return rng.standard_normal(shape, dtype=np.float32) * np.float32(0.02)
+
+        self.w = {"qkv": w((self.H + 2 * self.Hkv) * self.hd, d), "o": w(d, self.H * self.hd),
+                  "gu": w(2 * ff, d), "down": w(d, ff), "lm": w(128256 // 16, d)}
+        self.np = np
+
+    def _layer(self, n, ctx):
+        np, H, Hkv, hd, d = self.np, self.H, self.Hkv, self.hd, self.d
+        x = np.ones((n, d), dtype=np.float32)
+        h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + 1e-5)
+        qkv = h @ self.w["qkv"].T
+        q = qkv[:, :H * hd].reshape(n, H, hd)
+        k = np.concatenate([np.ones((ctx - n, Hkv, hd), np.float32),
+                            qkv[:, H * hd:(H + Hkv) * hd].reshape(n, Hkv, hd)])
+        v = np.concatenate([np.ones((ctx - n, Hkv, hd), np.float32),
+                            qkv[:, (H + Hkv) * hd:].reshape(n, Hkv, hd)])
+        mask = np.arange(ctx)[None, :] <= np.arange(ctx - n, ctx)[:, None]
+        att = np.empty((n, H, hd), np.float32)
+        for hh in range(H):
+            s = (q[:, hh] @ k[:, hh // (H // Hkv)].T) * np.float32(hd ** -0.5)
+            s = np.where(mask, s, -np.inf)
+            p = np.exp(s - s.max(axis=1, keepdims=True))
+            att[:, hh] = (p @ v[:, hh // (H // Hkv)]) / p.sum(axis=1, keepdims=True)
+        x = x + att.reshape(n, H * hd) @ self.w["o"].T
+        h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + 1e-5)
+        gu = h @ self.w["gu"].T
+        g, u = gu[:, :self.ff], gu[:, self.ff:]
+        return x + (g / (1 + np.exp(-g)) * u) @ self.w["down"].T
+
+    def rotation_seconds(self, calls):
+        """calls [(session, actor, cached, computed)] -> (seconds, description)."""
+        np = self.np
+        total = sum(c[3] for c in calls)
+        sample, got = [], 0
+        for c in sorted(calls, key=lambda c: -c[3]):  # the rotation's largest calls first
+            if got >= self.SAMPLE_TOKENS or c[3] == 0:
+                break
+            n = min(c[3], self.SAMPLE_TOKENS - got)
+            sample.append((n, c[2] + c[3]))  # the last n tokens of the call, full context
+            got += n
+        t0 = time.perf_counter()
+        for n, ctx in sample:
+            self._layer(n, ctx)
+        t_layer = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        np.ones((len(calls), self.d), np.float32) @ self.w["lm"].T
+        t_lm = (time.perf_counter() - t1) * 16
+        secs = (t_layer / max(1, got)) * total * 32 + t_lm
+        return secs, (f"1 layer x {got} sampled tokens {t_layer:.3f}s -> x{total} computed tokens "
+                      f"x32 layers, lm_head {len(calls)} rows {t_lm:.3f}s")
+
+
+def reference_rotations(args, ws, rank, steps, warm):
+    """The reference's CPU path over this bench's workload, rotation by rotation: its own
+    PropertyGraph::load of the synthetic graph JSONL, Orchestrator + ScriptedProvider (the same
+    questions and replies as the GPU arm, rank `rank`'s shard), KvCacheState (capacity, priority)
+    and Retriever (node_info k, RetrieveNode over its VectorIndex) -- oracle/_ref, timed exactly
+    -- plus the prefill tensor math it lacks (CpuDecoderSlice, extrapolated).  `warm` untimed
+    rotations first (cache warm + warm-up, as the GPU arm).  Returns per-step dicts."""
+    import oracle
+
+    synth = load_synth()
+    tag = f"{os.getpid()}_{args.nodes}_{args.seed}"
+    gpath = synth.powerlaw_graph_jsonl(args.nodes, 8, args.seed, f"/tmp/glmx_c2_graph_{tag}.jsonl")
+    n_q, pool_n, _ = workload_shape(args, ws)
+    sessions = synth.graph_cot_questions(args.nodes, n_q * ws, args.seed,
+                                         question_pool=pool_n)[rank::ws]
+    tpath = synth.write_jsonl(synth.scripted_replies(sessions), f"/tmp/glmx_c2_trace_{tag}.jsonl")
+    run = oracle.RefScriptedRun(oracle.RefGraph(path=gpath), tpath,
+                                [{"id": sid, "text": q} for sid, _, q in sessions], args.lanes,
+                                args.capacity, 0, args.k)
+    for _ in range(warm):
+        run.rotation()
+    dec = CpuDecoderSlice(args.seed)
+    out = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        calls = run.rotation()
+        t_book = time.perf_counter() - t0
+        t_math, desc = dec.rotation_seconds(calls)
+        out.append({"tokens": sum(c[2] + c[3] for c in calls),
+                    "computed": sum(c[3] for c in calls), "calls": len(calls),
+                    "t_book": t_book, "t_math": t_math, "desc": desc})
+    for p in (gpath, tpath):
+        try:
+            os.remove(p)
+        except OSError:
+            pass
+    return out
+
+
+def summarize_reference(rows):
+    tok = sum(r["tokens"] for r in rows)
+    t_book = sum(r["t_book"] for r in rows)
+    t_math = sum(r["t_math"] for r in rows)
+    value = tok / (t_book + t_math)
+    cores, model = host_cpu()
+    sample = (f"{len(rows)} rotations ({sum(r['calls'] for r in rows)} calls, {tok} prompt tokens, "
+              f"{sum(r['computed'] for r in rows)} computed): reference Orchestrator + "
+              f"ScriptedProvider + KvCacheState + Retriever (oracle/_ref) {t_book:.3f}s timed, + "
+              f"fp32 numpy prefill math {t_math:.2f}s (per rotation: {rows[-1]['desc']}); "
+              f"host: {cores} threads, {model}")
+    return value, cores, sample
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the reference's own CPU path (oracle/_ref bookkeeping + the fp32 decoder
-    restatement) on the host cores, rank 0 only."""
+    """--impl reference: the reference's own CPU path on this bench's workload (rank 0 only)."""
     if rank != 0:
         return
-    import paper_2511_01633_b200 as glmx  # only for the synthetic graph + workload text
-    from paper_2511_01633_b200.workload import GraphCoTWorkload
-
-    g = glmx.PropertyGraph.synth_powerlaw(args.nodes, 8, seed=args.seed, device=0)
-    path = f"/tmp/glmx_bench_graph_{args.nodes}_{args.seed}.jsonl"
-    if not os.path.exists(path):
-        g.save(path)
-    ret = glmx.Retriever(g, chunk_k=args.k, vocab=0)
-    wl = GraphCoTWorkload(None, ret, n_queries=args.lanes * 4, lanes=args.lanes, seed=args.seed)
-    from oracle import kv_prefill_inputs
-
-    def step_sample():
-        calls = wl.next_calls()
-        wl.advance(calls)
-        sub = calls[:4]
-        toks = [kv_prefill_inputs(c.segments) + (c.session.sid,) for c in sub]
-        nodes = [g.node_id(c.session.sources[min(c.session.round, len(c.session.sources) - 1)])
-                 for c in sub]
-        return toks, nodes
-
-    vals = []
-    for i in range(args.warmup + args.steps):
-        toks, nodes = step_sample()
-        v, cores, sample = cpu_baseline_sample(toks, nodes, path)
-        if i >= args.warmup:
-            vals.append(v)
-    value = sum(vals) / len(vals)
+    rows = reference_rotations(args, ws, rank, args.steps, args.cache_warm + args.warmup)
+    value, cores, sample = summarize_reference(rows)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-           "config": {"workload": "C2: Graph-CoT scripted sessions, 100k-node power-law graph, "
-                                  "k=16, Llama-3-8B shape", "lanes": args.lanes},
+           "scaling": "weak", "dtype": "f32", "data": "synthetic",
+           "config": bench_config(args, ws, not args.no_pipeline),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                            "sample": "per step: " + sample},
+                            "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "data": "synthetic"}
+           "cache_hit_token_frac": 1 - sum(r["computed"] for r in rows) / max(1, sum(r["tokens"] for r in rows))}
     print(json.dumps(out))
 
 
@@ -281,7 +399,11 @@ def standalone_kernels(glmx, g, ret, peaks, tc_peak_burst):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
@@ -315,10 +437,8 @@ def main():
                            headroom_pages=4096)
     eng = glmx.Engine(model, kv, max_requests=args.lanes, max_batch_tokens=args.lanes * 1024,
                       max_decode=8, max_context=8192)
-    rotations = args.warmup + args.steps
     # enough queries (per rank) that every lane stays busy through the timed rotations
-    n_q = args.lanes * (rotations // 6 + 2)
-    pool_n = args.question_pool if args.question_pool >= 0 else (n_q * ws) // 2
+    n_q, pool_n, _ = workload_shape(args, ws)
     nidx = glmx.NodeIndex(g)  # RetrieveNode: device VectorIndex + retrieval LRU (K5)
     wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed,
                           question_pool=pool_n, node_index=nidx)
@@ -359,7 +479,8 @@ def main():
             for _ in range(k):
                 yield step()
 
-    for _ in rotations(args.warmup):
+    # steady state: the cache-warm rotations, then the warm-up steps (both untimed)
+    for _ in rotations(args.cache_warm + args.warmup):
         pass
     # per-kernel-category CUDA events on the engine stream during the timed steps (host cost
     # ~1 us per event record, <1% of a step)
@@ -379,7 +500,7 @@ def main():
     fwd_ms = 0.0
     cat_ms = {"attention": 0.0, "kv_append": 0.0, "gemm": 0.0, "elementwise": 0.0}
     work = {"attn_flops": 0.0, "attn_bytes": 0.0, "append_bytes": 0.0, "linear_flops": 0.0}
-    h2d = d2h = 0
+    io0 = eng.io_bytes(), g.io_bytes()
     chunk_ms = 0.0
     k1_bytes = 0
     k5_launches = 0
@@ -410,10 +531,6 @@ def main():
         if wk["computed_tokens"] >= 2048:  # K2 in its bandwidth regime (large prefill batches)
             k2_big_ms += tm["kv_append"]
             k2_big_bytes += wk["append_bytes"]
-        # host->device per step: packed batch metadata + chunk node ids; device->host: greedy ids
-        # + chunk bytes/tokens
-        h2d += int(wk["computed_tokens"]) * 16 + r.calls * (16 + 8 * 520) + r.chunks * 4
-        d2h += r.calls * 4 + r.chunks * 1200
     ev1.record()
     torch.cuda.synchronize()
     if prof_range:
@@ -422,6 +539,12 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     wall_ms = ev0.elapsed_time(ev1)
+    # host<->device bytes of the timed steps, counted by the engine (packed batch metadata up,
+    # greedy ids down) and the graph (RetrieveNode query embeddings + K1 node ids up, winners +
+    # chunk bytes / offsets / token ids / spans down)
+    io1 = eng.io_bytes(), g.io_bytes()
+    h2d = (io1[0][0] - io0[0][0]) + (io1[1][0] - io0[1][0])
+    d2h = (io1[0][1] - io0[0][1]) + (io1[1][1] - io0[1][1])
 
     eng.set_profiling(0)
     tm = dict(cat_ms, forward=fwd_ms)
@@ -566,18 +689,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "C2: Graph-CoT scripted sessions (classify -> reason/act per hop "
-                               "-> finish), synthetic 100k-node power-law graph, top-k=16 vertex "
-                               "chunks, Llama-3-8B-shaped random-init bf16, paged KV pool",
-                   "lanes_per_gpu": args.lanes, "nodes": args.nodes, "k": args.k,
-                   "question_pool": pool_n,
-                   "kv_capacity_blocks": args.capacity, "block_tokens": 16,
-                   "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
-                   "parallelism": f"query-sharded x{ws}", "routing": args.routing,
-                   "host_pipelining": pipelined,
-                   "gemm_algorithms": {"tuned_up_to_tokens": args.gemm_tune_tokens,
-                                       "buckets_with_winner": gemm_tuned,
-                                       "tune_s": round(t_tune, 2)}},
+        "config": bench_config(args, ws, pipelined, pool_n),
+        "gemm_algorithms": {"tuned_up_to_tokens": args.gemm_tune_tokens,
+                            "buckets_with_winner": gemm_tuned, "tune_s": round(t_tune, 2)},
         "raw_computed_tokens_per_s": computed / (fwd_ms * 1e-3),
         "cache_hit_token_frac": cached / max(1.0, tokens),
         "calls": calls, "queries_finished": finished,
@@ -601,15 +715,10 @@ def main():
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:
-        from oracle import kv_prefill_inputs
-
-        path = f"/tmp/glmx_bench_graph_{args.nodes}_{args.seed}.jsonl"
-        g.save(path)
-        sub = wl.next_calls()[:8]
-        toks = [kv_prefill_inputs(c.segments) + (c.session.sid,) for c in sub]
-        nodes = [g.node_id(c.session.sources[min(c.session.round, len(c.session.sources) - 1)])
-                 for c in sub]
-        v, cores, sample = cpu_baseline_sample(toks, nodes, path)
+        # the reference's CPU path on a bounded sample of the same rotations (3 timed rotations
+        # after the same warm-up), on this host's cores
+        rows = reference_rotations(args, ws, rank, 3, args.cache_warm + args.warmup)
+        v, cores, sample = summarize_reference(rows)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                                "sample": sample}
     print(json.dumps(out))

@@ -179,6 +179,10 @@ uint64_t glmx_graph_edge_count(const glmx_graph* g);
 int64_t glmx_graph_node_index(const glmx_graph* g, const char* id);
 int64_t glmx_graph_node_id(const glmx_graph* g, uint64_t idx, char* buf, uint64_t cap);
 int64_t glmx_graph_degree(const glmx_graph* g, uint64_t idx); /* total_degree (:209-213) */
+/* Bytes the graph's K1 chunk builds and K5 RetrieveNode scans moved since load: out2[0]
+ * host->device (node ids, query embeddings), out2[1] device->host (chunk bytes, offsets, token
+ * ids / spans, nearest winners). */
+int glmx_graph_io_bytes(const glmx_graph* g, uint64_t out2[2]);
 /* PropertyGraph::node(id).attributes[key] (graph_store.hpp:27-75) in its canonical rendering
  * (render_attr_value, attr.hpp:38-48); kind (nullable): 0 string, 1 int, 2 double, 3 bool,
  * 4 list.  Returns the value's byte length, or -1 when the node has no such attribute. */

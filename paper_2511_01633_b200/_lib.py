@@ -121,6 +121,7 @@ _SIGS = {
     "glmx_graph_node_index": (C.c_int64, [C.c_void_p, C.c_char_p]),
     "glmx_graph_node_id": (C.c_int64, [C.c_void_p, C.c_uint64, C.c_char_p, C.c_uint64]),
     "glmx_graph_degree": (C.c_int64, [C.c_void_p, C.c_uint64]),
+    "glmx_graph_io_bytes": (C.c_int, [C.c_void_p, u64p]),
     "glmx_graph_node_attr": (C.c_int64, [C.c_void_p, C.c_uint64, C.c_char_p, C.c_char_p,
                                          C.c_uint64, i32p]),
     "glmx_chunk_build": (C.c_int, [C.c_void_p, C.POINTER(ChunkConfig), i32p, C.c_uint64,

@@ -392,6 +392,11 @@ int64_t glmx_graph_node_attr(const glmx_graph* g, uint64_t idx, const char* key,
     }
   return -1;
 }
+int glmx_graph_io_bytes(const glmx_graph* g, uint64_t out2[2]) {
+  out2[0] = g->h2d_bytes;
+  out2[1] = g->d2h_bytes;
+  return GLMX_OK;
+}
 int64_t glmx_graph_degree(const glmx_graph* g, uint64_t idx) {
   if (idx >= g->host.n()) return -1;
   return g->host.w_total[idx];

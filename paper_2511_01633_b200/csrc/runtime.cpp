@@ -195,6 +195,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   g->d_temp.reserve(std::max(t32, t64));
   int32_t* big_count = reinterpret_cast<int32_t*>(g->d_toff.as<uint32_t>() + n + 1);
   GLMX_CUDA(cudaMemcpyAsync(g->d_nodes.p, node_idx, n * 4, cudaMemcpyHostToDevice, s));
+  g->h2d_bytes += n * 4;
   GLMX_CUDA(cudaMemsetAsync(g->d_len.p, 0, (n + 1) * 8, s));
   GLMX_CUDA(cudaMemsetAsync(g->d_tidx.as<uint32_t>() + n, 0, 4, s));
   GLMX_CUDA(cudaEventRecord(g->ev0, s));
@@ -212,6 +213,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   if (bound > (64ull << 20)) {
     GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
     GLMX_CUDA(cudaStreamSynchronize(s));
+    g->d2h_bytes += 8;
   } else {
     total = bound;
   }
@@ -229,6 +231,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_toff.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
   GLMX_CUDA(cudaStreamSynchronize(s));
+  g->d2h_bytes += 12;
   GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));
   const uint64_t ntok = ntok32;
   if (total_bytes) *total_bytes = total;
@@ -237,17 +240,28 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   if (bytes_cap < total || (tok_cap < ntok && (out_tok_ids || out_tok_begin || out_tok_end)))
     throw Error(GLMX_ERR_ARG, "chunk output buffers too small");
   GLMX_CUDA(cudaMemcpyAsync(out_bytes, g->d_bytes.p, total, cudaMemcpyDeviceToHost, s));
-  if (out_byte_offsets)
+  g->d2h_bytes += total;
+  if (out_byte_offsets) {
     GLMX_CUDA(cudaMemcpyAsync(out_byte_offsets, g->d_off.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-  if (out_tok_ids && cfg->vocab)
+    g->d2h_bytes += (n + 1) * 8;
+  }
+  if (out_tok_ids && cfg->vocab) {
     GLMX_CUDA(cudaMemcpyAsync(out_tok_ids, g->d_tid.p, ntok * 4, cudaMemcpyDeviceToHost, s));
-  if (out_tok_begin)
+    g->d2h_bytes += ntok * 4;
+  }
+  if (out_tok_begin) {
     GLMX_CUDA(cudaMemcpyAsync(out_tok_begin, g->d_tbeg.p, ntok * 8, cudaMemcpyDeviceToHost, s));
-  if (out_tok_end)
+    g->d2h_bytes += ntok * 8;
+  }
+  if (out_tok_end) {
     GLMX_CUDA(cudaMemcpyAsync(out_tok_end, g->d_tend.p, ntok * 8, cudaMemcpyDeviceToHost, s));
+    g->d2h_bytes += ntok * 8;
+  }
   std::vector<uint32_t> toff32(out_tok_offsets ? n + 1 : 0);
-  if (out_tok_offsets)
+  if (out_tok_offsets) {
     GLMX_CUDA(cudaMemcpyAsync(toff32.data(), g->d_toff.p, (n + 1) * 4, cudaMemcpyDeviceToHost, s));
+    g->d2h_bytes += (n + 1) * 4;
+  }
   GLMX_CUDA(cudaStreamSynchronize(s));
   if (out_tok_offsets)
     for (uint64_t i = 0; i <= n; ++i) out_tok_offsets[i] = toff32[i];
@@ -1521,6 +1535,8 @@ int retrieve_impl(glmx_graph* g, const char* bytes, const uint64_t* offs, uint64
     g->d_qemb.reserve(q.size() * 4);
     g->d_best.reserve(static_cast<size_t>(nq) * 8);
     GLMX_CUDA(cudaMemcpyAsync(g->d_qemb.p, q.data(), q.size() * 4, cudaMemcpyHostToDevice, s));
+    g->h2d_bytes += q.size() * 4;
+    g->d2h_bytes += static_cast<uint64_t>(nq) * 8;
     GLMX_CUDA(cudaMemsetAsync(g->d_best.p, 0, static_cast<size_t>(nq) * 8, s));
     GLMX_CUDA(cudaEventRecord(g->ev0, s));
     nearest_top1(g->d_emb.as<float>(), static_cast<int>(g->idx_node.size()), dpad, g->d_qemb.as<float>(), nq,

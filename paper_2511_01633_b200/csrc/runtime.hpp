@@ -77,6 +77,7 @@ struct glmx_graph {
   glmx::TextLru lru{1024};
   int64_t stats[3] = {0, 0, 0};  // cache_hits, cache_misses, index_probes
   float last_retrieve_ms = 0.f;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // K1 / K5 host<->device copies (glmx_graph_io_bytes)
   void upload();
   ~glmx_graph();
 };

@@ -73,6 +73,12 @@ class PropertyGraph:
             lib().glmx_graph_node_attr(self.h, int(idx), key.encode(), buf, n, C.byref(kind))
         return buf.raw[:n].decode(), kind.value
 
+    def io_bytes(self):
+        """(host->device, device->host) bytes of K1 / K5 calls on this graph since load."""
+        out = (C.c_uint64 * 2)()
+        check(lib().glmx_graph_io_bytes(self.h, out))
+        return int(out[0]), int(out[1])
+
     def total_degree(self, idx):
         return lib().glmx_graph_degree(self.h, idx)
 

@@ -18,3 +18,14 @@ b, _ = Decoder(cfg, W, emulate_bf16=True).forward(ids)
 err = np.abs(a - b)
 print(f"fp32 vs bf16-emulated: max {err.max():.4f} mean {err.mean():.4f} p99.9 {np.quantile(err, .999):.4f} std(logits) {a.std():.3f}  ({time.time()-t:.1f}s)")
 print("within 2e-2+1e-2|ref|:", bool(np.all(err <= 2e-2 + 1e-2 * np.abs(a))))
+
+# chaos floor: the bf16-emulating oracle against itself with 1e-7 relative weight noise
+rng2 = np.random.default_rng(1)
+def pert(m): return (m * (1 + 1e-7 * rng2.standard_normal(m.shape, dtype=np.float32))).astype(np.float32)
+Wp = dict(W, layers=[{k: (pert(v) if v.ndim == 2 else v) for k, v in l.items()} for l in W["layers"]])
+c, _ = Decoder(cfg, Wp, emulate_bf16=True).forward(ids)
+e = np.abs(b - c)
+print(f"bf16-emulated vs bf16-emulated(1e-7 weight noise): max {e.max():.4f} mean {e.mean():.5f} "
+      f"in 2e-2/1e-2: {np.mean(e <= 2e-2 + 1e-2 * np.abs(b)):.5f}")
+c32, _ = Decoder(cfg, Wp).forward(ids)
+print(f"fp32 vs fp32(1e-7 weight noise): max {np.abs(a - c32).max():.2e}")
