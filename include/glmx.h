@@ -114,6 +114,10 @@ int glmx_kv_counters(const glmx_kv* kv, int64_t out6[6]);
 uint64_t glmx_kv_resident(const glmx_kv* kv, uint64_t* ids, int32_t* tiers, uint64_t* last_used,
                           int32_t* pages, uint64_t cap);
 /* CacheBlock::session of a resident block (cache.hpp:17-23); -1 when not resident */
+/* KvCacheState::block (cache.hpp:80): 1 and the block's CacheBlock fields (cache.hpp:17-23) when
+ * `id` is resident, else 0 (all out-params nullable) */
+int32_t glmx_kv_block(const glmx_kv* kv, uint64_t id, int32_t* tier, uint64_t* last_used,
+                      uint64_t* parent, int32_t* has_parent);
 int64_t glmx_kv_block_session(const glmx_kv* kv, uint64_t id, char* buf, uint64_t cap);
 /* snapshot_json (cache.cpp:178-189); returns the full length */
 int64_t glmx_kv_snapshot_json(const glmx_kv* kv, char* buf, uint64_t cap);

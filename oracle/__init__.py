@@ -34,6 +34,8 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE, "port"], check=True)
     if ref and os.path.isdir(REFERENCE_ROOT):
         subprocess.run(["make", "-s", "-C", HERE, "ref", "-j8"], check=True)
+        # the compiled drop-in proof (reference run_bench over integration/'s KvCacheState)
+        subprocess.run(["make", "-s", "-C", HERE, "dropin", "-j8"], check=True)
 
 
 def pack_tokens(tokens):

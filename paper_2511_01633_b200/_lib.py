@@ -93,6 +93,7 @@ _SIGS = {
     "glmx_kv_force_insert": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_uint64, C.c_char_p]),
     "glmx_kv_counters": (C.c_int, [C.c_void_p, i64p]),
     "glmx_kv_resident": (C.c_uint64, [C.c_void_p, u64p, i32p, u64p, i32p, C.c_uint64]),
+    "glmx_kv_block": (C.c_int32, [C.c_void_p, C.c_uint64, i32p, u64p, u64p, i32p]),
     "glmx_kv_block_session": (C.c_int64, [C.c_void_p, C.c_uint64, C.c_char_p, C.c_uint64]),
     "glmx_kv_snapshot_json": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_uint64]),
     "glmx_kv_chain_ids": (C.c_uint64, [C.c_char_p, u64p, C.c_uint64, C.c_uint32, u64p]),

@@ -213,6 +213,17 @@ uint64_t glmx_kv_resident(const glmx_kv* kv, uint64_t* ids, int32_t* tiers, uint
   return v.size();
 }
 
+int32_t glmx_kv_block(const glmx_kv* kv, uint64_t id, int32_t* tier, uint64_t* last_used,
+                      uint64_t* parent, int32_t* has_parent) {
+  const Block* b = kv->bk->block(id);
+  if (!b) return 0;
+  if (tier) *tier = b->tier;
+  if (last_used) *last_used = b->last_used;
+  if (parent) *parent = b->parent;
+  if (has_parent) *has_parent = b->has_parent ? 1 : 0;
+  return 1;
+}
+
 int64_t glmx_kv_block_session(const glmx_kv* kv, uint64_t id, char* buf, uint64_t cap) {
   const Block* b = kv->bk->block(id);
   if (!b) return -1;
