@@ -43,9 +43,12 @@ def parse():
     p.add_argument("--capacity", type=int, default=16384)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--question-pool", type=int, default=192,
-                   help="draw questions with replacement from this many candidates (reference "
-                        "generate_workload style); 0 = all unique")
+    p.add_argument("--question-pool", type=int, default=0,
+                   help="draw every question with replacement from this many candidates; 0 = the "
+                        "stationary stream of --repeat-frac")
+    p.add_argument("--repeat-frac", type=float, default=0.22,
+                   help="share of questions repeating one of the previous 256 (the reference's "
+                        "generate_workload(7, 1024, 0.5) repeats 22%%: 799 unique of 1024)")
     p.add_argument("--cache-warm", type=int, default=64,
                    help="untimed rotations before the warm-up steps that bring the prefix cache "
                         "to its steady state (the value then does not drift with --steps)")
@@ -87,6 +90,7 @@ def bench_config(args, ws, pipelined=True, pool_n=None):
                         "chunks, Llama-3-8B-shaped random-init bf16, paged KV pool",
             "lanes_per_gpu": args.lanes, "nodes": args.nodes, "k": args.k,
             "question_pool": args.question_pool if pool_n is None else pool_n,
+            "question_repeat_frac": args.repeat_frac if args.question_pool == 0 else None,
             "cache_warm_rotations": args.cache_warm,
             "kv_capacity_blocks": args.capacity, "block_tokens": 16, "policy": "priority",
             "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
@@ -300,8 +304,8 @@ def reference_rotations(args, ws, rank, steps, warm):
     tag = f"{os.getpid()}_{args.nodes}_{args.seed}"
     gpath = synth.powerlaw_graph_jsonl(args.nodes, 8, args.seed, f"/tmp/glmx_c2_graph_{tag}.jsonl")
     n_q, pool_n, _ = workload_shape(args, ws)
-    sessions = synth.graph_cot_questions(args.nodes, n_q * ws, args.seed,
-                                         question_pool=pool_n)[rank::ws]
+    sessions = synth.graph_cot_questions(args.nodes, n_q * ws, args.seed, question_pool=pool_n,
+                                         repeat_frac=args.repeat_frac)[rank::ws]
     tpath = synth.write_jsonl(synth.scripted_replies(sessions), f"/tmp/glmx_c2_trace_{tag}.jsonl")
     run = oracle.RefScriptedRun(oracle.RefGraph(path=gpath), tpath,
                                 [{"id": sid, "text": q} for sid, _, q in sessions], args.lanes,
@@ -441,7 +445,7 @@ def main():
     n_q, pool_n, _ = workload_shape(args, ws)
     nidx = glmx.NodeIndex(g)  # RetrieveNode: device VectorIndex + retrieval LRU (K5)
     wl = GraphCoTWorkload(eng, ret, n_queries=n_q * ws, lanes=args.lanes, seed=args.seed,
-                          question_pool=pool_n, node_index=nidx)
+                          question_pool=pool_n, node_index=nidx, repeat_frac=args.repeat_frac)
     if args.routing == "affinity":
         from paper_2511_01633_b200.sharding import shard_by_affinity
         wl.sessions = shard_by_affinity(wl.sessions, rank, ws, key=lambda s: s.question)

@@ -8,11 +8,12 @@ Orchestrator and ScriptedProvider (oracle/_ref) the same graph, questions and re
 
 * ``powerlaw_graph_jsonl`` writes exactly the JSONL of ``glmx_graph_synth_powerlaw`` +
   ``glmx_graph_save_jsonl`` (host/graph.cpp synth_powerlaw / serialize_jsonl; pinned by
-  tests/test_retrieve_node.py): splitmix64 draws, out-edge targets floor(n * u^3) (hub degree
+  tests/test_synth.py): splitmix64 draws, out-edge targets floor(n * u^3) (hub degree
   ~ n^(2/3)), ids zero-padded so byte order == index order.
 * ``graph_cot_questions`` is the question stream of GraphCoTWorkload: "Which item is linked from
-  all of: a; b?" over 2-4 source nodes drawn with a power-law skew, questions drawn with
-  replacement from a pool (as generate_workload picks clusters, workload.cpp:216-225).
+  all of: a; b?" over 2-4 source nodes drawn with a power-law skew; questions recur either at the
+  reference generator's measured rate (a stationary stream) or drawn from a fixed pool (as
+  generate_workload picks clusters with replacement, workload.cpp:216-225).
 * ``scripted_replies`` is the ScriptedProvider trace (scripted.hpp:12-17) of those sessions in the
   Rule agent's formats (rule.cpp:156-236): classify "no" -> per source node "Missing: vertex
   chunks for: <id>" + an action printing NodeInfo(RetrieveNode("<id>")) -> "Finish: <first id>".
@@ -30,7 +31,6 @@ _NOUN = ("lattice", "widget", "gasket", "spindle", "crucible", "bobbin", "ratche
          "flange", "tumbler", "sprocket", "mandrel", "ferrule", "plinth", "luggage", "brazier")
 _BRAND = ("acme", "orion", "zephyr", "halcyon", "vertex", "quanta")
 _CAT = ("tools", "kitchen", "garden", "office", "sport", "audio")
-_M64 = (1 << 64) - 1
 
 
 def _splitmix(seed, k0, count):
@@ -84,20 +84,31 @@ def powerlaw_graph_jsonl(n_nodes, edges_per_node, seed, path):
 
 
 def graph_cot_questions(n_nodes, n_queries, seed=0, min_hops=2, max_hops=4, skew=2.5,
-                        question_pool=0):
-    """[(session id, [source node indices], question text)] of GraphCoTWorkload."""
+                        question_pool=0, repeat_frac=0.0, repeat_window=256):
+    """[(session id, [source node indices], question text)] of GraphCoTWorkload.
+
+    question_pool > 0: every question is drawn with replacement from that many candidates.
+    repeat_frac > 0 (no pool): a stationary stream -- each question repeats one of the previous
+    `repeat_window` questions with probability repeat_frac, else it is fresh.  The reference's
+    own generator repeats 22% of its questions (generate_workload(7, 1024, 0.5) on synth_graph(7,
+    5000): 799 unique of 1024).  Either way the draws are sequential, so the first k questions do
+    not depend on n_queries."""
     rnd = random.Random(seed)
     pool = []
     for _ in range(question_pool):
         m = rnd.randint(min_hops, max_hops)
         pool.append([min(n_nodes - 1, int(n_nodes * rnd.random() ** skew)) for _ in range(m)])
-    out = []
+    out, hist = [], []
     for q in range(n_queries):
         if pool:
             src = list(pool[rnd.randrange(len(pool))])
+        elif repeat_frac > 0 and hist and rnd.random() < repeat_frac:
+            recent = hist[-repeat_window:]
+            src = list(recent[rnd.randrange(len(recent))])
         else:
             m = rnd.randint(min_hops, max_hops)
             src = [min(n_nodes - 1, int(n_nodes * rnd.random() ** skew)) for _ in range(m)]
+        hist.append(src)
         ids = [node_id(v) for v in src]
         out.append((f"q{q:05d}", src, "Which item is linked from all of: " + "; ".join(ids) + "?"))
     return out

@@ -77,7 +77,7 @@ class RotationResult:
 class GraphCoTWorkload:
     def __init__(self, engine, retriever, n_queries, lanes, seed=0, min_hops=2, max_hops=4,
                  skew=2.5, templates=None, node_ids=None, overlap_retrieval=True,
-                 question_pool=0, node_index=None):
+                 question_pool=0, node_index=None, repeat_frac=0.0, repeat_window=256):
         self.engine = engine
         # node_index (NodeIndex): the action's RetrieveNode("<id>") is resolved by the K5 nearest
         # scan + retrieval LRU (retriever.cpp:49-66) instead of taking the scripted source node
@@ -94,7 +94,8 @@ class GraphCoTWorkload:
         # across sessions (and, sharded i mod N, across GPUs)
         self.sessions = []
         for sid, src, _ in synth.graph_cot_questions(g.node_count(), n_queries, seed, min_hops,
-                                                     max_hops, skew, question_pool):
+                                                     max_hops, skew, question_pool, repeat_frac,
+                                                     repeat_window):
             ids = [g.node_id(v) for v in src]
             question = "Which item is linked from all of: " + "; ".join(ids) + "?"
             self.sessions.append(Session(sid, src, question))
