@@ -62,7 +62,7 @@ struct DecodeRope {
   const __nv_bfloat16* qkv;  // [rows][(H + 2 Hkv) * hd]
   const int32_t* pos;        // [rows]
   const int64_t* slot;       // [rows] pool slot (page * B + offset) of the new key
-  const float* inv_freq;     // [hd / 2]
+  const float2* rope_cs;     // [rows][hd / 2] (cos, sin) of the forward (rope_table)
 };
 void paged_attention_decode_rope(const AttnParams& p, const DecodeRope& r, int n_req, int n_split,
                                  float* part_o, float2* part_ml, cudaStream_t s);

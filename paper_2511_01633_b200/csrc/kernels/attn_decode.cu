@@ -105,10 +105,19 @@ decode_attn_kernel(AttnParams p, DecodeRope rp, int n_split, float* __restrict__
     // rounded to bf16 like the separate K2 kernel's q / pool writes
     const int heads = p.H + 2 * p.Hkv;
     const __nv_bfloat16* row = rp.qkv + static_cast<int64_t>(qrow) * heads * kHd + sl * 8;
-    const float ps = static_cast<float>(rp.pos[qrow]);
     float cs[8], sn[8];
+    {
+      const float4* tab = reinterpret_cast<const float4*>(rp.rope_cs + static_cast<int64_t>(qrow) * (kHd / 2) +
+                                                          (sl & 7) * 8);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) sincosf(ps * rp.inv_freq[(sl & 7) * 8 + j], &sn[j], &cs[j]);
+      for (int j = 0; j < 4; ++j) {
+        const float4 v = __ldg(tab + j);
+        cs[2 * j] = v.x;
+        sn[2 * j] = v.y;
+        cs[2 * j + 1] = v.z;
+        sn[2 * j + 1] = v.w;
+      }
+    }
     auto rope8 = [&](const uint4& u, float (&out)[8]) {
       float f[8], o[8];
       bf8(u, f);

@@ -203,17 +203,18 @@ rope_kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __re
 
 
 // K2, warp-per-(token, head group) form (head_dim 128: 8 lanes per head, 4 heads per pass, 16
-// heads per warp = blockIdx.y's group): a lane's cos/sin of its 8 rotation pairs are computed once
-// and reused across the warp's heads; the 4 passes issue all 8 loads of a lane before any store.
+// heads per warp = blockIdx.y's group): a lane's cos/sin of its 8 rotation pairs come from the
+// forward's RoPE table (rope_table: one sincosf per (token, pair) per forward instead of per layer
+// and head group; the large-argument sincosf path was a third of K2's issue slots) and are reused
+// across the warp's heads; the 4 passes issue all 8 loads of a lane before any store.
 // Small prefill batches (a few hundred tokens) still spread over the SMs with one round trip per
 // warp; mid-size batches (~3-5k tokens) fill the machine in one wave instead of the 1.2 waves of
 // 2-token CTAs.
 template <int kPassU>
 __global__ void __launch_bounds__(256)
-rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
-                           const int64_t* __restrict__ slot, int T, int H, int Hkv,
-                           const float* __restrict__ inv_freq, PoolGeom pool, uint32_t layer,
-                           __nv_bfloat16* __restrict__ q_out) {
+rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const float2* __restrict__ rope_cs,
+                           const int64_t* __restrict__ slot, int T, int H, int Hkv, PoolGeom pool,
+                           uint32_t layer, __nv_bfloat16* __restrict__ q_out) {
   constexpr int kHd = 128, kHalf = 64, kChunks = 8, kHeadsPerPass = 32 / kChunks;
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -239,10 +240,16 @@ rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t*
       }
     }
     float cs[8], sn[8];
-    if (p0 * kHeadsPerPass < H + Hkv) {
-      const float p = static_cast<float>(pos[t]);
+    if (p0 * kHeadsPerPass < H + Hkv) {  // the token's (cos, sin) row of the forward's table
+      const float4* tab = reinterpret_cast<const float4*>(rope_cs + static_cast<int64_t>(t) * kHalf + c * 8);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sincosf(p * inv_freq[c * 8 + j], &sn[j], &cs[j]);
+      for (int j = 0; j < 4; ++j) {
+        const float4 v = __ldg(tab + j);
+        cs[2 * j] = v.x;
+        sn[2 * j] = v.y;
+        cs[2 * j + 1] = v.z;
+        sn[2 * j + 1] = v.w;
+      }
     }
 #pragma unroll
     for (int i = 0; i < kPassU; ++i) {
@@ -457,24 +464,42 @@ void rmsnorm(const float* x, const int32_t* rows, int T, int d, const __nv_bfloa
   GLMX_CHECK_LAUNCH();
 }
 
+__global__ void rope_table_kernel(const int32_t* __restrict__ pos, int T, int half,
+                                  const float* __restrict__ inv_freq, float2* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(T) * half) return;
+  float sn, cs;
+  sincosf(static_cast<float>(pos[i / half]) * inv_freq[i % half], &sn, &cs);
+  out[i] = make_float2(cs, sn);
+}
+
+void rope_table(const int32_t* pos, int T, int half, const float* inv_freq, float2* out,
+                cudaStream_t s) {
+  if (T <= 0) return;
+  const int64_t n = static_cast<int64_t>(T) * half;
+  rope_table_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(pos, T, half, inv_freq, out);
+  GLMX_CHECK_LAUNCH();
+}
+
 void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t* slot, int T,
-                    int H, int Hkv, int hd, const float* inv_freq, const PoolGeom& pool,
-                    uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s) {
+                    int H, int Hkv, int hd, const float* inv_freq, const float2* rope_cs,
+                    const PoolGeom& pool, uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s) {
   if (T <= 0) return;
   if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
   if (hd == 128) {
     // 16 heads per warp; decode-sized batches (< 1024 tokens) 4 heads per warp and 2 warps per
     // CTA, so a 64-token step still spreads over ~380 CTAs with one load round trip each
     const int passes = static_cast<int>(ceil_div(H + 2 * Hkv, 4));
+    if (!rope_cs) throw Error(GLMX_ERR_ARG, "head_dim 128 append needs the forward's RoPE table");
     if (T < 1024) {
       rope_kv_append_warp_kernel<1><<<dim3(static_cast<int>(ceil_div(T, 2)), passes), 64, 0, s>>>(
-          qkv, pos, slot, T, H, Hkv, inv_freq, pool, layer, q_out);
+          qkv, rope_cs, slot, T, H, Hkv, pool, layer, q_out);
     } else {
       constexpr int kPassU = 4;
       rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, 8)),
                                                 static_cast<int>(ceil_div(passes, kPassU))),
-                                           256, 0, s>>>(qkv, pos, slot, T, H, Hkv, inv_freq, pool,
-                                                        layer, q_out);
+                                           256, 0, s>>>(qkv, rope_cs, slot, T, H, Hkv, pool, layer,
+                                                        q_out);
     }
     GLMX_CHECK_LAUNCH();
     return;

@@ -31,11 +31,16 @@ void embed_gather(const int32_t* tokens, int T, const __nv_bfloat16* embed, int 
 // out[t] = bf16(x[t] * rsqrt(mean(x^2) + eps) * w)   (x fp32 residual stream)
 void rmsnorm(const float* x, const int32_t* rows, int T, int d, const __nv_bfloat16* w,
              float eps, __nv_bfloat16* out, cudaStream_t s);
+// RoPE table of a forward: out[t][i] = (cos, sin)(float(pos[t]) * inv_freq[i]), i < half; shared
+// by every layer's K2 append and the fused decode attention.
+void rope_table(const int32_t* pos, int T, int half, const float* inv_freq, float2* out,
+                cudaStream_t s);
 // K2 append fused with RoPE: qkv [T][(H+2Hkv)*hd] -> q_out [T][H][hd] (roped), K (roped) and V
-// into the pool pages given by slot[t] = page * B + offset.
+// into the pool pages given by slot[t] = page * B + offset.  head_dim 128 reads the angles from
+// rope_cs (rope_table); other head dims compute them from pos / inv_freq.
 void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t* slot, int T,
-                    int H, int Hkv, int hd, const float* inv_freq, const PoolGeom& pool,
-                    uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s);
+                    int H, int Hkv, int hd, const float* inv_freq, const float2* rope_cs,
+                    const PoolGeom& pool, uint32_t layer, __nv_bfloat16* q_out, cudaStream_t s);
 void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStream_t s);
 // dst[i] = src[idx[i]] (decode: first tokens into decode row order)
 void gather_i32(const int32_t* src, const int32_t* idx, int n, int32_t* dst, cudaStream_t s);

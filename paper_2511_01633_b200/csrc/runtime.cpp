@@ -12,6 +12,15 @@
 using namespace glmx;
 
 namespace {
+
+// Non-blocking stream at the device's greatest (high) or least (low) priority.
+cudaStream_t make_stream(bool high) {
+  int least = 0, greatest = 0;
+  GLMX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  cudaStream_t s = nullptr;
+  GLMX_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, high ? greatest : least));
+  return s;
+}
 constexpr size_t kBlasWsBytes = 64ull << 20;  // cuBLAS / cuBLASLt workspace per model
 }
 
@@ -111,7 +120,9 @@ void glmx_graph::upload() {
   dev.entry_off = static_cast<const uint32_t*>(put(host.entry_off.data(), host.entry_off.size() * 4));
   for (size_t i = 0; i + 1 < host.entry_off.size(); ++i)
     max_entry = std::max(max_entry, host.entry_off[i + 1] - host.entry_off[i]);
-  GLMX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  // the graph stream (K1 chunks, K5 RetrieveNode) runs beside the prefill at the lowest priority:
+  // the forward's CTAs are dispatched first whenever an SM frees up
+  stream = make_stream(false);
   {
     uint32_t* st = static_cast<uint32_t*>(put(nullptr, host.n() * 4));
     entry_stats(dev.entry_bytes, dev.entry_off, static_cast<uint32_t>(host.n()), st, stream);
@@ -543,7 +554,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->kv = kv;
   e->cfg = *cfg;
   DeviceGuard g(m->device);
-  GLMX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  e->stream = make_stream(true);  // the forward outranks the graph stream
   e->blas_ws.reserve(kBlasWsBytes);
   GLMX_CUDA(cudaEventCreateWithFlags(&e->h2d_done, cudaEventDisableTiming));
   GLMX_CUDA(cudaEventCreateWithFlags(&e->fwd_done, cudaEventDisableTiming));
@@ -561,6 +572,7 @@ glmx_engine* engine_create_impl(glmx_model* m, glmx_kv* kv, const glmx_engine_co
   e->h.reserve(T * d * 2);
   e->qkv.reserve(T * (H + 2 * Hkv) * hd * 2);
   e->q.reserve(T * H * hd * 2);
+  e->rope_cs.reserve(T * (hd / 2) * sizeof(float2));
   make_q_tensor_map(e->q.p, T, static_cast<int>(H), static_cast<int>(Hkv), e->q_map);
   e->attn.reserve(T * H * hd * 2);
   e->gu.reserve(T * 2 * ff * 2);
@@ -732,6 +744,7 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
   {
     Prof p(e, kCatOther);
     embed_gather(d_tokens, T, m->embed, d, e->x.as<float>(), s);
+    rope_table(pos, T, static_cast<int>(hd / 2), m->inv_freq, e->rope_cs.as<float2>(), s);
   }
   for (uint32_t l = 0; l < c.n_layers; ++l) {
     const LayerW& w = m->layers[l];
@@ -748,13 +761,13 @@ void forward(glmx_engine* e, int T, int R, int n_work, int n_last, const int32_t
     if (!fuse) {
       Prof p(e, kCatAppend);
       rope_kv_append(e->qkv.as<__nv_bfloat16>(), pos, slot, T, H, Hkv, hd, m->inv_freq,
-                     e->kv->geom, l, e->q.as<__nv_bfloat16>(), s);
+                     e->rope_cs.as<float2>(), e->kv->geom, l, e->q.as<__nv_bfloat16>(), s);
     }
     {
       Prof p(e, kCatAttn);
       ap.layer = l;
       if (fuse)
-        paged_attention_decode_rope(ap, DecodeRope{e->qkv.as<__nv_bfloat16>(), pos, slot, m->inv_freq},
+        paged_attention_decode_rope(ap, DecodeRope{e->qkv.as<__nv_bfloat16>(), pos, slot, e->rope_cs.as<float2>()},
                                     R, e->dec_split, e->part_o.as<float>(), e->part_ml.as<float2>(), s);
       else
         paged_attention_tc(ap, e->kv_map, e->kv_rows, e->q_map, sc, s);
@@ -1430,6 +1443,11 @@ int rope_append_run_impl(const void* qkv, const int32_t* pos, const int64_t* slo
   DBuf d_inv;
   d_inv.reserve(inv.size() * 4);
   GLMX_CUDA(cudaMemcpyAsync(d_inv.p, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice, s));
+  // the engine builds this table once per forward (rope_table) and shares it across the layers:
+  // outside the timed launches here too
+  DBuf d_cs;
+  d_cs.reserve(T * (hd / 2) * sizeof(float2));
+  rope_table(pos, static_cast<int>(T), hd / 2, d_inv.as<float>(), d_cs.as<float2>(), s);
   PoolGeom geom{static_cast<__nv_bfloat16*>(pool_base), n_layers, static_cast<uint32_t>(Hkv),
                 block_tokens, static_cast<uint32_t>(hd)};
   cudaEvent_t e0, e1;
@@ -1440,7 +1458,8 @@ int rope_append_run_impl(const void* qkv, const int32_t* pos, const int64_t* slo
     GLMX_CUDA(cudaEventRecord(e0, s));
     for (int i = 0; i < reps; ++i)
       rope_kv_append(static_cast<const __nv_bfloat16*>(qkv), pos, slot, static_cast<int>(T), H, Hkv,
-                     hd, d_inv.as<float>(), geom, layer, static_cast<__nv_bfloat16*>(q_out), s);
+                     hd, d_inv.as<float>(), d_cs.as<float2>(), geom, layer,
+                     static_cast<__nv_bfloat16*>(q_out), s);
     GLMX_CUDA(cudaEventRecord(e1, s));
     GLMX_CUDA(cudaEventSynchronize(e1));
     GLMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));

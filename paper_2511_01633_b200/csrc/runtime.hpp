@@ -115,6 +115,7 @@ struct glmx_engine {
 
   // activations
   DBuf x, h, qkv, q, attn, gu, act, hl, logits, next_tok, amax_keys, dec_in;
+  DBuf rope_cs;  // [T][hd / 2] (cos, sin) of the forward's positions (one table for all layers)
   // batch metadata (device) + pinned host staging (single H2D)
   DBuf meta;
   void* h_meta = nullptr;  // the staging slot in use (one of h_ring)

@@ -54,30 +54,36 @@ for P in args.prefix:
             while len(nb.split()) < P - 80:
                 nb += ret.chunk_build([rnd.randrange(g.node_count())]).texts[0] + "\n"
             notebooks.append(nb)
-            last.append(ret.chunk_build([rnd.randrange(g.node_count())]).texts[0] + "\n")
+            # one fresh last chunk per replay: every measured prefill reuses the cached notebook
+            # and computes a new suffix (chunk + question)
+            last.append([ret.chunk_build([rnd.randrange(g.node_count())]).texts[0] + "\n"
+                         for _ in range(args.replays + 1)])
         q = "Which item is linked from all of: v0000001; v0000002?"
         from paper_2511_01633_b200.workload import Call, GraphCoTWorkload, Session
         sess = [Session(f"c5_{P}_{k}_{b}", [0], q) for b in range(B)]
         warm_calls = [Call(sess[b], "reasoning", t.render_reasoning(q, notebooks[b]), "") for b in range(B)]
-        meas_calls = [Call(sess[b], "reasoning", t.render_reasoning(q, notebooks[b] + last[b]), "") for b in range(B)]
+        meas_calls = [[Call(sess[b], "reasoning", t.render_reasoning(q, notebooks[b] + last[b][r]), "")
+                       for b in range(B)] for r in range(args.replays + 1)]
         wl = GraphCoTWorkload.__new__(GraphCoTWorkload)
         wl.engine = eng
         wl.prefill(warm_calls[:1])
         for b in range(1, B):
             wl.prefill(warm_calls[b:b + 1])
-        reps, _ = wl.prefill(meas_calls)
+        wl.prefill(meas_calls[0])  # warm-up of the measured shape
         eng.set_profiling(2)
-        attn = 0.0
-        fwd = 0.0
-        for _ in range(args.replays):
-            eng.replay_forward()
+        attn = fwd = flops = byts = 0.0
+        for r in range(1, args.replays + 1):
+            reps, _ = wl.prefill(meas_calls[r])
             tm = eng.last_timings()
+            wk = eng.last_work()
             attn += tm["attention"]
             fwd += tm["forward"]
+            flops += wk["attn_flops"]
+            byts += wk["attn_bytes"]
         eng.set_profiling(0)
         attn /= args.replays
         fwd /= args.replays
-        wk = eng.last_work()
+        wk = {"attn_flops": flops / args.replays, "attn_bytes": byts / args.replays}
         tfl = wk["attn_flops"] / (attn * 1e-3) / 1e12
         gbs = wk["attn_bytes"] / (attn * 1e-3) / 1e9
         s = sum(r.computed_tokens + r.tail_tokens for r in reps) / B
@@ -93,7 +99,7 @@ for P in args.prefix:
                "prefill_tokens_per_s_32l": sum(r.cached_tokens + r.computed_tokens + r.tail_tokens
                                                for r in reps) / (fwd * 1e-3 * 32 / cfg.n_layers),
                "attn_share": attn / fwd,
-               "impl": os.environ.get("GLMX_ATTN", "tc")}
+               "impl": "tc"}
         rows.append(row)
         print(json.dumps(row), flush=True)
     del eng, kv
