@@ -71,6 +71,9 @@ def parse():
                    help="before timing, pick cuBLAS algorithms for the projection GEMMs per M "
                         "bucket up to this many batch tokens (glmx_model_tune_gemms); 0 keeps "
                         "cublasGemmEx's default choice")
+    p.add_argument("--no-reuse", action="store_true",
+                   help="A/B leg: KV reuse off (cache hits recomputed into scratch pages, same "
+                        "bookkeeping and prompts); the metric stays prompt tokens/s")
     return p.parse_args()
 
 
@@ -95,7 +98,8 @@ def bench_config(args, ws, pipelined=True, pool_n=None):
             "kv_capacity_blocks": args.capacity, "block_tokens": 16, "policy": "priority",
             "l2": "inputs > L2 (16 GB weights + KV pool read every step)",
             "parallelism": f"query-sharded x{ws}", "routing": args.routing,
-            "host_pipelining": pipelined}
+            "host_pipelining": pipelined,
+            **({"kv_reuse": False} if getattr(args, "no_reuse", False) else {})}
 
 
 def self_launch(args):
@@ -458,6 +462,8 @@ def main():
                            headroom_pages=4096)
     eng = glmx.Engine(model, kv, max_requests=args.lanes, max_batch_tokens=args.lanes * 1024,
                       max_decode=8, max_context=8192)
+    if args.no_reuse:
+        eng.set_reuse(False)
     # enough queries (per rank) that every lane stays busy through the timed rotations
     n_q, pool_n, _ = workload_shape(args, ws)
     nidx = glmx.NodeIndex(g)  # RetrieveNode: device VectorIndex + retrieval LRU (K5)

@@ -351,6 +351,10 @@ int glmx_engine_last_timings(const glmx_engine* e, float out7[7]);
  * Q in + O out), [2] K2 bytes (qkv read + q write + K/V page writes), [3] linear FLOPs, [4] computed tokens, [5] context tokens */
 int glmx_engine_last_work(const glmx_engine* e, double out6[6]);
 void glmx_engine_set_profiling(glmx_engine* e, int32_t on);
+/* KV reuse switch for the reuse on/off A/B: 0 -> every prompt token is computed,
+ * cache hits included (their KV is recomputed into scratch pages; the cached pages are not
+ * touched); bookkeeping and reports are unchanged.  Default 1. */
+void glmx_engine_set_reuse(glmx_engine* e, int32_t on);
 /* Bytes the engine moved between host and device since it was created: out2[0] host->device
  * (batch and decode-step metadata: token ids, positions, slots, block tables, the attention
  * schedule, peer-copy lists — the used part of each section only), out2[1] device->host

@@ -156,6 +156,7 @@ _SIGS = {
     "glmx_engine_last_timings": (C.c_int, [C.c_void_p, f32p]),
     "glmx_engine_last_work": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "glmx_engine_set_profiling": (None, [C.c_void_p, C.c_int32]),
+    "glmx_engine_set_reuse": (None, [C.c_void_p, C.c_int32]),
     "glmx_pool_copy": (C.c_int, [C.c_void_p, C.c_void_p, i32p, i32p, C.c_uint64, C.c_void_p]),
     "glmx_pool_last_copy_ms": (C.c_float, [C.c_void_p]),
     "glmx_rope_kv_append_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,

@@ -603,6 +603,7 @@ int glmx_engine_last_work(const glmx_engine* e, double out6[6]) {  // of the las
   return GLMX_OK;
 }
 void glmx_engine_set_profiling(glmx_engine* e, int32_t level) { e->profiling = level; }
+void glmx_engine_set_reuse(glmx_engine* e, int32_t on) { e->reuse = on ? 1 : 0; }
 int glmx_engine_io_bytes(const glmx_engine* e, uint64_t out2[2]) {
   out2[0] = e->h2d_bytes;
   out2[1] = e->d2h_bytes;

@@ -913,7 +913,17 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
       // Cross-GPU prefix hit: the run of freshly inserted blocks that directly extends the local
       // hit prefix and is resident on a peer is copied instead of computed (bookkeeping already
       // counted them as misses, like independent per-GPU caches).
-      if (reuse_blocks == pr.hit_blocks && !kv->peer_dir.empty()) {
+      uint64_t first_written = std::min(pr.hit_blocks, reuse_blocks);
+      if (!e->reuse) {
+        // reuse off (A/B): the hit blocks' KV is recomputed into scratch pages; their cached
+        // pages stay as they are
+        for (uint64_t b = 0; b < pr.hit_blocks; ++b) {
+          st.pages[b] = bk.pool().alloc();
+          st.scratch.push_back(st.pages[b]);
+        }
+        reuse_blocks = 0;
+        first_written = pr.hit_blocks;
+      } else if (reuse_blocks == pr.hit_blocks && !kv->peer_dir.empty()) {
         for (uint64_t b = pr.hit_blocks; b < full && pr.fresh[b]; ++b) {
           auto it = kv->peer_dir.find(pr.ids[b]);
           if (it == kv->peer_dir.end()) break;
@@ -928,7 +938,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
       // every block from reuse_blocks on is written by this batch (peer copy or K2 append):
       // no longer stale for the requests staged after this one (the append of a layer precedes
       // its attention); re-marked if the batch fails before its forward is enqueued
-      for (uint64_t b = std::min(pr.hit_blocks, reuse_blocks); b < full; ++b) {
+      for (uint64_t b = first_written; b < full; ++b) {
         if (st.pages[b] < 0) {  // a force_insert'ed block without a page
           if (bk.block(pr.ids[b])) {
             st.pages[b] = bk.ensure_page(pr.ids[b]);

@@ -188,6 +188,7 @@ struct glmx_engine {
   int dec_split = 0;      // > 0: the staged batch is all one-token rows -> K3d with this many splits
   DBuf part_o, part_ml;
 
+  int reuse = 1;          // 0: hits recomputed into scratch pages (reuse on/off A/B)
   // profiling
   int profiling = 0;
   struct Span {

@@ -132,6 +132,10 @@ class Engine:
     def set_profiling(self, on=True):
         lib().glmx_engine_set_profiling(self.h, int(on))
 
+    def set_reuse(self, on=True):
+        """KV reuse on/off (A/B): off recomputes cache hits into scratch pages."""
+        lib().glmx_engine_set_reuse(self.h, int(on))
+
     @staticmethod
     def pack_requests(requests):
         n = len(requests)

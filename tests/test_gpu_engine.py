@@ -393,3 +393,31 @@ def test_c3_shaped_run_bookkeeping_matches_reference():
     row = __import__("json").loads(out.stdout.strip().splitlines()[-1])
     assert row["bookkeeping_identical_to_reference"]
     assert sum(row["counters"]["evictions_by_tier"]) > 0  # the pool was under pressure
+
+
+def test_reuse_off_recomputes_hits_with_same_bookkeeping():
+    """Reuse on/off A/B switch (bench.py --no-reuse): with reuse off the cache hits are recomputed
+    into scratch pages -- reports and cache state are the reference's, logits stay within the
+    north-star tolerance of the fp32 oracle, and the cached pages are untouched (a later reuse-on
+    prefill of the same prompt gives the same logits as before)."""
+    model, kv, eng = make(glmx.TINY)
+    dec = Decoder(glmx.TINY, model.export_all())
+    p = words(90)
+    warm = [glmx.Request(p, [(0, 30, 0), (30, 90, 3)], "a")]
+    eng.prefill(warm)
+    reqs = [glmx.Request(p[:80] + words(7, "x"), [(0, 30, 0), (30, 87, 3)], "b"),
+            glmx.Request(p[:64], [(0, 64, 2)], "c")]
+    _, _, on_logits = eng.prefill(reqs, want_logits=True)
+    snap = kv.snapshot()
+    eng.set_reuse(False)
+    reps, first, off_logits = eng.prefill(reqs, want_logits=True)
+    eng.set_reuse(True)
+    assert [(r.cached_tokens, r.computed_tokens, r.tail_tokens) for r in reps] == [
+        (80, 0, 7), (64, 0, 0)]
+    assert kv.snapshot()["resident_blocks"] == snap["resident_blocks"]
+    for i, r in enumerate(reqs):
+        ref = dec.forward(token_ids(r.tokens, glmx.TINY.vocab))[0]
+        check_logits(off_logits[i], ref)
+        check_logits(on_logits[i], ref)
+    _, _, again = eng.prefill(reqs, want_logits=True)
+    np.testing.assert_array_equal(again, on_logits)
