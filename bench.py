@@ -382,7 +382,7 @@ def standalone_kernels(glmx, g, ret, peaks, tc_peak_burst):
     by = 8 * len(nodes) + 8 * deg + 2 * tb + 20 * tt
     out["K1"] = {"workload": "65536 chunks (k=16) of the bench graph", "ms": ms,
                  "achieved": by / ms / 1e6, "unit": "GB/s", "frac": by / ms / 1e6 / peaks["hbm_gbs"],
-                 "note": "issue-bound byte work (render, whitespace mask, fnv1a): ncu in profiles/"}
+                 "note": "latency/issue-bound byte work (text render + table-driven tokens): ncu in profiles/r2_ncu_k1_v4.txt"}
     H, Hkv, hd, B, P, s, nb = 32, 8, 128, 16, 8192, 128, 8
     ctx = P + s
     per = (ctx + B - 1) // B
@@ -738,7 +738,7 @@ def main():
         "kernels": kernels,
         # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
         # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
-        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 3 * k1_rotations + k5_launches),
+        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations + k5_launches),
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:

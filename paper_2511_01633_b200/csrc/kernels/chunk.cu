@@ -1,22 +1,24 @@
 // K1 — batched vertex-chunk assembly (Retriever::node_info + render_chunk, retriever.cpp:9-30,
-// 74-121; tokenize, tokenizer.hpp:14-25).  One WARP per chunk end to end:
+// 74-121; tokenize, tokenizer.hpp:14-25).
 //
-//   select  : CSR row gather of the de-duplicated neighbour set into registers (<= 4 keys per
-//             lane, rows up to 128), then a warp-level top-k by repeated selection: the 64-bit key
-//             w<<32 | ~idx (weight desc, node index asc) is reduced with two REDUX max steps
-//             (weight word, then index word among the lanes holding the top weight) per pick.
-//             Rows longer than 128 (hubs) or k > 64 are queued for the CTA path: bitonic sort in
-//             shared memory over a 1024-key window that the row streams through.
-//             The chunk's byte length is a warp sum of the selected entries' lengths.
-//   scan    : exclusive sums of chunk lengths (cub) -> byte offsets.
-//   render  : the warp scatters the pre-rendered per-node entries "<id> {k:v,...}" between the
-//             literal separators (warp exclusive scan of entry lengths for the piece offsets), then
-//             counts the chunk's whitespace tokens with ballots over its own bytes.
-//   scan    : exclusive sums of token counts -> token offsets.
-//   emit    : per 32-byte window a ballot marks token starts; each start lane walks to its token
-//             end and hashes the bytes (fnv1a -> id); spans are written at the token offset.
-//             Tokens fuse across entry boundaries exactly as in the text ("[neighbours:(n3",
-//             "type:item}),(u1").
+// Ingest-time tables (the graph is immutable):
+//   ranked adjacency : per (weight mode, directed) variant, every CSR row sorted by (weight desc,
+//                      node index asc) -- node_info's stable_sort order (retriever.cpp:97-113) --
+//                      plus exclusive prefix sums along the rows of the piece bytes (entry + 3),
+//                      piece tokens and irregular entries: top-k of a row is its first k entries,
+//                      and a chunk's byte length / token count are two differences of prefixes
+//   entry tokens     : per regular entry (first and last byte non-space, >= 2 tokens) the spans
+//                      and fnv1a hashes of its interior tokens, its first-token length and its
+//                      last token's offset + fnv1a state
+// Per batch (chunk_build): one thread per chunk computes (k', byte length, token count, regular)
+// from the prefixes -> two exclusive scans -> one WARP per chunk renders and tokenises:
+//   render  : lane s copies piece s ("[Node:" E_v / "(" E_j ")" with "," separators) into a
+//             per-warp shared-memory buffer at the 16-byte phase of its global destination with
+//             4-byte funnel-shifted stores; the buffer goes out as 16-byte stores.
+//   tokenize: regular chunks take the table-driven tokenizer (emit_fast: only the k + 3 junction
+//             tokens are hashed; interior tokens are copied from the tables), others the byte
+//             level one (whitespace ballots + per-token fnv1a).  Tokens fuse across entry
+//             boundaries exactly as in the text ("[neighbours:(n3", "type:item}),(u1").
 // All of it is integer/byte work: HBM/latency bound, no tensor cores.
 #include <cub/cub.cuh>
 
@@ -26,9 +28,6 @@
 namespace glmx {
 
 namespace {
-
-constexpr int kSelThreads = 256;
-constexpr int kWindow = 1024;
 
 // Whitespace tokens a neighbour piece [","] "(" E ")" adds to the chunk, from the entry's stats
 // (kernels entry_stats_kernel): the piece is T(E) + 2 tokens, minus one where "(" fuses with E's
@@ -42,363 +41,183 @@ __device__ __forceinline__ uint32_t piece_tokens(uint32_t st) {
   return 1u + T - L - R;
 }
 
-__device__ __forceinline__ void bitonic_sort_desc(uint64_t* s, int n) {
-  // n is a power of two <= kWindow; all threads of the CTA participate.
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
-        int lo = 2 * i - (i & (stride - 1));
-        int hi = lo + stride;
-        bool desc = ((lo & size) == 0);
-        uint64_t a = s[lo], b = s[hi];
-        if ((a < b) == desc) {
-          s[lo] = b;
-          s[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
-  }
+
+// regular entry: non-empty, first and last byte non-space, >= 2 tokens (head != tail)
+__device__ __forceinline__ bool entry_regular(uint32_t st) {
+  return (st >> 29) == 7u && (st & 0x1FFFFFFFu) >= 2;
 }
 
-__global__ void __launch_bounds__(kSelThreads)
-chunk_select_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ node_idx, int n_req,
-                    const int32_t* __restrict__ big_list, const int32_t* __restrict__ big_count,
-                    int32_t* __restrict__ sel, int32_t* __restrict__ sel_count,
-                    uint64_t* __restrict__ byte_len, uint32_t* __restrict__ tok_count) {
-  __shared__ uint64_t keys[kWindow];
-  const int n_big = *big_count;
-  for (int bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
-  __syncthreads();  // keys / acc reuse across iterations
-  const int r = big_list[bi];
-  const int32_t v = node_idx[r];
-  const uint32_t* off = p.directed ? g.dir_off : g.und_off;
-  const int32_t* idx = p.directed ? g.dir_idx : g.und_idx;
-  const int32_t* w = p.weight_mode ? g.w_by_type : g.w_total;
-  const uint32_t beg = off[v], end = off[v + 1];
-  const int deg = static_cast<int>(end - beg);
-  const int k = min(p.k, deg);
-
-  int have = 0;  // sorted survivors at keys[0, have)
-  uint32_t next = beg;
-  if (k > 0) {
-    while (next < end) {
-      const int room = kWindow - have;
-      const int take = min(static_cast<int>(end - next), room);
-      int total = have + take;
-      int pw = 32;
-      while (pw < total) pw <<= 1;
-      for (int i = threadIdx.x; i < pw - have; i += blockDim.x) {
-        uint64_t key = 0;  // below every real key: real neighbours have weight >= 1
-        if (i < take) {
-          int32_t u = idx[next + i];
-          key = (static_cast<uint64_t>(static_cast<uint32_t>(w[u])) << 32) |
-                (0xFFFFFFFFu - static_cast<uint32_t>(u));
-        }
-        keys[have + i] = key;
-      }
-      __syncthreads();
-      bitonic_sort_desc(keys, pw);
-      next += take;
-      have = k;
-    }
-  }
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    int32_t u = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(keys[j] & 0xFFFFFFFFu));
-    sel[static_cast<int64_t>(r) * p.k_stride + j] = u;
-  }
-  // byte length: "[Node:" E "]\n[neighbours:" {","}"(" E ")" "]"
-  __shared__ unsigned long long acc;
-  __shared__ unsigned int tacc;
-  if (threadIdx.x == 0) {
-    acc = 0;
-    tacc = 0;
-  }
-  __syncthreads();
-  unsigned long long part = 0;
-  unsigned int tpart = 0;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    int32_t u = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(keys[j] & 0xFFFFFFFFu));
-    part += (g.entry_off[u + 1] - g.entry_off[u]) + 2 + (j > 0 ? 1 : 0);
-    tpart += piece_tokens(g.ent_stat[u]);
-  }
-  atomicAdd(&acc, part);
-  atomicAdd(&tacc, tpart);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    sel_count[r] = k;
-    byte_len[r] = acc + 6 + (g.entry_off[v + 1] - g.entry_off[v]) + 14 + 1;
-    tok_count[r] = tacc + piece_tokens(g.ent_stat[v]) + 2;
-  }
-  }
+// Per chunk r: k' = min(k, deg), byte length, whitespace token count and the regular flag (bit 31
+// of sel_count), from the ranked-adjacency prefixes.
+struct ChunkLen {
+  uint64_t bytes;
+  uint32_t toks;
+  uint32_t sel;
+};
+__device__ __forceinline__ ChunkLen chunk_len(const DevGraph& g, const RankedAdj& ra, int k,
+                                              int32_t v) {
+  const uint32_t row = ra.off[v], deg = ra.off[v + 1] - row;
+  const uint32_t kk = min(static_cast<uint32_t>(k), deg);
+  const uint32_t sv = g.ent_stat[v];
+  const uint64_t pb = ra.pbytes[row + kk] - ra.pbytes[row];
+  ChunkLen c;
+  // "[Node:" E_v "]\n[neighbours:" {(","), "(" E ")"} "]"
+  c.bytes = 6 + (g.entry_off[v + 1] - g.entry_off[v]) + 14 + (kk ? pb - 1 : 0) + 1;
+  c.toks = piece_tokens(sv) + 2 + (ra.ptoks[row + kk] - ra.ptoks[row]);
+  const bool irregular = !entry_regular(sv) || ra.pirr[row + kk] != ra.pirr[row];
+  c.sel = kk | (irregular ? 0x80000000u : 0u);
+  return c;
 }
 
-constexpr int kWarpKeys = 4;                 // keys per lane on the warp path
-constexpr int kWarpMaxDeg = 32 * kWarpKeys;  // longer rows take the CTA path
-constexpr int kWarpMaxK = 64;
+// Lengths + both exclusive scans in one single-pass kernel (decoupled look-back): tile t (kLenTile
+// chunks, blockIdx order) publishes its aggregate, sums its predecessors' aggregates / inclusive
+// prefixes back to the first inclusive one, then publishes its own inclusive prefix.  Status words
+// carry the call's epoch, so the state needs no reset between calls.  Outputs byte_off[0..n] and
+// tok_off[0..n] ([n] = totals) and sel_count.
+constexpr int kLenThreads = 256, kLenItems = 4, kLenTile = kLenThreads * kLenItems;
 
-__device__ __forceinline__ uint32_t entry_len(const DevGraph& g, int32_t u) {
-  return g.entry_off[u + 1] - g.entry_off[u];
-}
-
-
-// Warp path of select (8 warps per CTA, one chunk each).  Rows that do not fit are appended to
-// big_list for chunk_select_kernel.
-__global__ void __launch_bounds__(256)
-chunk_select_warp_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ node_idx,
-                         int n_req, int32_t* __restrict__ sel, int32_t* __restrict__ sel_count,
-                         uint64_t* __restrict__ byte_len, uint32_t* __restrict__ tok_count,
-                         int32_t* __restrict__ big_list, int32_t* __restrict__ big_count) {
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (r >= n_req) return;
-  const int32_t v = node_idx[r];
-  const uint32_t* off = p.directed ? g.dir_off : g.und_off;
-  const int32_t* idx = p.directed ? g.dir_idx : g.und_idx;
-  const int32_t* w = p.weight_mode ? g.w_by_type : g.w_total;
-  const uint32_t beg = off[v], end = off[v + 1];
-  const int deg = static_cast<int>(end - beg);
-  const int k = min(p.k, deg);
-  if (deg > kWarpMaxDeg || k > kWarpMaxK) {
-    if (lane == 0) big_list[atomicAdd(big_count, 1)] = r;
-    return;
-  }
-  if (deg <= 32) {
-    // one key per lane: a 15-stage warp bitonic sort (descending) leaves the j-th pick in lane j
-    uint64_t kk = 0;
-    if (lane < deg) {
-      const int32_t u = idx[beg + lane];
-      kk = (static_cast<uint64_t>(static_cast<uint32_t>(w[u])) << 32) |
-           (0xFFFFFFFFu - static_cast<uint32_t>(u));
-    }
+__global__ void __launch_bounds__(kLenThreads)
+chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict__ node_idx,
+                      int n_req, int32_t* __restrict__ sel_count, uint64_t* __restrict__ byte_off,
+                      uint32_t* __restrict__ tok_off, ScanState st, uint32_t epoch,
+                      int32_t* __restrict__ irr_list, int32_t* __restrict__ irr_count) {
+  using BS64 = cub::BlockScan<uint64_t, kLenThreads>;
+  using BS32 = cub::BlockScan<uint32_t, kLenThreads>;
+  __shared__ typename BS64::TempStorage t64;
+  __shared__ typename BS32::TempStorage t32;
+  __shared__ uint64_t pre_b;
+  __shared__ uint32_t pre_t;
+  const int tile = blockIdx.x;
+  const int r0 = tile * kLenTile + threadIdx.x * kLenItems;
+  ChunkLen c[kLenItems];
+  uint64_t sb = 0;
+  uint32_t stk = 0;
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        const uint64_t o = __shfl_xor_sync(0xffffffffu, kk, stride);
-        const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
-        kk = keep_max ? (o > kk ? o : kk) : (o < kk ? o : kk);
+  for (int i = 0; i < kLenItems; ++i) {
+    c[i] = ChunkLen{0, 0, 0};
+    if (r0 + i < n_req) c[i] = chunk_len(g, ra, k, node_idx[r0 + i]);
+    sb += c[i].bytes;
+    stk += c[i].toks;
+  }
+  uint64_t xb, agg_b;
+  uint32_t xt, agg_t;
+  BS64(t64).ExclusiveSum(sb, xb, agg_b);
+  BS32(t32).ExclusiveSum(stk, xt, agg_t);
+  if (threadIdx.x < 32) {
+    // warp 0: publish the aggregate, then look back over windows of 32 predecessors at once
+    const int lane = threadIdx.x;
+    uint64_t pb = 0;
+    uint32_t pt = 0;
+    if (tile > 0) {
+      if (lane == 0) {
+        st.bytes[tile] = agg_b;
+        st.toks[tile] = agg_t;
+        __threadfence();
+        atomicExch(st.flag + tile, (epoch << 2) | 1u);  // aggregate available
       }
-    }
-    uint32_t bytes = 0, toks = 0;
-    if (lane < k) {
-      const int32_t u = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(kk));
-      sel[static_cast<int64_t>(r) * p.k_stride + lane] = u;
-      bytes = entry_len(g, u) + 2 + (lane > 0 ? 1 : 0);
-      toks = piece_tokens(g.ent_stat[u]);
+      for (int w = tile - 1; w >= 0; w -= 32) {
+        const int p = w - lane;  // lane 0 = nearest predecessor
+        uint32_t f = (epoch << 2) | 1u;
+        if (p >= 0) {
+          do {
+            f = *reinterpret_cast<volatile uint32_t*>(st.flag + p);
+          } while ((f >> 2) != epoch);
+        }
+        __threadfence();
+        const uint32_t incl = __ballot_sync(0xffffffffu, p >= 0 && (f & 3u) == 2u);
+        const int stop = incl ? __ffs(incl) - 1 : 32;  // nearest predecessor with a prefix
+        uint64_t vb = 0;
+        uint32_t vt = 0;
+        if (p >= 0 && lane <= stop) {
+          if (lane == stop) {
+            vb = *reinterpret_cast<volatile uint64_t*>(st.ibytes + p);
+            vt = *reinterpret_cast<volatile uint32_t*>(st.itoks + p);
+          } else {
+            vb = *reinterpret_cast<volatile uint64_t*>(st.bytes + p);
+            vt = *reinterpret_cast<volatile uint32_t*>(st.toks + p);
+          }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+          vb += __shfl_xor_sync(0xffffffffu, vb, d);
+          vt += __shfl_xor_sync(0xffffffffu, vt, d);
+        }
+        pb += vb;
+        pt += vt;
+        if (incl) break;
+      }
     }
     if (lane == 0) {
-      bytes += 6 + entry_len(g, v) + 14 + 1;
-      toks += piece_tokens(g.ent_stat[v]) + 2;
+      st.ibytes[tile] = pb + agg_b;
+      st.itoks[tile] = pt + agg_t;
+      __threadfence();
+      atomicExch(st.flag + tile, (epoch << 2) | 2u);  // inclusive prefix available
+      pre_b = pb;
+      pre_t = pt;
     }
-    bytes = __reduce_add_sync(0xffffffffu, bytes);
-    toks = __reduce_add_sync(0xffffffffu, toks);
-    if (lane == 0) {
-      sel_count[r] = k;
-      byte_len[r] = bytes;
-      tok_count[r] = toks;
+  }
+  __syncthreads();
+  uint64_t ob = pre_b + xb;
+  uint32_t ot = pre_t + xt;
+#pragma unroll
+  for (int i = 0; i < kLenItems; ++i) {
+    const int r = r0 + i;
+    if (r < n_req) {
+      byte_off[r] = ob;
+      tok_off[r] = ot;
+      sel_count[r] = static_cast<int32_t>(c[i].sel);
+      if (c[i].sel >> 31) irr_list[atomicAdd(irr_count, 1)] = r;
     }
+    ob += c[i].bytes;
+    ot += c[i].toks;
+    if (r == n_req - 1) {
+      byte_off[n_req] = ob;
+      tok_off[n_req] = ot;
+    }
+  }
+}
+
+// ranked adjacency: sort keys w << 32 | ~u (descending == weight desc, index asc)
+__global__ void rank_keys_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ w,
+                                 uint64_t e_count, uint64_t* __restrict__ keys) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= e_count) return;
+  const int32_t u = idx[e];
+  keys[e] = (static_cast<uint64_t>(static_cast<uint32_t>(w[u])) << 32) |
+            (0xFFFFFFFFu - static_cast<uint32_t>(u));
+}
+
+// sorted keys -> neighbour indices + per-entry values of the three prefixes (the value arrays
+// have e_count + 1 slots; the last is 0 so the exclusive scans also yield the totals)
+__global__ void rank_fill_kernel(DevGraph g, const uint64_t* __restrict__ sorted, uint64_t e_count,
+                                 int32_t* __restrict__ ridx, uint64_t* __restrict__ vb,
+                                 uint32_t* __restrict__ vt, uint32_t* __restrict__ vi) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e > e_count) return;
+  if (e == e_count) {
+    vb[e] = 0;
+    vt[e] = 0;
+    vi[e] = 0;
     return;
   }
-  // lane holds neighbours lane, lane+32, ... ; key 0 = empty (real weights are >= 1)
-  uint64_t key[kWarpKeys];
-#pragma unroll
-  for (int i = 0; i < kWarpKeys; ++i) {
-    const int e = lane + 32 * i;
-    key[i] = 0;
-    if (e < deg) {
-      const int32_t u = idx[beg + e];
-      key[i] = (static_cast<uint64_t>(static_cast<uint32_t>(w[u])) << 32) |
-               (0xFFFFFFFFu - static_cast<uint32_t>(u));
-    }
-  }
-  uint64_t best = key[0];
-#pragma unroll
-  for (int i = 1; i < kWarpKeys; ++i) best = key[i] > best ? key[i] : best;
-  int32_t* out = sel + static_cast<int64_t>(r) * p.k_stride;
-  int32_t pick[kWarpMaxK / 32] = {-1, -1};  // picks j with j % 32 == lane
-  for (int j = 0; j < k; ++j) {
-    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(best >> 32));
-    const bool cand = static_cast<uint32_t>(best >> 32) == hi;
-    const uint32_t lo = __reduce_max_sync(0xffffffffu, cand ? static_cast<uint32_t>(best) : 0u);
-    const bool mine = cand && static_cast<uint32_t>(best) == lo;  // unique: indices differ
-    const int32_t u = static_cast<int32_t>(0xFFFFFFFFu - lo);
-    if (lane == (j & 31)) {
-      out[j] = u;
-      pick[j >> 5] = u;
-    }
-    if (mine) {  // drop the winner, recompute this lane's best
-      uint64_t nb = 0;
-#pragma unroll
-      for (int i = 0; i < kWarpKeys; ++i) {
-        if (key[i] == best) key[i] = 0;
-        nb = key[i] > nb ? key[i] : nb;
-      }
-      best = nb;
-    }
-  }
-  // byte and token lengths of this lane's pieces: the entry loads of all picks issue together
-  uint32_t bytes = 0, toks = 0;
-#pragma unroll
-  for (int i = 0; i < kWarpMaxK / 32; ++i) {
-    const int32_t u = pick[i];
-    if (u >= 0) {
-      bytes += entry_len(g, u) + 2 + (lane + 32 * i > 0 ? 1 : 0);  // [","] "(" E ")"
-      toks += piece_tokens(g.ent_stat[u]);
-    }
-  }
-  if (lane == 0) {
-    bytes += 6 + entry_len(g, v) + 14 + 1;
-    toks += piece_tokens(g.ent_stat[v]) + 2;
-  }
-  bytes = __reduce_add_sync(0xffffffffu, bytes);
-  toks = __reduce_add_sync(0xffffffffu, toks);
-  if (lane == 0) {
-    sel_count[r] = k;
-    byte_len[r] = bytes;
-    tok_count[r] = toks;
-  }
-}
-
-
-
-// CTA path for hub rows (degree > 128) with k <= 64: each of the 8 warps streams its share of
-// the row in 128-key slabs (4 keys per lane, loads of two slabs in flight) and keeps a running
-// top-k in registers (slots j = lane, lane + 32); a slab whose keys are all below the current
-// k-th best is skipped after one ballot.  The 8 partial top-k lists meet in shared memory and
-// warp 0 selects the final k with the same REDUX picks as the warp path.
-template <int kPer>
-__device__ __forceinline__ int warp_pick_topk(uint64_t (&pool)[kPer], int k, uint64_t (&held)[2],
-                                              int lane) {
-  uint64_t best = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) best = pool[i] > best ? pool[i] : best;
-  held[0] = held[1] = 0;
-  int got = 0;
-  for (int j = 0; j < k; ++j) {
-    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(best >> 32));
-    const bool cand = static_cast<uint32_t>(best >> 32) == hi;
-    const uint32_t lo = __reduce_max_sync(0xffffffffu, cand ? static_cast<uint32_t>(best) : 0u);
-    if (hi == 0 && lo == 0) break;  // fewer than k keys so far
-    const uint64_t win = (static_cast<uint64_t>(hi) << 32) | lo;
-    if (lane == (j & 31)) {
-      if (j < 32) held[0] = win;
-      else held[1] = win;
-    }
-    if (cand && static_cast<uint32_t>(best) == lo) {
-      uint64_t nb = 0;
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        if (pool[i] == win) pool[i] = 0;
-        nb = pool[i] > nb ? pool[i] : nb;
-      }
-      best = nb;
-    }
-    ++got;
-  }
-  return got;
-}
-
-__global__ void __launch_bounds__(256)
-chunk_select_hub_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ node_idx, int n_req,
-                        const int32_t* __restrict__ big_list, const int32_t* __restrict__ big_count,
-                        int32_t* __restrict__ sel, int32_t* __restrict__ sel_count,
-                        uint64_t* __restrict__ byte_len, uint32_t* __restrict__ tok_count) {
-  __shared__ uint64_t wtop[8][kWarpMaxK];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_big = *big_count;
-  const uint32_t* off = p.directed ? g.dir_off : g.und_off;
-  const int32_t* idx = p.directed ? g.dir_idx : g.und_idx;
-  const int32_t* w = p.weight_mode ? g.w_by_type : g.w_total;
-  for (int bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
-    const int r = big_list[bi];
-    const int32_t v = node_idx[r];
-    const uint32_t beg = off[v], end = off[v + 1];
-    const int deg = static_cast<int>(end - beg);
-    const int k = min(p.k, deg);
-    uint64_t held[2] = {0, 0};
-    uint64_t thr = 0;  // k-th best key of this warp once it holds k keys
-    for (int c0 = warp * 256; c0 < deg; c0 += 8 * 256) {
-      // two 128-key slabs: 8 independent idx loads, then 8 weight gathers
-      int32_t u[8];
-      uint64_t key[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int e = c0 + lane + 32 * i;
-        u[i] = e < deg ? idx[beg + e] : -1;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        key[i] = 0;
-        if (u[i] >= 0) {
-          const uint64_t kk = (static_cast<uint64_t>(static_cast<uint32_t>(w[u[i]])) << 32) |
-                              (0xFFFFFFFFu - static_cast<uint32_t>(u[i]));
-          key[i] = kk > thr ? kk : 0;
-        }
-      }
-      bool any = false;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) any |= key[i] != 0;
-      if (!__any_sync(0xffffffffu, any)) continue;
-      uint64_t pool[10] = {held[0], held[1], key[0], key[1], key[2], key[3],
-                           key[4], key[5], key[6], key[7]};
-      const int got = warp_pick_topk<10>(pool, k, held, lane);
-      const uint64_t hk = __shfl_sync(0xffffffffu, k > 32 ? held[1] : held[0], (k - 1) & 31);
-      thr = got == k ? hk : 0;
-    }
-    wtop[warp][lane] = held[0];
-    if (lane + 32 < kWarpMaxK) wtop[warp][lane + 32] = held[1];
-    __syncthreads();
-    if (warp == 0) {
-      // 8 x k candidates (k <= 64): 16 per lane
-      uint64_t pool[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int e = lane + 32 * i;  // candidate e = warp e / 64, slot e % 64
-        pool[i] = wtop[e >> 6][e & 63];
-      }
-      uint64_t fin[2];
-      warp_pick_topk<16>(pool, k, fin, lane);
-      int32_t* out = sel + static_cast<int64_t>(r) * p.k_stride;
-      uint32_t bytes = 0, toks = 0;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int j = lane + 32 * i;
-        if (j < k) {
-          const int32_t uu = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(fin[i]));
-          out[j] = uu;
-          bytes += entry_len(g, uu) + 2 + (j > 0 ? 1 : 0);
-          toks += piece_tokens(g.ent_stat[uu]);
-        }
-      }
-      if (lane == 0) {
-        bytes += 6 + entry_len(g, v) + 14 + 1;
-        toks += piece_tokens(g.ent_stat[v]) + 2;
-      }
-      bytes = __reduce_add_sync(0xffffffffu, bytes);
-      toks = __reduce_add_sync(0xffffffffu, toks);
-      if (lane == 0) {
-        sel_count[r] = k;
-        byte_len[r] = bytes;
-        tok_count[r] = toks;
-      }
-    }
-    __syncthreads();  // wtop reuse
-  }
+  const int32_t u = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(sorted[e]));
+  ridx[e] = u;
+  const uint32_t st = g.ent_stat[u];
+  vb[e] = (g.entry_off[u + 1] - g.entry_off[u]) + 3;
+  vt[e] = piece_tokens(st);
+  vi[e] = entry_regular(st) ? 0u : 1u;
 }
 
 // ---------------------------------------------------------------------------------- render+emit
 // One warp per chunk: the chunk is assembled in a per-warp shared-memory buffer placed at the
 // same 16-byte phase as its global destination, written out with 16-byte stores, and tokenised
-// from shared memory — the text is never read back from HBM.  Entry bytes are fetched as 16-byte
-// aligned words: the words of all pieces of a round (the centre entry + up to 31 neighbours) are
-// numbered by a warp scan, each lane finds its piece by a shuffle binary search, and four loads
-// per lane are in flight before any byte is scattered.  Chunks longer than the buffer are built
-// in place in global memory by the same code.
+// without reading the text back from HBM.  Lane s copies piece s (entry bytes as aligned 4-byte
+// words, realigned to the destination by funnel shifts, ragged ends byte by byte).  Chunks longer
+// than the buffer are built in place in global memory by the same code.
 constexpr int kRW = 4;         // warps (chunks) per CTA
-constexpr int kBuf = 6144;     // staged chunk bytes per warp
+constexpr int kBuf = 4096;     // staged chunk bytes per warp
 constexpr int kSeg = 1024;     // bytes per token-start compaction segment
-constexpr int kWordsU = 4;     // 16-byte loads in flight per lane
+constexpr int kWordsU = 2;     // 16-byte loads in flight per lane (2: 48 registers, 10 CTAs/SM)
 
 // h % vocab for a 64-bit h by Barrett reduction with m = floor((2^64 - 1) / vocab): the estimate
 // q = hi64(h * m) is at most 2 below the true quotient.
@@ -448,17 +267,82 @@ __device__ __forceinline__ uint32_t next_start(const uint32_t* sp, uint32_t q, u
   return min(Q, (w << 5) + __ffs(st) - 1);
 }
 
-// Assemble chunk bytes [0, n) at buf (shared or global).  Returns nothing; buf[n-1] = ']'.
+// One 16-byte source word x (entry bytes [base, base + 16)) of a segment [src, end) whose byte p
+// goes to dstp + p, stored as destination-aligned 4-byte words of the source words realigned by a
+// funnel shift (nx = the next source word).  A segment's bytes are framed by known separator
+// bytes -- 3 before (pre, in the top 3 bytes) and up to 3 after (post, low bytes), e.g. ")" ","
+// "(" between neighbour entries -- so every word inside [src - 3, ext_end) is written whole, the
+// frame bytes merged in, and no entry byte needs a byte store.  Adjacent segments' frames are the
+// same separator bytes, and a 4-byte word never holds bytes of two entries, so each word has one
+// writer.  Words of the first block that start before base + q (j = -1) cover the frame before
+// src.
+__device__ __forceinline__ void put_block(char* dstp, uint4 x, uint32_t nx, uint32_t base,
+                                          uint32_t src, uint32_t end, uint32_t ext_end,
+                                          uint32_t pre, uint32_t post) {
+  const uint32_t q = (0u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dstp))) & 3u;
+  const uint32_t w[6] = {0u, x.x, x.y, x.z, x.w, nx};
+  if (base + q >= src + 4 && base + q + 16 <= end) {
+    // interior block: its four words hold entry bytes only
+    char* d = dstp + base + q;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      reinterpret_cast<uint32_t*>(d)[j] = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
+    return;
+  }
+  // positions biased by +16 so that j = -1 at base 0 stays unsigned
+  const uint32_t bs = src + 16, be = end + 16, bx = ext_end + 16;
+  const bool first = base <= src;
+#pragma unroll
+  for (int j = -1; j < 4; ++j) {
+    // p = source position of the word's first byte (+16); j = -1 is the word before the block's
+    // first aligned one: in the segment's first block it holds frame bytes + the entry's first
+    // bytes, in later blocks it is the previous block's j = 3 word
+    const uint32_t p = base + 16 + q + 4 * j;
+    if (p + 3 >= bs && p + 4 <= bx && (j >= 0 || first)) {
+      uint32_t v = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
+      if (p < bs) {  // 1..3 frame bytes before src
+        const uint32_t m = bs - p;
+        v = (v & (0xFFFFFFFFu << (8 * m))) | (pre >> (8 * (4 - m)));
+      }
+      if (p + 4 > be) {  // 1..3 entry bytes, then the frame after end
+        const uint32_t keep = be - p;
+        v = (v & (0xFFFFFFFFu >> (32 - 8 * keep))) | (post << (8 * keep));
+      }
+      *reinterpret_cast<uint32_t*>(dstp + static_cast<int32_t>(p - 16u)) = v;
+    }
+  }
+}
+
+// The bytes [max(lo, pad), min(lo + 16, Q)) of a staged 16-byte word: 4-byte stores where a
+// quarter is whole, byte stores for the rest.
+__device__ __forceinline__ void put_edge16(char* gbase, const char* sb, uint32_t lo, uint32_t pad,
+                                           uint32_t Q) {
+#pragma unroll
+  for (uint32_t c = 0; c < 16; c += 4) {
+    const uint32_t a = lo + c;
+    if (a >= pad && a + 4 <= Q) {
+      *reinterpret_cast<uint32_t*>(gbase + a) = *reinterpret_cast<const uint32_t*>(sb + a);
+    } else if (a + 4 > pad && a < Q) {
+      for (uint32_t b = max(a, pad); b < min(a + 4, Q); ++b) gbase[b] = sb[b];
+    }
+  }
+}
+
+// Assemble chunk bytes [0, n) at buf (shared or global): "[Node:" E_v "]\n[neighbours:"
+// {(","), "(" E_j ")"} "]".  Per round of 32 segments (the centre entry + up to 31 neighbour
+// pieces) the 16-byte source words of all segments are numbered by a warp scan; each lane finds
+// its segment by a shuffle binary search and keeps kWordsU loads in flight before it stores.
 __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
-                                            const int32_t* __restrict__ mine, char* buf, int lane) {
+                                            const int32_t* __restrict__ mine, char* buf, int lane,
+                                            bool staged) {
   const uint32_t ev = g.entry_off[v];
   const uint32_t ec = g.entry_off[v + 1] - ev;
   if (lane < 6) buf[lane] = "[Node:"[lane];
   if (lane < 14) buf[6 + ec + lane] = "]\n[neighbours:"[lane];
-  uint32_t o = 6 + ec + 14;  // offset of the next neighbour piece
+  uint32_t o = 6 + ec + 14;  // offset of the next round's first neighbour piece
   const uint4* words = reinterpret_cast<const uint4*>(g.entry_bytes);
+  const uint32_t* words4 = reinterpret_cast<const uint32_t*>(g.entry_bytes);
   for (int s0 = 0; s0 <= k; s0 += 32) {
-    // segment s = s0 + lane: s == 0 is the centre entry, s >= 1 neighbour piece j = s - 1
     const int s = s0 + lane;
     uint32_t src = 0, len = 0, dst = 0, plen = 0;
     if (s == 0) {
@@ -466,11 +350,10 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
       len = ec;
       dst = 6;
     } else if (s <= k) {
-      const int j = s - 1;
-      const int32_t u = mine[j];
+      const int32_t u = mine[s - 1];
       src = g.entry_off[u];
       len = g.entry_off[u + 1] - src;
-      plen = len + 2 + (j > 0 ? 1u : 0u);
+      plen = len + 2 + (s > 1 ? 1u : 0u);
     }
     uint32_t pincl = plen;
 #pragma unroll
@@ -487,7 +370,10 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
       dst = pst + c + 1;
     }
     o += __shfl_sync(0xffffffffu, pincl, 31);
-    // 16-byte words covering [src, src + len), numbered across the round's segments
+    // unstaged: the last piece's frame ")]" is 2 bytes, so put_block skips a final word that would
+    // reach past the chunk; its one entry byte is stored here
+    if (!staged && s >= 1 && s == k && len) buf[dst + len - 1] = g.entry_bytes[src + len - 1];
+    // 16-byte source words covering [src, src + len), numbered across the round's segments
     const uint32_t wc = len ? ((src + len - 1) >> 4) - (src >> 4) + 1 : 0;
     uint32_t wincl = wc;
 #pragma unroll
@@ -499,7 +385,8 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
     const uint32_t wexcl = wincl - wc;
     for (uint32_t w0 = 0; w0 < W; w0 += 32 * kWordsU) {
       uint4 x[kWordsU];
-      uint32_t qsrc[kWordsU], qlen[kWordsU], qdst[kWordsU], qword[kWordsU];
+      uint32_t nx[kWordsU], qsrc[kWordsU], qlen[kWordsU], qdst[kWordsU], qword[kWordsU];
+      int qseg[kWordsU];
 #pragma unroll
       for (int t = 0; t < kWordsU; ++t) {
         const uint32_t wi = w0 + t * 32 + lane;
@@ -514,44 +401,25 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
         qlen[t] = __shfl_sync(0xffffffffu, len, q);
         qdst[t] = __shfl_sync(0xffffffffu, dst, q);
         qword[t] = (qsrc[t] >> 4) + (wi - qe);
-        x[t] = wi < W ? __ldg(words + qword[t]) : make_uint4(0, 0, 0, 0);
-        if (wi >= W) qlen[t] = 0;
+        qseg[t] = s0 + q;
+        const bool in = wi < W;
+        x[t] = in ? __ldg(words + qword[t]) : make_uint4(0, 0, 0, 0);
+        nx[t] = in ? __ldg(words4 + 4 * (qword[t] + 1)) : 0u;
+        if (!in) qlen[t] = 0;
       }
 #pragma unroll
       for (int t = 0; t < kWordsU; ++t) {
-        const uint32_t base = qword[t] << 4;
-        const uint32_t xs[4] = {x[t].x, x[t].y, x[t].z, x[t].w};
-        if (qlen[t] && base >= qsrc[t] && base + 16 <= qsrc[t] + qlen[t]) {
-          // interior word: realign the 16 bytes to the destination's 4-byte phase s and store
-          // 3 aligned words (funnel shifts) plus 4 edge bytes (4 words when s == 0)
-          char* d = buf + qdst[t] + (base - qsrc[t]);
-          const uint32_t s = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(d)) & 3u;
-          if (s == 0) {
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(d);
-            d4[0] = xs[0];
-            d4[1] = xs[1];
-            d4[2] = xs[2];
-            d4[3] = xs[3];
-          } else {
-            const uint32_t sh = 8 * (4 - s);
-            uint32_t* a4 = reinterpret_cast<uint32_t*>(d + (4 - s));
-            a4[0] = __funnelshift_r(xs[0], xs[1], sh);
-            a4[1] = __funnelshift_r(xs[1], xs[2], sh);
-            a4[2] = __funnelshift_r(xs[2], xs[3], sh);
-#pragma unroll
-            for (uint32_t j = 0; j < 3; ++j) {
-              if (j < 4 - s) d[j] = static_cast<char>(xs[0] >> (8 * j));
-              if (j < s) d[16 - s + j] = static_cast<char>(xs[3] >> (8 * (4 - s + j)));
-            }
-          }
-        } else {
-#pragma unroll
-          for (int b = 0; b < 16; ++b) {
-            const uint32_t gp = base + b;
-            if (gp >= qsrc[t] && gp < qsrc[t] + qlen[t])
-              buf[qdst[t] + (gp - qsrc[t])] = static_cast<char>(xs[b >> 2] >> ((b & 3) * 8));
-          }
-        }
+        if (!qlen[t]) continue;
+        // the segment's frame: "de:" E_v "]\n[" / "s:(" E_1 / ")" "," "(" E_j / ")" "," "(" or
+        // ")" "]" after the last piece
+        const int sg = qseg[t];
+        const uint32_t pre = sg == 0 ? 0x3A656400u : sg == 1 ? 0x283A7300u : 0x282C2900u;
+        const bool last = sg >= 1 && sg == k;
+        const uint32_t post = sg == 0 ? 0x5B0A5Du : last ? 0x5D29u : 0x282C29u;
+        const uint32_t end = qsrc[t] + qlen[t];
+        // staged: the buffer has slack past the chunk, so the last frame may take a 3rd byte
+        put_block(buf + qdst[t] - qsrc[t], x[t], nx[t], qword[t] << 4, qsrc[t], end,
+                  end + (last && !staged ? 2u : 3u), pre, post);
       }
     }
   }
@@ -559,35 +427,195 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kRW * 32, 7)
-chunk_render_emit_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ node_idx,
-                         int n_req, const int32_t* __restrict__ sel,
-                         const int32_t* __restrict__ sel_count,
-                         const uint64_t* __restrict__ byte_off, const uint32_t* __restrict__ tok_off,
-                         uint32_t vocab, uint64_t vmagic, char* __restrict__ out,
-                         int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
-                         uint64_t* __restrict__ tok_end) {
-  __shared__ __align__(16) char sbuf[kRW][kBuf + 16];
-  __shared__ uint32_t smask[kRW][kBuf / 32 + 1];
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int r = blockIdx.x * kRW + wi;
-  if (r >= n_req) return;
-  const int32_t v = node_idx[r];
-  const int k = sel_count[r];
-  const int32_t* mine = sel + static_cast<int64_t>(r) * p.k_stride;
-  const uint64_t goff = byte_off[r];
-  const uint32_t n = static_cast<uint32_t>(byte_off[r + 1] - goff);
+constexpr uint64_t kFnvBasis = 14695981039346656037ULL, kFnvPrime = 1099511628211ULL;
+__host__ __device__ constexpr uint64_t fnv_lit(const char* c, uint64_t h = kFnvBasis) {
+  return *c ? fnv_lit(c + 1, (h ^ static_cast<unsigned char>(*c)) * kFnvPrime) : h;
+}
+constexpr uint64_t kNodeState = fnv_lit("[Node:");         // first token of every chunk
+constexpr uint64_t kNbrState = fnv_lit("[neighbours:(");   // first neighbour junction
+constexpr uint64_t kNbrEmpty = fnv_lit("[neighbours:]");   // k = 0: the whole last token
+
+__device__ __forceinline__ uint64_t fnv_byte(uint64_t h, unsigned char c) {
+  return (h ^ c) * kFnvPrime;
+}
+
+__device__ __forceinline__ void put_token(uint32_t o, uint32_t b, uint32_t e, uint64_t h,
+                                          uint32_t vocab, uint64_t vmagic, int32_t* tok_id,
+                                          uint64_t* tok_begin, uint64_t* tok_end) {
+  tok_begin[o] = b;
+  tok_end[o] = e;
+  if (vocab) tok_id[o] = static_cast<int32_t>(mod_vocab(h, vocab, vmagic));
+}
+
+// Fast tokenizer of a chunk whose pieces are all regular entries (DevGraph::ent_head != 0).  The
+// chunk's tokens, in order:
+//   J_0 = "[Node:" + head(E_v), interior(E_v), T_v = tail(E_v) + "]"            (centre piece 0)
+//   J_s = sep + head(E_s), interior(E_s)    (neighbour piece s >= 1; sep = "[neighbours:(" for
+//         s = 1, else tail(E_{s-1}) + "),(")
+//   last = tail(E_k) + ")]"   (k = 0: "[neighbours:]")
+// Lane s of a round computes J_s (its hash continues from E_{s-1}'s precomputed tail state over
+// the separator and E_s's first-token bytes); the interior tokens are copied from the tables,
+// lanes striding over the round's interior tokens.
+__device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
+                                          const int32_t* __restrict__ mine, uint32_t n, uint32_t t,
+                                          uint32_t vocab, uint64_t vmagic, int32_t* tok_id,
+                                          uint64_t* tok_begin, uint64_t* tok_end, int lane) {
+  const uint32_t ev = g.entry_off[v], lv = g.entry_off[v + 1] - ev;
+  uint32_t prev_dst = 0, prev_tail = 0;
+  uint64_t prev_ts = 0;
+  uint32_t o = 6 + lv + 14;  // byte offset of the next neighbour piece
+  uint32_t tb = t;           // first token of the round
+  for (int s0 = 0; s0 <= k; s0 += 32) {
+    const int s = s0 + lane;
+    const bool act = s <= k;
+    int32_t u = v;
+    uint32_t eo = ev, len = lv, dst = 6, plen = 0;
+    if (act && s > 0) {
+      u = mine[s - 1];
+      eo = g.entry_off[u];
+      len = g.entry_off[u + 1] - eo;
+      plen = len + 2 + (s > 1 ? 1u : 0u);
+    }
+    uint32_t pincl = plen;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, pincl, d);
+      if (lane >= d) pincl += x;
+    }
+    if (s > 0) dst = o + (pincl - plen) + (s > 1 ? 2u : 1u);
+    o += __shfl_sync(0xffffffffu, pincl, 31);
+    uint32_t hl = 0, tl = 0, io = 0, ni = 0;
+    uint64_t ts = 0;
+    if (act) {
+      hl = g.ent_head[u];
+      tl = g.ent_tail[u];
+      ts = g.ent_tstate[u];
+      io = g.ent_ioff[u];
+      ni = g.ent_ioff[u + 1] - io;
+    }
+    const uint32_t grp = act ? ni + (s == 0 ? 2u : 1u) : 0u;
+    uint32_t gin = grp, iin = ni;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, gin, d);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, iin, d);
+      if (lane >= d) {
+        gin += x;
+        iin += y;
+      }
+    }
+    const uint32_t gex = gin - grp, iex = iin - ni;
+    const uint32_t gtot = __shfl_sync(0xffffffffu, gin, 31);
+    const uint32_t itot = __shfl_sync(0xffffffffu, iin, 31);
+    uint32_t pd = __shfl_up_sync(0xffffffffu, dst, 1), pt = __shfl_up_sync(0xffffffffu, tl, 1);
+    uint64_t pts = __shfl_up_sync(0xffffffffu, ts, 1);
+    if (lane == 0) {
+      pd = prev_dst;
+      pt = prev_tail;
+      pts = prev_ts;
+    }
+    if (act) {
+      uint64_t h;
+      uint32_t b;
+      if (s == 0) {
+        h = kNodeState;
+        b = 0;
+      } else if (s == 1) {
+        h = kNbrState;
+        b = 6 + lv + 2;
+      } else {
+        h = fnv_byte(fnv_byte(fnv_byte(pts, ')'), ','), '(');
+        b = pd + pt;
+      }
+      const unsigned char* hb = reinterpret_cast<const unsigned char*>(g.entry_bytes) + eo;
+      for (uint32_t q = 0; q < hl; ++q) h = fnv_byte(h, hb[q]);
+      put_token(tb + gex, b, dst + hl, h, vocab, vmagic, tok_id, tok_begin, tok_end);
+      if (s == 0)
+        put_token(tb + gex + 1 + ni, dst + tl, dst + len + 1, fnv_byte(ts, ']'), vocab, vmagic,
+                  tok_id, tok_begin, tok_end);
+      if (s == k) {
+        if (k == 0)
+          put_token(tb + gex + grp, 6 + lv + 2, n, kNbrEmpty, vocab, vmagic, tok_id, tok_begin,
+                    tok_end);
+        else
+          put_token(tb + gex + grp, dst + tl, n, fnv_byte(fnv_byte(ts, ')'), ']'), vocab, vmagic,
+                    tok_id, tok_begin, tok_end);
+      }
+    }
+    // interior tokens of the round's pieces, lanes striding over them (two per lane per
+    // iteration: both record loads are in flight before the stores)
+    for (uint32_t i0 = 0; i0 < itot; i0 += 64) {
+      uint32_t jj[2], qg[2], qd[2];
+      uint4 rec[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t i = i0 + 32 * h + lane;
+        int q = 0;  // last piece whose first interior token is <= i
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t e = __shfl_sync(0xffffffffu, iex, q + step);
+          if (e <= i) q += step;
+        }
+        const uint32_t qiex = __shfl_sync(0xffffffffu, iex, q);
+        const uint32_t qio = __shfl_sync(0xffffffffu, io, q);
+        qg[h] = __shfl_sync(0xffffffffu, gex, q);
+        qd[h] = __shfl_sync(0xffffffffu, dst, q);
+        jj[h] = i - qiex;
+        rec[h] = i < itot ? __ldg(g.itok + qio + jj[h]) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (i0 + 32 * h + lane < itot)
+          put_token(tb + qg[h] + 1 + jj[h], qd[h] + rec[h].x, qd[h] + rec[h].y,
+                    (static_cast<uint64_t>(rec[h].w) << 32) | rec[h].z, vocab, vmagic, tok_id,
+                    tok_begin, tok_end);
+    }
+    tb += gtot;
+    prev_dst = __shfl_sync(0xffffffffu, dst, 31);
+    prev_tail = __shfl_sync(0xffffffffu, tl, 31);
+    prev_ts = __shfl_sync(0xffffffffu, ts, 31);
+  }
+}
+
+// Text of a regular chunk (its tokens come from chunk_tokens_kernel).
+__device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
+                                            const int32_t* __restrict__ mine, uint64_t goff,
+                                            uint32_t n, char* __restrict__ out, char* sb, int lane) {
+  if (n <= kBuf) {
+    const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
+    build_chunk(g, v, k, mine, sb + pad, lane, true);
+    char* gbase = out + (goff - pad);
+    const uint32_t nw16 = (Q + 15) >> 4;
+    for (uint32_t i = lane; i < nw16; i += 32) {
+      const uint32_t lo = 16 * i, hi = lo + 16;
+      if (lo >= pad && hi <= Q) {
+        *reinterpret_cast<uint4*>(gbase + lo) = *reinterpret_cast<const uint4*>(sb + lo);
+      } else {
+        put_edge16(gbase, sb, lo, pad, Q);
+      }
+    }
+  } else {
+    build_chunk(g, v, k, mine, out + goff, lane, false);
+  }
+}
+
+// Text and tokens of an irregular chunk (the byte-level tokenizer over a whitespace mask).
+__device__ __forceinline__ void render_slow(const DevGraph& g, int32_t v, int k,
+                                            const int32_t* __restrict__ mine, uint64_t goff,
+                                            uint32_t n, uint32_t t, uint32_t vocab, uint64_t vmagic,
+                                            char* __restrict__ out, int32_t* __restrict__ tok_id,
+                                            uint64_t* __restrict__ tok_begin,
+                                            uint64_t* __restrict__ tok_end, char* sbw,
+                                            uint32_t* sp, int lane) {
   const bool staged = n <= kBuf;
   char* gdst = out + goff;
-  uint32_t* sp = smask[wi];
   // token-start list of the unstaged path (chunks > kBuf), which leaves the staging buffer free
-  uint32_t* list = reinterpret_cast<uint32_t*>(sbuf[wi]);
-  uint32_t t = tok_off[r];
+  uint32_t* list = reinterpret_cast<uint32_t*>(sbw);
   if (staged) {
     // staged span: smem bytes [pad, Q) hold the chunk at the 16-byte phase of its destination
-    char* sb = sbuf[wi];
+    char* sb = sbw;
     const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
-    build_chunk(g, v, k, mine, sb + pad, lane);
+    build_chunk(g, v, k, mine, sb + pad, lane, true);
     // per 16-byte word (one per lane): text out (aligned words as one 16-byte store, the two edge
     // words byte by byte) and 16 whitespace bits; bytes outside [pad, Q) count as spaces
     char* gbase = out + (goff - pad);
@@ -601,7 +629,7 @@ chunk_render_emit_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ 
         if (lo >= pad && hi <= Q) {
           *reinterpret_cast<uint4*>(gbase + lo) = x;
         } else {
-          for (uint32_t q = max(lo, pad); q < min(hi, Q); ++q) gbase[q] = sb[q];
+          put_edge16(gbase, sb, lo, pad, Q);
         }
         bits = space_bits4(x.x) | (space_bits4(x.y) << 4) | (space_bits4(x.z) << 8) |
                (space_bits4(x.w) << 12);
@@ -646,7 +674,7 @@ chunk_render_emit_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ 
     return;
   }
   // longer than the buffer: built in place in global memory, tokenised from there
-  build_chunk(g, v, k, mine, gdst, lane);
+  build_chunk(g, v, k, mine, gdst, lane, false);
   const char* src = gdst;
   for (uint32_t s0 = 0; s0 < n; s0 += kSeg) {
     uint32_t cnt = 0;
@@ -675,6 +703,43 @@ chunk_render_emit_kernel(DevGraph g, ChunkParams p, const int32_t* __restrict__ 
   }
 }
 
+// Regular chunks (kIrr = false): one warp per chunk renders the text, at high occupancy (no
+// whitespace mask).  Irregular chunks (kIrr = true): a small grid walks the list the scan kernel
+// compacted and runs the byte-level path.  Output capacity overflow: see chunk_render_emit.
+template <bool kIrr>
+__global__ void __launch_bounds__(kRW * 32, kIrr ? 7 : 10)
+chunk_render_kernel(DevGraph g, RankedAdj ra, const int32_t* __restrict__ node_idx, int n_req,
+                    const int32_t* __restrict__ sel_count, const uint64_t* __restrict__ byte_off,
+                    const uint32_t* __restrict__ tok_off, uint32_t vocab, uint64_t vmagic,
+                    char* __restrict__ out, int32_t* __restrict__ tok_id,
+                    uint64_t* __restrict__ tok_begin, uint64_t* __restrict__ tok_end,
+                    uint64_t bytes_cap, uint64_t tok_cap, int32_t* __restrict__ overflow,
+                    const int32_t* __restrict__ irr_list, const int32_t* __restrict__ irr_count) {
+  __shared__ __align__(16) char sbuf[kRW][kBuf + 16];
+  __shared__ uint32_t smask[kIrr ? kRW : 1][kIrr ? kBuf / 32 + 1 : 1];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int n_items = kIrr ? *irr_count : n_req;
+  for (int i = blockIdx.x * kRW + wi; i < n_items; i += gridDim.x * kRW) {
+    const int r = kIrr ? irr_list[i] : i;
+    const uint64_t goff = byte_off[r], gend = byte_off[r + 1];
+    if (gend > bytes_cap || tok_off[r + 1] > tok_cap) {  // the host grows the buffers and reruns
+      if (lane == 0) *overflow = 1;
+      continue;
+    }
+    const uint32_t kr = static_cast<uint32_t>(sel_count[r]);
+    if (!kIrr && (kr >> 31)) continue;
+    const int32_t v = node_idx[r];
+    const int k = static_cast<int>(kr & 0x7FFFFFFFu);
+    const int32_t* mine = ra.idx + ra.off[v];  // the top-k are the first k of the ranked row
+    const uint32_t n = static_cast<uint32_t>(gend - goff);
+    if constexpr (kIrr)
+      render_slow(g, v, k, mine, goff, n, tok_off[r], vocab, vmagic, out, tok_id, tok_begin,
+                  tok_end, sbuf[wi], smask[wi], lane);
+    else
+      render_text(g, v, k, mine, goff, n, out, sbuf[wi], lane);
+  }
+}
+
 // Per-entry whitespace stats for the token count of a chunk: bits 0-28 number of whitespace
 // tokens, 29 first byte is not a space, 30 last byte is not a space, 31 non-empty.
 __global__ void entry_stats_kernel(const char* __restrict__ bytes, const uint32_t* __restrict__ off,
@@ -697,40 +762,167 @@ __global__ void entry_stats_kernel(const char* __restrict__ bytes, const uint32_
   }
   st[i] = w;
 }
+
+__global__ void entry_interior_counts_kernel(const uint32_t* __restrict__ st, uint32_t n,
+                                             uint32_t* __restrict__ cnt) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) cnt[i] = entry_regular(st[i]) ? (st[i] & 0x1FFFFFFFu) - 2 : 0u;
+  if (i == n) cnt[i] = 0;
+}
+
+// one thread per entry (ingest time): spans + fnv1a hashes of the interior tokens, the first
+// token's length, the last token's offset and its fnv1a state
+__global__ void entry_tokens_kernel(const char* __restrict__ bytes, const uint32_t* __restrict__ off,
+                                    const uint32_t* __restrict__ st, uint32_t n,
+                                    const uint32_t* __restrict__ ioff, uint32_t* __restrict__ head,
+                                    uint32_t* __restrict__ tail, uint64_t* __restrict__ tstate,
+                                    uint4* __restrict__ itok) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (!entry_regular(st[i])) {
+    head[i] = 0;
+    tail[i] = 0;
+    tstate[i] = 0;
+    return;
+  }
+  const uint32_t b = off[i], e = off[i + 1], T = st[i] & 0x1FFFFFFFu;
+  uint32_t tok = 0, o = ioff[i];
+  uint32_t q = b;
+  while (q < e) {
+    while (q < e && dev_is_space(static_cast<unsigned char>(bytes[q]))) ++q;
+    if (q >= e) break;
+    const uint32_t t0 = q;
+    uint64_t h = 14695981039346656037ULL;
+    while (q < e && !dev_is_space(static_cast<unsigned char>(bytes[q]))) {
+      h = (h ^ static_cast<unsigned char>(bytes[q])) * 1099511628211ULL;
+      ++q;
+    }
+    if (tok == 0) {
+      head[i] = q - b;
+    } else if (tok == T - 1) {
+      tail[i] = t0 - b;
+      tstate[i] = h;
+    } else {
+      itok[o++] = make_uint4(t0 - b, q - b, static_cast<uint32_t>(h), static_cast<uint32_t>(h >> 32));
+    }
+    ++tok;
+  }
+}
+// Tokens of the regular chunks (the table-driven tokenizer, no shared memory): a separate
+// kernel from the text so that each runs at its own occupancy.
+__global__ void __launch_bounds__(128, 12)
+chunk_tokens_kernel(DevGraph g, RankedAdj ra, const int32_t* __restrict__ node_idx, int n_req,
+                    const int32_t* __restrict__ sel_count, const uint64_t* __restrict__ byte_off,
+                    const uint32_t* __restrict__ tok_off, uint32_t vocab, uint64_t vmagic,
+                    int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
+                    uint64_t* __restrict__ tok_end, uint64_t bytes_cap, uint64_t tok_cap) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (r >= n_req) return;
+  const uint32_t kr = static_cast<uint32_t>(sel_count[r]);
+  if (kr >> 31) return;  // irregular: tokenised by the render kernel
+  const uint64_t goff = byte_off[r], gend = byte_off[r + 1];
+  if (gend > bytes_cap || tok_off[r + 1] > tok_cap) return;  // overflow: rerun after growing
+  const int32_t v = node_idx[r];
+  emit_fast(g, v, static_cast<int>(kr), ra.idx + ra.off[v], static_cast<uint32_t>(gend - goff),
+            tok_off[r], vocab, vmagic, tok_id, tok_begin, tok_end, lane);
+}
+
 }  // namespace
 
-void chunk_select(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
-                  int32_t* sel, int32_t* sel_count, uint64_t* byte_len, uint32_t* tok_count,
-                  int32_t* big_list, int32_t* big_count, cudaStream_t s) {
-  GLMX_CUDA(cudaMemsetAsync(big_count, 0, 4, s));
-  chunk_select_warp_kernel<<<static_cast<int>(ceil_div(n_req, 8)), 256, 0, s>>>(
-      g, p, node_idx, n_req, sel, sel_count, byte_len, tok_count, big_list, big_count);
-  GLMX_CHECK_LAUNCH();
-  // CTA path for hub rows / large k: a fixed grid walks the queued requests (warp-merge top-k for
-  // k <= 64, the bitonic window for larger k)
-  if (p.k <= kWarpMaxK)
-    chunk_select_hub_kernel<<<std::min(n_req, kNumSMs * 4), 256, 0, s>>>(
-        g, p, node_idx, n_req, big_list, big_count, sel, sel_count, byte_len, tok_count);
-  else
-    chunk_select_kernel<<<std::min(n_req, kNumSMs * 4), kSelThreads, 0, s>>>(
-        g, p, node_idx, n_req, big_list, big_count, sel, sel_count, byte_len, tok_count);
+int chunk_scan_tiles(int n_req) { return static_cast<int>(ceil_div(n_req, kLenTile)); }
+
+void chunk_lengths_scan(const DevGraph& g, const RankedAdj& ra, int k, const int32_t* node_idx,
+                        int n_req, int32_t* sel_count, uint64_t* byte_off, uint32_t* tok_off,
+                        const ScanState& st, uint32_t epoch, int32_t* irr_list, int32_t* irr_count,
+                        cudaStream_t s) {
+  chunk_len_scan_kernel<<<chunk_scan_tiles(n_req), kLenThreads, 0, s>>>(
+      g, ra, k, node_idx, n_req, sel_count, byte_off, tok_off, st, epoch, irr_list, irr_count);
   GLMX_CHECK_LAUNCH();
 }
 
-void chunk_render_emit(const DevGraph& g, const ChunkParams& p, const int32_t* node_idx, int n_req,
-                       const int32_t* sel, const int32_t* sel_count, const uint64_t* byte_off,
-                       const uint32_t* tok_off, uint32_t vocab, char* out, int32_t* tok_id,
-                       uint64_t* tok_begin, uint64_t* tok_end, cudaStream_t s) {
+void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* node_idx, int n_req,
+                       const int32_t* sel_count, const uint64_t* byte_off, const uint32_t* tok_off,
+                       uint32_t vocab, char* out, int32_t* tok_id, uint64_t* tok_begin,
+                       uint64_t* tok_end, uint64_t bytes_cap, uint64_t tok_cap, int32_t* overflow,
+                       const int32_t* irr_list, const int32_t* irr_count, cudaStream_t s,
+                       cudaStream_t s2, cudaEvent_t fork, cudaEvent_t join) {
   const uint64_t vmagic = vocab ? ~uint64_t(0) / vocab : 0;
-  chunk_render_emit_kernel<<<static_cast<int>(ceil_div(n_req, kRW)), kRW * 32, 0, s>>>(
-      g, p, node_idx, n_req, sel, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id,
-      tok_begin, tok_end);
+  GLMX_CUDA(cudaEventRecord(fork, s));
+  GLMX_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+  chunk_tokens_kernel<<<static_cast<int>(ceil_div(n_req, 4)), 128, 0, s2>>>(
+      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, tok_id, tok_begin,
+      tok_end, bytes_cap, tok_cap);
   GLMX_CHECK_LAUNCH();
+  chunk_render_kernel<false><<<static_cast<int>(ceil_div(n_req, kRW)), kRW * 32, 0, s>>>(
+      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin,
+      tok_end, bytes_cap, tok_cap, overflow, irr_list, irr_count);
+  GLMX_CHECK_LAUNCH();
+  chunk_render_kernel<true><<<2 * kNumSMs, kRW * 32, 0, s>>>(
+      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin,
+      tok_end, bytes_cap, tok_cap, overflow, irr_list, irr_count);
+  GLMX_CHECK_LAUNCH();
+  GLMX_CUDA(cudaEventRecord(join, s2));
+  GLMX_CUDA(cudaStreamWaitEvent(s, join, 0));
+}
+
+size_t rank_sort_temp_bytes(uint64_t e_count, uint32_t n) {
+  size_t t = 0;
+  cub::DeviceSegmentedSort::SortKeysDescending(nullptr, t, static_cast<const uint64_t*>(nullptr),
+                                               static_cast<uint64_t*>(nullptr),
+                                               static_cast<int64_t>(e_count), static_cast<int64_t>(n),
+                                               static_cast<const uint32_t*>(nullptr),
+                                               static_cast<const uint32_t*>(nullptr));
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, static_cast<uint64_t*>(nullptr),
+                                static_cast<uint64_t*>(nullptr), static_cast<int64_t>(e_count + 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, static_cast<uint32_t*>(nullptr),
+                                static_cast<uint32_t*>(nullptr), static_cast<int64_t>(e_count + 1));
+  return std::max(t, std::max(t1, t2));
+}
+
+void rank_adjacency(const DevGraph& g, const uint32_t* off, const int32_t* idx, const int32_t* w,
+                    uint64_t e_count, uint32_t n, void* temp, size_t temp_bytes, uint64_t* keys,
+                    uint64_t* sorted, int32_t* ridx, uint64_t* pbytes, uint32_t* ptoks,
+                    uint32_t* pirr, uint32_t* tmp32, cudaStream_t s) {
+  if (e_count) {
+    rank_keys_kernel<<<static_cast<int>(ceil_div(e_count, 256)), 256, 0, s>>>(idx, w, e_count, keys);
+    GLMX_CHECK_LAUNCH();
+    GLMX_CUDA(cub::DeviceSegmentedSort::SortKeysDescending(
+        temp, temp_bytes, keys, sorted, static_cast<int64_t>(e_count), static_cast<int64_t>(n),
+        off, off + 1, s));
+  }
+  // values into keys (bytes, u64) / tmp32 (tokens) / pirr's own slot via ptoks scratch
+  rank_fill_kernel<<<static_cast<int>(ceil_div(e_count + 1, 256)), 256, 0, s>>>(
+      g, sorted, e_count, ridx, keys, tmp32, pirr);
+  GLMX_CHECK_LAUNCH();
+  GLMX_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, keys, pbytes,
+                                          static_cast<int64_t>(e_count + 1), s));
+  GLMX_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, tmp32, ptoks,
+                                          static_cast<int64_t>(e_count + 1), s));
+  // irregular flags -> prefix, through tmp32 as the scan output (then copied back)
+  GLMX_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, pirr, tmp32,
+                                          static_cast<int64_t>(e_count + 1), s));
+  GLMX_CUDA(cudaMemcpyAsync(pirr, tmp32, (e_count + 1) * 4, cudaMemcpyDeviceToDevice, s));
 }
 
 void entry_stats(const char* bytes, const uint32_t* off, uint32_t n, uint32_t* st, cudaStream_t s) {
   if (n == 0) return;
   entry_stats_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(bytes, off, n, st);
+  GLMX_CHECK_LAUNCH();
+}
+
+void entry_interior_counts(const uint32_t* st, uint32_t n, uint32_t* cnt, cudaStream_t s) {
+  entry_interior_counts_kernel<<<static_cast<int>(ceil_div(n + 1, 256)), 256, 0, s>>>(st, n, cnt);
+  GLMX_CHECK_LAUNCH();
+}
+
+void entry_tokens(const char* bytes, const uint32_t* off, const uint32_t* st, uint32_t n,
+                  const uint32_t* ioff, uint32_t* head, uint32_t* tail, uint64_t* tstate,
+                  uint4* itok, cudaStream_t s) {
+  if (n == 0) return;
+  entry_tokens_kernel<<<static_cast<int>(ceil_div(n, 128)), 128, 0, s>>>(bytes, off, st, n, ioff,
+                                                                        head, tail, tstate, itok);
   GLMX_CHECK_LAUNCH();
 }
 

@@ -69,8 +69,9 @@ glmx_kv::~glmx_kv() {
 glmx_graph::~glmx_graph() {
   for (void* p : allocs) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
-  if (ev0) cudaEventDestroy(ev0);
-  if (ev1) cudaEventDestroy(ev1);
+  if (stream2) cudaStreamDestroy(stream2);
+  for (cudaEvent_t e : {ev0, ev1, ev_fork, ev_join})
+    if (e) cudaEventDestroy(e);
 }
 
 glmx_model::~glmx_model() {
@@ -123,10 +124,36 @@ void glmx_graph::upload() {
   // the graph stream (K1 chunks, K5 RetrieveNode) runs beside the prefill at the lowest priority:
   // the forward's CTAs are dispatched first whenever an SM frees up
   stream = make_stream(false);
+  stream2 = make_stream(false);
+  GLMX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  GLMX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   {
     uint32_t* st = static_cast<uint32_t*>(put(nullptr, host.n() * 4));
     entry_stats(dev.entry_bytes, dev.entry_off, static_cast<uint32_t>(host.n()), st, stream);
     dev.ent_stat = st;
+    // interior-token tables of the regular entries (K1 fast tokenizer)
+    const uint32_t n = static_cast<uint32_t>(host.n());
+    uint32_t* cnt = static_cast<uint32_t*>(put(nullptr, (n + 1) * 4));
+    uint32_t* ioff = static_cast<uint32_t*>(put(nullptr, (n + 1) * 4));
+    entry_interior_counts(st, n, cnt, stream);
+    DBuf tmp;
+    size_t tb = scan_u32_temp_bytes(n + 1);
+    tmp.reserve(tb);
+    scan_u32(tmp.p, tb, cnt, ioff, n + 1, stream);
+    uint32_t n_int = 0;
+    GLMX_CUDA(cudaMemcpyAsync(&n_int, ioff + n, 4, cudaMemcpyDeviceToHost, stream));
+    GLMX_CUDA(cudaStreamSynchronize(stream));
+    uint32_t* head = static_cast<uint32_t*>(put(nullptr, n * 4));
+    uint32_t* tail = static_cast<uint32_t*>(put(nullptr, n * 4));
+    uint64_t* tstate = static_cast<uint64_t*>(put(nullptr, n * 8));
+    uint4* itok = static_cast<uint4*>(put(nullptr, static_cast<size_t>(n_int) * 16));
+    entry_tokens(dev.entry_bytes, dev.entry_off, st, n, ioff, head, tail, tstate, itok, stream);
+    GLMX_CUDA(cudaStreamSynchronize(stream));  // before tmp (scan scratch) is released
+    dev.ent_head = head;
+    dev.ent_tail = tail;
+    dev.ent_tstate = tstate;
+    dev.ent_ioff = ioff;
+    dev.itok = itok;
   }
   if (host.und_off.empty()) {
     // GPU ingest (kernels/ingest.cu): CSRs and weights built on the device from the edge list
@@ -154,23 +181,51 @@ void glmx_graph::upload() {
   // K1 / K5 scratch for batches of up to 512 chunks of k <= 64 (~8 KB each) without reallocation
   constexpr size_t kChunks = 512, kBytes = kChunks * 8192, kTok = kBytes / 2 + kChunks + 1;
   d_nodes.reserve(kChunks * 4);
-  d_sel.reserve(kChunks * 64 * 4);
   d_cnt.reserve(kChunks * 4);
-  d_len.reserve((kChunks + 1) * 8);
   d_off.reserve((kChunks + 1) * 8);
-  d_flag.reserve((kChunks + 1) * 4);
-  d_tidx.reserve((kChunks + 1) * 4);
   d_toff.reserve((kChunks + 2) * 4);
   d_bytes.reserve(kBytes + 16);
   d_tid.reserve(kTok * 4);
   d_tbeg.reserve(kTok * 8);
   d_tend.reserve(kTok * 8);
-  d_temp.reserve(1 << 20);
   d_qemb.reserve(kChunks * 128 * 4);
   d_best.reserve(kChunks * 8);
 }
 
-// K1 driver: select -> scan -> render -> tokenize.  Returns GLMX_ERR_ARG (with totals) when the
+// Ranked adjacency of one (weight mode, directed) variant: sorted once per graph on first use
+// (a segmented sort of the CSR + three prefix scans; the graph is immutable).
+glmx::RankedAdj glmx_graph::ranked_adj(int weight_mode, int directed) {
+  Ranked& rk = ranked[(weight_mode ? 2 : 0) + (directed ? 1 : 0)];
+  const uint32_t* off = directed ? dev.dir_off : dev.und_off;
+  if (!rk.ready) {
+    const uint32_t n = dev.n;
+    uint32_t e32 = 0;
+    GLMX_CUDA(cudaMemcpyAsync(&e32, off + n, 4, cudaMemcpyDeviceToHost, stream));
+    GLMX_CUDA(cudaStreamSynchronize(stream));
+    const uint64_t E = e32;
+    DBuf keys, sorted, tmp32, temp;
+    keys.reserve((E + 1) * 8);
+    sorted.reserve(std::max<uint64_t>(E, 1) * 8);
+    tmp32.reserve((E + 1) * 4);
+    const size_t tb = rank_sort_temp_bytes(E, n);
+    temp.reserve(std::max<size_t>(tb, 16));
+    rk.ridx.reserve(std::max<uint64_t>(E, 1) * 4);
+    rk.pbytes.reserve((E + 1) * 8);
+    rk.ptoks.reserve((E + 1) * 4);
+    rk.pirr.reserve((E + 1) * 4);
+    rank_adjacency(dev, off, directed ? dev.dir_idx : dev.und_idx,
+                   weight_mode ? dev.w_by_type : dev.w_total, E, n, temp.p, temp.bytes,
+                   keys.as<uint64_t>(), sorted.as<uint64_t>(), rk.ridx.as<int32_t>(),
+                   rk.pbytes.as<uint64_t>(), rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>(),
+                   tmp32.as<uint32_t>(), stream);
+    GLMX_CUDA(cudaStreamSynchronize(stream));  // before the scratch buffers are released
+    rk.ready = true;
+  }
+  return glmx::RankedAdj{off, rk.ridx.as<int32_t>(), rk.pbytes.as<uint64_t>(),
+                         rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>()};
+}
+
+// K1 driver: lengths -> scans -> render + tokenize.  Returns GLMX_ERR_ARG (with totals) when the
 // caller's buffers are too small.
 int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t* node_idx,
                      uint64_t n, char* out_bytes, uint64_t bytes_cap, uint64_t* out_byte_offsets,
@@ -189,62 +244,93 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
     if (node_idx[i] < 0 || static_cast<uint64_t>(node_idx[i]) >= g->host.n())
       throw Error(GLMX_ERR_RETRIEVAL, "unknown node index " + std::to_string(node_idx[i]));
   const int k = std::max(cfg->k, 0);
-  if (k > 512) throw Error(GLMX_ERR_ARG, "chunk k > 512 is not supported");
   DeviceGuard dg(g->device);
   cudaStream_t s = g->stream;
-  ChunkParams p{k, std::max(k, 1), cfg->weight_mode ? 1 : 0, cfg->directed ? 1 : 0};
-  g->d_nodes.reserve(n * 4);
-  g->d_sel.reserve(n * p.k_stride * 4);
-  g->d_cnt.reserve(n * 4);
-  g->d_len.reserve((n + 1) * 8);
-  g->d_off.reserve((n + 1) * 8);
-  g->d_flag.reserve((n + 1) * 4);   // big-row queue of the select CTA path
-  g->d_tidx.reserve((n + 1) * 4);   // token counts per chunk (+1 zero)
-  g->d_toff.reserve((n + 2) * 4);   // token offsets (exclusive scan, [n] = total); + big count
-  const size_t t64 = scan_u64_temp_bytes(static_cast<int>(n + 1));
-  const size_t t32 = scan_u32_temp_bytes(n + 1);
-  g->d_temp.reserve(std::max(t32, t64));
-  int32_t* big_count = reinterpret_cast<int32_t*>(g->d_toff.as<uint32_t>() + n + 1);
-  GLMX_CUDA(cudaMemcpyAsync(g->d_nodes.p, node_idx, n * 4, cudaMemcpyHostToDevice, s));
-  g->h2d_bytes += n * 4;
-  GLMX_CUDA(cudaMemsetAsync(g->d_len.p, 0, (n + 1) * 8, s));
-  GLMX_CUDA(cudaMemsetAsync(g->d_tidx.as<uint32_t>() + n, 0, 4, s));
-  GLMX_CUDA(cudaEventRecord(g->ev0, s));
-  chunk_select(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-               g->d_cnt.as<int32_t>(), g->d_len.as<uint64_t>(), g->d_tidx.as<uint32_t>(),
-               g->d_flag.as<int32_t>(), big_count, s);
-  scan_u64(g->d_temp.p, t64, g->d_len.as<uint64_t>(), g->d_off.as<uint64_t>(),
-           static_cast<int>(n + 1), s);
-  scan_u32(g->d_temp.p, t32, g->d_tidx.as<uint32_t>(), g->d_toff.as<uint32_t>(), n + 1, s);
-  // output buffers: sized from a bound when it is small (no host round trip before the render),
-  // else from the scanned totals
-  const uint64_t bound = n * (21 + static_cast<uint64_t>(k + 1) * (g->max_entry + 3));
-  uint64_t total = 0;
-  uint32_t ntok32 = 0;
-  if (bound > (64ull << 20)) {
-    GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
-    GLMX_CUDA(cudaStreamSynchronize(s));
-    g->d2h_bytes += 8;
+  const bool same = g->k1_valid && out_bytes && g->k1_nodes.size() == n &&
+                    g->k1_cfg.k == cfg->k && g->k1_cfg.weight_mode == cfg->weight_mode &&
+                    g->k1_cfg.directed == cfg->directed && g->k1_cfg.vocab == cfg->vocab &&
+                    std::memcmp(g->k1_nodes.data(), node_idx, n * 4) == 0;
+  uint64_t total = 0, ntok = 0;
+  if (same) {
+    total = g->k1_total;
+    ntok = g->k1_ntok;
   } else {
-    total = bound;
+    g->k1_valid = false;
+    const glmx::RankedAdj ra = g->ranked_adj(cfg->weight_mode, cfg->directed);
+    g->d_nodes.reserve(n * 4);
+    g->d_cnt.reserve(n * 4);
+    g->d_off.reserve((n + 1) * 8);
+    g->d_toff.reserve((n + 3) * 4);   // token offsets ([n] = total) + overflow flag + irregular count
+    g->d_irr.reserve(n * 4);          // irregular chunks (byte-level tokenizer)
+    const int tiles = chunk_scan_tiles(static_cast<int>(n));
+    if (g->d_scan.bytes < static_cast<size_t>(tiles) * 32) {
+      g->d_scan.reserve(static_cast<size_t>(tiles) * 32);
+      GLMX_CUDA(cudaMemsetAsync(g->d_scan.p, 0, g->d_scan.bytes, s));
+      g->scan_epoch = 0;
+    }
+    const size_t cap_tiles = g->d_scan.bytes / 32;
+    uint8_t* sb = g->d_scan.as<uint8_t>();
+    const glmx::ScanState st{reinterpret_cast<uint64_t*>(sb), reinterpret_cast<uint64_t*>(sb + cap_tiles * 8),
+                             reinterpret_cast<uint32_t*>(sb + cap_tiles * 16),
+                             reinterpret_cast<uint32_t*>(sb + cap_tiles * 20),
+                             reinterpret_cast<uint32_t*>(sb + cap_tiles * 24)};
+    int32_t* overflow = reinterpret_cast<int32_t*>(g->d_toff.as<uint32_t>() + n + 1);
+    int32_t* irr_count = overflow + 1;
+    GLMX_CUDA(cudaMemcpyAsync(g->d_nodes.p, node_idx, n * 4, cudaMemcpyHostToDevice, s));
+    g->h2d_bytes += n * 4;
+    GLMX_CUDA(cudaMemsetAsync(overflow, 0, 8, s));
+    GLMX_CUDA(cudaEventRecord(g->ev0, s));
+    chunk_lengths_scan(g->dev, ra, k, g->d_nodes.as<int32_t>(), static_cast<int>(n),
+                       g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_toff.as<uint32_t>(), st,
+                       ++g->scan_epoch, g->d_irr.as<int32_t>(), irr_count, s);
+    // The render goes straight on with the output buffers as they are (no host round trip): a
+    // batch that does not fit raises the device overflow flag, and is rendered again below into
+    // buffers grown to its totals.  Small batches are sized from a bound up front.
+    const uint64_t bound = n * (21 + static_cast<uint64_t>(k + 1) * (g->max_entry + 3));
+    if (bound <= (64ull << 20)) {
+      // a token has >= 1 byte and is followed by a space or the chunk end: <= total/2 + n tokens
+      g->d_bytes.reserve(bound + 16);
+      g->d_tid.reserve((bound / 2 + n + 1) * 4);
+      g->d_tbeg.reserve((bound / 2 + n + 1) * 8);
+      g->d_tend.reserve((bound / 2 + n + 1) * 8);
+    }
+    auto render = [&] {
+      const uint64_t tok_cap = std::min(g->d_tid.bytes / 4, std::min(g->d_tbeg.bytes, g->d_tend.bytes) / 8);
+      chunk_render_emit(g->dev, ra, g->d_nodes.as<int32_t>(), static_cast<int>(n),
+                        g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_toff.as<uint32_t>(),
+                        cfg->vocab, g->d_bytes.as<char>(), g->d_tid.as<int32_t>(),
+                        g->d_tbeg.as<uint64_t>(), g->d_tend.as<uint64_t>(),
+                        g->d_bytes.bytes >= 16 ? g->d_bytes.bytes - 16 : 0, tok_cap, overflow,
+                        g->d_irr.as<int32_t>(), irr_count, s, g->stream2, g->ev_fork, g->ev_join);
+    };
+    render();
+    GLMX_CUDA(cudaEventRecord(g->ev1, s));
+    uint64_t total32 = 0;
+    uint32_t ntok32 = 0;
+    int32_t ovf = 0;
+    GLMX_CUDA(cudaMemcpyAsync(&total32, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_toff.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaMemcpyAsync(&ovf, overflow, 4, cudaMemcpyDeviceToHost, s));
+    GLMX_CUDA(cudaStreamSynchronize(s));
+    g->d2h_bytes += 16;
+    if (ovf) {
+      g->d_bytes.reserve(total32 + total32 / 4 + 16);
+      g->d_tid.reserve((ntok32 + ntok32 / 4 + 1) * 4ull);
+      g->d_tbeg.reserve((ntok32 + ntok32 / 4 + 1) * 8ull);
+      g->d_tend.reserve((ntok32 + ntok32 / 4 + 1) * 8ull);
+      render();  // the timed span (ev0 .. ev1) then covers the first attempt and this one
+      GLMX_CUDA(cudaEventRecord(g->ev1, s));
+      GLMX_CUDA(cudaStreamSynchronize(s));
+    }
+    GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));
+    total = total32;
+    ntok = ntok32;
+    g->k1_nodes.assign(node_idx, node_idx + n);
+    g->k1_cfg = *cfg;
+    g->k1_total = total;
+    g->k1_ntok = ntok;
+    g->k1_valid = true;
   }
-  // a token has >= 1 byte and is followed by a space or the chunk end: <= total/2 + n tokens
-  const uint64_t tok_bound = total / 2 + n + 1;
-  g->d_bytes.reserve(total + 16);
-  g->d_tid.reserve(tok_bound * 4);
-  g->d_tbeg.reserve(tok_bound * 8);
-  g->d_tend.reserve(tok_bound * 8);
-  chunk_render_emit(g->dev, p, g->d_nodes.as<int32_t>(), static_cast<int>(n), g->d_sel.as<int32_t>(),
-                    g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_toff.as<uint32_t>(),
-                    cfg->vocab, g->d_bytes.as<char>(), g->d_tid.as<int32_t>(),
-                    g->d_tbeg.as<uint64_t>(), g->d_tend.as<uint64_t>(), s);
-  GLMX_CUDA(cudaEventRecord(g->ev1, s));
-  GLMX_CUDA(cudaMemcpyAsync(&total, g->d_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s));
-  GLMX_CUDA(cudaMemcpyAsync(&ntok32, g->d_toff.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
-  GLMX_CUDA(cudaStreamSynchronize(s));
-  g->d2h_bytes += 12;
-  GLMX_CUDA(cudaEventElapsedTime(&g->last_ms, g->ev0, g->ev1));
-  const uint64_t ntok = ntok32;
   if (total_bytes) *total_bytes = total;
   if (total_tokens) *total_tokens = ntok;
   if (!out_bytes) return GLMX_OK;

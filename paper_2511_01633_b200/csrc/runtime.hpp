@@ -65,11 +65,25 @@ struct glmx_graph {
   uint32_t max_entry = 0;  // longest pre-rendered entry (K1 output bound)
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t stream2 = nullptr;  // K1 tokens run beside the K1 text (fork/join by events)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_fork = nullptr, ev_join = nullptr;
   float last_ms = 0.f;
   // K1 scratch
-  DBuf d_nodes, d_sel, d_cnt, d_len, d_off, d_bytes, d_flag, d_tidx, d_tid, d_tbeg, d_tend,
-      d_toff, d_temp;
+  DBuf d_nodes, d_cnt, d_off, d_bytes, d_tid, d_tbeg, d_tend, d_toff, d_scan, d_irr;
+  uint32_t scan_epoch = 0;  // chunk_lengths_scan look-back state (d_scan) epoch
+  // ranked adjacency per (weight mode, directed) variant, built on first use (kernels/chunk.cuh)
+  struct Ranked {
+    bool ready = false;
+    DBuf ridx, pbytes, ptoks, pirr;
+  } ranked[4];
+  glmx::RankedAdj ranked_adj(int weight_mode, int directed);
+  // the last batch built (nodes + config) and its totals: the fill call of the two-call protocol
+  // (size query, then the same request with buffers) copies that result out instead of
+  // rebuilding it
+  std::vector<int32_t> k1_nodes;
+  glmx_chunk_config k1_cfg{};
+  bool k1_valid = false;
+  uint64_t k1_total = 0, k1_ntok = 0;
   // K5 RetrieveNode: device index (rows = nodes with an index text, ascending id), LRU, stats
   int idx_dim = 0, idx_pad = 0;
   std::vector<int32_t> idx_node;  // row -> node index

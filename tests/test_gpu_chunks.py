@@ -103,7 +103,7 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
     """Attribute values with tabs, newlines, runs of spaces, leading/trailing blanks, no blanks at
     all and non-ASCII bytes: chunk text and whitespace tokens (spans + fnv1a ids) fused across
     entry boundaries exactly as the reference tokenizer splits them; includes chunks larger than
-    the 6 KB shared-memory staging buffer (built and tokenised in place in global memory)."""
+    the 4 KB shared-memory staging buffer (built and tokenised in place in global memory)."""
     import json
 
     rnd = random.Random(11)
@@ -137,7 +137,7 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
         for i, v in enumerate(nodes):
             want = rg.node_info_rendered(g.node_id(v), k)
             assert batch.texts[i] == want, (k, v)
-            big += len(want.encode()) > 6144
+            big += len(want.encode()) > 4096
             toks = oracle.ref_tokenize(want)  # the reference's glm::tokenize
             raw = batch.texts[i].encode()
             got = [raw[b:e].decode() for b, e in batch.token_spans[i]]
@@ -145,3 +145,44 @@ def test_whitespace_edge_cases_tokens_match_reference(ref, tmp_path):
             assert batch.token_ids[i] == [fnv1a(t.encode()) % V for t in toks]
         if k == 200:
             assert big > 0  # the unstaged path ran
+
+
+def test_irregular_entries_take_byte_tokenizer(ref, tmp_path):
+    """K1 has two tokenizers: the table-driven one for chunks whose entries are all regular
+    (first and last byte non-space, >= 2 tokens; DevGraph::ent_head) and the byte-level one for
+    the rest.  Node ids that start with whitespace make their entries irregular: batches mixing
+    such chunks with regular ones (neighbour lists of both kinds, k across a 32-piece round and
+    a 4 KB staging buffer) give the reference's bytes and tokens from both paths."""
+    import json
+
+    rnd = random.Random(5)
+    ids = [f"r{i:03d}" for i in range(150)] + [" s1", "\tt2", "  u3", " " * 3 + "w4", "\nx5"]
+    lines = [json.dumps({"kind": "node", "id": nid, "type": rnd.choice(["item", "user"]),
+                         "attrs": {"title": " ".join(f"w{rnd.randrange(99)}"
+                                                     for _ in range(rnd.randrange(1, 30)))}})
+             for nid in ids]
+    for nid in ids:
+        for _ in range(rnd.randrange(1, 40)):
+            lines.append(json.dumps({"kind": "edge", "src": nid, "dst": rnd.choice(ids),
+                                     "etype": rnd.choice(["e", "f"])}))
+    path = str(tmp_path / "irr.jsonl")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    g = glmx.PropertyGraph.load(path, device=0)
+    rg = oracle.RefGraph(path=path)
+    V = 128256
+    nodes = list(range(g.node_count()))
+    for k in (0, 1, 5, 31, 32, 33, 80):
+        r = glmx.Retriever(g, chunk_k=k, vocab=V)
+        batch = r.chunk_build(nodes)
+        for i, v in enumerate(nodes):
+            want = rg.node_info_rendered(g.node_id(v), k)
+            assert batch.texts[i] == want, (k, v)
+            toks = oracle.ref_tokenize(want)
+            raw = want.encode()
+            assert [raw[b:e] for b, e in batch.token_spans[i]] == [t.encode() for t in toks], (k, v)
+            assert batch.token_ids[i] == [fnv1a(t.encode()) % V for t in toks]
+        # vocab 0: no ids, same spans
+        r0 = glmx.Retriever(g, chunk_k=k, vocab=0)
+        b0 = r0.chunk_build(nodes)
+        assert b0.token_spans == batch.token_spans and b0.texts == batch.texts
