@@ -10,15 +10,22 @@
 //   entry tokens     : per regular entry (first and last byte non-space, >= 2 tokens) the spans
 //                      and fnv1a hashes of its interior tokens, its first-token length and its
 //                      last token's offset + fnv1a state
-// Per batch (chunk_build): one thread per chunk computes (k', byte length, token count, regular)
-// from the prefixes -> two exclusive scans -> one WARP per chunk renders and tokenises:
-//   render  : lane s copies piece s ("[Node:" E_v / "(" E_j ")" with "," separators) into a
-//             per-warp shared-memory buffer at the 16-byte phase of its global destination with
-//             4-byte funnel-shifted stores; the buffer goes out as 16-byte stores.
-//   tokenize: regular chunks take the table-driven tokenizer (emit_fast: only the k + 3 junction
-//             tokens are hashed; interior tokens are copied from the tables), others the byte
-//             level one (whitespace ballots + per-token fnv1a).  Tokens fuse across entry
-//             boundaries exactly as in the text ("[neighbours:(n3", "type:item}),(u1").
+// Per batch (chunk_build):
+//   chunk_len_scan : one thread per chunk computes (k', byte length, token count, regular flag)
+//                    from the prefixes; both exclusive scans in the same single-pass kernel
+//                    (warp-cooperative decoupled look-back); irregular chunks compacted to a list
+//   chunk_regular  : CTA = 4 text warps + 4 token warps for 4 chunks.  Text: per round of 32
+//                    pieces the 16-byte source words are numbered by a warp scan, each lane finds
+//                    its piece by a shuffle binary search, realigns the words to the destination
+//                    with funnel shifts and stores them whole (the separator bytes framing each
+//                    entry are merged into its edge words), into a per-warp smem buffer at the
+//                    destination's 16-byte phase, then 16-byte stores.  Tokens (emit_fast): the
+//                    k + 3 junction tokens hashed from the neighbouring entries' precomputed
+//                    states over the separator and first-token bytes; interior tokens copied from
+//                    the tables (ids precomputed per vocab).
+//   chunk_irregular: a small grid over the irregular list: byte-level tokenizer over a whitespace
+//                    mask (per-token fnv1a).
+// Tokens fuse across entry boundaries exactly as in the text ("[neighbours:(n3", "type:item}),(u1").
 // All of it is integer/byte work: HBM/latency bound, no tensor cores.
 #include <cub/cub.cuh>
 
@@ -53,6 +60,7 @@ struct ChunkLen {
   uint64_t bytes;
   uint32_t toks;
   uint32_t sel;
+  uint32_t row;
 };
 __device__ __forceinline__ ChunkLen chunk_len(const DevGraph& g, const RankedAdj& ra, int k,
                                               int32_t v) {
@@ -66,6 +74,7 @@ __device__ __forceinline__ ChunkLen chunk_len(const DevGraph& g, const RankedAdj
   c.toks = piece_tokens(sv) + 2 + (ra.ptoks[row + kk] - ra.ptoks[row]);
   const bool irregular = !entry_regular(sv) || ra.pirr[row + kk] != ra.pirr[row];
   c.sel = kk | (irregular ? 0x80000000u : 0u);
+  c.row = row;
   return c;
 }
 
@@ -80,7 +89,8 @@ __global__ void __launch_bounds__(kLenThreads)
 chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict__ node_idx,
                       int n_req, int32_t* __restrict__ sel_count, uint64_t* __restrict__ byte_off,
                       uint32_t* __restrict__ tok_off, ScanState st, uint32_t epoch,
-                      int32_t* __restrict__ irr_list, int32_t* __restrict__ irr_count) {
+                      int32_t* __restrict__ irr_list, int32_t* __restrict__ irr_count,
+                      int2* __restrict__ vrow) {
   using BS64 = cub::BlockScan<uint64_t, kLenThreads>;
   using BS32 = cub::BlockScan<uint32_t, kLenThreads>;
   __shared__ typename BS64::TempStorage t64;
@@ -90,12 +100,17 @@ chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict
   const int tile = blockIdx.x;
   const int r0 = tile * kLenTile + threadIdx.x * kLenItems;
   ChunkLen c[kLenItems];
+  int32_t vv[kLenItems];
   uint64_t sb = 0;
   uint32_t stk = 0;
 #pragma unroll
   for (int i = 0; i < kLenItems; ++i) {
-    c[i] = ChunkLen{0, 0, 0};
-    if (r0 + i < n_req) c[i] = chunk_len(g, ra, k, node_idx[r0 + i]);
+    c[i] = ChunkLen{0, 0, 0, 0};
+    vv[i] = 0;
+    if (r0 + i < n_req) {
+      vv[i] = node_idx[r0 + i];
+      c[i] = chunk_len(g, ra, k, vv[i]);
+    }
     sb += c[i].bytes;
     stk += c[i].toks;
   }
@@ -166,6 +181,7 @@ chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict
       byte_off[r] = ob;
       tok_off[r] = ot;
       sel_count[r] = static_cast<int32_t>(c[i].sel);
+      vrow[r] = make_int2(vv[i], static_cast<int32_t>(c[i].row));
       if (c[i].sel >> 31) irr_list[atomicAdd(irr_count, 1)] = r;
     }
     ob += c[i].bytes;
@@ -217,7 +233,7 @@ __global__ void rank_fill_kernel(DevGraph g, const uint64_t* __restrict__ sorted
 constexpr int kRW = 4;         // warps (chunks) per CTA
 constexpr int kBuf = 4096;     // staged chunk bytes per warp
 constexpr int kSeg = 1024;     // bytes per token-start compaction segment
-constexpr int kWordsU = 2;     // 16-byte loads in flight per lane (2: 48 registers, 10 CTAs/SM)
+constexpr int kWordsU = 2;     // 16-byte loads in flight per lane
 
 // h % vocab for a 64-bit h by Barrett reduction with m = floor((2^64 - 1) / vocab): the estimate
 // q = hi64(h * m) is at most 2 below the true quotient.
@@ -350,9 +366,9 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
       len = ec;
       dst = 6;
     } else if (s <= k) {
-      const int32_t u = mine[s - 1];
-      src = g.entry_off[u];
-      len = g.entry_off[u + 1] - src;
+      const uint2 ol = __ldg(reinterpret_cast<const uint2*>(g.ent + mine[s - 1]));  // (off, len)
+      src = ol.x;
+      len = ol.y;
       plen = len + 2 + (s > 1 ? 1u : 0u);
     }
     uint32_t pincl = plen;
@@ -460,7 +476,7 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
                                           const int32_t* __restrict__ mine, uint32_t n, uint32_t t,
                                           uint32_t vocab, uint64_t vmagic, int32_t* tok_id,
                                           uint64_t* tok_begin, uint64_t* tok_end, int lane) {
-  const uint32_t ev = g.entry_off[v], lv = g.entry_off[v + 1] - ev;
+  const uint32_t lv = g.entry_off[v + 1] - g.entry_off[v];
   uint32_t prev_dst = 0, prev_tail = 0;
   uint64_t prev_ts = 0;
   uint32_t o = 6 + lv + 14;  // byte offset of the next neighbour piece
@@ -468,14 +484,16 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
   for (int s0 = 0; s0 <= k; s0 += 32) {
     const int s = s0 + lane;
     const bool act = s <= k;
-    int32_t u = v;
-    uint32_t eo = ev, len = lv, dst = 6, plen = 0;
-    if (act && s > 0) {
-      u = mine[s - 1];
-      eo = g.entry_off[u];
-      len = g.entry_off[u + 1] - eo;
-      plen = len + 2 + (s > 1 ? 1u : 0u);
+    // the piece's entry record: two 16-byte loads of one 32-byte line
+    uint4 ra4 = make_uint4(0, 0, 0, 0), rb4 = make_uint4(0, 0, 0, 0);
+    if (act) {
+      const uint4* rp = reinterpret_cast<const uint4*>(g.ent + (s > 0 ? mine[s - 1] : v));
+      ra4 = __ldg(rp);
+      rb4 = __ldg(rp + 1);
     }
+    const uint32_t eo = ra4.x, len = ra4.y;
+    uint32_t dst = 6, plen = 0;
+    if (act && s > 0) plen = len + 2 + (s > 1 ? 1u : 0u);
     uint32_t pincl = plen;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -484,15 +502,8 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
     }
     if (s > 0) dst = o + (pincl - plen) + (s > 1 ? 2u : 1u);
     o += __shfl_sync(0xffffffffu, pincl, 31);
-    uint32_t hl = 0, tl = 0, io = 0, ni = 0;
-    uint64_t ts = 0;
-    if (act) {
-      hl = g.ent_head[u];
-      tl = g.ent_tail[u];
-      ts = g.ent_tstate[u];
-      io = g.ent_ioff[u];
-      ni = g.ent_ioff[u + 1] - io;
-    }
+    const uint32_t hl = ra4.z, tl = ra4.w, io = rb4.x, ni = rb4.y;
+    const uint64_t ts = (static_cast<uint64_t>(rb4.w) << 32) | rb4.z;
     const uint32_t grp = act ? ni + (s == 0 ? 2u : 1u) : 0u;
     uint32_t gin = grp, iin = ni;
 #pragma unroll
@@ -545,8 +556,8 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
     // interior tokens of the round's pieces, lanes striding over them (two per lane per
     // iteration: both record loads are in flight before the stores)
     for (uint32_t i0 = 0; i0 < itot; i0 += 64) {
-      uint32_t jj[2], qg[2], qd[2];
-      uint4 rec[2];
+      uint32_t jj[2], qg[2], qd[2], id[2];
+      uint2 sp[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t i = i0 + 32 * h + lane;
@@ -561,14 +572,19 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
         qg[h] = __shfl_sync(0xffffffffu, gex, q);
         qd[h] = __shfl_sync(0xffffffffu, dst, q);
         jj[h] = i - qiex;
-        rec[h] = i < itot ? __ldg(g.itok + qio + jj[h]) : make_uint4(0, 0, 0, 0);
+        const bool in = i < itot;
+        sp[h] = in ? __ldg(g.itok_span + qio + jj[h]) : make_uint2(0, 0);
+        id[h] = in && vocab ? __ldg(g.itok_id + qio + jj[h]) : 0u;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (i0 + 32 * h + lane < itot)
-          put_token(tb + qg[h] + 1 + jj[h], qd[h] + rec[h].x, qd[h] + rec[h].y,
-                    (static_cast<uint64_t>(rec[h].w) << 32) | rec[h].z, vocab, vmagic, tok_id,
-                    tok_begin, tok_end);
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t o = tb + qg[h] + 1 + jj[h];
+        if (i0 + 32 * h + lane < itot) {
+          tok_begin[o] = qd[h] + sp[h].x;
+          tok_end[o] = qd[h] + sp[h].y;
+          if (vocab) tok_id[o] = static_cast<int32_t>(id[h]);
+        }
+      }
     }
     tb += gtot;
     prev_dst = __shfl_sync(0xffffffffu, dst, 31);
@@ -577,7 +593,7 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
   }
 }
 
-// Text of a regular chunk (its tokens come from chunk_tokens_kernel).
+// Text of a regular chunk (its tokens come from emit_fast in the same CTA's token warps).
 __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
                                             const int32_t* __restrict__ mine, uint64_t goff,
                                             uint32_t n, char* __restrict__ out, char* sb, int lane) {
@@ -703,40 +719,32 @@ __device__ __forceinline__ void render_slow(const DevGraph& g, int32_t v, int k,
   }
 }
 
-// Regular chunks (kIrr = false): one warp per chunk renders the text, at high occupancy (no
-// whitespace mask).  Irregular chunks (kIrr = true): a small grid walks the list the scan kernel
-// compacted and runs the byte-level path.  Output capacity overflow: see chunk_render_emit.
-template <bool kIrr>
-__global__ void __launch_bounds__(kRW * 32, kIrr ? 7 : 10)
-chunk_render_kernel(DevGraph g, RankedAdj ra, const int32_t* __restrict__ node_idx, int n_req,
-                    const int32_t* __restrict__ sel_count, const uint64_t* __restrict__ byte_off,
-                    const uint32_t* __restrict__ tok_off, uint32_t vocab, uint64_t vmagic,
-                    char* __restrict__ out, int32_t* __restrict__ tok_id,
-                    uint64_t* __restrict__ tok_begin, uint64_t* __restrict__ tok_end,
-                    uint64_t bytes_cap, uint64_t tok_cap, int32_t* __restrict__ overflow,
-                    const int32_t* __restrict__ irr_list, const int32_t* __restrict__ irr_count) {
+// Irregular chunks: a small grid walks the list chunk_len_scan compacted and runs the
+// byte-level path (text + tokens over a whitespace mask).  Output capacity overflow: see
+// chunk_render_emit.
+__global__ void __launch_bounds__(kRW * 32)
+chunk_irregular_kernel(DevGraph g, RankedAdj ra, const uint64_t* __restrict__ byte_off,
+                       const uint32_t* __restrict__ tok_off, const int32_t* __restrict__ sel_count,
+                       uint32_t vocab, uint64_t vmagic, char* __restrict__ out,
+                       int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
+                       uint64_t* __restrict__ tok_end, uint64_t bytes_cap, uint64_t tok_cap,
+                       int32_t* __restrict__ overflow, const int32_t* __restrict__ irr_list,
+                       const int32_t* __restrict__ irr_count, const int2* __restrict__ vrow) {
   __shared__ __align__(16) char sbuf[kRW][kBuf + 16];
-  __shared__ uint32_t smask[kIrr ? kRW : 1][kIrr ? kBuf / 32 + 1 : 1];
+  __shared__ uint32_t smask[kRW][kBuf / 32 + 1];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int n_items = kIrr ? *irr_count : n_req;
+  const int n_items = *irr_count;
   for (int i = blockIdx.x * kRW + wi; i < n_items; i += gridDim.x * kRW) {
-    const int r = kIrr ? irr_list[i] : i;
+    const int r = irr_list[i];
     const uint64_t goff = byte_off[r], gend = byte_off[r + 1];
     if (gend > bytes_cap || tok_off[r + 1] > tok_cap) {  // the host grows the buffers and reruns
       if (lane == 0) *overflow = 1;
       continue;
     }
-    const uint32_t kr = static_cast<uint32_t>(sel_count[r]);
-    if (!kIrr && (kr >> 31)) continue;
-    const int32_t v = node_idx[r];
-    const int k = static_cast<int>(kr & 0x7FFFFFFFu);
-    const int32_t* mine = ra.idx + ra.off[v];  // the top-k are the first k of the ranked row
-    const uint32_t n = static_cast<uint32_t>(gend - goff);
-    if constexpr (kIrr)
-      render_slow(g, v, k, mine, goff, n, tok_off[r], vocab, vmagic, out, tok_id, tok_begin,
-                  tok_end, sbuf[wi], smask[wi], lane);
-    else
-      render_text(g, v, k, mine, goff, n, out, sbuf[wi], lane);
+    const int2 vr = vrow[r];  // node, first entry of its ranked row (chunk_len_scan)
+    const int k = static_cast<int>(static_cast<uint32_t>(sel_count[r]) & 0x7FFFFFFFu);
+    render_slow(g, vr.x, k, ra.idx + vr.y, goff, static_cast<uint32_t>(gend - goff), tok_off[r],
+                vocab, vmagic, out, tok_id, tok_begin, tok_end, sbuf[wi], smask[wi], lane);
   }
 }
 
@@ -776,7 +784,7 @@ __global__ void entry_tokens_kernel(const char* __restrict__ bytes, const uint32
                                     const uint32_t* __restrict__ st, uint32_t n,
                                     const uint32_t* __restrict__ ioff, uint32_t* __restrict__ head,
                                     uint32_t* __restrict__ tail, uint64_t* __restrict__ tstate,
-                                    uint4* __restrict__ itok) {
+                                    uint2* __restrict__ itok_span, uint64_t* __restrict__ itok_hash) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (!entry_regular(st[i])) {
@@ -803,41 +811,94 @@ __global__ void entry_tokens_kernel(const char* __restrict__ bytes, const uint32
       tail[i] = t0 - b;
       tstate[i] = h;
     } else {
-      itok[o++] = make_uint4(t0 - b, q - b, static_cast<uint32_t>(h), static_cast<uint32_t>(h >> 32));
+      itok_span[o] = make_uint2(t0 - b, q - b);
+      itok_hash[o++] = h;
     }
     ++tok;
   }
 }
-// Tokens of the regular chunks (the table-driven tokenizer, no shared memory): a separate
-// kernel from the text so that each runs at its own occupancy.
-__global__ void __launch_bounds__(128, 12)
-chunk_tokens_kernel(DevGraph g, RankedAdj ra, const int32_t* __restrict__ node_idx, int n_req,
-                    const int32_t* __restrict__ sel_count, const uint64_t* __restrict__ byte_off,
-                    const uint32_t* __restrict__ tok_off, uint32_t vocab, uint64_t vmagic,
-                    int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
-                    uint64_t* __restrict__ tok_end, uint64_t bytes_cap, uint64_t tok_cap) {
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
+__global__ void entry_records_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ head,
+                                     const uint32_t* __restrict__ tail, const uint64_t* __restrict__ tstate,
+                                     const uint32_t* __restrict__ ioff, uint32_t n,
+                                     EntryRec* __restrict__ rec) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  EntryRec r;
+  r.off = off[i];
+  r.len = off[i + 1] - r.off;
+  r.head = head[i];
+  r.tail = tail[i];
+  r.ioff = ioff[i];
+  r.ni = ioff[i + 1] - r.ioff;
+  r.tstate = tstate[i];
+  rec[i] = r;
+}
+
+__global__ void token_ids_kernel(const uint64_t* __restrict__ hash, uint32_t n, uint32_t vocab,
+                                 uint64_t vmagic, uint32_t* __restrict__ ids) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = mod_vocab(hash[i], vocab, vmagic);
+}
+
+// Regular chunks, text and tokens in one launch: warps 0-3 of a CTA render the text of chunks
+// 4b..4b+3 (render_text), warps 4-7 emit their tokens (emit_fast), so the two halves of a chunk
+// run side by side on every SM.
+__global__ void __launch_bounds__(2 * kRW * 32, 5)
+chunk_regular_kernel(DevGraph g, RankedAdj ra, int n_req, const int32_t* __restrict__ sel_count,
+                     const uint64_t* __restrict__ byte_off, const uint32_t* __restrict__ tok_off,
+                     uint32_t vocab, uint64_t vmagic, char* __restrict__ out,
+                     int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
+                     uint64_t* __restrict__ tok_end, uint64_t bytes_cap, uint64_t tok_cap,
+                     int32_t* __restrict__ overflow, const int2* __restrict__ vrow) {
+  __shared__ __align__(16) char sbuf[kRW][kBuf + 16];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const bool text = wi < kRW;
+  const int r = blockIdx.x * kRW + (text ? wi : wi - kRW);
   if (r >= n_req) return;
-  const uint32_t kr = static_cast<uint32_t>(sel_count[r]);
-  if (kr >> 31) return;  // irregular: tokenised by the render kernel
   const uint64_t goff = byte_off[r], gend = byte_off[r + 1];
-  if (gend > bytes_cap || tok_off[r + 1] > tok_cap) return;  // overflow: rerun after growing
-  const int32_t v = node_idx[r];
-  emit_fast(g, v, static_cast<int>(kr), ra.idx + ra.off[v], static_cast<uint32_t>(gend - goff),
-            tok_off[r], vocab, vmagic, tok_id, tok_begin, tok_end, lane);
+  if (gend > bytes_cap || tok_off[r + 1] > tok_cap) {  // the host grows the buffers and reruns
+    if (lane == 0) *overflow = 1;
+    return;
+  }
+  const uint32_t kr = static_cast<uint32_t>(sel_count[r]);
+  if (kr >> 31) return;  // irregular: chunk_irregular_kernel
+  const int2 vr = vrow[r];
+  const int k = static_cast<int>(kr);
+  const uint32_t n = static_cast<uint32_t>(gend - goff);
+  if (text)
+    render_text(g, vr.x, k, ra.idx + vr.y, goff, n, out, sbuf[wi], lane);
+  else
+    emit_fast(g, vr.x, k, ra.idx + vr.y, n, tok_off[r], vocab, vmagic, tok_id, tok_begin, tok_end,
+              lane);
 }
 
 }  // namespace
+
+void entry_records(const uint32_t* off, const uint32_t* head, const uint32_t* tail,
+                   const uint64_t* tstate, const uint32_t* ioff, uint32_t n, EntryRec* rec,
+                   cudaStream_t s) {
+  if (n == 0) return;
+  entry_records_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(off, head, tail, tstate,
+                                                                          ioff, n, rec);
+  GLMX_CHECK_LAUNCH();
+}
+
+void chunk_token_ids(const uint64_t* hash, uint32_t n, uint32_t vocab, uint32_t* ids,
+                     cudaStream_t s) {
+  if (n == 0 || vocab == 0) return;
+  token_ids_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(hash, n, vocab,
+                                                                      ~uint64_t(0) / vocab, ids);
+  GLMX_CHECK_LAUNCH();
+}
 
 int chunk_scan_tiles(int n_req) { return static_cast<int>(ceil_div(n_req, kLenTile)); }
 
 void chunk_lengths_scan(const DevGraph& g, const RankedAdj& ra, int k, const int32_t* node_idx,
                         int n_req, int32_t* sel_count, uint64_t* byte_off, uint32_t* tok_off,
                         const ScanState& st, uint32_t epoch, int32_t* irr_list, int32_t* irr_count,
-                        cudaStream_t s) {
+                        int2* vrow, cudaStream_t s) {
   chunk_len_scan_kernel<<<chunk_scan_tiles(n_req), kLenThreads, 0, s>>>(
-      g, ra, k, node_idx, n_req, sel_count, byte_off, tok_off, st, epoch, irr_list, irr_count);
+      g, ra, k, node_idx, n_req, sel_count, byte_off, tok_off, st, epoch, irr_list, irr_count, vrow);
   GLMX_CHECK_LAUNCH();
 }
 
@@ -845,25 +906,17 @@ void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* no
                        const int32_t* sel_count, const uint64_t* byte_off, const uint32_t* tok_off,
                        uint32_t vocab, char* out, int32_t* tok_id, uint64_t* tok_begin,
                        uint64_t* tok_end, uint64_t bytes_cap, uint64_t tok_cap, int32_t* overflow,
-                       const int32_t* irr_list, const int32_t* irr_count, cudaStream_t s,
-                       cudaStream_t s2, cudaEvent_t fork, cudaEvent_t join) {
+                       const int32_t* irr_list, const int32_t* irr_count, const int2* vrow,
+                       cudaStream_t s) {
   const uint64_t vmagic = vocab ? ~uint64_t(0) / vocab : 0;
-  GLMX_CUDA(cudaEventRecord(fork, s));
-  GLMX_CUDA(cudaStreamWaitEvent(s2, fork, 0));
-  chunk_tokens_kernel<<<static_cast<int>(ceil_div(n_req, 4)), 128, 0, s2>>>(
-      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, tok_id, tok_begin,
-      tok_end, bytes_cap, tok_cap);
+  chunk_regular_kernel<<<static_cast<int>(ceil_div(n_req, kRW)), 2 * kRW * 32, 0, s>>>(
+      g, ra, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin, tok_end,
+      bytes_cap, tok_cap, overflow, vrow);
   GLMX_CHECK_LAUNCH();
-  chunk_render_kernel<false><<<static_cast<int>(ceil_div(n_req, kRW)), kRW * 32, 0, s>>>(
-      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin,
-      tok_end, bytes_cap, tok_cap, overflow, irr_list, irr_count);
+  chunk_irregular_kernel<<<2 * kNumSMs, kRW * 32, 0, s>>>(
+      g, ra, byte_off, tok_off, sel_count, vocab, vmagic, out, tok_id, tok_begin, tok_end,
+      bytes_cap, tok_cap, overflow, irr_list, irr_count, vrow);
   GLMX_CHECK_LAUNCH();
-  chunk_render_kernel<true><<<2 * kNumSMs, kRW * 32, 0, s>>>(
-      g, ra, node_idx, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin,
-      tok_end, bytes_cap, tok_cap, overflow, irr_list, irr_count);
-  GLMX_CHECK_LAUNCH();
-  GLMX_CUDA(cudaEventRecord(join, s2));
-  GLMX_CUDA(cudaStreamWaitEvent(s, join, 0));
 }
 
 size_t rank_sort_temp_bytes(uint64_t e_count, uint32_t n) {
@@ -919,10 +972,11 @@ void entry_interior_counts(const uint32_t* st, uint32_t n, uint32_t* cnt, cudaSt
 
 void entry_tokens(const char* bytes, const uint32_t* off, const uint32_t* st, uint32_t n,
                   const uint32_t* ioff, uint32_t* head, uint32_t* tail, uint64_t* tstate,
-                  uint4* itok, cudaStream_t s) {
+                  uint2* itok_span, uint64_t* itok_hash, cudaStream_t s) {
   if (n == 0) return;
   entry_tokens_kernel<<<static_cast<int>(ceil_div(n, 128)), 128, 0, s>>>(bytes, off, st, n, ioff,
-                                                                        head, tail, tstate, itok);
+                                                                        head, tail, tstate, itok_span,
+                                                                        itok_hash);
   GLMX_CHECK_LAUNCH();
 }
 

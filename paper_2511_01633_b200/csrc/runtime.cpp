@@ -69,9 +69,8 @@ glmx_kv::~glmx_kv() {
 glmx_graph::~glmx_graph() {
   for (void* p : allocs) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
-  if (stream2) cudaStreamDestroy(stream2);
-  for (cudaEvent_t e : {ev0, ev1, ev_fork, ev_join})
-    if (e) cudaEventDestroy(e);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
 }
 
 glmx_model::~glmx_model() {
@@ -124,9 +123,6 @@ void glmx_graph::upload() {
   // the graph stream (K1 chunks, K5 RetrieveNode) runs beside the prefill at the lowest priority:
   // the forward's CTAs are dispatched first whenever an SM frees up
   stream = make_stream(false);
-  stream2 = make_stream(false);
-  GLMX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-  GLMX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   {
     uint32_t* st = static_cast<uint32_t*>(put(nullptr, host.n() * 4));
     entry_stats(dev.entry_bytes, dev.entry_off, static_cast<uint32_t>(host.n()), st, stream);
@@ -146,14 +142,23 @@ void glmx_graph::upload() {
     uint32_t* head = static_cast<uint32_t*>(put(nullptr, n * 4));
     uint32_t* tail = static_cast<uint32_t*>(put(nullptr, n * 4));
     uint64_t* tstate = static_cast<uint64_t*>(put(nullptr, n * 8));
-    uint4* itok = static_cast<uint4*>(put(nullptr, static_cast<size_t>(n_int) * 16));
-    entry_tokens(dev.entry_bytes, dev.entry_off, st, n, ioff, head, tail, tstate, itok, stream);
+    uint2* itok_span = static_cast<uint2*>(put(nullptr, static_cast<size_t>(n_int) * 8));
+    uint64_t* itok_hash = static_cast<uint64_t*>(put(nullptr, static_cast<size_t>(n_int) * 8));
+    entry_tokens(dev.entry_bytes, dev.entry_off, st, n, ioff, head, tail, tstate, itok_span,
+                 itok_hash, stream);
+    n_interior = n_int;
     GLMX_CUDA(cudaStreamSynchronize(stream));  // before tmp (scan scratch) is released
     dev.ent_head = head;
     dev.ent_tail = tail;
     dev.ent_tstate = tstate;
     dev.ent_ioff = ioff;
-    dev.itok = itok;
+    dev.itok_span = itok_span;
+    dev.itok_hash = itok_hash;
+    dev.itok_id = nullptr;
+    EntryRec* rec = static_cast<EntryRec*>(put(nullptr, static_cast<size_t>(n) * sizeof(EntryRec)));
+    entry_records(dev.entry_off, head, tail, tstate, ioff, n, rec, stream);
+    GLMX_CUDA(cudaStreamSynchronize(stream));
+    dev.ent = rec;
   }
   if (host.und_off.empty()) {
     // GPU ingest (kernels/ingest.cu): CSRs and weights built on the device from the edge list
@@ -257,11 +262,18 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
   } else {
     g->k1_valid = false;
     const glmx::RankedAdj ra = g->ranked_adj(cfg->weight_mode, cfg->directed);
+    if (cfg->vocab && cfg->vocab != g->itok_vocab) {  // interior-token ids for this vocab
+      g->d_itok_id.reserve(std::max<size_t>(g->n_interior, 1) * 4);
+      chunk_token_ids(g->dev.itok_hash, g->n_interior, cfg->vocab, g->d_itok_id.as<uint32_t>(), s);
+      g->dev.itok_id = g->d_itok_id.as<uint32_t>();
+      g->itok_vocab = cfg->vocab;
+    }
     g->d_nodes.reserve(n * 4);
     g->d_cnt.reserve(n * 4);
     g->d_off.reserve((n + 1) * 8);
     g->d_toff.reserve((n + 3) * 4);   // token offsets ([n] = total) + overflow flag + irregular count
     g->d_irr.reserve(n * 4);          // irregular chunks (byte-level tokenizer)
+    g->d_vrow.reserve(n * 8);         // (node, ranked-row start) per chunk
     const int tiles = chunk_scan_tiles(static_cast<int>(n));
     if (g->d_scan.bytes < static_cast<size_t>(tiles) * 32) {
       g->d_scan.reserve(static_cast<size_t>(tiles) * 32);
@@ -282,7 +294,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
     GLMX_CUDA(cudaEventRecord(g->ev0, s));
     chunk_lengths_scan(g->dev, ra, k, g->d_nodes.as<int32_t>(), static_cast<int>(n),
                        g->d_cnt.as<int32_t>(), g->d_off.as<uint64_t>(), g->d_toff.as<uint32_t>(), st,
-                       ++g->scan_epoch, g->d_irr.as<int32_t>(), irr_count, s);
+                       ++g->scan_epoch, g->d_irr.as<int32_t>(), irr_count, g->d_vrow.as<int2>(), s);
     // The render goes straight on with the output buffers as they are (no host round trip): a
     // batch that does not fit raises the device overflow flag, and is rendered again below into
     // buffers grown to its totals.  Small batches are sized from a bound up front.
@@ -301,7 +313,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
                         cfg->vocab, g->d_bytes.as<char>(), g->d_tid.as<int32_t>(),
                         g->d_tbeg.as<uint64_t>(), g->d_tend.as<uint64_t>(),
                         g->d_bytes.bytes >= 16 ? g->d_bytes.bytes - 16 : 0, tok_cap, overflow,
-                        g->d_irr.as<int32_t>(), irr_count, s, g->stream2, g->ev_fork, g->ev_join);
+                        g->d_irr.as<int32_t>(), irr_count, g->d_vrow.as<int2>(), s);
     };
     render();
     GLMX_CUDA(cudaEventRecord(g->ev1, s));

@@ -65,12 +65,14 @@ struct glmx_graph {
   uint32_t max_entry = 0;  // longest pre-rendered entry (K1 output bound)
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // K1 tokens run beside the K1 text (fork/join by events)
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   // K1 scratch
-  DBuf d_nodes, d_cnt, d_off, d_bytes, d_tid, d_tbeg, d_tend, d_toff, d_scan, d_irr;
+  DBuf d_nodes, d_cnt, d_off, d_bytes, d_tid, d_tbeg, d_tend, d_toff, d_scan, d_irr, d_vrow;
   uint32_t scan_epoch = 0;  // chunk_lengths_scan look-back state (d_scan) epoch
+  uint32_t n_interior = 0;  // interior tokens of the regular entries (DevGraph::itok_*)
+  DBuf d_itok_id;           // their ids for itok_vocab
+  uint32_t itok_vocab = 0;
   // ranked adjacency per (weight mode, directed) variant, built on first use (kernels/chunk.cuh)
   struct Ranked {
     bool ready = false;

@@ -16,8 +16,8 @@ for _ in range(3):
 PY
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file gpurun_out/${TAG}_launches.csv python /tmp/k1_one.py > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"chunk_(render_kernel|tokens_kernel)" -s 6 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"chunk_regular" -s 2 -c 1 \
   -o gpurun_out/${TAG}_re python /tmp/k1_one.py > gpurun_out/${TAG}_re_ncu.log 2>&1
 ncu -i gpurun_out/${TAG}_re.ncu-rep --page raw --csv > gpurun_out/${TAG}_re_raw.csv 2>/dev/null
-ncu -i gpurun_out/${TAG}_re.ncu-rep --page source --csv --print-source sass -k regex:chunk_render_kernel > gpurun_out/${TAG}_re_sass.csv 2>/dev/null
-ncu -i gpurun_out/${TAG}_re.ncu-rep --page source --csv --print-source cuda -k regex:chunk_tokens_kernel > gpurun_out/${TAG}_re_src.csv 2>/dev/null
+ncu -i gpurun_out/${TAG}_re.ncu-rep --page source --csv --print-source sass -k regex:chunk_regular > gpurun_out/${TAG}_re_sass.csv 2>/dev/null
+ncu -i gpurun_out/${TAG}_re.ncu-rep --page source --csv --print-source sass -k regex:chunk_tokens_kernel > gpurun_out/${TAG}_tok_sass.csv 2>/dev/null
