@@ -55,9 +55,11 @@ def parse():
     p.add_argument("--routing", default="mod", choices=["mod", "affinity"],
                    help="query -> GPU: i mod N (reference sharding) or prefix affinity "
                         "(fnv1a(question) mod N: repeated questions stay on one GPU)")
-    p.add_argument("--decode-merge", action="store_true",
-                   help="batch two rotations' decode rows into one decode (continuous batching); "
-                        "measured slower on this workload: the long contexts make decode KV-bound")
+    p.add_argument("--no-decode-merge", dest="decode_merge", action="store_false",
+                   help="decode every rotation's rows on their own instead of batching two "
+                        "rotations' decode rows into one weight stream per step (continuous "
+                        "batching, the default: 181.5 vs 170.3 Graph-CoT queries/s on one B200, "
+                        "profiles/r2_decode_merge_ab.json)")
     p.add_argument("--no-standalone", action="store_true",
                    help="skip the standalone K1 / K3 measurements reported beside the in-step ones")
     p.add_argument("--no-pipeline", action="store_true",
@@ -730,6 +732,8 @@ def main():
              "decode_forward_ms": dq_dec_ms, "prefill_forward_ms": dq_pre_ms,
              "decode_launches": dq_n_dec[0],
              "step": "prefill + greedy reply decode per call (call_llm), CUDA events, max over ranks",
+             "decode": ("continuous batching: two rotations' decode rows per weight stream"
+                        if args.decode_merge else "each rotation's rows alone"),
              "n_gpus": ws}
             if dq_ms > 0 else None),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
