@@ -84,7 +84,9 @@ def workload_shape(args, ws):
     fixed and the question stream is a prefix-stable draw (synth.graph_cot_questions), so the
     rotations that are timed do not depend on --steps."""
     rotations = args.cache_warm + args.warmup + args.steps
-    n_q = args.lanes * (rotations // 6 + 2)
+    # queries for every rotation the GPU arm runs: + the per-kernel breakdown steps and the
+    # Graph-CoT decode phase (the stream is prefix-stable, so this does not change the timed ones)
+    n_q = args.lanes * ((rotations + args.steps + getattr(args, "decode_steps", 0)) // 6 + 2)
     return n_q, args.question_pool, rotations
 
 
@@ -135,13 +137,19 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.rows = []
+        self.first = 0
         self.proc = None
+
+    def mark(self):
+        """The timed region starts: only samples from here on count (nvidia-smi is started
+        earlier, so its start-up latency does not eat the samples of a short region)."""
+        self.first = len(self.rows)
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -162,7 +170,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        rows = self.rows
+        rows = self.rows[self.first:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = sorted(float(r[0]) for r in rows)
@@ -508,18 +516,24 @@ def main():
             for _ in range(k):
                 yield step()
 
-    # steady state: the cache-warm rotations, then the warm-up steps (both untimed)
-    for _ in rotations(args.cache_warm + args.warmup):
-        pass
-    # per-kernel-category CUDA events on the engine stream during the timed steps (host cost
-    # ~1 us per event record, <1% of a step)
-    eng.set_profiling(2)
-    peer0 = kv.peer_hits() if px is not None else 0
+    # steady state: the cache-warm rotations, then the warm-up steps (both untimed); the clock
+    # sampler starts during the warm-up
     sampler = ClockSampler(local)
+    for i, _ in enumerate(rotations(args.cache_warm + args.warmup)):
+        if i == args.cache_warm:
+            sampler.start()
+    if args.warmup <= 0:
+        sampler.start()
+    # the timed steps carry one CUDA event pair per forward (profiling 1: the forward's device
+    # time); the per-kernel-category breakdown is taken over the same number of further steps
+    # right after (profiling 2: an event pair around every kernel group), so its event records
+    # stay out of the headline
+    eng.set_profiling(1)
+    peer0 = kv.peer_hits() if px is not None else 0
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     prof_range = os.environ.get("GLMX_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     if prof_range:
         torch.cuda.cudart().cudaProfilerStart()
@@ -527,20 +541,14 @@ def main():
     ev0.record()
     tokens = computed = cached = calls = chunks = finished = 0
     fwd_ms = 0.0
-    cat_ms = {"attention": 0.0, "kv_append": 0.0, "gemm": 0.0, "elementwise": 0.0}
-    work = {"attn_flops": 0.0, "attn_bytes": 0.0, "append_bytes": 0.0, "linear_flops": 0.0}
     io0 = eng.io_bytes(), g.io_bytes()
     chunk_ms = 0.0
     k1_bytes = 0
     k5_launches = 0
     k5_ms = 0.0
     k1_rotations = 0
-    k2_big_ms = k2_big_bytes = 0.0
     for r in rotations(args.steps):
-        tm = eng.last_timings()
-        fwd_ms += tm["forward"]
-        for k in cat_ms:
-            cat_ms[k] += tm[k]
+        fwd_ms += eng.last_timings()["forward"]
         if r.chunks:
             chunk_ms += r.chunk_ms
             k1_bytes += r.chunk_bytes
@@ -554,12 +562,6 @@ def main():
         chunks += r.chunks
         k1_rotations += 1 if r.chunks else 0
         finished += r.finished
-        wk = eng.last_work()
-        for k in work:
-            work[k] += wk[k]
-        if wk["computed_tokens"] >= 2048:  # K2 in its bandwidth regime (large prefill batches)
-            k2_big_ms += tm["kv_append"]
-            k2_big_bytes += wk["append_bytes"]
     ev1.record()
     torch.cuda.synchronize()
     if prof_range:
@@ -575,9 +577,6 @@ def main():
     h2d = (io1[0][0] - io0[0][0]) + (io1[1][0] - io0[1][0])
     d2h = (io1[0][1] - io0[0][1]) + (io1[1][1] - io0[1][1])
 
-    eng.set_profiling(0)
-    tm = dict(cat_ms, forward=fwd_ms)
-    wk = work
 
     # phase 2 (after the measured prefill steps): the complete call_llm step — prefill + greedy
     # decode of each reply — for Graph-CoT queries/s; rotations sequential (decode continues the
@@ -623,6 +622,27 @@ def main():
         if ws > 1:
             dist.barrier()
         dq_ms = d0.elapsed_time(d1)
+    # per-kernel-category breakdown (device time of each kernel group + its algorithmic work),
+    # over as many prefill rotations as were timed, after the Graph-CoT phase
+    eng.set_profiling(2)
+    cat_ms = {"attention": 0.0, "kv_append": 0.0, "gemm": 0.0, "elementwise": 0.0}
+    work = {"attn_flops": 0.0, "attn_bytes": 0.0, "append_bytes": 0.0, "linear_flops": 0.0}
+    bd_fwd_ms = 0.0
+    k2_big_ms = k2_big_bytes = 0.0
+    for r in rotations(args.steps):
+        tm = eng.last_timings()
+        bd_fwd_ms += tm["forward"]
+        for k in cat_ms:
+            cat_ms[k] += tm[k]
+        wk = eng.last_work()
+        for k in work:
+            work[k] += wk[k]
+        if wk["computed_tokens"] >= 2048:  # K2 in its bandwidth regime (large prefill batches)
+            k2_big_ms += tm["kv_append"]
+            k2_big_bytes += wk["append_bytes"]
+    eng.set_profiling(0)
+    tm = dict(cat_ms, forward=bd_fwd_ms)
+    wk = work
     peer_blocks = float(kv.peer_hits() - peer0) if px is not None else 0.0
     vals = torch.tensor([tokens, computed, cached, calls, finished, peer_blocks, dq_fin, dq_dec],
                         dtype=torch.float64, device=red_dev)
