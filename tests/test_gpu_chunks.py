@@ -186,3 +186,40 @@ def test_irregular_entries_take_byte_tokenizer(ref, tmp_path):
         r0 = glmx.Retriever(g, chunk_k=k, vocab=0)
         b0 = r0.chunk_build(nodes)
         assert b0.token_spans == batch.token_spans and b0.texts == batch.texts
+
+
+def test_fill_call_after_other_batch_is_rebuilt(ref, tmp_path):
+    """glmx_chunk_build's fill call reuses the size query's result only for the same node list and
+    configuration: a size query for one batch followed by a fill call for another (or for the same
+    nodes under another k / vocab) returns the second batch's chunks."""
+    import ctypes as C
+
+    from paper_2511_01633_b200._lib import check, lib
+
+    g = glmx.PropertyGraph.synth_powerlaw(3000, 6, seed=2, device=0)
+    path = str(tmp_path / "g.jsonl")
+    g.save(path)
+    rg = oracle.RefGraph(path=path)
+    a, b = [5, 17, 300], [9, 9, 2000, 41]
+    r16 = glmx.Retriever(g, chunk_k=16, vocab=32000)
+    r4 = glmx.Retriever(g, chunk_k=4, vocab=32000)
+
+    def fill(r, nodes):
+        n = len(nodes)
+        arr = (C.c_int32 * n)(*nodes)
+        tb, tt = C.c_uint64(), C.c_uint64()
+        out = C.create_string_buffer(1 << 16)
+        boff = (C.c_uint64 * (n + 1))()
+        check(lib().glmx_chunk_build(g.h, C.byref(r.cfg), arr, n, out, 1 << 16, boff, None, None,
+                                     None, 0, None, C.byref(tb), C.byref(tt)))
+        raw = out.raw
+        return [raw[boff[i]:boff[i + 1]].decode() for i in range(n)]
+
+    for size_r, size_nodes, fill_r, fill_nodes, k in ((r16, a, r16, b, 16), (r16, b, r4, b, 4)):
+        n = len(size_nodes)
+        arr = (C.c_int32 * n)(*size_nodes)
+        tb, tt = C.c_uint64(), C.c_uint64()
+        check(lib().glmx_chunk_build(g.h, C.byref(size_r.cfg), arr, n, None, 0, None, None, None,
+                                     None, 0, None, C.byref(tb), C.byref(tt)))
+        got = fill(fill_r, fill_nodes)
+        assert got == [rg.node_info_rendered(g.node_id(v), k) for v in fill_nodes]
