@@ -297,15 +297,9 @@ __device__ __forceinline__ void put_block(char* dstp, uint4 x, uint32_t nx, uint
                                           uint32_t pre, uint32_t post) {
   const uint32_t q = (0u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dstp))) & 3u;
   const uint32_t w[6] = {0u, x.x, x.y, x.z, x.w, nx};
-  if (base + q >= src + 4 && base + q + 16 <= end) {
-    // interior block: its four words hold entry bytes only
-    char* d = dstp + base + q;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      reinterpret_cast<uint32_t*>(d)[j] = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
-    return;
-  }
-  // positions biased by +16 so that j = -1 at base 0 stays unsigned
+  // positions biased by +16 so that j = -1 at base 0 stays unsigned; branch-free: every word's
+  // value is formed with selects and the store is predicated (the lanes of a warp sit at
+  // different blocks of different segments)
   const uint32_t bs = src + 16, be = end + 16, bx = ext_end + 16;
   const bool first = base <= src;
 #pragma unroll
@@ -314,18 +308,14 @@ __device__ __forceinline__ void put_block(char* dstp, uint4 x, uint32_t nx, uint
     // first aligned one: in the segment's first block it holds frame bytes + the entry's first
     // bytes, in later blocks it is the previous block's j = 3 word
     const uint32_t p = base + 16 + q + 4 * j;
-    if (p + 3 >= bs && p + 4 <= bx && (j >= 0 || first)) {
-      uint32_t v = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
-      if (p < bs) {  // 1..3 frame bytes before src
-        const uint32_t m = bs - p;
-        v = (v & (0xFFFFFFFFu << (8 * m))) | (pre >> (8 * (4 - m)));
-      }
-      if (p + 4 > be) {  // 1..3 entry bytes, then the frame after end
-        const uint32_t keep = be - p;
-        v = (v & (0xFFFFFFFFu >> (32 - 8 * keep))) | (post << (8 * keep));
-      }
+    const uint32_t f = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
+    const bool lo = p < bs, hi = p + 4 > be;           // frame bytes before / after the entry
+    const uint32_t m = lo ? bs - p : 0u;               // 1..3
+    const uint32_t keep = hi ? be - p : 4u;            // 1..3
+    uint32_t v = lo ? (f & (0xFFFFFFFFu << (8 * m))) | (pre >> (8 * (4 - m))) : f;
+    v = hi ? (v & (0xFFFFFFFFu >> (32 - 8 * keep))) | (post << (8 * keep)) : v;
+    if (p + 3 >= bs && p + 4 <= bx && (j >= 0 || first))
       *reinterpret_cast<uint32_t*>(dstp + static_cast<int32_t>(p - 16u)) = v;
-    }
   }
 }
 
@@ -601,15 +591,13 @@ __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
     const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
     build_chunk(g, v, k, mine, sb + pad, lane, true);
     char* gbase = out + (goff - pad);
-    const uint32_t nw16 = (Q + 15) >> 4;
-    for (uint32_t i = lane; i < nw16; i += 32) {
-      const uint32_t lo = 16 * i, hi = lo + 16;
-      if (lo >= pad && hi <= Q) {
-        *reinterpret_cast<uint4*>(gbase + lo) = *reinterpret_cast<const uint4*>(sb + lo);
-      } else {
-        put_edge16(gbase, sb, lo, pad, Q);
-      }
-    }
+    // whole 16-byte words [a16, z16) as 16-byte stores; the < 16 ragged bytes at each end as one
+    // byte per lane (lanes 0-15 the head, 16-31 the tail)
+    const uint32_t a16 = (pad + 15) & ~15u, z16 = Q & ~15u;
+    for (uint32_t lo = a16 + 16 * lane; lo < z16; lo += 512)
+      *reinterpret_cast<uint4*>(gbase + lo) = *reinterpret_cast<const uint4*>(sb + lo);
+    const uint32_t b = lane < 16 ? pad + lane : max(z16, a16) + (lane - 16);
+    if (lane < 16 ? b < min(a16, Q) : b < Q) gbase[b] = sb[b];
   } else {
     build_chunk(g, v, k, mine, out + goff, lane, false);
   }
