@@ -284,38 +284,19 @@ __device__ __forceinline__ uint32_t next_start(const uint32_t* sp, uint32_t q, u
 }
 
 // One 16-byte source word x (entry bytes [base, base + 16)) of a segment [src, end) whose byte p
-// goes to dstp + p, stored as destination-aligned 4-byte words of the source words realigned by a
-// funnel shift (nx = the next source word).  A segment's bytes are framed by known separator
-// bytes -- 3 before (pre, in the top 3 bytes) and up to 3 after (post, low bytes), e.g. ")" ","
-// "(" between neighbour entries -- so every word inside [src - 3, ext_end) is written whole, the
-// frame bytes merged in, and no entry byte needs a byte store.  Adjacent segments' frames are the
-// same separator bytes, and a 4-byte word never holds bytes of two entries, so each word has one
-// writer.  Words of the first block that start before base + q (j = -1) cover the frame before
-// src.
+// goes to dstp + p: the destination-aligned 4-byte words that lie wholly inside the entry, each a
+// funnel shift of two source words (nx = the next source word), predicated stores.  The <= 3
+// ragged bytes at each end of the entry are stored by the segment's own lane (build_chunk), so
+// every byte has exactly one writer.
 __device__ __forceinline__ void put_block(char* dstp, uint4 x, uint32_t nx, uint32_t base,
-                                          uint32_t src, uint32_t end, uint32_t ext_end,
-                                          uint32_t pre, uint32_t post) {
+                                          uint32_t src, uint32_t end) {
   const uint32_t q = (0u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dstp))) & 3u;
-  const uint32_t w[6] = {0u, x.x, x.y, x.z, x.w, nx};
-  // positions biased by +16 so that j = -1 at base 0 stays unsigned; branch-free: every word's
-  // value is formed with selects and the store is predicated (the lanes of a warp sit at
-  // different blocks of different segments)
-  const uint32_t bs = src + 16, be = end + 16, bx = ext_end + 16;
-  const bool first = base <= src;
+  const uint32_t w[5] = {x.x, x.y, x.z, x.w, nx};
 #pragma unroll
-  for (int j = -1; j < 4; ++j) {
-    // p = source position of the word's first byte (+16); j = -1 is the word before the block's
-    // first aligned one: in the segment's first block it holds frame bytes + the entry's first
-    // bytes, in later blocks it is the previous block's j = 3 word
-    const uint32_t p = base + 16 + q + 4 * j;
-    const uint32_t f = q ? __funnelshift_r(w[j + 1], w[j + 2], 8 * q) : w[j + 1];
-    const bool lo = p < bs, hi = p + 4 > be;           // frame bytes before / after the entry
-    const uint32_t m = lo ? bs - p : 0u;               // 1..3
-    const uint32_t keep = hi ? be - p : 4u;            // 1..3
-    uint32_t v = lo ? (f & (0xFFFFFFFFu << (8 * m))) | (pre >> (8 * (4 - m))) : f;
-    v = hi ? (v & (0xFFFFFFFFu >> (32 - 8 * keep))) | (post << (8 * keep)) : v;
-    if (p + 3 >= bs && p + 4 <= bx && (j >= 0 || first))
-      *reinterpret_cast<uint32_t*>(dstp + static_cast<int32_t>(p - 16u)) = v;
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t p0 = base + q + 4 * j;  // source position of the word's first byte
+    const uint32_t v = q ? __funnelshift_r(w[j], w[j + 1], 8 * q) : w[j];
+    if (p0 >= src && p0 + 4 <= end) *reinterpret_cast<uint32_t*>(dstp + p0) = v;
   }
 }
 
@@ -339,8 +320,7 @@ __device__ __forceinline__ void put_edge16(char* gbase, const char* sb, uint32_t
 // pieces) the 16-byte source words of all segments are numbered by a warp scan; each lane finds
 // its segment by a shuffle binary search and keeps kWordsU loads in flight before it stores.
 __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
-                                            const int32_t* __restrict__ mine, char* buf, int lane,
-                                            bool staged) {
+                                            const int32_t* __restrict__ mine, char* buf, int lane) {
   const uint32_t ev = g.entry_off[v];
   const uint32_t ec = g.entry_off[v + 1] - ev;
   if (lane < 6) buf[lane] = "[Node:"[lane];
@@ -376,9 +356,16 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
       dst = pst + c + 1;
     }
     o += __shfl_sync(0xffffffffu, pincl, 31);
-    // unstaged: the last piece's frame ")]" is 2 bytes, so put_block skips a final word that would
-    // reach past the chunk; its one entry byte is stored here
-    if (!staged && s >= 1 && s == k && len) buf[dst + len - 1] = g.entry_bytes[src + len - 1];
+    // the entry's ragged ends (bytes outside its destination-aligned whole words): <= 3 + 3 bytes
+    if (s <= k && len) {
+      const char* sp = g.entry_bytes + src;
+      char* dp = buf + dst;
+      const uint32_t ph = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dp)) & 3u;
+      const uint32_t head = min(len, (4u - ph) & 3u);
+      const uint32_t tail = max(head, len - ((ph + len) & 3u));
+      for (uint32_t i = 0; i < head; ++i) dp[i] = sp[i];
+      for (uint32_t i = tail; i < len; ++i) dp[i] = sp[i];
+    }
     // 16-byte source words covering [src, src + len), numbered across the round's segments
     const uint32_t wc = len ? ((src + len - 1) >> 4) - (src >> 4) + 1 : 0;
     uint32_t wincl = wc;
@@ -392,7 +379,6 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
     for (uint32_t w0 = 0; w0 < W; w0 += 32 * kWordsU) {
       uint4 x[kWordsU];
       uint32_t nx[kWordsU], qsrc[kWordsU], qlen[kWordsU], qdst[kWordsU], qword[kWordsU];
-      int qseg[kWordsU];
 #pragma unroll
       for (int t = 0; t < kWordsU; ++t) {
         const uint32_t wi = w0 + t * 32 + lane;
@@ -407,26 +393,14 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
         qlen[t] = __shfl_sync(0xffffffffu, len, q);
         qdst[t] = __shfl_sync(0xffffffffu, dst, q);
         qword[t] = (qsrc[t] >> 4) + (wi - qe);
-        qseg[t] = s0 + q;
         const bool in = wi < W;
         x[t] = in ? __ldg(words + qword[t]) : make_uint4(0, 0, 0, 0);
         nx[t] = in ? __ldg(words4 + 4 * (qword[t] + 1)) : 0u;
         if (!in) qlen[t] = 0;
       }
 #pragma unroll
-      for (int t = 0; t < kWordsU; ++t) {
-        if (!qlen[t]) continue;
-        // the segment's frame: "de:" E_v "]\n[" / "s:(" E_1 / ")" "," "(" E_j / ")" "," "(" or
-        // ")" "]" after the last piece
-        const int sg = qseg[t];
-        const uint32_t pre = sg == 0 ? 0x3A656400u : sg == 1 ? 0x283A7300u : 0x282C2900u;
-        const bool last = sg >= 1 && sg == k;
-        const uint32_t post = sg == 0 ? 0x5B0A5Du : last ? 0x5D29u : 0x282C29u;
-        const uint32_t end = qsrc[t] + qlen[t];
-        // staged: the buffer has slack past the chunk, so the last frame may take a 3rd byte
-        put_block(buf + qdst[t] - qsrc[t], x[t], nx[t], qword[t] << 4, qsrc[t], end,
-                  end + (last && !staged ? 2u : 3u), pre, post);
-      }
+      for (int t = 0; t < kWordsU; ++t)
+        put_block(buf + qdst[t] - qsrc[t], x[t], nx[t], qword[t] << 4, qsrc[t], qsrc[t] + qlen[t]);
     }
   }
   if (lane == 0) buf[o] = ']';
@@ -589,7 +563,7 @@ __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
                                             uint32_t n, char* __restrict__ out, char* sb, int lane) {
   if (n <= kBuf) {
     const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
-    build_chunk(g, v, k, mine, sb + pad, lane, true);
+    build_chunk(g, v, k, mine, sb + pad, lane);
     char* gbase = out + (goff - pad);
     // whole 16-byte words [a16, z16) as 16-byte stores; the < 16 ragged bytes at each end as one
     // byte per lane (lanes 0-15 the head, 16-31 the tail)
@@ -599,7 +573,7 @@ __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
     const uint32_t b = lane < 16 ? pad + lane : max(z16, a16) + (lane - 16);
     if (lane < 16 ? b < min(a16, Q) : b < Q) gbase[b] = sb[b];
   } else {
-    build_chunk(g, v, k, mine, out + goff, lane, false);
+    build_chunk(g, v, k, mine, out + goff, lane);
   }
 }
 
@@ -619,7 +593,7 @@ __device__ __forceinline__ void render_slow(const DevGraph& g, int32_t v, int k,
     // staged span: smem bytes [pad, Q) hold the chunk at the 16-byte phase of its destination
     char* sb = sbw;
     const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
-    build_chunk(g, v, k, mine, sb + pad, lane, true);
+    build_chunk(g, v, k, mine, sb + pad, lane);
     // per 16-byte word (one per lane): text out (aligned words as one 16-byte store, the two edge
     // words byte by byte) and 16 whitespace bits; bytes outside [pad, Q) count as spaces
     char* gbase = out + (goff - pad);
@@ -678,7 +652,7 @@ __device__ __forceinline__ void render_slow(const DevGraph& g, int32_t v, int k,
     return;
   }
   // longer than the buffer: built in place in global memory, tokenised from there
-  build_chunk(g, v, k, mine, gdst, lane, false);
+  build_chunk(g, v, k, mine, gdst, lane);
   const char* src = gdst;
   for (uint32_t s0 = 0; s0 < n; s0 += kSeg) {
     uint32_t cnt = 0;
@@ -831,7 +805,7 @@ __global__ void token_ids_kernel(const uint64_t* __restrict__ hash, uint32_t n, 
 // Regular chunks, text and tokens in one launch: warps 0-3 of a CTA render the text of chunks
 // 4b..4b+3 (render_text), warps 4-7 emit their tokens (emit_fast), so the two halves of a chunk
 // run side by side on every SM.
-__global__ void __launch_bounds__(2 * kRW * 32, 5)
+__global__ void __launch_bounds__(2 * kRW * 32, 6)
 chunk_regular_kernel(DevGraph g, RankedAdj ra, int n_req, const int32_t* __restrict__ sel_count,
                      const uint64_t* __restrict__ byte_off, const uint32_t* __restrict__ tok_off,
                      uint32_t vocab, uint64_t vmagic, char* __restrict__ out,
