@@ -453,6 +453,9 @@ def main():
     torch.cuda.set_device(local)
     shared_gpu = ws > n_dev
     if ws > 1:
+        # the communicator set-up (rings / NVLS over NVSwitch) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if shared_gpu:  # NCCL refuses two ranks on one GPU: control plane over gloo
             dist.init_process_group("gloo")
         else:
