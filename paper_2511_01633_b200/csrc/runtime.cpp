@@ -1,5 +1,15 @@
 #include "runtime.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
+namespace {
+// NVTX range over a host-side phase (bookkeeping, staging, K1/K5 batches, decode, page copies)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -237,6 +247,7 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
                      int32_t* out_tok_ids, uint64_t* out_tok_begin, uint64_t* out_tok_end,
                      uint64_t tok_cap, uint64_t* out_tok_offsets, uint64_t* total_bytes,
                      uint64_t* total_tokens) {
+  NvtxRange nvtx_range("glmx.k1.chunk_build");
   if (g->device < 0) throw Error(GLMX_ERR_NO_DEVICE, "graph has no device");
   if (n == 0) {
     if (total_bytes) *total_bytes = 0;
@@ -410,6 +421,7 @@ glmx_kv* kv_create_impl(const glmx_kv_config* cfg) {
 
 void pool_copy_impl(glmx_kv* src, glmx_kv* dst, const int32_t* sp, const int32_t* dp, uint64_t n,
                     cudaStream_t s) {
+  NvtxRange nvtx_range("glmx.k4.pool_copy");
   if (!src->has_pool() || !dst->has_pool()) throw Error(GLMX_ERR_NO_DEVICE, "pool copy needs device pools");
   if (src->page_bytes != dst->page_bytes) throw Error(GLMX_ERR_ARG, "pool geometries differ");
   for (uint64_t i = 0; i < n; ++i)
@@ -613,12 +625,17 @@ cudaEvent_t next_event(glmx_engine* e) {
   return ev;
 }
 
+// A kernel group of the forward: an NVTX range (host-side enqueue; an NVTX-aware profiler maps
+// the group's kernels to it) and, when profiling, a CUDA event pair on the engine stream.
 struct Prof {
   glmx_engine* e;
   int cat;
   cudaEvent_t a = nullptr;
   // profiling 1: whole forward + copies only; 2: every kernel category
   Prof(glmx_engine* e_, int c) : e(e_), cat(c) {
+    static const char* const kNames[] = {"glmx.forward", "glmx.attention", "glmx.kv_append",
+                                         "glmx.gemm", "glmx.elementwise", "glmx.h2d", "glmx.d2h"};
+    nvtxRangePushA(kNames[c]);
     if (e->profiling >= 2 || (e->profiling == 1 && (c == 0 || c >= 5))) {
       a = next_event(e);
       GLMX_CUDA(cudaEventRecord(a, e->stream));
@@ -630,6 +647,7 @@ struct Prof {
       cudaEventRecord(b, e->stream);
       e->spans.push_back({a, b, cat, e->prof_tag ? e->prof_tag : e->batch_seq});
     }
+    nvtxRangePop();
   }
 };
 
@@ -934,6 +952,7 @@ int engine_wait_impl(glmx_engine* e, int32_t* first_token, uint64_t cap);
 int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs,
                         glmx_prefill_report* reports, int32_t* first_token, float* logits_out,
                         bool async) {
+  NvtxRange nvtx_range("glmx.prefill");
   if (e->pending.size() >= 2) throw Error(GLMX_ERR_ARG, "two batches in flight: wait for one first");
   if (async && logits_out) throw Error(GLMX_ERR_ARG, "logits are only returned by the synchronous step");
   if (!async)
@@ -1196,6 +1215,7 @@ int engine_prefill_impl(glmx_engine* e, uint64_t n_req, const glmx_request* reqs
 // Completes the oldest in-flight prefill batch: waits for it, publishes its timings and work,
 // writes its greedy first tokens (-1 for empty prompts).  Returns the batch's request count.
 int engine_wait_impl(glmx_engine* e, int32_t* first_token, uint64_t cap) {
+  NvtxRange nvtx_range("glmx.wait");
   if (e->pending.empty()) throw Error(GLMX_ERR_ARG, "no prefill batch in flight");
   DeviceGuard dg(e->m->device);
   glmx_engine::Pending pd = std::move(e->pending.front());
@@ -1248,6 +1268,7 @@ int engine_decode_defer(glmx_engine* e, const uint32_t* steps) {
 // the tokens.  The next prefill may be staged in between (its staging uses the next pinned
 // slots; the decode's pages and device buffers are stream-ordered before it).
 int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
+  NvtxRange nvtx_range("glmx.decode");
   if (!e->has_batch) throw Error(GLMX_ERR_ARG, "decode needs a prefill batch");
   if (e->dec_pending) throw Error(GLMX_ERR_ARG, "a decode is already enqueued: collect it first");
   glmx_model* m = e->m;
@@ -1357,6 +1378,7 @@ int engine_decode_enqueue(glmx_engine* e, const uint32_t* steps) {
 // out_tokens [staged rows][max_steps]; out_prev (nullable) [deferred rows][max_steps] for the
 // rows of a batch whose decode was deferred into this one.
 int engine_decode_collect(glmx_engine* e, int32_t* out_tokens, int32_t* out_prev, float* last_logits) {
+  NvtxRange nvtx_range("glmx.decode_collect");
   if (!e->dec_pending) throw Error(GLMX_ERR_ARG, "no decode enqueued");
   e->dec_pending = false;
   const int R = e->dec_R, Rd = e->dec_R_def;
@@ -1618,6 +1640,7 @@ int index_build_impl(glmx_graph* g, int dim, uint64_t lru_capacity) {
 // resolved after the one GPU scan that serves every probe of the batch).
 int retrieve_impl(glmx_graph* g, const char* bytes, const uint64_t* offs, uint64_t n,
                   int32_t* out_node, uint8_t* out_hit) {
+  NvtxRange nvtx_range("glmx.k5.retrieve");
   if (g->idx_pad == 0) throw Error(GLMX_ERR_ARG, "no index: call glmx_index_build first");
   if (g->idx_node.empty() && n) throw Error(GLMX_ERR_RETRIEVAL, "EmptyIndex: the index has no entries");
   std::vector<int64_t> val(n);
