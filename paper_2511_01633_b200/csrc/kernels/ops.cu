@@ -487,11 +487,12 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
   if (T <= 0) return;
   if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
   if (hd == 128) {
-    // 16 heads per warp; decode-sized batches (< 1024 tokens) 4 heads per warp and 2 warps per
-    // CTA, so a 64-token step still spreads over ~380 CTAs with one load round trip each
+    // 16 heads per warp; small batches (< 768 tokens) 4 heads per warp and 2 warps per CTA, so a
+    // few hundred tokens still spread over the SMs with one load round trip each (measured
+    // crossover: 450 tokens 5.5 vs 6.3 us, 1000 tokens 8.3 vs 6.3 us)
     const int passes = static_cast<int>(ceil_div(H + 2 * Hkv, 4));
     if (!rope_cs) throw Error(GLMX_ERR_ARG, "head_dim 128 append needs the forward's RoPE table");
-    if (T < 1024) {
+    if (T < 768) {
       rope_kv_append_warp_kernel<1><<<dim3(static_cast<int>(ceil_div(T, 2)), passes), 64, 0, s>>>(
           qkv, rope_cs, slot, T, H, Hkv, pool, layer, q_out);
     } else {

@@ -31,6 +31,7 @@ from paper_2511_01633_b200.ops import rope_kv_append  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--skip", nargs="*", default=[])
+ap.add_argument("--k2-tokens", type=int, nargs="+", default=[520, 2750, 4965, 16384])
 args = ap.parse_args()
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
 HBM = peaks["hbm_gbs"]
@@ -43,7 +44,7 @@ def emit(row):
 
 H, Hkv, hd, B, L = 32, 8, 128, 16, 32
 if "K2" not in args.skip:
-    for T in [520, 2750, 4965, 16384]:
+    for T in args.k2_tokens:
         n_pages = (T + B - 1) // B + 8
         pool = torch.zeros((n_pages, L, 2, Hkv, B, hd), dtype=torch.bfloat16, device="cuda")
         qkv = torch.randn((T, (H + 2 * Hkv) * hd), device="cuda").to(torch.bfloat16)
