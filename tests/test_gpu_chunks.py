@@ -223,3 +223,26 @@ def test_fill_call_after_other_batch_is_rebuilt(ref, tmp_path):
                                      None, 0, None, C.byref(tb), C.byref(tt)))
         got = fill(fill_r, fill_nodes)
         assert got == [rg.node_info_rendered(g.node_id(v), k) for v in fill_nodes]
+
+
+def test_large_batch_grows_buffers_on_device_overflow(ref, tmp_path):
+    """A batch whose size bound exceeds the preallocated outputs (12000 chunks at k=64) takes the
+    device overflow path: the render sees the capacities, raises the flag, and the host grows the
+    buffers and renders again; every chunk (sampled against the reference) and the token stream
+    come out as from small batches."""
+    g = glmx.PropertyGraph.synth_powerlaw(20000, 8, seed=9, device=0)
+    path = str(tmp_path / "g.jsonl")
+    g.save(path)
+    rg = oracle.RefGraph(path=path)
+    rnd = random.Random(3)
+    nodes = [rnd.randrange(g.node_count()) for _ in range(12000)]
+    V = 128256
+    r = glmx.Retriever(g, chunk_k=64, vocab=V)
+    big = r.chunk_build(nodes)
+    small = r.chunk_build(nodes[:50])
+    assert big.texts[:50] == small.texts and big.token_ids[:50] == small.token_ids
+    for i in rnd.sample(range(len(nodes)), 40):
+        want = rg.node_info_rendered(g.node_id(nodes[i]), 64)
+        assert big.texts[i] == want
+        raw = want.encode()
+        assert [raw[b:e] for b, e in big.token_spans[i]] == oracle.ref_tokenize(raw)
