@@ -736,7 +736,8 @@ def main():
     value = tokens / (fwd_ms * 1e-3)
     e2e = tokens / (wall_ms * 1e-3)
     n_layers = cfg.n_layers
-    launches_per_fwd = 1 + 5 * n_layers + 3  # embed, 5 per layer, final norm + split argmax (2)
+    # embed + RoPE table, 5 per layer (RMSNorm, K2, K3, RMSNorm, SwiGLU), final norm + split argmax
+    launches_per_fwd = 2 + 5 * n_layers + 3
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wall_ms / args.steps, "higher_is_better": True,
@@ -763,9 +764,11 @@ def main():
                 "d2h_bytes_per_step": d2h // args.steps},
         "roofline": roof,
         "kernels": kernels,
-        # own kernels in the timed region: forward + argmax per step, 4 K1 launches per rotation
-        # that built chunks (cub scans and cuBLAS GEMMs are library launches, not counted)
-        "gpu_launches": int(args.steps * (launches_per_fwd + 1) + 4 * k1_rotations + k5_launches),
+        # own kernels in the timed region: the forward's per step (K3's combine pass, launched
+        # only for split items, not counted), 3 K1 launches per rotation that built chunks
+        # (length+scan, regular chunks, irregular chunks), one K5 scan per rotation that probed
+        # the index (cuBLAS GEMMs are library launches, not counted)
+        "gpu_launches": int(args.steps * launches_per_fwd + 3 * k1_rotations + k5_launches),
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:
