@@ -320,7 +320,7 @@ __device__ __forceinline__ void put_edge16(char* gbase, const char* sb, uint32_t
 // pieces) the 16-byte source words of all segments are numbered by a warp scan; each lane finds
 // its segment by a shuffle binary search and keeps kWordsU loads in flight before it stores.
 __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
-                                            const int32_t* __restrict__ mine, char* buf, int lane) {
+                                            const EntryRec* __restrict__ mine, char* buf, int lane) {
   const uint32_t ev = g.entry_off[v];
   const uint32_t ec = g.entry_off[v + 1] - ev;
   if (lane < 6) buf[lane] = "[Node:"[lane];
@@ -336,7 +336,7 @@ __device__ __forceinline__ void build_chunk(const DevGraph& g, int32_t v, int k,
       len = ec;
       dst = 6;
     } else if (s <= k) {
-      const uint2 ol = __ldg(reinterpret_cast<const uint2*>(g.ent + mine[s - 1]));  // (off, len)
+      const uint2 ol = __ldg(reinterpret_cast<const uint2*>(mine + (s - 1)));  // (off, len)
       src = ol.x;
       len = ol.y;
       plen = len + 2 + (s > 1 ? 1u : 0u);
@@ -437,7 +437,7 @@ __device__ __forceinline__ void put_token(uint32_t o, uint32_t b, uint32_t e, ui
 // the separator and E_s's first-token bytes); the interior tokens are copied from the tables,
 // lanes striding over the round's interior tokens.
 __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
-                                          const int32_t* __restrict__ mine, uint32_t n, uint32_t t,
+                                          const EntryRec* __restrict__ mine, uint32_t n, uint32_t t,
                                           uint32_t vocab, uint64_t vmagic, int32_t* tok_id,
                                           uint64_t* tok_begin, uint64_t* tok_end, int lane) {
   const uint32_t lv = g.entry_off[v + 1] - g.entry_off[v];
@@ -451,7 +451,7 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
     // the piece's entry record: two 16-byte loads of one 32-byte line
     uint4 ra4 = make_uint4(0, 0, 0, 0), rb4 = make_uint4(0, 0, 0, 0);
     if (act) {
-      const uint4* rp = reinterpret_cast<const uint4*>(g.ent + (s > 0 ? mine[s - 1] : v));
+      const uint4* rp = reinterpret_cast<const uint4*>(s > 0 ? mine + (s - 1) : g.ent + v);
       ra4 = __ldg(rp);
       rb4 = __ldg(rp + 1);
     }
@@ -559,7 +559,7 @@ __device__ __forceinline__ void emit_fast(const DevGraph& g, int32_t v, int k,
 
 // Text of a regular chunk (its tokens come from emit_fast in the same CTA's token warps).
 __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
-                                            const int32_t* __restrict__ mine, uint64_t goff,
+                                            const EntryRec* __restrict__ mine, uint64_t goff,
                                             uint32_t n, char* __restrict__ out, char* sb, int lane) {
   if (n <= kBuf) {
     const uint32_t pad = static_cast<uint32_t>(goff & 15), Q = pad + n;
@@ -579,7 +579,7 @@ __device__ __forceinline__ void render_text(const DevGraph& g, int32_t v, int k,
 
 // Text and tokens of an irregular chunk (the byte-level tokenizer over a whitespace mask).
 __device__ __forceinline__ void render_slow(const DevGraph& g, int32_t v, int k,
-                                            const int32_t* __restrict__ mine, uint64_t goff,
+                                            const EntryRec* __restrict__ mine, uint64_t goff,
                                             uint32_t n, uint32_t t, uint32_t vocab, uint64_t vmagic,
                                             char* __restrict__ out, int32_t* __restrict__ tok_id,
                                             uint64_t* __restrict__ tok_begin,
@@ -705,7 +705,7 @@ chunk_irregular_kernel(DevGraph g, RankedAdj ra, const uint64_t* __restrict__ by
     }
     const int2 vr = vrow[r];  // node, first entry of its ranked row (chunk_len_scan)
     const int k = static_cast<int>(static_cast<uint32_t>(sel_count[r]) & 0x7FFFFFFFu);
-    render_slow(g, vr.x, k, ra.idx + vr.y, goff, static_cast<uint32_t>(gend - goff), tok_off[r],
+    render_slow(g, vr.x, k, ra.recs + vr.y, goff, static_cast<uint32_t>(gend - goff), tok_off[r],
                 vocab, vmagic, out, tok_id, tok_begin, tok_end, sbuf[wi], smask[wi], lane);
   }
 }
@@ -828,10 +828,18 @@ chunk_regular_kernel(DevGraph g, RankedAdj ra, int n_req, const int32_t* __restr
   const int k = static_cast<int>(kr);
   const uint32_t n = static_cast<uint32_t>(gend - goff);
   if (text)
-    render_text(g, vr.x, k, ra.idx + vr.y, goff, n, out, sbuf[wi], lane);
+    render_text(g, vr.x, k, ra.recs + vr.y, goff, n, out, sbuf[wi], lane);
   else
-    emit_fast(g, vr.x, k, ra.idx + vr.y, n, tok_off[r], vocab, vmagic, tok_id, tok_begin, tok_end,
+    emit_fast(g, vr.x, k, ra.recs + vr.y, n, tok_off[r], vocab, vmagic, tok_id, tok_begin, tok_end,
               lane);
+}
+
+// the ranked neighbours' entry records, in rank order (the chunk kernels read a row's pieces as
+// one contiguous run instead of idx -> ent gathers)
+__global__ void rank_recs_kernel(DevGraph g, const int32_t* __restrict__ ridx, uint64_t e_count,
+                                 EntryRec* __restrict__ recs) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < e_count) recs[e] = g.ent[ridx[e]];
 }
 
 }  // namespace
@@ -899,7 +907,7 @@ size_t rank_sort_temp_bytes(uint64_t e_count, uint32_t n) {
 void rank_adjacency(const DevGraph& g, const uint32_t* off, const int32_t* idx, const int32_t* w,
                     uint64_t e_count, uint32_t n, void* temp, size_t temp_bytes, uint64_t* keys,
                     uint64_t* sorted, int32_t* ridx, uint64_t* pbytes, uint32_t* ptoks,
-                    uint32_t* pirr, uint32_t* tmp32, cudaStream_t s) {
+                    uint32_t* pirr, uint32_t* tmp32, EntryRec* recs, cudaStream_t s) {
   if (e_count) {
     rank_keys_kernel<<<static_cast<int>(ceil_div(e_count, 256)), 256, 0, s>>>(idx, w, e_count, keys);
     GLMX_CHECK_LAUNCH();
@@ -919,6 +927,10 @@ void rank_adjacency(const DevGraph& g, const uint32_t* off, const int32_t* idx, 
   GLMX_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, pirr, tmp32,
                                           static_cast<int64_t>(e_count + 1), s));
   GLMX_CUDA(cudaMemcpyAsync(pirr, tmp32, (e_count + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  if (e_count) {
+    rank_recs_kernel<<<static_cast<int>(ceil_div(e_count, 256)), 256, 0, s>>>(g, ridx, e_count, recs);
+    GLMX_CHECK_LAUNCH();
+  }
 }
 
 void entry_stats(const char* bytes, const uint32_t* off, uint32_t n, uint32_t* st, cudaStream_t s) {

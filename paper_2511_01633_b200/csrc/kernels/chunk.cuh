@@ -50,6 +50,7 @@ struct DevGraph {
 struct RankedAdj {
   const uint32_t* off;  // CSR row offsets (und_off or dir_off)
   const int32_t* idx;
+  const EntryRec* recs;  // ent[idx[e]]: the ranked neighbours' records, contiguous per row
   const uint64_t* pbytes;
   const uint32_t* ptoks;
   const uint32_t* pirr;
@@ -87,12 +88,13 @@ void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* no
                        const int32_t* irr_list, const int32_t* irr_count, const int2* vrow,
                        cudaStream_t s);
 // ranked adjacency of one CSR (off[0..n], idx) under weights w: keys/sorted scratch of e_count
-// u64, tmp32 of e_count + 1; outputs ridx[e_count], pbytes/ptoks/pirr[e_count + 1]
+// u64, tmp32 of e_count + 1; outputs ridx[e_count], pbytes/ptoks/pirr[e_count + 1], recs[e_count]
+// (g.ent must be built)
 size_t rank_sort_temp_bytes(uint64_t e_count, uint32_t n);
 void rank_adjacency(const DevGraph& g, const uint32_t* off, const int32_t* idx, const int32_t* w,
                     uint64_t e_count, uint32_t n, void* temp, size_t temp_bytes, uint64_t* keys,
                     uint64_t* sorted, int32_t* ridx, uint64_t* pbytes, uint32_t* ptoks,
-                    uint32_t* pirr, uint32_t* tmp32, cudaStream_t s);
+                    uint32_t* pirr, uint32_t* tmp32, EntryRec* recs, cudaStream_t s);
 // per-entry whitespace stats (DevGraph::ent_stat), once at graph upload
 void entry_stats(const char* bytes, const uint32_t* off, uint32_t n, uint32_t* st, cudaStream_t s);
 // per-entry interior-token counts (-> ent_ioff by an exclusive scan), then the token tables

@@ -228,16 +228,17 @@ glmx::RankedAdj glmx_graph::ranked_adj(int weight_mode, int directed) {
     rk.pbytes.reserve((E + 1) * 8);
     rk.ptoks.reserve((E + 1) * 4);
     rk.pirr.reserve((E + 1) * 4);
+    rk.recs.reserve(std::max<uint64_t>(E, 1) * sizeof(glmx::EntryRec));
     rank_adjacency(dev, off, directed ? dev.dir_idx : dev.und_idx,
                    weight_mode ? dev.w_by_type : dev.w_total, E, n, temp.p, temp.bytes,
                    keys.as<uint64_t>(), sorted.as<uint64_t>(), rk.ridx.as<int32_t>(),
                    rk.pbytes.as<uint64_t>(), rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>(),
-                   tmp32.as<uint32_t>(), stream);
+                   tmp32.as<uint32_t>(), rk.recs.as<glmx::EntryRec>(), stream);
     GLMX_CUDA(cudaStreamSynchronize(stream));  // before the scratch buffers are released
     rk.ready = true;
   }
-  return glmx::RankedAdj{off, rk.ridx.as<int32_t>(), rk.pbytes.as<uint64_t>(),
-                         rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>()};
+  return glmx::RankedAdj{off, rk.ridx.as<int32_t>(), rk.recs.as<glmx::EntryRec>(),
+                         rk.pbytes.as<uint64_t>(), rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>()};
 }
 
 // K1 driver: lengths -> scans -> render + tokenize.  Returns GLMX_ERR_ARG (with totals) when the

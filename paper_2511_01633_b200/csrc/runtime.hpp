@@ -76,7 +76,7 @@ struct glmx_graph {
   // ranked adjacency per (weight mode, directed) variant, built on first use (kernels/chunk.cuh)
   struct Ranked {
     bool ready = false;
-    DBuf ridx, pbytes, ptoks, pirr;
+    DBuf ridx, pbytes, ptoks, pirr, recs;
   } ranked[4];
   glmx::RankedAdj ranked_adj(int weight_mode, int directed);
   // the last batch built (nodes + config) and its totals: the fill call of the two-call protocol
