@@ -83,7 +83,7 @@ __device__ __forceinline__ ChunkLen chunk_len(const DevGraph& g, const RankedAdj
 // prefixes back to the first inclusive one, then publishes its own inclusive prefix.  Status words
 // carry the call's epoch, so the state needs no reset between calls.  Outputs byte_off[0..n] and
 // tok_off[0..n] ([n] = totals) and sel_count.
-constexpr int kLenThreads = 256, kLenItems = 4, kLenTile = kLenThreads * kLenItems;
+constexpr int kLenThreads = 256, kLenItems = 1, kLenTile = kLenThreads * kLenItems;
 
 __global__ void __launch_bounds__(kLenThreads)
 chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict__ node_idx,
