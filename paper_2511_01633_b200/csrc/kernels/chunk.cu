@@ -191,6 +191,7 @@ chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict
       tok_off[n_req] = ot;
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // ranked adjacency: sort keys w << 32 | ~u (descending == weight desc, index asc)
@@ -816,6 +817,9 @@ chunk_regular_kernel(DevGraph g, RankedAdj ra, int n_req, const int32_t* __restr
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const bool text = wi < kRW;
   const int r = blockIdx.x * kRW + (text ? wi : wi - kRW);
+  // launched as a programmatic dependent of chunk_len_scan: the CTAs are resident while the scan
+  // finishes and wait here for its outputs
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (r >= n_req) return;
   const uint64_t goff = byte_off[r], gend = byte_off[r + 1];
   if (gend > bytes_cap || tok_off[r + 1] > tok_cap) {  // the host grows the buffers and reruns
@@ -879,9 +883,21 @@ void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* no
                        const int32_t* irr_list, const int32_t* irr_count, const int2* vrow,
                        cudaStream_t s) {
   const uint64_t vmagic = vocab ? ~uint64_t(0) / vocab : 0;
-  chunk_regular_kernel<<<static_cast<int>(ceil_div(n_req, kRW)), 2 * kRW * 32, 0, s>>>(
-      g, ra, n_req, sel_count, byte_off, tok_off, vocab, vmagic, out, tok_id, tok_begin, tok_end,
-      bytes_cap, tok_cap, overflow, vrow);
+  // programmatic dependent launch: the regular-chunk CTAs start while the length+scan kernel
+  // drains (griddepcontrol.wait in the kernel orders them after its writes)
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(static_cast<unsigned>(ceil_div(n_req, kRW)));
+  lc.blockDim = dim3(2 * kRW * 32);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  GLMX_CUDA(cudaLaunchKernelEx(&lc, chunk_regular_kernel, g, ra, n_req, sel_count, byte_off,
+                               tok_off, vocab, vmagic, out, tok_id, tok_begin, tok_end, bytes_cap,
+                               tok_cap, overflow, vrow));
   GLMX_CHECK_LAUNCH();
   chunk_irregular_kernel<<<2 * kNumSMs, kRW * 32, 0, s>>>(
       g, ra, byte_off, tok_off, sel_count, vocab, vmagic, out, tok_id, tok_begin, tok_end,
