@@ -14,7 +14,7 @@
 //   chunk_len_scan : one thread per chunk computes (k', byte length, token count, regular flag)
 //                    from the prefixes; both exclusive scans in the same single-pass kernel
 //                    (warp-cooperative decoupled look-back); irregular chunks compacted to a list
-//   chunk_regular  : CTA = 4 text warps + 4 token warps for 4 chunks.  Text: per round of 32
+//   chunk_regular  : CTA = a text warp + a token warp for one chunk.  Text: per round of 32
 //                    pieces the 16-byte source words are numbered by a warp scan, each lane finds
 //                    its piece by a shuffle binary search, realigns the words to the destination
 //                    with funnel shifts and stores them whole (the separator bytes framing each
@@ -231,7 +231,12 @@ __global__ void rank_fill_kernel(DevGraph g, const uint64_t* __restrict__ sorted
 // without reading the text back from HBM.  Lane s copies piece s (entry bytes as aligned 4-byte
 // words, realigned to the destination by funnel shifts, ragged ends byte by byte).  Chunks longer
 // than the buffer are built in place in global memory by the same code.
-constexpr int kRW = 4;         // warps (chunks) per CTA
+constexpr int kRW = 4;         // warps (chunks) per CTA of the irregular-chunk kernel
+// chunks per CTA of chunk_regular (one text + one token warp each): one, so a CTA's slot frees as
+// soon as its own two warps finish (one-box A/B: 155 us vs 155-157 with 4 chunks per CTA, and a
+// tighter spread)
+constexpr int kRegW = 1;
+constexpr int kRegBlocks = 48 / (2 * kRegW);  // CTAs per SM at 40 registers (48 warps)
 constexpr int kBuf = 4096;     // staged chunk bytes per warp
 constexpr int kSeg = 1024;     // bytes per token-start compaction segment
 constexpr int kWordsU = 2;     // 16-byte loads in flight per lane
@@ -803,20 +808,20 @@ __global__ void token_ids_kernel(const uint64_t* __restrict__ hash, uint32_t n, 
   if (i < n) ids[i] = mod_vocab(hash[i], vocab, vmagic);
 }
 
-// Regular chunks, text and tokens in one launch: warps 0-3 of a CTA render the text of chunks
-// 4b..4b+3 (render_text), warps 4-7 emit their tokens (emit_fast), so the two halves of a chunk
-// run side by side on every SM.
-__global__ void __launch_bounds__(2 * kRW * 32, 6)
+// Regular chunks, text and tokens in one launch: warp w < kRegW of a CTA renders the text of chunk
+// kRegW * b + w (render_text), warp kRegW + w emits its tokens (emit_fast), so the two halves of a
+// chunk run side by side on every SM.
+__global__ void __launch_bounds__(2 * kRegW * 32, kRegBlocks)
 chunk_regular_kernel(DevGraph g, RankedAdj ra, int n_req, const int32_t* __restrict__ sel_count,
                      const uint64_t* __restrict__ byte_off, const uint32_t* __restrict__ tok_off,
                      uint32_t vocab, uint64_t vmagic, char* __restrict__ out,
                      int32_t* __restrict__ tok_id, uint64_t* __restrict__ tok_begin,
                      uint64_t* __restrict__ tok_end, uint64_t bytes_cap, uint64_t tok_cap,
                      int32_t* __restrict__ overflow, const int2* __restrict__ vrow) {
-  __shared__ __align__(16) char sbuf[kRW][kBuf + 16];
+  __shared__ __align__(16) char sbuf[kRegW][kBuf + 16];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const bool text = wi < kRW;
-  const int r = blockIdx.x * kRW + (text ? wi : wi - kRW);
+  const bool text = wi < kRegW;
+  const int r = blockIdx.x * kRegW + (text ? wi : wi - kRegW);
   // launched as a programmatic dependent of chunk_len_scan: the CTAs are resident while the scan
   // finishes and wait here for its outputs
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -886,8 +891,8 @@ void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* no
   // programmatic dependent launch: the regular-chunk CTAs start while the length+scan kernel
   // drains (griddepcontrol.wait in the kernel orders them after its writes)
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(static_cast<unsigned>(ceil_div(n_req, kRW)));
-  lc.blockDim = dim3(2 * kRW * 32);
+  lc.gridDim = dim3(static_cast<unsigned>(ceil_div(n_req, kRegW)));
+  lc.blockDim = dim3(2 * kRegW * 32);
   lc.dynamicSmemBytes = 0;
   lc.stream = s;
   cudaLaunchAttribute attr[1];
