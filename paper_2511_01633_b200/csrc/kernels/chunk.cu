@@ -109,7 +109,12 @@ chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict
     vv[i] = 0;
     if (r0 + i < n_req) {
       vv[i] = node_idx[r0 + i];
-      c[i] = chunk_len(g, ra, k, vv[i]);
+      if (ra.lens) {
+        const uint4 l = __ldg(ra.lens + vv[i]);
+        c[i] = ChunkLen{l.x, l.y, l.z, l.w};
+      } else {
+        c[i] = chunk_len(g, ra, k, vv[i]);
+      }
     }
     sb += c[i].bytes;
     stk += c[i].toks;
@@ -192,6 +197,13 @@ chunk_len_scan_kernel(DevGraph g, RankedAdj ra, int k, const int32_t* __restrict
     }
   }
   asm volatile("griddepcontrol.launch_dependents;");
+}
+
+__global__ void chunk_len_table_kernel(DevGraph g, RankedAdj ra, int k, uint4* __restrict__ out) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= g.n) return;
+  const ChunkLen c = chunk_len(g, ra, k, static_cast<int32_t>(v));
+  out[v] = make_uint4(static_cast<uint32_t>(c.bytes), c.toks, c.sel, c.row);
 }
 
 // ranked adjacency: sort keys w << 32 | ~u (descending == weight desc, index asc)
@@ -867,6 +879,14 @@ void chunk_token_ids(const uint64_t* hash, uint32_t n, uint32_t vocab, uint32_t*
   if (n == 0 || vocab == 0) return;
   token_ids_kernel<<<static_cast<int>(ceil_div(n, 256)), 256, 0, s>>>(hash, n, vocab,
                                                                       ~uint64_t(0) / vocab, ids);
+  GLMX_CHECK_LAUNCH();
+}
+
+void chunk_len_table(const DevGraph& g, const RankedAdj& ra, int k, uint4* out, cudaStream_t s) {
+  if (g.n == 0) return;
+  RankedAdj r = ra;
+  r.lens = nullptr;
+  chunk_len_table_kernel<<<static_cast<int>(ceil_div(g.n, 256)), 256, 0, s>>>(g, r, k, out);
   GLMX_CHECK_LAUNCH();
 }
 

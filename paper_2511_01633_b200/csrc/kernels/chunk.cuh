@@ -51,11 +51,15 @@ struct RankedAdj {
   const uint32_t* off;  // CSR row offsets (und_off or dir_off)
   const int32_t* idx;
   const EntryRec* recs;  // ent[idx[e]]: the ranked neighbours' records, contiguous per row
+  const uint4* lens;     // per node for the batch's k: {bytes, tokens, k' | irregular << 31, row}
+                         // (chunk_len_table), or null
   const uint64_t* pbytes;
   const uint32_t* ptoks;
   const uint32_t* pirr;
 };
 
+// The per-node chunk lengths for one k (chunk_len_scan reads them with one load per chunk)
+void chunk_len_table(const DevGraph& g, const RankedAdj& ra, int k, uint4* out, cudaStream_t s);
 // Decoupled look-back state of chunk_lengths_scan: per tile aggregate + inclusive prefix + a
 // status word (epoch << 2 | 1 aggregate / 2 inclusive); sized chunk_scan_tiles(n)
 struct ScanState {

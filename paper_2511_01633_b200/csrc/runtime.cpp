@@ -237,7 +237,7 @@ glmx::RankedAdj glmx_graph::ranked_adj(int weight_mode, int directed) {
     GLMX_CUDA(cudaStreamSynchronize(stream));  // before the scratch buffers are released
     rk.ready = true;
   }
-  return glmx::RankedAdj{off, rk.ridx.as<int32_t>(), rk.recs.as<glmx::EntryRec>(),
+  return glmx::RankedAdj{off, rk.ridx.as<int32_t>(), rk.recs.as<glmx::EntryRec>(), nullptr,
                          rk.pbytes.as<uint64_t>(), rk.ptoks.as<uint32_t>(), rk.pirr.as<uint32_t>()};
 }
 
@@ -273,7 +273,15 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
     ntok = g->k1_ntok;
   } else {
     g->k1_valid = false;
-    const glmx::RankedAdj ra = g->ranked_adj(cfg->weight_mode, cfg->directed);
+    glmx::RankedAdj ra = g->ranked_adj(cfg->weight_mode, cfg->directed);
+    // per-node lengths for this k (one kernel over the nodes when k or the variant changes)
+    const int64_t key = (static_cast<int64_t>(k) << 2) | (cfg->weight_mode ? 2 : 0) | (cfg->directed ? 1 : 0);
+    if (g->lens_key != key) {
+      g->d_lens.reserve(std::max<size_t>(g->dev.n, 1) * sizeof(uint4));
+      chunk_len_table(g->dev, ra, k, g->d_lens.as<uint4>(), s);
+      g->lens_key = key;
+    }
+    ra.lens = g->d_lens.as<uint4>();
     if (cfg->vocab && cfg->vocab != g->itok_vocab) {  // interior-token ids for this vocab
       g->d_itok_id.reserve(std::max<size_t>(g->n_interior, 1) * 4);
       chunk_token_ids(g->dev.itok_hash, g->n_interior, cfg->vocab, g->d_itok_id.as<uint32_t>(), s);
