@@ -924,6 +924,7 @@ void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* no
                                tok_off, vocab, vmagic, out, tok_id, tok_begin, tok_end, bytes_cap,
                                tok_cap, overflow, vrow));
   GLMX_CHECK_LAUNCH();
+  if (!irr_list) return;  // the graph has no irregular entries, so no irregular chunks
   chunk_irregular_kernel<<<2 * kNumSMs, kRW * 32, 0, s>>>(
       g, ra, byte_off, tok_off, sel_count, vocab, vmagic, out, tok_id, tok_begin, tok_end,
       bytes_cap, tok_cap, overflow, irr_list, irr_count, vrow);

@@ -84,7 +84,8 @@ void chunk_lengths_scan(const DevGraph& g, const RankedAdj& ra, int k, const int
 // are checked on the device: a chunk that does not fit sets *overflow and is skipped, and the
 // host grows the buffers and launches the render again (no host round trip before the render).
 // Regular chunks: one kernel whose CTAs pair 4 text warps with 4 token warps (table-driven
-// tokenizer); irregular chunks: a small grid over the list chunk_lengths_scan compacted.
+// tokenizer); irregular chunks: a small grid over the list chunk_lengths_scan compacted (not
+// launched when irr_list is null: the caller knows the graph has no irregular entries).
 void chunk_render_emit(const DevGraph& g, const RankedAdj& ra, const int32_t* node_idx, int n_req,
                        const int32_t* sel_count, const uint64_t* byte_off, const uint32_t* tok_off,
                        uint32_t vocab, char* out, int32_t* tok_id, uint64_t* tok_begin,

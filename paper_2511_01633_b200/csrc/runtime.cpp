@@ -157,7 +157,13 @@ void glmx_graph::upload() {
     entry_tokens(dev.entry_bytes, dev.entry_off, st, n, ioff, head, tail, tstate, itok_span,
                  itok_hash, stream);
     n_interior = n_int;
+    // irregular entries (entry_regular in chunk.cu: >= 2 tokens, first and last byte non-space):
+    // a graph without any never launches the byte-level chunk kernel
+    std::vector<uint32_t> hst(n);
+    GLMX_CUDA(cudaMemcpyAsync(hst.data(), st, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, stream));
     GLMX_CUDA(cudaStreamSynchronize(stream));  // before tmp (scan scratch) is released
+    n_irregular = 0;
+    for (uint32_t v : hst) n_irregular += ((v >> 29) == 7u && (v & 0x1FFFFFFFu) >= 2) ? 0u : 1u;
     dev.ent_head = head;
     dev.ent_tail = tail;
     dev.ent_tstate = tstate;
@@ -333,7 +339,8 @@ int chunk_build_impl(glmx_graph* g, const glmx_chunk_config* cfg, const int32_t*
                         cfg->vocab, g->d_bytes.as<char>(), g->d_tid.as<int32_t>(),
                         g->d_tbeg.as<uint64_t>(), g->d_tend.as<uint64_t>(),
                         g->d_bytes.bytes >= 16 ? g->d_bytes.bytes - 16 : 0, tok_cap, overflow,
-                        g->d_irr.as<int32_t>(), irr_count, g->d_vrow.as<int2>(), s);
+                        g->n_irregular ? g->d_irr.as<int32_t>() : nullptr, irr_count,
+                        g->d_vrow.as<int2>(), s);
     };
     render();
     GLMX_CUDA(cudaEventRecord(g->ev1, s));

@@ -70,6 +70,7 @@ struct glmx_graph {
   // K1 scratch
   DBuf d_nodes, d_cnt, d_off, d_bytes, d_tid, d_tbeg, d_tend, d_toff, d_scan, d_irr, d_vrow;
   uint32_t scan_epoch = 0;  // chunk_lengths_scan look-back state (d_scan) epoch
+  uint32_t n_irregular = 0;  // irregular entries (0: K1 skips its byte-level chunk kernel)
   uint32_t n_interior = 0;  // interior tokens of the regular entries (DevGraph::itok_*)
   DBuf d_lens;               // per-node chunk lengths for lens_key (chunk_len_table)
   int64_t lens_key = -1;     // (k, weight mode, directed) the table was built for
