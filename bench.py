@@ -697,7 +697,7 @@ def main():
     ]
     if chunk_ms > 0:
         k1_gbs = k1_bytes / (chunk_ms * 1e-3) / 1e9
-        kernels.append({"kernel": "K1 chunk_build (select+render+emit, 2 cub scans)",
+        kernels.append({"kernel": "K1 chunk_build (length+scan over the ranked adjacency, render+tokenize)",
                         "bound": "hbm", "achieved": k1_gbs, "peak": hbm, "unit": "GB/s",
                         "frac": k1_gbs / hbm, "ms_per_rotation": chunk_ms / max(1, k1_rotations),
                         "overlapped_with_prefill": True,
