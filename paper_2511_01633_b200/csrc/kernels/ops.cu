@@ -487,21 +487,18 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
   if (T <= 0) return;
   if (hd > 256 || hd % 16) throw Error(GLMX_ERR_ARG, "head_dim must be a multiple of 16, <= 256");
   if (hd == 128) {
-    // 16 heads per warp; small batches (< 768 tokens) 4 heads per warp and 2 warps per CTA, so a
-    // few hundred tokens still spread over the SMs with one load round trip each (measured
-    // crossover: 450 tokens 5.5 vs 6.3 us, 1000 tokens 8.3 vs 6.3 us)
+    // 3 passes (12 heads) per warp, 3 warps (tokens) per CTA: the 12 passes of a token split
+    // into 4 warps (Q | Q | Q+K | K+V), so every batch size spreads over the SMs with 3 loads in
+    // flight per lane.  Differential sweep with the input dirty in L2 (scripts/micro/k2_cfg.cu,
+    // profiles/r2_k2_launch_shapes.txt): 450 tokens 4.1 us (was 5.1 with 1 pass x 2 warps),
+    // 1536 6.6 (was 8.1 with 4 passes x 8 warps), 4096 13.3 (was 14.3), elsewhere equal.
     const int passes = static_cast<int>(ceil_div(H + 2 * Hkv, 4));
     if (!rope_cs) throw Error(GLMX_ERR_ARG, "head_dim 128 append needs the forward's RoPE table");
-    if (T < 768) {
-      rope_kv_append_warp_kernel<1><<<dim3(static_cast<int>(ceil_div(T, 2)), passes), 64, 0, s>>>(
-          qkv, rope_cs, slot, T, H, Hkv, pool, layer, q_out);
-    } else {
-      constexpr int kPassU = 4;
-      rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, 8)),
-                                                static_cast<int>(ceil_div(passes, kPassU))),
-                                           256, 0, s>>>(qkv, rope_cs, slot, T, H, Hkv, pool, layer,
-                                                        q_out);
-    }
+    constexpr int kPassU = 3, kWarps = 3;
+    rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, kWarps)),
+                                              static_cast<int>(ceil_div(passes, kPassU))),
+                                         kWarps * 32, 0, s>>>(qkv, rope_cs, slot, T, H, Hkv, pool,
+                                                              layer, q_out);
     GLMX_CHECK_LAUNCH();
     return;
   }
