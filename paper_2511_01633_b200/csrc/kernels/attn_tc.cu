@@ -84,7 +84,15 @@ void* g_attn_trace_ptr() {
   do {                                                                          \
     if (blockIdx.x == 0 && (j) < 1024) g_attn_trace[(ev) * 1024 + (j)] = clock64(); \
   } while (0)
+// CTA-level stamps of CTA 0 (kernel entry, setup done, teardown) in the last slots of event 15
+#define ATTN_TRACE_CTA(k)                                                          \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_attn_trace[15 * 1024 + 1023 - (k)] = clock64(); \
+  } while (0)
 #else
+#define ATTN_TRACE_CTA(k) \
+  do {                    \
+  } while (0)
 #define ATTN_TRACE(ev, j) \
   do {                    \
   } while (0)
@@ -139,6 +147,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   const uint32_t b_qfull = smem_addr(bars + kB0 + 6), b_qempty = smem_addr(bars + kB0 + 7);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + kB0 + 8);
 
+  ATTN_TRACE_CTA(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.H / p.Hkv;
   constexpr int kWarpProducer = kSoftmaxThreads / 32, kWarpMma = kWarpProducer + 1;
@@ -172,6 +181,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   const uint32_t t_s0 = tmem, t_o0 = tmem + kQT * kN;
+  ATTN_TRACE_CTA(1);
 
   if (warp == kWarpProducer || warp == kWarpVProducer) {
     // ---------------------------------------------------------------- TMA producers
@@ -547,6 +557,7 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   }
   tc_fence_before();
   __syncthreads();
+  ATTN_TRACE_CTA(2);
   if (warp == kWarpMma) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));

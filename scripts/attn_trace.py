@@ -59,6 +59,12 @@ if "--raw" in sys.argv:  # per-tile absolute timeline (cycles from the first sta
     t0 = min(x for e in ev for x in e[:n_t] if x)
     for j in range(n_t):
         print(j, " ".join(f"{(ev[e][j] - t0) if ev[e][j] else -1:7d}" for e in range(16)))
+cta = [buf[15 * 1024 + 1023 - k] for k in range(3)]
+if all(cta):
+    first_k = ev[14][0] if ev[14][0] else cta[1]
+    print(f"CTA 0: setup (barrier init + TMEM alloc) {cta[1] - cta[0]} cyc, setup -> first K issue "
+          f"{first_k - cta[1]} cyc, first K issue -> first S ready {ev[6][0] - first_k} cyc, "
+          f"last P -> teardown {cta[2] - max(ev[7][n_t - 1], ev[10][n_t - 1])} cyc, total {cta[2] - cta[0]} cyc")
 names = {"mma: wait P0": (0, 1), "mma: issue PV0+S0": (1, 2), "mma: wait P1": (2, 3),
          "mma: issue PV1+S1": (3, 4), "WG0: wait S0": (5, 6), "WG0: softmax": (6, 7),
          "WG1: wait S1": (8, 9), "WG1: softmax": (9, 10)}
