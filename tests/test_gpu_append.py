@@ -10,10 +10,22 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("T", [1, 7, 64, 767, 768, 1000, 2501])  # ragged CTA tails (3 tokens per CTA) and the old 768-token crossover
 def test_append_matches_reference(T):
+    check_append(T, 32, 8)
+
+
+# head counts whose 4-head passes do not fill the 3-pass warp groups evenly: C1's tiny decoder
+# (4 q / 2 kv: 2 passes, one partial group), 20 heads (5 passes: 3 + 2), MHA 8/8 (6 passes)
+@pytest.mark.parametrize("H,Hkv", [(4, 2), (12, 4), (8, 8)])
+@pytest.mark.parametrize("T", [1, 5, 301])
+def test_append_head_configs(T, H, Hkv):
+    check_append(T, H, Hkv)
+
+
+def check_append(T, H, Hkv):
     from paper_2511_01633_b200.ops import rope_kv_append
     from torch_refs import reference_rope
 
-    H, Hkv, hd, B, L, layer = 32, 8, 128, 16, 3, 2
+    hd, B, L, layer = 128, 16, 3, 2
     g = torch.Generator().manual_seed(T)
     n_pages = (T + B - 1) // B + 5
     qkv = torch.randn((T, (H + 2 * Hkv) * hd), generator=g).to(torch.bfloat16).cuda()
