@@ -128,24 +128,55 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region.
+
+    NVML (nvidia_ml_py) polled every 10 ms from a thread, each sample time-stamped, so a short
+    timed region (~0.7 s at the default --steps) still gets tens of samples and only samples
+    taken between mark() and stop() count.  (nvidia-smi -lms piped into Python is block-buffered:
+    its lines arrive in bursts, so the round-2 runs saw one sample per region.)  Falls back to
+    nvidia-smi when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
-        self.first = 0
+        self.rows = []  # (monotonic time, sm MHz, reasons bitmask)
+        self.t0 = self.t1 = None
         self.proc = None
+        self.nvml = None
+        self.max_mhz = None
+        self.halt = threading.Event()
 
     def mark(self):
-        """The timed region starts: only samples from here on count (nvidia-smi is started
+        """The timed region starts: only samples from here on count (the sampler is started
         earlier, so its start-up latency does not eat the samples of a short region)."""
-        self.first = len(self.rows)
+        self.t0 = time.monotonic()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:  # the CUDA device this rank runs on, whatever CUDA_VISIBLE_DEVICES maps it to
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(
+                uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
 
     def start(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.nvml = (nv, h)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -156,32 +187,52 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.halt.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            except Exception:
+                return
+            self.rows.append((time.monotonic(), sm, rs))
+            self.halt.wait(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.max_mhz = float(parts[1])
+                rs = 0
+                for (_, bit), v in zip(self.REASONS, parts[3:]):
+                    if v.lower().startswith("active"):
+                        rs |= bit
+                # nvidia-smi lines arrive buffered: their read time is not their sample time
+                self.rows.append((None, float(parts[0]), rs))
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        rows = self.rows[self.first:]
+        self.t1 = time.monotonic()
+        if self.nvml is None and self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        self.halt.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        self.thread.join(timeout=5)
+        t0 = self.t0 if self.t0 is not None else -1e30
+        rows = [r for r in self.rows if r[0] is None or t0 <= r[0] <= self.t1]
+        if not rows:  # a region shorter than the poll interval: the samples around it
+            rows = self.rows[-2:]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = sorted(float(r[0]) for r in rows)
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[3:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]),
-                "samples": len(rows), "reasons": sorted(reasons)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        sm = sorted(r[1] for r in rows)
+        reasons = sorted({n for r in rows for n, bit in self.REASONS if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": self.max_mhz,
+                "samples": len(rows), "source": "nvml" if self.nvml else "nvidia-smi",
+                "reasons": reasons}
 
 
 def load_traffic():
