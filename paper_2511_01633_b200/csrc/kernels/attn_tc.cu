@@ -179,6 +179,9 @@ paged_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map,
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // barriers and TMEM are set up while the K2 append before us drains (programmatic dependent
+  // launch); nothing global is read before this point
+  pdl_wait();
   const uint32_t tmem = *tmem_holder;
   const uint32_t t_s0 = tmem, t_o0 = tmem + kQT * kN;
   ATTN_TRACE_CTA(1);
@@ -664,8 +667,8 @@ void paged_attention_tc(const AttnParams& p, const void* kv_map, uint32_t rows_t
     attr[dev & 63].store(true, std::memory_order_release);
   }
   TcParams tp{p, rows_total, sc.pieces, sc.cta_off, sc.part_o, sc.part_ml, sc.partners};
-  paged_attn_tc_kernel<<<sc.grid, kThreads, kSmem, s>>>(*reinterpret_cast<const CUtensorMap*>(kv_map),
-                                                        *reinterpret_cast<const CUtensorMap*>(q_map), tp);
+  launch_pdl(paged_attn_tc_kernel, dim3(sc.grid), dim3(kThreads), kSmem, s,
+             *reinterpret_cast<const CUtensorMap*>(kv_map), *reinterpret_cast<const CUtensorMap*>(q_map), tp);
   GLMX_CHECK_LAUNCH();
   if (sc.n_combine > 0) {
     attn_combine_kernel<<<dim3(sc.n_combine, kQT * kM / 8), 256, 0, s>>>(p, sc.combine, sc.part_o, sc.part_ml);

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../host/common.hpp"
 
@@ -19,6 +20,30 @@
 #define GLMX_CHECK_LAUNCH() GLMX_CUDA(cudaGetLastError())
 
 namespace glmx {
+
+// Programmatic dependent launch: a kernel that reads its predecessor's output is launched with
+// programmatic stream serialization so its grid is set up (and its CTAs fill SMs as the
+// predecessor's last CTAs retire) before the predecessor has finished; pdl_wait() at the kernel's
+// top blocks until the predecessor grid has completed and its writes are visible.  A kernel
+// launched without the attribute passes pdl_wait() at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  GLMX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 
 constexpr int kNumSMs = 148;
 

@@ -81,6 +81,7 @@ rmsnorm_reg_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows
                    const __nv_bfloat16* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out) {
   constexpr int kV = D / 4 / NT;  // float4 per thread
   __shared__ float red[32];
+  pdl_wait();
   const int t = blockIdx.x;
   const int64_t src = rows ? rows[t] : t;
   const float4* xr = reinterpret_cast<const float4*>(x + src * D);
@@ -216,6 +217,7 @@ rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const float2* 
                            const int64_t* __restrict__ slot, int T, int H, int Hkv, PoolGeom pool,
                            uint32_t layer, __nv_bfloat16* __restrict__ q_out) {
   constexpr int kHd = 128, kHalf = 64, kChunks = 8, kHeadsPerPass = 32 / kChunks;
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -293,6 +295,7 @@ rope_kv_append_warp_kernel(const __nv_bfloat16* __restrict__ qkv, const float2* 
 // divide is hoisted by iterating rows in the grid's y dimension.
 __global__ void __launch_bounds__(256)
 swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ff, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
   const int vec_per_row = ff / 8;
   for (int t = blockIdx.y; t < T; t += gridDim.y) {
     const uint4* g4 = reinterpret_cast<const uint4*>(gu + static_cast<int64_t>(t) * 2 * ff);
@@ -458,7 +461,7 @@ void rmsnorm(const float* x, const int32_t* rows, int T, int d, const __nv_bfloa
              float eps, __nv_bfloat16* out, cudaStream_t s) {
   if (T <= 0) return;
   if (d == 4096)
-    rmsnorm_reg_kernel<256, 4096><<<T, 256, 0, s>>>(x, rows, w, eps, out);
+    launch_pdl(rmsnorm_reg_kernel<256, 4096>, dim3(T), dim3(256), 0, s, x, rows, w, eps, out);
   else
     rmsnorm_kernel<256><<<T, 256, 0, s>>>(x, rows, d, w, eps, out);
   GLMX_CHECK_LAUNCH();
@@ -495,10 +498,9 @@ void rope_kv_append(const __nv_bfloat16* qkv, const int32_t* pos, const int64_t*
     const int passes = static_cast<int>(ceil_div(H + 2 * Hkv, 4));
     if (!rope_cs) throw Error(GLMX_ERR_ARG, "head_dim 128 append needs the forward's RoPE table");
     constexpr int kPassU = 3, kWarps = 3;
-    rope_kv_append_warp_kernel<kPassU><<<dim3(static_cast<int>(ceil_div(T, kWarps)),
-                                              static_cast<int>(ceil_div(passes, kPassU))),
-                                         kWarps * 32, 0, s>>>(qkv, rope_cs, slot, T, H, Hkv, pool,
-                                                              layer, q_out);
+    launch_pdl(rope_kv_append_warp_kernel<kPassU>,
+               dim3(static_cast<int>(ceil_div(T, kWarps)), static_cast<int>(ceil_div(passes, kPassU))),
+               dim3(kWarps * 32), 0, s, qkv, rope_cs, slot, T, H, Hkv, pool, layer, q_out);
     GLMX_CHECK_LAUNCH();
     return;
   }
@@ -513,7 +515,7 @@ void swiglu(const __nv_bfloat16* gu, int T, int ff, __nv_bfloat16* out, cudaStre
   if (ff % 8) throw Error(GLMX_ERR_ARG, "d_ff must be a multiple of 8");
   const int xb = static_cast<int>(ceil_div(ff / 8, 256));
   dim3 grid(xb, std::min(T, 65535));
-  swiglu_kernel<<<grid, 256, 0, s>>>(gu, T, ff, out);
+  launch_pdl(swiglu_kernel, grid, dim3(256), 0, s, gu, T, ff, out);
   GLMX_CHECK_LAUNCH();
 }
 
